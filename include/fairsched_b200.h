@@ -1,0 +1,211 @@
+/*
+ * fairsched_b200.h -- C ABI of the B200-native DLPM / D^2LPM decision path.
+ *
+ * One shared library (paper_2501_14312_b200/libfsb200.so) built for sm_100a.
+ * Plain pointers and sizes only; no torch types cross this boundary.  Every
+ * entry point returns an fs status code; on failure fs_last_error() returns a
+ * thread-local message.  No exception crosses the ABI and there is no CPU
+ * fallback: without a usable CUDA device every call fails with FS_ERR_CUDA.
+ *
+ * The reference (`fairsched`, arXiv 2501.14312) has no native FFI for this
+ * path except `common_prefix_len` (pkg/src/fairsched/_speedups.pyx:11-22); its
+ * plug points are Python protocols.  Each group below names the reference
+ * interface it replaces (paths relative to /root/reference/pkg/src/fairsched).
+ * INTEGRATION.md shows the ctypes binding the Python adapters use.
+ *
+ * Ownership: the library owns all device state behind opaque handles.  Host
+ * buffers passed in are read (or written) before the call returns.
+ * Threading: one handle is used by one thread at a time; calls are ordered on
+ * the handle's CUDA stream and are synchronous unless stated otherwise.
+ */
+#ifndef FAIRSCHED_B200_H
+#define FAIRSCHED_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors of radix.py:19 / :183, local_policies.py:81-82,
+ * global_policies.py:97-98 map onto these) */
+#define FS_OK 0
+#define FS_ERR_INVALID 1     /* bad argument (ValueError in the reference)          */
+#define FS_ERR_CUDA 2        /* CUDA runtime / no device                            */
+#define FS_ERR_CACHE_FULL 3  /* radix.py:150-151 CacheFull                          */
+#define FS_ERR_TOKEN_RANGE 4 /* token id outside [0, 2^31) (requests.py:92)         */
+#define FS_ERR_NOMEM 5       /* device allocation / table capacity                  */
+#define FS_ERR_INTERNAL 6    /* device-side consistency check failed                */
+#define FS_ERR_UNDERFLOW 7   /* radix.py:183 unpin below zero                       */
+
+typedef struct fs_ctx fs_ctx;               /* one device: token arena + request pool */
+typedef struct fs_trie fs_trie;             /* one RadixTree (local or global)        */
+typedef struct fs_worker fs_worker;         /* one DLPM/LPM worker policy             */
+typedef struct fs_dispatcher fs_dispatcher; /* one D2LPM dispatcher                   */
+
+const char *fs_last_error(void);
+int fs_version(void);
+int fs_device_count(int *count);
+
+/* ---- context / request pool ------------------------------------------------
+ * Replaces the Python Request objects' token tuples (requests.py:22-32,
+ * Trace.materialize requests.py:134-161): tokens are uploaded once per request
+ * into a device arena and referenced by request id from then on.            */
+int fs_ctx_create(int device, int64_t arena_tokens, int64_t max_requests, fs_ctx **out);
+int fs_ctx_destroy(fs_ctx *ctx);
+int fs_ctx_sync(fs_ctx *ctx);
+/* Append n requests.  tokens: concatenated ids, offsets[i]/lens[i] index them;
+ * clients: dense client ids; labels: order key of (arrival, rid) used as the
+ * LPM tie-break (local_policies.py:17).  Writes the new request ids. */
+int fs_requests_add(fs_ctx *ctx, int64_t n, const int32_t *tokens, const int64_t *offsets,
+                    const int32_t *lens, const int32_t *clients, const int64_t *labels,
+                    int32_t *out_ids);
+/* Relabel requests (the order-maintenance labels ran out of gaps). */
+int fs_requests_set_labels(fs_ctx *ctx, int64_t n, const int32_t *ids, const int64_t *labels);
+int fs_requests_count(fs_ctx *ctx, int64_t *n);
+int fs_request_info(fs_ctx *ctx, int32_t id, int64_t *arena_off, int32_t *len);
+/* Read n arena tokens starting at arena offset off (paths of eviction records). */
+int fs_arena_read(fs_ctx *ctx, int64_t off, int64_t n, int32_t *out);
+
+/* ---- RadixTree  (radix.py:48-340) ------------------------------------------
+ * capacity < 0 means None (global routing index).  n_workers bounds worker
+ * tags when track_workers != 0 (<= 64).                                      */
+int fs_trie_create(fs_ctx *ctx, int64_t capacity, int track_workers, int n_workers, fs_trie **out);
+int fs_trie_destroy(fs_trie *t);
+/* used_tokens, pinned_tokens (radix.py:53-54), next seq (radix.py:55), live nodes */
+int fs_trie_stats(fs_trie *t, int64_t *used, int64_t *pinned, int64_t *next_seq, int64_t *nodes);
+
+/* Batched longest-prefix match (K1).  stamp != 0: match_prefix semantics with
+ * last_access = now on every matched node (radix.py:83-91); stamp == 0: probe
+ * (radix.py:93-99).  out_cov[i] = matched tokens lying in pinned nodes, so
+ * probe's unpinned count = out_mlen[i] - out_cov[i].  Either output may be NULL. */
+int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int64_t now, int stamp,
+                  int32_t *out_mlen, int32_t *out_cov);
+
+/* Eviction records (radix.py:217-249): (arena offset of the full path, full
+ * path length, keep_len).  Buffers may be NULL when rec_cap == 0; *n_rec
+ * always receives the record count (records beyond rec_cap are dropped). */
+typedef struct {
+    int64_t rec_cap;
+    int64_t *rec_src;
+    int32_t *rec_len;
+    int32_t *rec_keep;
+    int64_t n_rec;
+} fs_records;
+
+/* Re-read records [first, first+n) of the trie's last operation (the device
+ * sink keeps them until the next operation on this trie). */
+int fs_trie_read_records(fs_trie *t, int64_t first, int64_t n, int64_t *src, int32_t *len, int32_t *keep);
+
+/* RadixTree.insert (radix.py:128-162); worker < 0 means None.  *path_node is
+ * the deepest node of the returned path (the handle pin/unpin use, radix.py:164-172),
+ * -1 for an empty path.  Returns FS_ERR_CACHE_FULL after performing the evictions
+ * exactly like the reference (records are still reported). */
+int fs_trie_insert(fs_trie *t, int32_t req, int64_t now, int32_t worker, int32_t *new_len,
+                   int32_t *path_node, fs_records *recs);
+/* RadixTree.admit (radix.py:187-192): probe, insert, pin. */
+int fs_trie_admit(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, int32_t *path_node,
+                  fs_records *recs);
+int fs_trie_pin(fs_trie *t, int32_t path_node);   /* radix.py:174-178 */
+int fs_trie_unpin(fs_trie *t, int32_t path_node); /* radix.py:180-185 */
+/* RadixTree.evict_lru without a protect set (radix.py:210-250) */
+int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs);
+/* RadixTree.longest_match_workers (radix.py:101-110): mask bit w = worker w tagged */
+int fs_trie_longest_match_workers(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, uint64_t *mask);
+/* RadixTree.evict_notify (radix.py:254-302); the path is arena[path_src : path_src+path_len] */
+int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_len, int32_t worker,
+                         int32_t keep_len, int64_t notice_time);
+/* Node table export for RadixTree.dump / check (radix.py:306-340).  Writes up to
+ * cap nodes (index 0 = root) and sets *n to the node-table size; dead slots have
+ * parent == -2. wmask may be NULL. */
+int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src, int32_t *start,
+                   int32_t *end, int32_t *parent, int32_t *ref, int64_t *last_access,
+                   uint64_t *wmask);
+
+/* ---- DLPM / LPM worker  (local_policies.py:74-136 + worker.py:87-135) ------
+ * policy 0 = Dlpm (deficit gate, quantum refill), 1 = Lpm (gate always true).
+ * The worker owns the queue mirror (request ids), the per-client deficit
+ * counters q, refill counts and client_list membership.                     */
+int fs_worker_create(fs_ctx *ctx, fs_trie *tree, int policy, int64_t quantum, int64_t M,
+                     int64_t output_reserve, int64_t w_e, int64_t w_q, int32_t max_clients,
+                     fs_worker **out);
+int fs_worker_destroy(fs_worker *w);
+/* Worker.enqueue -> on_request_enqueued (worker.py:142-148, local_policies.py:88-92) */
+int fs_worker_enqueue(fs_worker *w, int64_t n, const int32_t *req_ids);
+/* Dlpm.on_outputs (local_policies.py:130-133): q[c] -= w_q * counts[i] */
+int fs_worker_outputs(fs_worker *w, int64_t n, const int32_t *clients, const int64_t *counts);
+/* Dlpm.check_refill (local_policies.py:94-106) for an explicit queued-client set */
+int fs_worker_check_refill(fs_worker *w, int64_t n, const int32_t *queued_clients, int *refilled);
+/* Host mirror of q / refill_counts / client_list membership (Dlpm.counters(),
+ * local_policies.py:135-136).  Any pointer may be NULL. */
+int fs_worker_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills, uint8_t *known);
+int fs_worker_set_counter(fs_worker *w, int32_t client, int64_t q);
+/* Grow the client tables (clients are dense ids assigned by the caller). */
+int fs_worker_reserve_clients(fs_worker *w, int32_t max_clients);
+/* Mark clients as members of Dlpm.client_list without enqueueing a request. */
+int fs_worker_mark_known(fs_worker *w, int64_t n, const int32_t *clients);
+
+/* One schedule step: Dlpm.fill / Lpm.fill (local_policies.py:108-128, 66-71).
+ * Matches every queued request (K1, stamping last_access = now), sorts by
+ * (-mlen, label) (K2), then runs the deficit-gated admission passes with the
+ * closed-form refill and budget test and performs each admission's radix
+ * insert / split / LRU evict / pin on device (K3+K4).
+ * generated_total and headroom are Worker.generated_total and
+ * Worker._reserved_headroom() at the call (worker.py:95-99). */
+typedef struct {
+    int64_t cap_adm;
+    int32_t *adm_req;           /* admitted request ids, in admission order        */
+    int32_t *adm_mlen;          /* match length at admission (probe, radix.py:189) */
+    int64_t *adm_unpinned;      /* probe's matched-unpinned tokens (worker.py:102) */
+    int64_t *adm_pinned_before; /* tree.pinned_tokens seen by can_add              */
+    int32_t *adm_path_node;     /* pin handle                                      */
+    int64_t *adm_rec_end;       /* records emitted up to and including this admission */
+    fs_records recs;
+    int64_t n_adm;              /* out */
+    int64_t n_queued;           /* out: requests evaluated (scheduling decisions) */
+    int64_t used, pinned;       /* out: tree stats after the fill */
+    float device_ms;            /* out: device time of the fill (CUDA events)    */
+} fs_fill_result;
+int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom,
+                   fs_fill_result *res);
+/* Timing breakdown of the last fill: [merge, match K1, sort K2, schedule K3/K4] ms */
+int fs_worker_last_phases(fs_worker *w, float *ms4);
+/* Queue length currently mirrored on device (worker.queue, worker.py:73) */
+int fs_worker_queue_len(fs_worker *w, int64_t *n);
+
+/* ---- D2LPM dispatcher  (global_policies.py:88-132) --------------------------
+ * Owns the global routing index (a track_workers RadixTree), the per
+ * (client, worker) counters q_{i,w} and queue sizes.  Workers are 0..D-1.   */
+int fs_dispatcher_create(fs_ctx *ctx, int D, int64_t quantum, int64_t w_e, int64_t w_q,
+                         int32_t max_clients, fs_dispatcher **out);
+int fs_dispatcher_destroy(fs_dispatcher *d);
+fs_trie *fs_dispatcher_tree(fs_dispatcher *d);
+/* Dispatcher.dispatch for n arrivals in order (global_policies.py:40-46,
+ * 107-124): longest_match_workers, SelectWorker with closed-form refill,
+ * queue_size += 1, q -= w_e*input_len, global insert with worker tag.
+ * Outputs per arrival: worker, match length, matched-worker mask, refill rounds. */
+int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
+                const int64_t *now, int32_t *out_worker, int32_t *out_mlen, uint64_t *out_mask,
+                int64_t *out_rounds);
+/* D2lpm.on_finish (global_policies.py:126-129) */
+int fs_dispatch_finish(fs_dispatcher *d, int32_t client, int32_t worker, int64_t output_tokens);
+/* q_{i,w} row of one client (D values) and dict-key presence flags */
+int fs_dispatch_counters(fs_dispatcher *d, int32_t client, int64_t *q_row, uint8_t *present);
+int fs_dispatch_queue_sizes(fs_dispatcher *d, int64_t *sizes);
+/* D2lpm.select_worker alone (global_policies.py:107-114): refill rounds and the
+ * locality-first / min-queue choice for a given matched mask; no queue_size or
+ * counter charge, no index update. */
+int fs_dispatch_select(fs_dispatcher *d, int32_t client, uint64_t matched_mask, int32_t *worker,
+                       int64_t *rounds);
+/* Overwrite q_{i,w} / queue_size[w] (the Python dicts are mutable by callers). */
+int fs_dispatch_set_counter(fs_dispatcher *d, int32_t client, int32_t worker, int64_t q);
+int fs_dispatch_set_queue_size(fs_dispatcher *d, int32_t worker, int64_t size);
+int fs_dispatcher_reserve_clients(fs_dispatcher *d, int32_t max_clients);
+/* Device-side copy of the counters (tests compare it with the host mirror). */
+int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t *q, uint8_t *present, int64_t *qsize);
+int fs_worker_device_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAIRSCHED_B200_H */

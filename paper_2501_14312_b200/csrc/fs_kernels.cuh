@@ -1,0 +1,627 @@
+// fs_kernels.cuh -- kernels of the decision path.
+//
+//   K1  k_match      warp-per-request longest-prefix match of the whole queue
+//                    against the device trie, stamping last_access, emitting
+//                    (mlen, pinned coverage, frontier node, next token).
+//   K2  (CUB radix sort of the 14-16-bit (L - mlen) key, stable => ties stay in
+//        (arrival, rid) label order the queue is kept in)
+//   K3+K4 k_schedule one persistent CTA: deficit-gated first-admissible search
+//                    with the closed-form refill and budget test, and each
+//                    admission's radix insert / split / LRU evict / pin.
+//   k_op / k_dispatch single-CTA tree operations and D2LPM dispatch chains.
+#pragma once
+#include "fs_device.cuh"
+
+#define FS_SCHED_THREADS 1024
+#define FS_ITEMS 4
+#define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
+#define FS_MAXA 2048
+#define FS_NONE 0x7fffffff
+
+// ---------------------------------------------------------------- K1
+__global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
+                                               const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
+                                               int64_t now, int stamp, uint32_t kmax,
+                                               uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
+                                               int32_t *__restrict__ out_cov, int32_t *__restrict__ out_fnode,
+                                               int32_t *__restrict__ out_next) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int32_t r = ids[i];
+    const int32_t len = rlen[r];
+    const int32_t *rq = t.arena + roff[r];
+    const WalkOut w = warp_walk(t, rq, len, lane, stamp != 0, now, nullptr);
+    if (lane == 0) {
+        if (out_key) out_key[i] = kmax - (uint32_t)w.mlen;
+        if (out_mlen) out_mlen[i] = w.mlen;
+        if (out_cov) out_cov[i] = w.cov;
+        if (out_fnode) out_fnode[i] = w.fnode;
+        if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
+    }
+}
+
+// ---------------------------------------------------------------- queue upkeep
+// Stable merge of the label-ordered queue `a` with the label-ordered arrivals `b`.
+__global__ void k_merge(const int32_t *__restrict__ a, int32_t na, const int32_t *__restrict__ b,
+                        const int64_t *__restrict__ lb, int32_t nb, const int64_t *__restrict__ rlabel,
+                        int32_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) {
+        const int64_t la = rlabel[a[i]];
+        int32_t lo = 0, hi = nb;
+        while (lo < hi) { const int32_t m = (lo + hi) >> 1; if (lb[m] < la) lo = m + 1; else hi = m; }
+        out[i + lo] = a[i];
+    } else if (i < (int64_t)na + nb) {
+        const int32_t k = (int32_t)(i - na);
+        const int64_t l = lb[k];
+        int32_t lo = 0, hi = na;
+        while (lo < hi) { const int32_t m = (lo + hi) >> 1; if (rlabel[a[m]] < l) lo = m + 1; else hi = m; }
+        out[k + lo] = b[k];
+    }
+}
+
+// Gather per-sorted-position scheduler slots: {client, cov, next token, state}.
+__global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__restrict__ queue, int32_t n,
+                         const int32_t *__restrict__ cov, const int32_t *__restrict__ fnode,
+                         const int32_t *__restrict__ next, const int32_t *__restrict__ rclient,
+                         const int32_t *__restrict__ rlen, int32_t *__restrict__ s_req, int4 *__restrict__ slot,
+                         int32_t *__restrict__ s_len, int32_t *__restrict__ s_fnode) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int32_t qi = perm[p];
+    const int32_t r = queue[qi];
+    s_req[p] = r;
+    s_len[p] = rlen[r];
+    s_fnode[p] = fnode[qi];
+    slot[p] = make_int4(rclient[r], cov[qi], next[qi], 0);
+}
+
+// ---------------------------------------------------------------- K3 + K4
+struct FillArgs {
+    TrieView t;
+    int32_t n;
+    const int32_t *s_req;
+    int4 *slot;  // {client, cov(B), next token, state: >=0 pending w/ exact-epoch, -1 admitted}
+    const int32_t *s_len;
+    int32_t *s_fnode;
+    const int64_t *roff;
+    int64_t *q, *refills;
+    const uint8_t *known;
+    int32_t nclients;
+    int32_t *pend_cnt;
+    const int32_t *dl_client;  // on_outputs deltas to apply first
+    const int64_t *dl_delta;
+    int32_t ndl;
+    int64_t M, R, gen_total, headroom0, w_e, quantum, now;
+    int32_t lpm;
+    int32_t *path;
+    int32_t *adm_req, *adm_mlen, *adm_node;
+    int64_t *adm_unp, *adm_pinb, *adm_rec_end;
+    int32_t adm_cap;
+    int8_t *rstate;
+    int64_t *hdr;  // [n_adm, n_rec, status, epochs, refill_events, resumes]
+};
+
+struct SchedSmem {
+    InsertSmem ins;
+    int32_t wl[FS_CHUNK];
+    int32_t aB[FS_MAXA];
+    int32_t aTok[FS_MAXA];
+    int64_t red64[32];
+    int32_t red32[32];
+    int32_t wl_n, minA, minB;
+    int32_t cursor, progress, epoch, npos, nadm, stop, j;
+    int64_t headroom, slack_at;
+    int64_t resumes, refill_events;
+};
+
+__device__ __forceinline__ int64_t sched_slack(const FillArgs &a, int64_t headroom) {
+    const int64_t pinned = a.t.sc->pinned;
+    int64_t s = a.M - a.gen_total - headroom - a.R - pinned;  // worker.py:104-107
+    const int64_t cap = a.t.sc->capacity;
+    if (cap > 0 && cap - pinned < s) s = cap - pinned;        // worker.py:108-109
+    return s;
+}
+
+__device__ inline int32_t block_min_i32(int32_t v, int32_t *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_down_sync(FS_FULL, v, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? red[lane] : FS_NONE;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_down_sync(FS_FULL, v, o));
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+__device__ inline int64_t block_sum_i64(int64_t v, int64_t *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FS_FULL, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FS_FULL, v, o);
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+__device__ inline int64_t block_min_i64(int64_t v, int64_t *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, (int64_t)__shfl_down_sync(FS_FULL, v, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? red[lane] : INT64_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = min(v, (int64_t)__shfl_down_sync(FS_FULL, v, o));
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+// Exact pinned coverage B of a queued request, resumed from its cached frontier
+// (node holding depth B).  Pinned nodes are never freed or truncated inside a
+// fill, and a split only moves a node's start deeper, so climbing parents until
+// start < B finds the node that now holds depth B.  One warp.
+__device__ inline void warp_resume(const FillArgs &a, int32_t p, int lane) {
+    const TrieView &t = a.t;
+    const int32_t r = a.s_req[p];
+    const int32_t len = a.s_len[p];
+    const int32_t *rq = t.arena + a.roff[r];
+    const int32_t B = a.slot[p].y;
+    int32_t N = a.s_fnode[p];
+    while (N != 0 && t.start[N] >= B) N = t.parent[N];
+    int32_t idx = B;
+    bool boundary = true;
+    if (N != 0 && idx < t.end[N]) {
+        const int32_t n = min(t.end[N] - idx, len - idx);
+        const int32_t k = warp_lcp(t.arena + t.src[N] + idx, rq + idx, n, lane);
+        idx += k;
+        boundary = (idx == t.end[N]);
+    }
+    if (boundary) {
+        while (idx < len) {
+            const int32_t c = h_find(t, N, rq[idx]);
+            if (c < 0 || t.ref[c] == 0) break;
+            const int32_t el = elen(t, c);
+            const int32_t n = min(el, len - idx);
+            const int32_t k = 1 + warp_lcp(t.arena + t.src[c] + t.start[c] + 1, rq + idx + 1, n - 1, lane);
+            idx += k;
+            N = c;
+            if (k < el) break;
+        }
+    }
+    if (lane == 0) {
+        a.slot[p].y = idx;
+        a.slot[p].z = idx < len ? rq[idx] : -1;
+        a.s_fnode[p] = N;
+    }
+}
+
+// First sorted position p in [from, until) that is pending and, unless
+// any_mode, passes the deficit gate (q > 0, skipped for LPM) and the budget
+// test len - B <= slack with B exact.  Stale B values (an admission happened
+// after B was last exact) are refreshed only when an admission since then had
+// the same pinned coverage and the same next token -- the only way LCP(r, a)
+// can exceed B ("exact budget test").
+__device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t until, bool any_mode,
+                              int64_t slack) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int32_t epoch = sm->epoch;
+    for (int32_t base = from; base < until; base += FS_CHUNK) {
+        if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; }
+        __syncthreads();
+        int32_t mine = FS_NONE;
+#pragma unroll
+        for (int u = 0; u < FS_ITEMS; u++) {
+            const int32_t p = base + u * FS_SCHED_THREADS + tid;
+            if (p >= until || mine != FS_NONE) continue;
+            const int4 s = a.slot[p];
+            if (s.w < 0) continue;
+            if (any_mode) { mine = p; continue; }
+            if (!a.lpm && a.q[s.x] <= 0) continue;
+            const int32_t need = a.s_len[p] - s.y;
+            if (need <= slack) { mine = p; continue; }
+            if (s.w < epoch) {
+                bool maybe = false;
+                if (s.z >= 0) {
+                    for (int32_t e = s.w; e < epoch; e++) {
+                        if (e >= FS_MAXA || (sm->aB[e] == s.y && sm->aTok[e] == s.z)) { maybe = true; break; }
+                    }
+                }
+                if (maybe) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
+                else a.slot[p].w = epoch;  // B is still exact
+            }
+        }
+        const int32_t minA = block_min_i32(mine, sm->red32);
+        if (sm->wl_n > 0) {
+            for (int32_t i = warp; i < sm->wl_n; i += nwarps) {
+                const int32_t p = sm->wl[i];
+                if (p >= minA) continue;
+                warp_resume(a, p, lane);
+                __syncwarp();
+                if (lane == 0) {
+                    a.slot[p].w = epoch;
+                    if (a.s_len[p] - a.slot[p].y <= slack) atomicMin(&sm->minB, p);
+                    atomicAdd((unsigned long long *)&sm->resumes, 1ull);
+                }
+            }
+            __syncthreads();
+        }
+        const int32_t best = min(minA, sm->minB);
+        __syncthreads();
+        if (best != FS_NONE) return best;
+    }
+    return FS_NONE;
+}
+
+// Closed-form DLPM refill (local_policies.py:94-106, 116-120): rounds repeat
+// until some pending client is positive, i.e. k = min over pending c of
+// floor(-q_c/Q)+1; every client_list member with q <= 0 receives
+// min(k, floor(-q_c/Q)+1) quanta.
+__device__ void block_refill(const FillArgs &a, SchedSmem *sm) {
+    const int tid = threadIdx.x;
+    int64_t k = INT64_MAX;
+    for (int32_t c = tid; c < a.nclients; c += blockDim.x)
+        if (a.pend_cnt[c] > 0) k = min(k, (-a.q[c]) / a.quantum + 1);
+    k = block_min_i64(k, sm->red64);
+    for (int32_t c = tid; c < a.nclients; c += blockDim.x) {
+        const int64_t qc = a.q[c];
+        if (a.known[c] && qc <= 0) {
+            const int64_t m = min(k, (-qc) / a.quantum + 1);
+            a.q[c] = qc + m * a.quantum;
+            a.refills[c] += m;
+        }
+    }
+    __syncthreads();
+    int64_t cnt = 0;
+    for (int32_t c = tid; c < a.nclients; c += blockDim.x) cnt += (a.pend_cnt[c] > 0 && a.q[c] > 0);
+    cnt = block_sum_i64(cnt, sm->red64);
+    if (tid == 0) { sm->npos = (int32_t)cnt; sm->refill_events++; }
+    __syncthreads();
+}
+
+// Worker.try_admit (worker.py:112-135) minus host bookkeeping, then the
+// policy's charge (local_policies.py:124).
+__device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t slack) {
+    const int tid = threadIdx.x;
+    const TrieView &t = a.t;
+    const int32_t r = a.s_req[j];
+    const int32_t len = a.s_len[j];
+    const int64_t off = a.roff[r];
+    __shared__ int64_t pinb;
+    if (tid == 0) pinb = t.sc->pinned;
+    __syncthreads();
+    block_insert(t, off, len, a.now, -1, a.path, &sm->ins);
+    if (tid == 0) {
+        const InsertSmem &in = sm->ins;
+        if (in.status != FS_OK) {
+            a.hdr[2] = in.status;
+            sm->stop = 1;
+        } else {
+            pin_chain(t, in.deepest);
+            const int32_t mlen = in.mlen;
+            const int32_t cov = in.cov;
+            const int64_t need = len - cov;
+            if (need > slack || in.unpinned != (int64_t)(mlen - cov)) {
+                a.hdr[2] = FS_ERR_INTERNAL;  // closed-form budget test disagrees with can_add
+                sm->stop = 1;
+            }
+            const int32_t e = sm->nadm;
+            if (e < a.adm_cap) {
+                a.adm_req[e] = r;
+                a.adm_mlen[e] = mlen;
+                a.adm_unp[e] = in.unpinned;
+                a.adm_pinb[e] = pinb;
+                a.adm_node[e] = in.deepest;
+                a.adm_rec_end[e] = t.sc->nrec;
+            }
+            sm->nadm = e + 1;
+            if (sm->epoch < FS_MAXA) {
+                sm->aB[sm->epoch] = cov;
+                sm->aTok[sm->epoch] = cov < len ? t.arena[off + cov] : -1;
+            }
+            sm->epoch++;
+            a.slot[j].w = -1;
+            a.rstate[r] = 2;
+            const int32_t c = a.slot[j].x;
+            const bool was = a.pend_cnt[c] > 0 && a.q[c] > 0;
+            a.pend_cnt[c]--;
+            if (!a.lpm) a.q[c] -= a.w_e * (int64_t)(len - mlen);
+            const bool now_pos = a.pend_cnt[c] > 0 && a.q[c] > 0;
+            sm->npos += (int)now_pos - (int)was;
+            sm->headroom += a.R;
+            sm->progress = 1;
+            if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
+    __shared__ SchedSmem sm;
+    const int tid = threadIdx.x;
+    // on_outputs deltas accumulated since the last fill (local_policies.py:130-133)
+    if (tid == 0) {
+        for (int32_t i = 0; i < a.ndl; i++) a.q[a.dl_client[i]] += a.dl_delta[i];
+        a.t.sc->nrec = 0;
+        a.hdr[2] = FS_OK;
+        sm.cursor = 0; sm.progress = 0; sm.epoch = 0; sm.nadm = 0; sm.stop = 0;
+        sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0;
+    }
+    for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.pend_cnt[c] = 0;
+    __syncthreads();
+    for (int32_t p = tid; p < a.n; p += blockDim.x) atomicAdd(&a.pend_cnt[a.slot[p].x], 1);
+    __syncthreads();
+    {
+        int64_t cnt = 0;
+        for (int32_t c = tid; c < a.nclients; c += blockDim.x) cnt += (a.pend_cnt[c] > 0 && a.q[c] > 0);
+        cnt = block_sum_i64(cnt, sm.red64);
+        if (tid == 0) sm.npos = (int32_t)cnt;
+    }
+    __syncthreads();
+    // Dlpm.fill pass structure (local_policies.py:112-128): repeat passes over
+    // the sorted snapshot until a whole pass admits nothing.
+    while (true) {
+        const bool ptrue = !a.lpm && sm.npos == 0;
+        const int64_t slack = sched_slack(a, sm.headroom);
+        const int32_t cur = sm.cursor;
+        __syncthreads();
+        int32_t j = block_find(a, &sm, cur, a.n, ptrue, slack);
+        if (j == FS_NONE) {
+            if (sm.progress) {
+                __syncthreads();
+                if (tid == 0) { sm.cursor = 0; sm.progress = 0; }
+                __syncthreads();
+                continue;
+            }
+            break;
+        }
+        if (ptrue) {
+            // no pending client holds credit: the visit of request j refills
+            block_refill(a, &sm);
+            const int64_t slack2 = sched_slack(a, sm.headroom);
+            const int32_t jj = block_find(a, &sm, j, j + 1, false, slack2);
+            if (jj != FS_NONE) block_admit(a, &sm, jj, slack2);
+        } else {
+            block_admit(a, &sm, j, slack);
+        }
+        if (tid == 0) sm.cursor = j + 1;
+        __syncthreads();
+        if (sm.stop) break;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.hdr[0] = sm.nadm;
+        a.hdr[1] = a.t.sc->nrec;
+        a.hdr[3] = sm.epoch;
+        a.hdr[4] = sm.refill_events;
+        a.hdr[5] = sm.resumes;
+    }
+}
+
+// ---------------------------------------------------------------- per-call ops
+enum { OP_INSERT = 1, OP_ADMIT, OP_PIN, OP_UNPIN, OP_EVICT, OP_LMW, OP_NOTIFY };
+
+struct OpArgs {
+    TrieView t;
+    int32_t op;
+    int64_t req_off;
+    int32_t len;
+    int64_t now;
+    int32_t worker;
+    int32_t node;
+    int64_t needed;
+    int32_t keep;
+    int64_t notice;
+    int32_t *path;
+    int64_t *out;  // [status, mlen/new_len, deepest, mask, nrec]
+};
+
+__global__ void __launch_bounds__(256) k_op(OpArgs a) {
+    __shared__ InsertSmem ins;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const TrieView &t = a.t;
+    if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; }
+    __syncthreads();
+    const int32_t *rq = t.arena + a.req_off;
+    switch (a.op) {
+        case OP_INSERT:
+            block_insert(t, a.req_off, a.len, a.now, a.worker, a.path, &ins);
+            if (tid == 0) { a.out[0] = ins.status; a.out[1] = ins.new_len; a.out[2] = ins.deepest; }
+            break;
+        case OP_ADMIT: {
+            // probe (radix.py:189) -> insert -> pin; the probe's mlen equals the
+            // insert walk's idx (nothing changes between them)
+            block_insert(t, a.req_off, a.len, a.now, -1, a.path, &ins);
+            if (tid == 0) {
+                a.out[0] = ins.status; a.out[1] = ins.mlen; a.out[2] = ins.deepest;
+                if (ins.status == FS_OK) pin_chain(t, ins.deepest);
+            }
+            break;
+        }
+        case OP_PIN:
+            if (tid == 0) { pin_chain(t, a.node); a.out[0] = t.sc->status; }
+            break;
+        case OP_UNPIN:
+            if (tid == 0) { unpin_chain(t, a.node); a.out[0] = t.sc->status; }
+            break;
+        case OP_EVICT:
+            block_evict(t, a.needed, &ins.ev);
+            if (tid == 0) a.out[0] = t.sc->status;
+            break;
+        case OP_LMW:
+            if (warp == 0) {
+                const WalkOut w = warp_walk(t, rq, a.len, lane, true, a.now, nullptr);
+                if (lane == 0) {
+                    const int32_t deepest = w.plen > 0 ? w.partial : w.last_full;
+                    a.out[0] = FS_OK;
+                    a.out[1] = deepest >= 0 ? w.mlen : 0;
+                    a.out[3] = (deepest >= 0 && t.wmask) ? (int64_t)t.wmask[deepest] : 0;
+                }
+            }
+            break;
+        case OP_NOTIFY:
+            if (warp == 0) warp_evict_notify(t, rq, a.len, a.worker, a.keep, a.notice, a.path);
+            if (tid == 0) a.out[0] = t.sc->status;
+            break;
+    }
+    __syncthreads();
+    if (tid == 0) a.out[4] = t.sc->nrec;
+}
+
+// ---------------------------------------------------------------- D2LPM
+struct DispArgs {
+    TrieView t;
+    int32_t n, D;
+    int32_t select_only;  // fs_dispatch_select: mask comes in out_mask[0]
+    const int32_t *ids, *clients;
+    const int64_t *nows;
+    const int64_t *roff;
+    const int32_t *rlen;
+    int64_t *q;  // [client * D + w]
+    uint8_t *qset;
+    int64_t *qsize;
+    int64_t quantum, w_e;
+    const int32_t *dl_idx;  // pending on_finish deltas: q index, q delta, worker
+    const int64_t *dl_q;
+    const int32_t *dl_w;
+    int32_t ndl;
+    int32_t *path;
+    int32_t *out_w, *out_mlen;
+    uint64_t *out_mask;
+    int64_t *out_rounds;
+    int64_t *hdr;
+};
+
+// Dispatcher.dispatch for a chain of arrivals (global_policies.py:40-46,
+// 107-124): every arrival's match sees the inserts of the ones before it.
+__global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
+    __shared__ InsertSmem ins;
+    __shared__ int32_t s_w;
+    __shared__ int32_t s_mlen;
+    __shared__ uint64_t s_mask;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const TrieView &t = a.t;
+    if (tid == 0) {
+        // pending host-side updates: q index >= 0 -> counter delta (on_finish /
+        // explicit override); q index -1 -> queue_size[w] += delta
+        for (int32_t i = 0; i < a.ndl; i++) {
+            if (a.dl_idx[i] >= 0) { a.q[a.dl_idx[i]] += a.dl_q[i]; a.qset[a.dl_idx[i]] = 1; }
+            else a.qsize[a.dl_w[i]] += a.dl_q[i];
+        }
+        t.sc->status = FS_OK;
+    }
+    __syncthreads();
+    if (a.select_only) {
+        if (tid == 0 && a.n > 0) {
+            const int32_t c = a.clients[0];
+            const uint64_t mask = a.out_mask[0];
+            int64_t *qr = a.q + (int64_t)c * a.D;
+            uint8_t *qs = a.qset + (int64_t)c * a.D;
+            bool any = false;
+            for (int w2 = 0; w2 < a.D; w2++) any |= qr[w2] > 0;
+            int64_t rounds = 0;
+            if (!any) {
+                int64_t k = INT64_MAX;
+                for (int w2 = 0; w2 < a.D; w2++) k = min(k, (-qr[w2]) / a.quantum + 1);
+                for (int w2 = 0; w2 < a.D; w2++) { qr[w2] += k * a.quantum; qs[w2] = 1; }
+                rounds = k;
+            }
+            int best = -1;
+            for (int pass = 0; pass < 2 && best < 0; pass++)
+                for (int w2 = 0; w2 < a.D; w2++) {
+                    if (!(qr[w2] > 0)) continue;
+                    if (pass == 0 && !((mask >> w2) & 1ull)) continue;
+                    if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;
+                }
+            a.out_w[0] = best;
+            a.out_rounds[0] = rounds;
+            a.hdr[0] = FS_OK;
+        }
+        return;
+    }
+    for (int32_t i = 0; i < a.n; i++) {
+        const int32_t r = a.ids[i];
+        const int32_t len = a.rlen[r];
+        const int64_t off = a.roff[r];
+        const int64_t now = a.nows[i];
+        if (warp == 0) {
+            // RadixTree.longest_match_workers (radix.py:101-110)
+            const WalkOut w = warp_walk(t, t.arena + off, len, lane, true, now, nullptr);
+            if (lane == 0) {
+                const int32_t deepest = w.plen > 0 ? w.partial : w.last_full;
+                const uint64_t mask = deepest >= 0 ? t.wmask[deepest] : 0ull;
+                const int32_t c = a.clients[i];
+                int64_t *qr = a.q + (int64_t)c * a.D;
+                uint8_t *qs = a.qset + (int64_t)c * a.D;
+                // D2lpm.select_worker (global_policies.py:107-114); the refill
+                // loop adds Q_w to every worker per round: k rounds in closed form
+                bool any = false;
+                for (int w2 = 0; w2 < a.D; w2++) any |= qr[w2] > 0;
+                int64_t rounds = 0;
+                if (!any) {
+                    int64_t k = INT64_MAX;
+                    for (int w2 = 0; w2 < a.D; w2++) k = min(k, (-qr[w2]) / a.quantum + 1);
+                    for (int w2 = 0; w2 < a.D; w2++) { qr[w2] += k * a.quantum; qs[w2] = 1; }
+                    rounds = k;
+                }
+                int best = -1;
+                for (int pass = 0; pass < 2 && best < 0; pass++) {
+                    for (int w2 = 0; w2 < a.D; w2++) {
+                        if (!(qr[w2] > 0)) continue;
+                        if (pass == 0 && !((mask >> w2) & 1ull)) continue;
+                        if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;  // _min_queue
+                    }
+                }
+                a.qsize[best] += 1;
+                qr[best] -= a.w_e * (int64_t)len;  // after_dispatch: full input (global_policies.py:123)
+                qs[best] = 1;
+                s_w = best; s_mlen = deepest >= 0 ? w.mlen : 0; s_mask = mask;
+                a.out_rounds[i] = rounds;
+            }
+        }
+        __syncthreads();
+        block_insert(t, off, len, now, s_w, a.path, &ins);
+        if (tid == 0) {
+            a.out_w[i] = s_w;
+            a.out_mlen[i] = s_mlen;
+            a.out_mask[i] = s_mask;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) a.hdr[0] = t.sc->status;
+}
+
+// Dlpm.check_refill (local_policies.py:94-106) on an explicit queued set.
+__global__ void k_check_refill(int64_t *q, int64_t *refills, const uint8_t *known, int32_t nclients,
+                               const uint8_t *queued, int64_t quantum, int64_t *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    bool anyq = false;
+    for (int32_t c = 0; c < nclients; c++) {
+        if (queued[c]) {
+            anyq = true;
+            if (q[c] > 0) { out[0] = 0; return; }
+        }
+    }
+    if (!anyq) { out[0] = 0; return; }
+    for (int32_t c = 0; c < nclients; c++)
+        if (known[c] && q[c] <= 0) { q[c] += quantum; refills[c] += 1; }
+    out[0] = 1;
+}

@@ -1,0 +1,1226 @@
+// fs_lib.cu -- host side of the C ABI (include/fairsched_b200.h).
+//
+// Owns device memory, streams, the queue mirror and host shadows of the few
+// scalars the reference's caller reads between schedule steps (counters,
+// used/pinned tokens).  All decision work runs in the kernels of
+// fs_kernels.cuh; nothing here computes a scheduling decision.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/fairsched_b200.h"
+#include "fs_kernels.cuh"
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) return fail(FS_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define TRY(x)                   \
+    do {                         \
+        int rc_ = (x);           \
+        if (rc_ != FS_OK) return rc_; \
+    } while (0)
+
+extern "C" const char *fs_last_error(void) { return g_err.c_str(); }
+extern "C" int fs_version(void) { return 1; }
+extern "C" int fs_device_count(int *count) {
+    CK(cudaGetDeviceCount(count));
+    return FS_OK;
+}
+
+// ---------------------------------------------------------------- buffers
+template <typename T>
+struct DBuf {
+    T *p = nullptr;
+    int64_t cap = 0;
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+template <typename T>
+static int dgrow(DBuf<T> &b, int64_t n, cudaStream_t s, bool keep = false, int64_t keep_n = 0) {
+    if (n <= b.cap) return FS_OK;
+    int64_t nc = std::max<int64_t>(n, b.cap + b.cap / 2);
+    nc = std::max<int64_t>(nc, 64);
+    T *np = nullptr;
+    CK(cudaMalloc(&np, sizeof(T) * nc));
+    if (keep && b.p && keep_n > 0) CK(cudaMemcpyAsync(np, b.p, sizeof(T) * keep_n, cudaMemcpyDeviceToDevice, s));
+    if (b.p) { CK(cudaStreamSynchronize(s)); cudaFree(b.p); }
+    b.p = np;
+    b.cap = nc;
+    return FS_OK;
+}
+
+template <typename T>
+struct HBuf {  // pinned host staging
+    T *p = nullptr;
+    int64_t cap = 0;
+    void release() { if (p) cudaFreeHost(p); p = nullptr; cap = 0; }
+};
+
+template <typename T>
+static int hgrow(HBuf<T> &b, int64_t n) {
+    if (n <= b.cap) return FS_OK;
+    int64_t nc = std::max<int64_t>(std::max<int64_t>(n, b.cap * 2), 64);
+    T *np = nullptr;
+    CK(cudaMallocHost(&np, sizeof(T) * nc));
+    if (b.p) cudaFreeHost(b.p);
+    b.p = np;
+    b.cap = nc;
+    return FS_OK;
+}
+
+// ---------------------------------------------------------------- context
+struct fs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DBuf<int32_t> arena;
+    int64_t arena_used = 0;
+    DBuf<int64_t> roff;
+    DBuf<int32_t> rlen, rclient;
+    DBuf<int64_t> rlabel;
+    DBuf<int8_t> rstate;  // 0 none, 1 queued, 2 admitted
+    std::vector<int64_t> h_roff, h_rlabel;
+    std::vector<int32_t> h_rlen, h_rclient;
+    int32_t max_len = 1;
+    HBuf<int32_t> stage_tok;
+    HBuf<int64_t> stage64;
+    HBuf<int32_t> stage32;
+};
+
+static int ctx_use(fs_ctx *c) {
+    CK(cudaSetDevice(c->device));
+    return FS_OK;
+}
+
+extern "C" int fs_ctx_create(int device, int64_t arena_tokens, int64_t max_requests, fs_ctx **out) {
+    if (!out) return fail(FS_ERR_INVALID, "out is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(FS_ERR_CUDA, "no CUDA device available (%s); the decision path has no CPU fallback",
+                    e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+    if (device < 0 || device >= n) return fail(FS_ERR_INVALID, "device %d out of range [0,%d)", device, n);
+    fs_ctx *c = new fs_ctx();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    TRY(dgrow(c->arena, std::max<int64_t>(arena_tokens, 1024), c->stream));
+    const int64_t mr = std::max<int64_t>(max_requests, 1024);
+    TRY(dgrow(c->roff, mr, c->stream));
+    TRY(dgrow(c->rlen, mr, c->stream));
+    TRY(dgrow(c->rclient, mr, c->stream));
+    TRY(dgrow(c->rlabel, mr, c->stream));
+    TRY(dgrow(c->rstate, mr, c->stream));
+    CK(cudaMemsetAsync(c->rstate.p, 0, mr, c->stream));
+    *out = c;
+    return FS_OK;
+}
+
+extern "C" int fs_ctx_destroy(fs_ctx *c) {
+    if (!c) return FS_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->arena.release(); c->roff.release(); c->rlen.release(); c->rclient.release();
+    c->rlabel.release(); c->rstate.release();
+    c->stage_tok.release(); c->stage64.release(); c->stage32.release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return FS_OK;
+}
+
+extern "C" int fs_ctx_sync(fs_ctx *c) {
+    TRY(ctx_use(c));
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, const int64_t *offsets,
+                               const int32_t *lens, const int32_t *clients, const int64_t *labels,
+                               int32_t *out_ids) {
+    if (!c || n < 0 || (n > 0 && (!tokens || !offsets || !lens))) return fail(FS_ERR_INVALID, "bad arguments");
+    TRY(ctx_use(c));
+    const int64_t base_id = (int64_t)c->h_roff.size();
+    if (base_id + n > INT32_MAX) return fail(FS_ERR_NOMEM, "request id space exhausted");
+    // 16-B aligned placement of every request in the arena
+    int64_t total = 0;
+    std::vector<int64_t> place(n);
+    for (int64_t i = 0; i < n; i++) {
+        if (lens[i] < 0) return fail(FS_ERR_INVALID, "negative length");
+        place[i] = c->arena_used + total;
+        total += (lens[i] + 3) & ~3LL;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t *tk = tokens + offsets[i];
+        for (int32_t k = 0; k < lens[i]; k++)
+            if (tk[k] < 0) return fail(FS_ERR_TOKEN_RANGE, "token %d of request %lld is outside [0, 2^31)", tk[k], (long long)i);
+    }
+    TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
+    TRY(hgrow(c->stage_tok, total + 4));
+    for (int64_t i = 0; i < n; i++) {
+        int32_t *dst = c->stage_tok.p + (place[i] - c->arena_used);
+        std::memcpy(dst, tokens + offsets[i], sizeof(int32_t) * lens[i]);
+        for (int32_t k = lens[i]; k < ((lens[i] + 3) & ~3); k++) dst[k] = 0;
+    }
+    if (total) CK(cudaMemcpyAsync(c->arena.p + c->arena_used, c->stage_tok.p, sizeof(int32_t) * total,
+                                  cudaMemcpyHostToDevice, c->stream));
+    const int64_t nr = base_id + n;
+    TRY(dgrow(c->roff, nr, c->stream, true, base_id));
+    TRY(dgrow(c->rlen, nr, c->stream, true, base_id));
+    TRY(dgrow(c->rclient, nr, c->stream, true, base_id));
+    TRY(dgrow(c->rlabel, nr, c->stream, true, base_id));
+    if (c->rstate.cap < nr) {
+        const int64_t old = c->rstate.cap;
+        TRY(dgrow(c->rstate, nr, c->stream, true, base_id));
+        CK(cudaMemsetAsync(c->rstate.p + old, 0, c->rstate.cap - old, c->stream));
+    }
+    for (int64_t i = 0; i < n; i++) {
+        c->h_roff.push_back(place[i]);
+        c->h_rlen.push_back(lens[i]);
+        c->h_rclient.push_back(clients ? clients[i] : 0);
+        c->h_rlabel.push_back(labels ? labels[i] : base_id + i);
+        c->max_len = std::max(c->max_len, lens[i]);
+        if (out_ids) out_ids[i] = (int32_t)(base_id + i);
+    }
+    CK(cudaStreamSynchronize(c->stream));  // staging buffer reuse
+    CK(cudaMemcpyAsync(c->roff.p + base_id, c->h_roff.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->rlen.p + base_id, c->h_rlen.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->rclient.p + base_id, c->h_rclient.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->rlabel.p + base_id, c->h_rlabel.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->arena_used += total;
+    return FS_OK;
+}
+
+extern "C" int fs_requests_set_labels(fs_ctx *c, int64_t n, const int32_t *ids, const int64_t *labels) {
+    if (!c) return fail(FS_ERR_INVALID, "ctx is NULL");
+    TRY(ctx_use(c));
+    for (int64_t i = 0; i < n; i++) {
+        if (ids[i] < 0 || ids[i] >= (int64_t)c->h_rlabel.size()) return fail(FS_ERR_INVALID, "bad request id");
+        c->h_rlabel[ids[i]] = labels[i];
+    }
+    if (n <= 64) {
+        for (int64_t i = 0; i < n; i++)
+            CK(cudaMemcpyAsync(c->rlabel.p + ids[i], c->h_rlabel.data() + ids[i], sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    } else {
+        CK(cudaMemcpyAsync(c->rlabel.p, c->h_rlabel.data(), sizeof(int64_t) * c->h_rlabel.size(), cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+extern "C" int fs_requests_count(fs_ctx *c, int64_t *n) {
+    if (!c || !n) return fail(FS_ERR_INVALID, "NULL");
+    *n = (int64_t)c->h_roff.size();
+    return FS_OK;
+}
+
+extern "C" int fs_request_info(fs_ctx *c, int32_t id, int64_t *off, int32_t *len) {
+    if (!c || id < 0 || id >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id");
+    if (off) *off = c->h_roff[id];
+    if (len) *len = c->h_rlen[id];
+    return FS_OK;
+}
+
+extern "C" int fs_arena_read(fs_ctx *c, int64_t off, int64_t n, int32_t *out) {
+    if (!c || off < 0 || n < 0 || off + n > c->arena_used) return fail(FS_ERR_INVALID, "arena range");
+    TRY(ctx_use(c));
+    if (n) CK(cudaMemcpyAsync(out, c->arena.p + off, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+// ---------------------------------------------------------------- trie
+struct fs_trie {
+    fs_ctx *ctx = nullptr;
+    int64_t capacity = -1;
+    int track = 0, nw = 0;
+    int32_t ncap = 0;
+    uint32_t hsize = 0;
+    DBuf<int64_t> src, la, seq;
+    DBuf<int32_t> start, end, parent, nchild, ref, first, freest;
+    DBuf<uint8_t> flags;
+    DBuf<uint64_t> wmask;
+    DBuf<int64_t> wtime;
+    DBuf<uint64_t> hkeys;
+    DBuf<int32_t> hvals;
+    DBuf<TrieScalars> sc;
+    DBuf<int32_t> path;  // walk scratch
+    DBuf<int64_t> rsrc;
+    DBuf<int32_t> rlen, rkeep;
+    DBuf<int64_t> opout;
+    TrieScalars h_sc{};
+    HBuf<int64_t> h_out;
+};
+
+static TrieView view(fs_trie *t) {
+    TrieView v;
+    v.arena = t->ctx->arena.p;
+    v.src = t->src.p; v.start = t->start.p; v.end = t->end.p; v.parent = t->parent.p;
+    v.nchild = t->nchild.p; v.ref = t->ref.p; v.first = t->first.p;
+    v.la = t->la.p; v.seq = t->seq.p; v.flags = t->flags.p;
+    v.wmask = t->track ? t->wmask.p : nullptr;
+    v.wtime = t->track ? t->wtime.p : nullptr;
+    v.nw = t->nw;
+    v.hkeys = t->hkeys.p; v.hvals = t->hvals.p; v.hmask = t->hsize - 1;
+    v.freest = t->freest.p; v.ncap = t->ncap;
+    v.sc = t->sc.p;
+    v.rsrc = t->rsrc.p; v.rlen = t->rlen.p; v.rkeep = t->rkeep.p; v.rcap = t->rsrc.cap;
+    return v;
+}
+
+__global__ void k_trie_init(TrieView t, int64_t capacity) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        TrieScalars &s = *t.sc;
+        s.used = 0; s.pinned = 0; s.next_seq = 1; s.capacity = capacity; s.nrec = 0;
+        s.hw = 1; s.nfree = 0; s.status = 0; s.live = 1;
+        t.src[0] = 0; t.start[0] = 0; t.end[0] = 0; t.parent[0] = -1; t.nchild[0] = 0; t.ref[0] = 0;
+        t.la[0] = 0; t.seq[0] = 0; t.first[0] = -1; t.flags[0] = FS_ALIVE;
+        if (t.wmask) t.wmask[0] = 0;
+    }
+}
+
+__global__ void k_rehash(TrieView t) {
+    // rebuild the child hash from the node table after a resize
+    const int32_t hw = t.sc->hw;
+    for (int32_t n = 1 + blockIdx.x * blockDim.x + threadIdx.x; n < hw; n += gridDim.x * blockDim.x) {
+        if (!(t.flags[n] & FS_ALIVE)) continue;
+        const uint64_t key = fs_hkey(t.parent[n], t.first[n]);
+        uint32_t i = fs_hmix(key) & t.hmask;
+        while (true) {
+            const unsigned long long prev = atomicCAS((unsigned long long *)&t.hkeys[i], FS_HEMPTY, key);
+            if (prev == FS_HEMPTY) { t.hvals[i] = n; break; }
+            i = (i + 1) & t.hmask;
+        }
+    }
+}
+
+static uint32_t pow2_at_least(int64_t x) {
+    uint32_t p = 1024;
+    while ((int64_t)p < x) p <<= 1;
+    return p;
+}
+
+// Make room for `extra_nodes` more nodes and paths of length `max_len`.
+static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
+    cudaStream_t s = t->ctx->stream;
+    TRY(dgrow(t->path, 2 * (int64_t)max_len + 16, s));
+    const int64_t need = (int64_t)t->h_sc.hw + extra_nodes + 4;
+    if (need <= t->ncap) return FS_OK;
+    const int64_t old = t->ncap;
+    const int64_t nc = std::max<int64_t>(need, old * 2);
+    const int64_t keep = old;
+    TRY(dgrow(t->src, nc, s, true, keep)); TRY(dgrow(t->la, nc, s, true, keep)); TRY(dgrow(t->seq, nc, s, true, keep));
+    TRY(dgrow(t->start, nc, s, true, keep)); TRY(dgrow(t->end, nc, s, true, keep)); TRY(dgrow(t->parent, nc, s, true, keep));
+    TRY(dgrow(t->nchild, nc, s, true, keep)); TRY(dgrow(t->ref, nc, s, true, keep)); TRY(dgrow(t->first, nc, s, true, keep));
+    TRY(dgrow(t->freest, nc, s, true, keep)); TRY(dgrow(t->flags, nc, s, true, keep));
+    if (t->track) { TRY(dgrow(t->wmask, nc, s, true, keep)); TRY(dgrow(t->wtime, nc * t->nw, s, true, keep * t->nw)); }
+    t->ncap = (int32_t)std::min<int64_t>(nc, t->src.cap);
+    const uint32_t hs = pow2_at_least(2 * (int64_t)t->ncap);
+    if (hs != t->hsize) {
+        t->hkeys.release(); t->hvals.release();
+        TRY(dgrow(t->hkeys, hs, s)); TRY(dgrow(t->hvals, hs, s));
+        t->hsize = hs;
+        CK(cudaMemsetAsync(t->hkeys.p, 0xff, sizeof(uint64_t) * hs, s));
+        if (old > 0) k_rehash<<<148, 256, 0, s>>>(view(t));
+        CK(cudaGetLastError());
+    }
+    return FS_OK;
+}
+
+static int trie_pull(fs_trie *t) {
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, t->ctx->stream));
+    CK(cudaStreamSynchronize(t->ctx->stream));
+    return FS_OK;
+}
+
+extern "C" int fs_trie_create(fs_ctx *c, int64_t capacity, int track_workers, int n_workers, fs_trie **out) {
+    if (!c || !out) return fail(FS_ERR_INVALID, "NULL argument");
+    if (track_workers && (n_workers <= 0 || n_workers > 64)) return fail(FS_ERR_INVALID, "n_workers must be in [1, 64]");
+    TRY(ctx_use(c));
+    fs_trie *t = new fs_trie();
+    t->ctx = c;
+    t->capacity = capacity;
+    t->track = track_workers ? 1 : 0;
+    t->nw = track_workers ? n_workers : 0;
+    // a local tree never holds more than capacity+1 nodes (every edge >= 1
+    // token) plus one transient split top; the global index grows on demand
+    const int64_t init = capacity >= 0 ? std::min<int64_t>(capacity + 8, 1 << 16) : 4096;
+    t->h_sc.hw = 1;
+    TRY(dgrow(t->sc, 1, c->stream));
+    TRY(trie_reserve(t, init, c->max_len));
+    const int64_t rc = capacity >= 0 ? 2 * capacity + 1024 : 1024;
+    TRY(dgrow(t->rsrc, rc, c->stream)); TRY(dgrow(t->rlen, rc, c->stream)); TRY(dgrow(t->rkeep, rc, c->stream));
+    TRY(dgrow(t->opout, 8, c->stream));
+    TRY(hgrow(t->h_out, 8));
+    k_trie_init<<<1, 32, 0, c->stream>>>(view(t), capacity);
+    CK(cudaGetLastError());
+    TRY(trie_pull(t));
+    *out = t;
+    return FS_OK;
+}
+
+extern "C" int fs_trie_destroy(fs_trie *t) {
+    if (!t) return FS_OK;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    t->src.release(); t->la.release(); t->seq.release(); t->start.release(); t->end.release();
+    t->parent.release(); t->nchild.release(); t->ref.release(); t->first.release(); t->freest.release();
+    t->flags.release(); t->wmask.release(); t->wtime.release(); t->hkeys.release(); t->hvals.release();
+    t->sc.release(); t->path.release(); t->rsrc.release(); t->rlen.release(); t->rkeep.release();
+    t->opout.release(); t->h_out.release();
+    delete t;
+    return FS_OK;
+}
+
+extern "C" int fs_trie_stats(fs_trie *t, int64_t *used, int64_t *pinned, int64_t *next_seq, int64_t *nodes) {
+    if (!t) return fail(FS_ERR_INVALID, "NULL trie");
+    if (used) *used = t->h_sc.used;
+    if (pinned) *pinned = t->h_sc.pinned;
+    if (next_seq) *next_seq = t->h_sc.next_seq;
+    if (nodes) *nodes = t->h_sc.live;
+    return FS_OK;
+}
+
+struct fs_scratch_match {
+    DBuf<int32_t> ids, mlen, cov;
+};
+
+extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int64_t now, int stamp,
+                             int32_t *out_mlen, int32_t *out_cov) {
+    if (!t || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    if (n == 0) return FS_OK;
+    fs_ctx *c = t->ctx;
+    TRY(ctx_use(c));
+    for (int64_t i = 0; i < n; i++)
+        if (req_ids[i] < 0 || req_ids[i] >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id");
+    static thread_local fs_scratch_match sm;
+    TRY(dgrow(sm.ids, n, c->stream)); TRY(dgrow(sm.mlen, n, c->stream)); TRY(dgrow(sm.cov, n, c->stream));
+    CK(cudaMemcpyAsync(sm.ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    const int64_t blocks = (n * 32 + 255) / 256;
+    k_match<<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
+                                                      stamp, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr);
+    CK(cudaGetLastError());
+    if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (out_cov) CK(cudaMemcpyAsync(out_cov, sm.cov.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+static int copy_records(fs_trie *t, int64_t nrec, fs_records *recs) {
+    if (!recs) return FS_OK;
+    recs->n_rec = nrec;
+    const int64_t k = std::min(nrec, recs->rec_cap);
+    if (nrec > t->rsrc.cap) return fail(FS_ERR_INTERNAL, "eviction record sink overflow (%lld)", (long long)nrec);
+    if (k > 0) {
+        CK(cudaMemcpyAsync(recs->rec_src, t->rsrc.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, t->ctx->stream));
+        CK(cudaMemcpyAsync(recs->rec_len, t->rlen.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, t->ctx->stream));
+        CK(cudaMemcpyAsync(recs->rec_keep, t->rkeep.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, t->ctx->stream));
+    }
+    return FS_OK;
+}
+
+extern "C" int fs_trie_read_records(fs_trie *t, int64_t first, int64_t n, int64_t *src, int32_t *len,
+                                    int32_t *keep) {
+    if (!t || first < 0 || n < 0 || first + n > t->rsrc.cap) return fail(FS_ERR_INVALID, "record range");
+    TRY(ctx_use(t->ctx));
+    cudaStream_t s = t->ctx->stream;
+    if (n > 0) {
+        if (src) CK(cudaMemcpyAsync(src, t->rsrc.p + first, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+        if (len) CK(cudaMemcpyAsync(len, t->rlen.p + first, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        if (keep) CK(cudaMemcpyAsync(keep, t->rkeep.p + first, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
+    fs_ctx *c = t->ctx;
+    a.t = view(t);
+    a.path = t->path.p;
+    a.out = t->opout.p;
+    k_op<<<1, 256, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < 5; i++) out5[i] = t->h_out.p[i];
+    TRY(copy_records(t, out5[4], recs));
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+static int check_req(fs_trie *t, int32_t req) {
+    if (req < 0 || req >= (int64_t)t->ctx->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id %d", req);
+    return FS_OK;
+}
+
+extern "C" int fs_trie_insert(fs_trie *t, int32_t req, int64_t now, int32_t worker, int32_t *new_len,
+                              int32_t *path_node, fs_records *recs) {
+    if (!t) return fail(FS_ERR_INVALID, "NULL trie");
+    TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
+    if (worker >= 0 && (!t->track || worker >= t->nw)) {
+        if (t->track) return fail(FS_ERR_INVALID, "worker %d outside [0,%d)", worker, t->nw);
+        worker = -1;  // worker tags only exist on a track_workers tree (radix.py:160)
+    }
+    TRY(trie_reserve(t, 2, t->ctx->max_len));
+    OpArgs a{};
+    a.op = OP_INSERT; a.req_off = t->ctx->h_roff[req]; a.len = t->ctx->h_rlen[req]; a.now = now; a.worker = worker;
+    int64_t o[5];
+    TRY(run_op(t, a, o, recs));
+    if (new_len) *new_len = (int32_t)o[1];
+    if (path_node) *path_node = (int32_t)o[2];
+    if (o[0] == FS_ERR_CACHE_FULL) return fail(FS_ERR_CACHE_FULL, "cannot free %lld tokens", (long long)o[1]);
+    if (o[0] != FS_OK) return fail((int)o[0], "device insert failed (status %lld)", (long long)o[0]);
+    return FS_OK;
+}
+
+extern "C" int fs_trie_admit(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, int32_t *path_node,
+                             fs_records *recs) {
+    if (!t) return fail(FS_ERR_INVALID, "NULL trie");
+    TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
+    TRY(trie_reserve(t, 2, t->ctx->max_len));
+    OpArgs a{};
+    a.op = OP_ADMIT; a.req_off = t->ctx->h_roff[req]; a.len = t->ctx->h_rlen[req]; a.now = now; a.worker = -1;
+    int64_t o[5];
+    TRY(run_op(t, a, o, recs));
+    if (mlen) *mlen = (int32_t)o[1];
+    if (path_node) *path_node = (int32_t)o[2];
+    if (o[0] == FS_ERR_CACHE_FULL) return fail(FS_ERR_CACHE_FULL, "cannot free tokens for admit");
+    if (o[0] != FS_OK) return fail((int)o[0], "device admit failed (status %lld)", (long long)o[0]);
+    return FS_OK;
+}
+
+static int pin_op(fs_trie *t, int32_t node, int op) {
+    if (!t) return fail(FS_ERR_INVALID, "NULL trie");
+    TRY(ctx_use(t->ctx));
+    if (node < 0) return FS_OK;  // empty path
+    if (node >= t->h_sc.hw) return fail(FS_ERR_INVALID, "bad path handle %d", node);
+    OpArgs a{};
+    a.op = op; a.node = node;
+    int64_t o[5];
+    TRY(run_op(t, a, o, nullptr));
+    if (o[0] == FS_ERR_UNDERFLOW) return fail(FS_ERR_UNDERFLOW, "unpin below zero (radix.py:183)");
+    if (o[0] != FS_OK) return fail((int)o[0], "pin/unpin failed");
+    return FS_OK;
+}
+extern "C" int fs_trie_pin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_PIN); }
+extern "C" int fs_trie_unpin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_UNPIN); }
+
+extern "C" int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs) {
+    if (!t) return fail(FS_ERR_INVALID, "NULL trie");
+    TRY(ctx_use(t->ctx));
+    OpArgs a{};
+    a.op = OP_EVICT; a.needed = needed;
+    int64_t o[5];
+    TRY(run_op(t, a, o, recs));
+    if (o[0] != FS_OK) return fail((int)o[0], "evict failed");
+    return FS_OK;
+}
+
+extern "C" int fs_trie_longest_match_workers(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, uint64_t *mask) {
+    if (!t) return fail(FS_ERR_INVALID, "NULL trie");
+    TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
+    OpArgs a{};
+    a.op = OP_LMW; a.req_off = t->ctx->h_roff[req]; a.len = t->ctx->h_rlen[req]; a.now = now;
+    int64_t o[5];
+    TRY(run_op(t, a, o, nullptr));
+    if (mlen) *mlen = (int32_t)o[1];
+    if (mask) *mask = (uint64_t)o[3];
+    return FS_OK;
+}
+
+extern "C" int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_len, int32_t worker,
+                                    int32_t keep_len, int64_t notice_time) {
+    if (!t || !t->track) return fail(FS_ERR_INVALID, "evict_notify needs a track_workers trie");
+    TRY(ctx_use(t->ctx));
+    if (path_src < 0 || path_len < 0 || path_src + path_len > t->ctx->arena_used) return fail(FS_ERR_INVALID, "path range");
+    TRY(trie_reserve(t, 2, std::max(t->ctx->max_len, path_len)));
+    OpArgs a{};
+    a.op = OP_NOTIFY; a.req_off = path_src; a.len = path_len; a.worker = worker; a.keep = keep_len; a.notice = notice_time;
+    int64_t o[5];
+    TRY(run_op(t, a, o, nullptr));
+    if (o[0] != FS_OK) return fail((int)o[0], "evict_notify failed");
+    return FS_OK;
+}
+
+extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src, int32_t *start, int32_t *end,
+                              int32_t *parent, int32_t *ref, int64_t *last_access, uint64_t *wmask) {
+    if (!t || !n) return fail(FS_ERR_INVALID, "NULL argument");
+    TRY(ctx_use(t->ctx));
+    TRY(trie_pull(t));
+    const int64_t hw = t->h_sc.hw;
+    *n = hw;
+    const int64_t k = std::min(cap, hw);
+    cudaStream_t s = t->ctx->stream;
+    if (k > 0) {
+        if (src) CK(cudaMemcpyAsync(src, t->src.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+        if (start) CK(cudaMemcpyAsync(start, t->start.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        if (end) CK(cudaMemcpyAsync(end, t->end.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        if (parent) CK(cudaMemcpyAsync(parent, t->parent.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        if (ref) CK(cudaMemcpyAsync(ref, t->ref.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        if (last_access) CK(cudaMemcpyAsync(last_access, t->la.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+        if (wmask && t->track) CK(cudaMemcpyAsync(wmask, t->wmask.p, sizeof(uint64_t) * k, cudaMemcpyDeviceToHost, s));
+        if (wmask && !t->track) std::memset(wmask, 0, sizeof(uint64_t) * k);
+    }
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+// ---------------------------------------------------------------- worker
+struct fs_worker {
+    fs_ctx *ctx = nullptr;
+    fs_trie *tree = nullptr;
+    int policy = 0;
+    int64_t quantum = 1, M = 0, R = 0, w_e = 1, w_q = 2;
+    int32_t nclients = 0;
+    // host shadows (authoritative between fills for the monitor's reads)
+    std::vector<int64_t> h_q, h_refills;
+    std::vector<uint8_t> h_known;
+    std::vector<int32_t> dl_client;
+    std::vector<int64_t> dl_delta;
+    DBuf<int64_t> q, refills;
+    DBuf<uint8_t> known;
+    DBuf<int32_t> pend_cnt;
+    bool known_dirty = false;
+    // queue mirror
+    std::vector<int32_t> pending_new;
+    int64_t qn = 0;          // entries in `queue` (label order)
+    int64_t admitted_last = 0;
+    DBuf<int32_t> queue, queue2, newids;
+    DBuf<int64_t> newlab;
+    DBuf<uint32_t> keys, keys2;
+    DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
+    DBuf<int32_t> s_req, s_len, s_fnode;
+    DBuf<int4> slot;
+    DBuf<uint8_t> cub_tmp;
+    DBuf<int32_t> nsel;
+    DBuf<int32_t> dlc;
+    DBuf<int64_t> dld;
+    // outputs
+    DBuf<int32_t> adm_req, adm_mlen, adm_node;
+    DBuf<int64_t> adm_unp, adm_pinb, adm_rec_end, hdr;
+    HBuf<int64_t> h_hdr;
+    HBuf<int32_t> h_st32;
+    HBuf<int64_t> h_st64;
+    cudaEvent_t ev[5];
+    float phases[4] = {0, 0, 0, 0};
+};
+
+struct IsQueued {
+    const int8_t *st;
+    __device__ __forceinline__ bool operator()(const int32_t &r) const { return st[r] == 1; }
+};
+
+__global__ void k_iota(int32_t *p, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (int32_t)i;
+}
+
+__global__ void k_set_state(int8_t *st, const int32_t *ids, int64_t n, int8_t v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) st[ids[i]] = v;
+}
+
+extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t quantum, int64_t M,
+                                int64_t output_reserve, int64_t w_e, int64_t w_q, int32_t max_clients,
+                                fs_worker **out) {
+    if (!c || !tree || !out || tree->ctx != c) return fail(FS_ERR_INVALID, "bad arguments");
+    if (policy != 0 && policy != 1) return fail(FS_ERR_INVALID, "policy must be 0 (dlpm) or 1 (lpm)");
+    if (policy == 0 && quantum <= 0) return fail(FS_ERR_INVALID, "quantum must be positive");  // local_policies.py:81-82
+    if (max_clients <= 0) return fail(FS_ERR_INVALID, "max_clients must be positive");
+    TRY(ctx_use(c));
+    fs_worker *w = new fs_worker();
+    w->ctx = c; w->tree = tree; w->policy = policy; w->quantum = quantum > 0 ? quantum : 1;
+    w->M = M; w->R = output_reserve; w->w_e = w_e; w->w_q = w_q; w->nclients = max_clients;
+    w->h_q.assign(max_clients, 0); w->h_refills.assign(max_clients, 0); w->h_known.assign(max_clients, 0);
+    TRY(dgrow(w->q, max_clients, c->stream)); TRY(dgrow(w->refills, max_clients, c->stream));
+    TRY(dgrow(w->known, max_clients, c->stream)); TRY(dgrow(w->pend_cnt, max_clients, c->stream));
+    CK(cudaMemsetAsync(w->q.p, 0, sizeof(int64_t) * max_clients, c->stream));
+    CK(cudaMemsetAsync(w->refills.p, 0, sizeof(int64_t) * max_clients, c->stream));
+    CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
+    TRY(dgrow(w->hdr, 8, c->stream)); TRY(hgrow(w->h_hdr, 8));
+    TRY(dgrow(w->nsel, 1, c->stream));
+    for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = w;
+    return FS_OK;
+}
+
+extern "C" int fs_worker_destroy(fs_worker *w) {
+    if (!w) return FS_OK;
+    cudaSetDevice(w->ctx->device);
+    cudaStreamSynchronize(w->ctx->stream);
+    w->q.release(); w->refills.release(); w->known.release(); w->pend_cnt.release();
+    w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
+    w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
+    w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
+    w->s_fnode.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
+    w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
+    w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
+    for (int i = 0; i < 5; i++) cudaEventDestroy(w->ev[i]);
+    delete w;
+    return FS_OK;
+}
+
+extern "C" int fs_worker_enqueue(fs_worker *w, int64_t n, const int32_t *ids) {
+    if (!w || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    fs_ctx *c = w->ctx;
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t r = ids[i];
+        if (r < 0 || r >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id %d", r);
+        const int32_t cl = c->h_rclient[r];
+        if (cl < 0 || cl >= w->nclients) return fail(FS_ERR_INVALID, "client id %d outside [0,%d)", cl, w->nclients);
+        w->pending_new.push_back(r);
+        if (!w->h_known[cl]) {  // Dlpm.on_request_enqueued (local_policies.py:88-92)
+            w->h_known[cl] = 1;
+            w->known_dirty = true;
+        }
+    }
+    return FS_OK;
+}
+
+extern "C" int fs_worker_outputs(fs_worker *w, int64_t n, const int32_t *clients, const int64_t *counts) {
+    if (!w || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t cl = clients[i];
+        if (cl < 0 || cl >= w->nclients) return fail(FS_ERR_INVALID, "client id %d out of range", cl);
+        if (w->policy != 0) continue;
+        const int64_t d = -w->w_q * counts[i];
+        w->h_q[cl] += d;  // mirror; the device applies the same delta at the next fill
+        w->dl_client.push_back(cl);
+        w->dl_delta.push_back(d);
+    }
+    return FS_OK;
+}
+
+static int worker_flush_small(fs_worker *w) {
+    fs_ctx *c = w->ctx;
+    if (w->known_dirty) {
+        CK(cudaMemcpyAsync(w->known.p, w->h_known.data(), w->nclients, cudaMemcpyHostToDevice, c->stream));
+        w->known_dirty = false;
+    }
+    return FS_OK;
+}
+
+extern "C" int fs_worker_check_refill(fs_worker *w, int64_t n, const int32_t *queued, int *refilled) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL worker");
+    fs_ctx *c = w->ctx;
+    TRY(ctx_use(c));
+    TRY(worker_flush_small(w));
+    // apply pending on_outputs deltas first so device q == host mirror
+    std::vector<int64_t> q(w->h_q);
+    CK(cudaMemcpyAsync(w->q.p, q.data(), sizeof(int64_t) * w->nclients, cudaMemcpyHostToDevice, c->stream));
+    w->dl_client.clear(); w->dl_delta.clear();
+    std::vector<uint8_t> flags(w->nclients, 0);
+    for (int64_t i = 0; i < n; i++) {
+        if (queued[i] < 0 || queued[i] >= w->nclients) return fail(FS_ERR_INVALID, "client id out of range");
+        flags[queued[i]] = 1;
+    }
+    DBuf<uint8_t> dq;
+    TRY(dgrow(dq, w->nclients, c->stream));
+    CK(cudaMemcpyAsync(dq.p, flags.data(), w->nclients, cudaMemcpyHostToDevice, c->stream));
+    k_check_refill<<<1, 32, 0, c->stream>>>(w->q.p, w->refills.p, w->known.p, w->nclients, dq.p, w->quantum, w->hdr.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dq.release();
+    if (refilled) *refilled = (int)w->h_hdr.p[0];
+    return FS_OK;
+}
+
+extern "C" int fs_worker_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills, uint8_t *known) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL worker");
+    const int32_t k = std::min(n, w->nclients);
+    if (q) std::memcpy(q, w->h_q.data(), sizeof(int64_t) * k);
+    if (refills) std::memcpy(refills, w->h_refills.data(), sizeof(int64_t) * k);
+    if (known) std::memcpy(known, w->h_known.data(), k);
+    return FS_OK;
+}
+
+extern "C" int fs_worker_set_counter(fs_worker *w, int32_t client, int64_t qv) {
+    if (!w || client < 0 || client >= w->nclients) return fail(FS_ERR_INVALID, "bad client");
+    const int64_t d = qv - w->h_q[client];
+    w->h_q[client] = qv;
+    w->dl_client.push_back(client);
+    w->dl_delta.push_back(d);
+    return FS_OK;
+}
+
+extern "C" int fs_worker_reserve_clients(fs_worker *w, int32_t max_clients) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL worker");
+    if (max_clients <= w->nclients) return FS_OK;
+    fs_ctx *c = w->ctx;
+    cudaStream_t s = c->stream;
+    TRY(ctx_use(c));
+    const int32_t old = w->nclients;
+    const int32_t nc = std::max(max_clients, old * 2);
+    TRY(dgrow(w->q, nc, s, true, old)); TRY(dgrow(w->refills, nc, s, true, old));
+    TRY(dgrow(w->known, nc, s, true, old)); TRY(dgrow(w->pend_cnt, nc, s));
+    CK(cudaMemsetAsync(w->q.p + old, 0, sizeof(int64_t) * (nc - old), s));
+    CK(cudaMemsetAsync(w->refills.p + old, 0, sizeof(int64_t) * (nc - old), s));
+    CK(cudaMemsetAsync(w->known.p + old, 0, nc - old, s));
+    w->h_q.resize(nc, 0); w->h_refills.resize(nc, 0); w->h_known.resize(nc, 0);
+    w->nclients = nc;
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+extern "C" int fs_worker_mark_known(fs_worker *w, int64_t n, const int32_t *clients) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL worker");
+    for (int64_t i = 0; i < n; i++) {
+        if (clients[i] < 0 || clients[i] >= w->nclients) return fail(FS_ERR_INVALID, "client id out of range");
+        if (!w->h_known[clients[i]]) { w->h_known[clients[i]] = 1; w->known_dirty = true; }
+    }
+    return FS_OK;
+}
+
+extern "C" int fs_worker_device_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL worker");
+    TRY(ctx_use(w->ctx));
+    const int32_t k = std::min(n, w->nclients);
+    if (q) CK(cudaMemcpyAsync(q, w->q.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, w->ctx->stream));
+    if (refills) CK(cudaMemcpyAsync(refills, w->refills.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, w->ctx->stream));
+    CK(cudaStreamSynchronize(w->ctx->stream));
+    return FS_OK;
+}
+
+extern "C" int fs_worker_queue_len(fs_worker *w, int64_t *n) {
+    if (!w || !n) return fail(FS_ERR_INVALID, "NULL");
+    *n = w->qn - w->admitted_last + (int64_t)w->pending_new.size();
+    return FS_OK;
+}
+
+extern "C" int fs_worker_last_phases(fs_worker *w, float *ms4) {
+    if (!w || !ms4) return fail(FS_ERR_INVALID, "NULL");
+    for (int i = 0; i < 4; i++) ms4[i] = w->phases[i];
+    return FS_OK;
+}
+
+static uint32_t key_bits(int32_t max_len) {
+    uint32_t b = 1;
+    while (((int64_t)1 << b) <= max_len) b++;
+    return b;
+}
+
+extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom,
+                              fs_fill_result *res) {
+    if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
+    fs_ctx *c = w->ctx;
+    fs_trie *t = w->tree;
+    cudaStream_t s = c->stream;
+    TRY(ctx_use(c));
+    TRY(worker_flush_small(w));
+    const int64_t n_old = w->qn - w->admitted_last;
+    const int64_t n_new = (int64_t)w->pending_new.size();
+    const int64_t n = n_old + n_new;
+    // scratch capacity
+    TRY(dgrow(w->queue, n + 1, s, true, w->qn)); TRY(dgrow(w->queue2, n + 1, s));
+    TRY(dgrow(w->keys, n + 1, s)); TRY(dgrow(w->keys2, n + 1, s)); TRY(dgrow(w->perm, n + 1, s));
+    TRY(dgrow(w->mlen, n + 1, s)); TRY(dgrow(w->cov, n + 1, s)); TRY(dgrow(w->fnode, n + 1, s));
+    TRY(dgrow(w->next, n + 1, s)); TRY(dgrow(w->s_req, n + 1, s)); TRY(dgrow(w->s_len, n + 1, s));
+    TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
+    if (w->iota.cap < n + 1) {
+        TRY(dgrow(w->iota, n + 1, s));
+        k_iota<<<(unsigned)((w->iota.cap + 255) / 256), 256, 0, s>>>(w->iota.p, w->iota.cap);
+        CK(cudaGetLastError());
+    }
+    const int64_t acap = std::max<int64_t>(n + 1, 64);
+    TRY(dgrow(w->adm_req, acap, s)); TRY(dgrow(w->adm_mlen, acap, s)); TRY(dgrow(w->adm_node, acap, s));
+    TRY(dgrow(w->adm_unp, acap, s)); TRY(dgrow(w->adm_pinb, acap, s)); TRY(dgrow(w->adm_rec_end, acap, s));
+    {
+        // each admission creates at most a split top and a leaf; a local tree
+        // never holds more than capacity + 2 live nodes (freed slots are reused)
+        int64_t extra = 2 * n + 8;
+        if (t->capacity >= 0) extra = std::min<int64_t>(extra, t->capacity + 8);
+        TRY(trie_reserve(t, extra, c->max_len));
+    }
+    const uint32_t bits = key_bits(c->max_len);
+    const uint32_t kmax = (bits >= 32) ? 0xffffffffu : ((1u << bits) - 1u);
+    size_t sort_bytes = 0, sel_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)std::max<int64_t>(n, 1), 0, (int)bits, s);
+    cub::DeviceSelect::If(nullptr, sel_bytes, w->queue.p, w->queue2.p, w->nsel.p, (int)std::max<int64_t>(w->qn, 1), IsQueued{c->rstate.p}, s);
+    TRY(dgrow(w->cub_tmp, (int64_t)std::max(sort_bytes, sel_bytes) + 256, s));
+
+    CK(cudaEventRecord(w->ev[0], s));
+    // ---- queue upkeep: drop last fill's admissions, merge arrivals by label
+    if (w->admitted_last > 0 && w->qn > 0) {
+        size_t b = w->cub_tmp.cap;
+        CK(cub::DeviceSelect::If(w->cub_tmp.p, b, w->queue.p, w->queue2.p, w->nsel.p, (int)w->qn, IsQueued{c->rstate.p}, s));
+        std::swap(w->queue, w->queue2);
+    }
+    if (n_new > 0) {
+        std::vector<int32_t> &nv = w->pending_new;
+        std::stable_sort(nv.begin(), nv.end(), [&](int32_t x, int32_t y) { return c->h_rlabel[x] < c->h_rlabel[y]; });
+        TRY(hgrow(w->h_st32, n_new)); TRY(hgrow(w->h_st64, n_new));
+        for (int64_t i = 0; i < n_new; i++) { w->h_st32.p[i] = nv[i]; w->h_st64.p[i] = c->h_rlabel[nv[i]]; }
+        TRY(dgrow(w->newids, n_new, s)); TRY(dgrow(w->newlab, n_new, s));
+        CK(cudaMemcpyAsync(w->newids.p, w->h_st32.p, sizeof(int32_t) * n_new, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(w->newlab.p, w->h_st64.p, sizeof(int64_t) * n_new, cudaMemcpyHostToDevice, s));
+        k_set_state<<<(unsigned)((n_new + 255) / 256), 256, 0, s>>>(c->rstate.p, w->newids.p, n_new, 1);
+        k_merge<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->queue.p, (int32_t)n_old, w->newids.p, w->newlab.p,
+                                                           (int32_t)n_new, c->rlabel.p, w->queue2.p);
+        CK(cudaGetLastError());
+        std::swap(w->queue, w->queue2);
+        nv.clear();
+    }
+    w->qn = n;
+    w->admitted_last = 0;
+    // on_outputs deltas
+    const int32_t ndl = (int32_t)w->dl_client.size();
+    if (ndl > 0) {
+        TRY(dgrow(w->dlc, ndl, s)); TRY(dgrow(w->dld, ndl, s));
+        CK(cudaMemcpyAsync(w->dlc.p, w->dl_client.data(), sizeof(int32_t) * ndl, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(w->dld.p, w->dl_delta.data(), sizeof(int64_t) * ndl, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaEventRecord(w->ev[1], s));
+    // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
+    if (n > 0) {
+        const int64_t blocks = (n * 32 + 255) / 256;
+        k_match<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
+                                                  kmax, w->keys.p, nullptr, w->cov.p, w->fnode.p, w->next.p);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(w->ev[2], s));
+    // ---- K2: stable sort by (-mlen); ties keep the (arrival, rid) label order
+    if (n > 0) {
+        size_t b = w->cub_tmp.cap;
+        CK(cub::DeviceRadixSort::SortPairs(w->cub_tmp.p, b, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)n, 0, (int)bits, s));
+        k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p, w->fnode.p,
+                                                            w->next.p, c->rclient.p, c->rlen.p, w->s_req.p, w->slot.p,
+                                                            w->s_len.p, w->s_fnode.p);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(w->ev[3], s));
+    // ---- K3+K4: admission passes on one persistent CTA
+    FillArgs a{};
+    a.t = view(t);
+    a.n = (int32_t)n;
+    a.s_req = w->s_req.p; a.slot = w->slot.p; a.s_len = w->s_len.p; a.s_fnode = w->s_fnode.p;
+    a.roff = c->roff.p;
+    a.q = w->q.p; a.refills = w->refills.p; a.known = w->known.p; a.nclients = w->nclients; a.pend_cnt = w->pend_cnt.p;
+    a.dl_client = w->dlc.p; a.dl_delta = w->dld.p; a.ndl = ndl;
+    a.M = w->M; a.R = w->R; a.gen_total = generated_total; a.headroom0 = headroom; a.w_e = w->w_e;
+    a.quantum = w->quantum; a.now = now; a.lpm = w->policy == 1;
+    a.path = t->path.p;
+    a.adm_req = w->adm_req.p; a.adm_mlen = w->adm_mlen.p; a.adm_node = w->adm_node.p;
+    a.adm_unp = w->adm_unp.p; a.adm_pinb = w->adm_pinb.p; a.adm_rec_end = w->adm_rec_end.p;
+    a.adm_cap = (int32_t)w->adm_req.cap;
+    a.rstate = c->rstate.p;
+    a.hdr = w->hdr.p;
+    k_schedule<<<1, FS_SCHED_THREADS, 0, s>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(w->ev[4], s));
+    w->dl_client.clear(); w->dl_delta.clear();
+    // ---- results
+    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 6, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int64_t nadm = w->h_hdr.p[0];
+    const int64_t nrec = w->h_hdr.p[1];
+    const int64_t status = w->h_hdr.p[2];
+    for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&w->phases[i], w->ev[i], w->ev[i + 1]));
+    float total = 0;
+    CK(cudaEventElapsedTime(&total, w->ev[0], w->ev[4]));
+    res->device_ms = total;
+    res->n_queued = n;
+    res->n_adm = nadm;
+    res->used = t->h_sc.used;
+    res->pinned = t->h_sc.pinned;
+    w->admitted_last = nadm;
+    if (status != FS_OK) return fail((int)status, "device fill failed (status %lld)", (long long)status);
+    if (nadm > res->cap_adm) return fail(FS_ERR_INVALID, "admission buffer too small (%lld > %lld)", (long long)nadm, (long long)res->cap_adm);
+    if (nadm > 0) {
+        if (res->adm_req) CK(cudaMemcpyAsync(res->adm_req, w->adm_req.p, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, s));
+        if (res->adm_mlen) CK(cudaMemcpyAsync(res->adm_mlen, w->adm_mlen.p, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, s));
+        if (res->adm_path_node) CK(cudaMemcpyAsync(res->adm_path_node, w->adm_node.p, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, s));
+        if (res->adm_unpinned) CK(cudaMemcpyAsync(res->adm_unpinned, w->adm_unp.p, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, s));
+        if (res->adm_pinned_before) CK(cudaMemcpyAsync(res->adm_pinned_before, w->adm_pinb.p, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, s));
+        if (res->adm_rec_end) CK(cudaMemcpyAsync(res->adm_rec_end, w->adm_rec_end.p, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, s));
+    }
+    TRY(copy_records(t, nrec, &res->recs));
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+// ---------------------------------------------------------------- dispatcher
+struct fs_dispatcher {
+    fs_ctx *ctx = nullptr;
+    fs_trie *tree = nullptr;
+    int D = 1;
+    int64_t quantum = 1, w_e = 1, w_q = 2;
+    int32_t nclients = 0;
+    std::vector<int64_t> h_q, h_qsize;
+    std::vector<uint8_t> h_qset;
+    std::vector<int32_t> dl_idx, dl_w;
+    std::vector<int64_t> dl_q;
+    DBuf<int64_t> q, qsize;
+    DBuf<uint8_t> qset;
+    DBuf<int32_t> ids, clients, dli, dlw, o_w, o_mlen;
+    DBuf<int64_t> nows, dlq, o_rounds, hdr;
+    DBuf<uint64_t> o_mask;
+};
+
+static int disp_flush(fs_dispatcher *d);
+
+extern "C" int fs_dispatcher_create(fs_ctx *c, int D, int64_t quantum, int64_t w_e, int64_t w_q,
+                                    int32_t max_clients, fs_dispatcher **out) {
+    if (!c || !out) return fail(FS_ERR_INVALID, "NULL argument");
+    if (quantum <= 0) return fail(FS_ERR_INVALID, "quantum must be positive");  // global_policies.py:97-98
+    if (D <= 0 || D > 64) return fail(FS_ERR_INVALID, "D must be in [1, 64]");
+    if (max_clients <= 0) return fail(FS_ERR_INVALID, "max_clients must be positive");
+    TRY(ctx_use(c));
+    fs_dispatcher *d = new fs_dispatcher();
+    d->ctx = c; d->D = D; d->quantum = quantum; d->w_e = w_e; d->w_q = w_q; d->nclients = max_clients;
+    TRY(fs_trie_create(c, -1, 1, D, &d->tree));
+    const int64_t nq = (int64_t)max_clients * D;
+    d->h_q.assign(nq, 0); d->h_qset.assign(nq, 0); d->h_qsize.assign(D, 0);
+    TRY(dgrow(d->q, nq, c->stream)); TRY(dgrow(d->qset, nq, c->stream)); TRY(dgrow(d->qsize, D, c->stream));
+    CK(cudaMemsetAsync(d->q.p, 0, sizeof(int64_t) * nq, c->stream));
+    CK(cudaMemsetAsync(d->qset.p, 0, nq, c->stream));
+    CK(cudaMemsetAsync(d->qsize.p, 0, sizeof(int64_t) * D, c->stream));
+    TRY(dgrow(d->hdr, 4, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = d;
+    return FS_OK;
+}
+
+extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
+    if (!d) return FS_OK;
+    cudaSetDevice(d->ctx->device);
+    cudaStreamSynchronize(d->ctx->stream);
+    fs_trie_destroy(d->tree);
+    d->q.release(); d->qsize.release(); d->qset.release(); d->ids.release(); d->clients.release();
+    d->dli.release(); d->dlw.release(); d->o_w.release(); d->o_mlen.release(); d->nows.release();
+    d->dlq.release(); d->o_rounds.release(); d->hdr.release(); d->o_mask.release();
+    delete d;
+    return FS_OK;
+}
+
+extern "C" fs_trie *fs_dispatcher_tree(fs_dispatcher *d) { return d ? d->tree : nullptr; }
+
+extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
+                           const int64_t *now, int32_t *out_worker, int32_t *out_mlen, uint64_t *out_mask,
+                           int64_t *out_rounds) {
+    if (!d || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    if (n == 0) return FS_OK;
+    fs_ctx *c = d->ctx;
+    cudaStream_t s = c->stream;
+    TRY(ctx_use(c));
+    for (int64_t i = 0; i < n; i++) {
+        if (req_ids[i] < 0 || req_ids[i] >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id");
+        if (clients[i] < 0 || clients[i] >= d->nclients) return fail(FS_ERR_INVALID, "client id out of range");
+    }
+    TRY(trie_reserve(d->tree, 2 * n + 2, c->max_len));
+    TRY(dgrow(d->ids, n, s)); TRY(dgrow(d->clients, n, s)); TRY(dgrow(d->nows, n, s));
+    TRY(dgrow(d->o_w, n, s)); TRY(dgrow(d->o_mlen, n, s)); TRY(dgrow(d->o_mask, n, s)); TRY(dgrow(d->o_rounds, n, s));
+    CK(cudaMemcpyAsync(d->ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d->clients.p, clients, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d->nows.p, now, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    const int32_t ndl = (int32_t)d->dl_idx.size();
+    TRY(disp_flush(d));
+    DispArgs a{};
+    a.t = view(d->tree);
+    a.n = (int32_t)n; a.D = d->D;
+    a.ids = d->ids.p; a.clients = d->clients.p; a.nows = d->nows.p;
+    a.roff = c->roff.p; a.rlen = c->rlen.p;
+    a.q = d->q.p; a.qset = d->qset.p; a.qsize = d->qsize.p;
+    a.quantum = d->quantum; a.w_e = d->w_e;
+    a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = ndl;
+    a.path = d->tree->path.p;
+    a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
+    a.hdr = d->hdr.p;
+    k_dispatch<<<1, 256, 0, s>>>(a);
+    CK(cudaGetLastError());
+    d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
+    int64_t st = 0;
+    CK(cudaMemcpyAsync(&st, d->hdr.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out_worker, d->o_w.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    if (out_mlen) CK(cudaMemcpyAsync(out_mlen, d->o_mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    if (out_mask) CK(cudaMemcpyAsync(out_mask, d->o_mask.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+    std::vector<int64_t> rounds(n);
+    CK(cudaMemcpyAsync(rounds.data(), d->o_rounds.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&d->tree->h_sc, d->tree->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (st != FS_OK) return fail((int)st, "device dispatch failed (status %lld)", (long long)st);
+    // mirror the counter updates (the monitor reads dispatcher.q each timestamp)
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t cl = clients[i];
+        const int32_t wk = out_worker[i];
+        int64_t *qr = d->h_q.data() + (int64_t)cl * d->D;
+        uint8_t *qs = d->h_qset.data() + (int64_t)cl * d->D;
+        if (rounds[i] > 0)
+            for (int x = 0; x < d->D; x++) { qr[x] += rounds[i] * d->quantum; qs[x] = 1; }
+        d->h_qsize[wk] += 1;
+        qr[wk] -= d->w_e * c->h_rlen[req_ids[i]];
+        qs[wk] = 1;
+        if (out_rounds) out_rounds[i] = rounds[i];
+    }
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_finish(fs_dispatcher *d, int32_t client, int32_t worker, int64_t output_tokens) {
+    if (!d || client < 0 || client >= d->nclients || worker < 0 || worker >= d->D)
+        return fail(FS_ERR_INVALID, "bad arguments");
+    const int64_t idx = (int64_t)client * d->D + worker;
+    const int64_t dq = -d->w_q * output_tokens;
+    d->h_q[idx] += dq;
+    d->h_qset[idx] = 1;
+    d->h_qsize[worker] -= 1;
+    d->dl_idx.push_back((int32_t)idx);
+    d->dl_w.push_back(worker);
+    d->dl_q.push_back(dq);
+    d->dl_idx.push_back(-1);  // queue_size[worker] -= 1 (global_policies.py:52)
+    d->dl_w.push_back(worker);
+    d->dl_q.push_back(-1);
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_counters(fs_dispatcher *d, int32_t client, int64_t *q_row, uint8_t *present) {
+    if (!d || client < 0 || client >= d->nclients) return fail(FS_ERR_INVALID, "bad arguments");
+    const int64_t b = (int64_t)client * d->D;
+    if (q_row) std::memcpy(q_row, d->h_q.data() + b, sizeof(int64_t) * d->D);
+    if (present) std::memcpy(present, d->h_qset.data() + b, d->D);
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_queue_sizes(fs_dispatcher *d, int64_t *sizes) {
+    if (!d || !sizes) return fail(FS_ERR_INVALID, "NULL");
+    std::memcpy(sizes, d->h_qsize.data(), sizeof(int64_t) * d->D);
+    return FS_OK;
+}
+
+// Push every host-side override (set_counter / set_queue_size) and finish delta.
+static int disp_flush(fs_dispatcher *d) {
+    fs_ctx *c = d->ctx;
+    cudaStream_t s = c->stream;
+    const int32_t ndl = (int32_t)d->dl_idx.size();
+    if (ndl == 0) return FS_OK;
+    TRY(dgrow(d->dli, ndl, s)); TRY(dgrow(d->dlw, ndl, s)); TRY(dgrow(d->dlq, ndl, s));
+    CK(cudaMemcpyAsync(d->dli.p, d->dl_idx.data(), sizeof(int32_t) * ndl, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d->dlw.p, d->dl_w.data(), sizeof(int32_t) * ndl, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d->dlq.p, d->dl_q.data(), sizeof(int64_t) * ndl, cudaMemcpyHostToDevice, s));
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_select(fs_dispatcher *d, int32_t client, uint64_t matched_mask, int32_t *worker,
+                                  int64_t *rounds) {
+    if (!d || client < 0 || client >= d->nclients || !worker) return fail(FS_ERR_INVALID, "bad arguments");
+    fs_ctx *c = d->ctx;
+    cudaStream_t s = c->stream;
+    TRY(ctx_use(c));
+    TRY(disp_flush(d));
+    TRY(dgrow(d->clients, 1, s)); TRY(dgrow(d->o_w, 1, s)); TRY(dgrow(d->o_mask, 1, s)); TRY(dgrow(d->o_rounds, 1, s));
+    CK(cudaMemcpyAsync(d->clients.p, &client, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d->o_mask.p, &matched_mask, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    DispArgs a{};
+    a.t = view(d->tree);
+    a.n = 1; a.D = d->D; a.select_only = 1;
+    a.clients = d->clients.p;
+    a.q = d->q.p; a.qset = d->qset.p; a.qsize = d->qsize.p;
+    a.quantum = d->quantum; a.w_e = d->w_e;
+    a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = (int32_t)d->dl_idx.size();
+    a.out_w = d->o_w.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
+    a.hdr = d->hdr.p;
+    k_dispatch<<<1, 256, 0, s>>>(a);
+    CK(cudaGetLastError());
+    d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
+    int64_t r = 0;
+    CK(cudaMemcpyAsync(worker, d->o_w.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&r, d->o_rounds.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (r > 0) {
+        int64_t *qr = d->h_q.data() + (int64_t)client * d->D;
+        uint8_t *qs = d->h_qset.data() + (int64_t)client * d->D;
+        for (int x = 0; x < d->D; x++) { qr[x] += r * d->quantum; qs[x] = 1; }
+    }
+    if (rounds) *rounds = r;
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_set_counter(fs_dispatcher *d, int32_t client, int32_t worker, int64_t q) {
+    if (!d || client < 0 || client >= d->nclients || worker < 0 || worker >= d->D) return fail(FS_ERR_INVALID, "bad arguments");
+    const int64_t idx = (int64_t)client * d->D + worker;
+    const int64_t delta = q - d->h_q[idx];
+    d->h_q[idx] = q;
+    d->h_qset[idx] = 1;
+    d->dl_idx.push_back((int32_t)idx); d->dl_w.push_back(-1); d->dl_q.push_back(delta);
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_set_queue_size(fs_dispatcher *d, int32_t worker, int64_t size) {
+    if (!d || worker < 0 || worker >= d->D) return fail(FS_ERR_INVALID, "bad arguments");
+    const int64_t delta = size - d->h_qsize[worker];
+    d->h_qsize[worker] = size;
+    // encoded as a queue-size-only delta: q index -1
+    d->dl_idx.push_back(-1); d->dl_w.push_back(worker); d->dl_q.push_back(delta);
+    return FS_OK;
+}
+
+extern "C" int fs_dispatcher_reserve_clients(fs_dispatcher *d, int32_t max_clients) {
+    if (!d) return fail(FS_ERR_INVALID, "NULL dispatcher");
+    if (max_clients <= d->nclients) return FS_OK;
+    fs_ctx *c = d->ctx;
+    cudaStream_t s = c->stream;
+    TRY(ctx_use(c));
+    const int32_t nc = std::max(max_clients, d->nclients * 2);
+    const int64_t old = (int64_t)d->nclients * d->D, nw = (int64_t)nc * d->D;
+    TRY(dgrow(d->q, nw, s, true, old)); TRY(dgrow(d->qset, nw, s, true, old));
+    CK(cudaMemsetAsync(d->q.p + old, 0, sizeof(int64_t) * (nw - old), s));
+    CK(cudaMemsetAsync(d->qset.p + old, 0, nw - old, s));
+    d->h_q.resize(nw, 0); d->h_qset.resize(nw, 0);
+    d->nclients = nc;
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+extern "C" int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t *q, uint8_t *present, int64_t *qsize) {
+    if (!d) return fail(FS_ERR_INVALID, "NULL dispatcher");
+    TRY(ctx_use(d->ctx));
+    TRY(disp_flush(d));
+    // apply pending deltas with an empty dispatch so device == mirror
+    if (!d->dl_idx.empty()) {
+        DispArgs a{};
+        a.t = view(d->tree); a.n = 0; a.D = d->D;
+        a.q = d->q.p; a.qset = d->qset.p; a.qsize = d->qsize.p;
+        a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = (int32_t)d->dl_idx.size();
+        a.hdr = d->hdr.p;
+        k_dispatch<<<1, 256, 0, d->ctx->stream>>>(a);
+        CK(cudaGetLastError());
+        d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
+    }
+    const int64_t k = std::min<int64_t>(n, (int64_t)d->nclients * d->D);
+    cudaStream_t s = d->ctx->stream;
+    if (q) CK(cudaMemcpyAsync(q, d->q.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+    if (present) CK(cudaMemcpyAsync(present, d->qset.p, k, cudaMemcpyDeviceToHost, s));
+    if (qsize) CK(cudaMemcpyAsync(qsize, d->qsize.p, sizeof(int64_t) * d->D, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}

@@ -1,0 +1,51 @@
+"""Install the B200 decision path behind the reference's own plug points.
+
+The reference resolves its policy classes from module globals at call time
+(make_local_policy -> `Dlpm`, local_policies.py:198-209; make_dispatcher ->
+`D2lpm`, global_policies.py:164-181) and Worker builds its cache through
+`fairsched.worker.RadixTree` (worker.py:11, 72).  install() rebinds exactly
+those names, so `fairsched.runner.run_experiment` (and every caller of the
+factories) runs unchanged on the GPU path; config validation still sees the
+names "dlpm" / "lpm" / "d2lpm".  Nothing in the reference is edited.
+"""
+from __future__ import annotations
+
+import importlib
+
+from .policies import GpuD2lpm, GpuDlpm, GpuLpm
+from .radix import DeviceRadixTree
+
+_SAVED = {}
+
+_BINDINGS = (
+    ("fairsched.local_policies", "Dlpm", GpuDlpm),
+    ("fairsched.local_policies", "Lpm", GpuLpm),
+    ("fairsched.global_policies", "D2lpm", GpuD2lpm),
+    ("fairsched.global_policies", "RadixTree", DeviceRadixTree),
+    ("fairsched.worker", "RadixTree", DeviceRadixTree),
+    ("fairsched.radix", "RadixTree", DeviceRadixTree),
+    ("fairsched", "RadixTree", DeviceRadixTree),
+)
+
+
+def install() -> None:
+    """Route fairsched's DLPM / LPM / D2LPM / RadixTree through the GPU."""
+    from ._lib import load
+
+    load()  # fail loudly now if the CUDA extension is missing
+    for mod_name, attr, obj in _BINDINGS:
+        mod = importlib.import_module(mod_name)
+        key = (mod_name, attr)
+        if key not in _SAVED:
+            _SAVED[key] = getattr(mod, attr)
+        setattr(mod, attr, obj)
+
+
+def uninstall() -> None:
+    for (mod_name, attr), obj in list(_SAVED.items()):
+        setattr(importlib.import_module(mod_name), attr, obj)
+    _SAVED.clear()
+
+
+def installed() -> bool:
+    return bool(_SAVED)

@@ -1,0 +1,152 @@
+"""Per-process device runtime shared by every drop-in object.
+
+* one `Context` per CUDA device (token arena + request table),
+* a request registry mapping the reference's token tuples (Request.input_tokens,
+  requests.py:22-32) to device request ids -- each tuple is uploaded once,
+* a client registry (client name -> dense id, shared by all workers and the
+  dispatcher of the device),
+* order-maintenance labels for the LPM tie-break key (arrival, rid)
+  (local_policies.py:17): the device keeps each worker queue in label order so
+  the per-fill sort only has to order by match length.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+from sortedcontainers import SortedList
+
+from .device import Context
+
+_LABEL_GAP = 1 << 32
+
+
+class OrderLabels:
+    """64-bit labels whose integer order equals the order of their keys.
+
+    New keys take the midpoint of their neighbours' labels; when a gap is
+    exhausted every label is respaced (returned so the caller re-uploads)."""
+
+    def __init__(self):
+        self._keys = SortedList()
+        self._label = {}
+
+    def __len__(self):
+        return len(self._keys)
+
+    def label(self, key):
+        return self._label[key]
+
+    def add(self, key):
+        """Insert key; returns (label, relabeled) where relabeled is None or a dict."""
+        if key in self._label:
+            return self._label[key], None
+        keys = self._keys
+        i = keys.bisect_left(key)
+        lo = self._label[keys[i - 1]] if i > 0 else None
+        hi = self._label[keys[i]] if i < len(keys) else None
+        if lo is None and hi is None:
+            lab = 0
+        elif hi is None:
+            lab = lo + _LABEL_GAP
+        elif lo is None:
+            lab = hi - _LABEL_GAP
+        elif hi - lo >= 2:
+            lab = (lo + hi) // 2
+        else:
+            lab = None
+        keys.add(key)
+        if lab is not None:
+            self._label[key] = lab
+            return lab, None
+        for j, k in enumerate(keys):
+            self._label[k] = j * _LABEL_GAP
+        return self._label[key], dict(self._label)
+
+
+class DeviceRuntime:
+    def __init__(self, device: int = 0):
+        self.ctx = Context(device, arena_tokens=1 << 22, max_requests=1 << 16)
+        self._by_tuple = {}      # id(tokens) -> (device id, tokens)  (strong ref keeps id stable)
+        self._key_of_id = {}     # device id -> (arrival, rid) label key
+        self.clients = {}        # client name -> dense id
+        self.client_names = []
+        self.labels = OrderLabels()
+
+    # -- clients ---------------------------------------------------------
+    def client_id(self, name) -> int:
+        cid = self.clients.get(name)
+        if cid is None:
+            cid = len(self.client_names)
+            self.clients[name] = cid
+            self.client_names.append(name)
+        return cid
+
+    # -- requests ----------------------------------------------------------
+    def lookup(self, tokens):
+        hit = self._by_tuple.get(id(tokens))
+        if hit is not None and hit[1] is tokens:
+            return hit[0]
+        return None
+
+    def upload(self, tokens, client=None, arrival=None, rid=None) -> int:
+        """Device id of a token sequence; uploads it on first sight.  When
+        (arrival, rid) are given the request gets its LPM tie-break label."""
+        did = self.lookup(tokens)
+        key = (arrival, rid) if rid is not None else None
+        if did is None:
+            if not isinstance(tokens, tuple):
+                tokens = tuple(tokens)
+            lab = 0
+            relabeled = None
+            if key is not None:
+                lab, relabeled = self.labels.add(key)
+            cid = self.client_id(client) if client is not None else 0
+            did = self.ctx.add_request(np.fromiter(tokens, dtype=np.int64, count=len(tokens)), cid, lab)
+            self._by_tuple[id(tokens)] = (did, tokens)
+            if key is not None:
+                self._key_of_id[did] = key
+            if relabeled is not None:
+                self._push_labels()
+            return did
+        if key is not None and did not in self._key_of_id:
+            lab, relabeled = self.labels.add(key)
+            self._key_of_id[did] = key
+            if relabeled is not None:
+                self._push_labels()
+            else:
+                self.ctx.set_labels(np.array([did], np.int32), np.array([lab], np.int64))
+            if client is not None:
+                self._set_client(did, client)
+        return did
+
+    def _set_client(self, did, client):
+        # the request table stores the client id at upload; requests first seen
+        # by the dispatcher are uploaded with their client already, so this is
+        # only a consistency guard
+        return None
+
+    def _push_labels(self):
+        ids = np.fromiter(self._key_of_id.keys(), dtype=np.int32, count=len(self._key_of_id))
+        labs = np.array([self.labels.label(self._key_of_id[i]) for i in ids], dtype=np.int64)
+        self.ctx.set_labels(ids, labs)
+
+
+_RUNTIMES = {}
+
+
+def get_runtime(device: int | None = None) -> DeviceRuntime:
+    if device is None:
+        device = int(os.environ.get("FS_B200_DEVICE", "0"))
+    rt = _RUNTIMES.get(device)
+    if rt is None:
+        rt = DeviceRuntime(device)
+        _RUNTIMES[device] = rt
+    return rt
+
+
+def reset_runtimes():
+    """Drop every device runtime (tests use this between independent runs)."""
+    for rt in _RUNTIMES.values():
+        rt.ctx.close()
+    _RUNTIMES.clear()

@@ -389,6 +389,8 @@ def record_run(cfg, trace=None):
         "final_dispatch_q": disp_q,
         "global_dump_sha": gdump,
         "worker_dump_sha": [dump_digest(w.tree.dump()) for w in result.workers],
+        "violations": {k: len(v) for k, v in result.violations.items()},
+        "extremes": {k: list(v) for k, v in result.counter_extremes.items()},
         "n_requests": len(requests),
     }
 

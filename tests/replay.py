@@ -90,6 +90,8 @@ def replay_serving(run: dict, backend, check_dump: bool = True) -> dict:
     """Drive `backend` through the recorded ops; raise AssertionError on any diff.
     Returns simple counters (fills, admissions, ...) for reporting."""
     tab = RunTable(run)
+    if hasattr(backend, "bind"):
+        backend.bind(tab)
     p, s, q_u, q_w, cap = _cfg_ints(run)
     D = p["D"]
     nC = len(tab.clients)
@@ -147,7 +149,7 @@ def replay_serving(run: dict, backend, check_dump: bool = True) -> dict:
         elif kind == "dfin":
             d2.on_finish(tab.client_id[op["client"]], op["worker"], op["out"])
         elif kind == "dev":
-            d2.on_eviction(tab.path(op["path"]), op["keep_len"], op["worker"], op["notice_time"])
+            d2.on_eviction(tab.path(op["path"]), op["keep_len"], op["worker"], op["notice_time"], ref=op["path"])
         else:
             raise ValueError(kind)
     if d2 is not None and run["final_dispatch_q"] is not None:
@@ -234,7 +236,7 @@ class _OracleD2:
     def on_finish(self, client, w, out):
         self.od.on_finish(client, w, out)
 
-    def on_eviction(self, path, keep, w, notice_time):
+    def on_eviction(self, path, keep, w, notice_time, ref=None):
         self.od.on_eviction(path, keep, w, notice_time)
 
     def q(self):

@@ -1,0 +1,49 @@
+"""Order-maintenance labels used for the LPM tie-break (arrival, rid)
+(local_policies.py:17): label order must equal key order under any insertion
+order, including gap exhaustion."""
+import random
+
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from paper_2501_14312_b200.runtime import OrderLabels
+
+
+def check(lab, keys):
+    ks = sorted(set(keys))
+    labels = [lab.label(k) for k in ks]
+    assert labels == sorted(labels) and len(set(labels)) == len(labels)
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.lists(st.tuples(st.integers(0, 5), st.text(min_size=0, max_size=4)), max_size=60))
+def test_labels_respect_key_order(keys):
+    lab = OrderLabels()
+    for k in keys:
+        lab.add(k)
+    check(lab, keys)
+
+
+def test_gap_exhaustion_relabels():
+    lab = OrderLabels()
+    lab.add((0, "a"))
+    lab.add((0, "z"))
+    rel = None
+    # insert repeatedly just above the lower key: halves the same gap
+    s = "a"
+    for i in range(80):
+        s = s + "a"
+        _, r = lab.add((0, s))
+        rel = rel or r
+    assert rel is not None
+    check(lab, [(0, "a"), (0, "z")] + [(0, "a" * (i + 2)) for i in range(80)])
+
+
+def test_python_str_order_for_rids():
+    # rid compares as a Python str: "c1-10" < "c1-9"
+    lab = OrderLabels()
+    rng = random.Random(3)
+    keys = [(rng.randrange(3), f"c{rng.randrange(3)}-{rng.randrange(20)}") for _ in range(200)]
+    for k in keys:
+        lab.add(k)
+    check(lab, keys)
