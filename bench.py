@@ -1,0 +1,322 @@
+"""Benchmark: DLPM scheduling decisions/s on the config-2 queue (BASELINE.json
+configs[1]: one worker, 100 clients, 64k queued 1-4k-token prompts with a
+Zipf(1.1) shared-prefix tree), plus the prefix-match kernel's HBM GB/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the decision path over the resident queue, driven the
+way the reference's serving loop drives it:
+  1. the previous step's batch completes: output charge w_q*8 per request
+     (Dlpm.on_outputs) and unpin of its paths (worker.py:209-213);
+  2. as many new requests arrive as were admitted (uploaded from host memory
+     through the C ABI, Worker.enqueue -> on_request_enqueued);
+  3. one schedule step over the whole queue (Dlpm.fill): K1 match + LRU stamp
+     of every queued request, K2 sort, K3/K4 deficit-gated admission with
+     radix insert / split / LRU evict / pin.
+Decisions per step = queued requests evaluated.  `value` is device time
+(CUDA events inside the library, inputs resident); `e2e` is host wall time of
+the same public-API calls including the H2D upload of arrivals and the D2H of
+the admission results.  N>1 (torchrun): one independent worker per GPU with
+its own 64k queue (weak scaling; the local DLPM fill has no cross-worker
+exchange).  The CPU baseline is the C oracle (a literal restatement of the
+reference's Dlpm.fill) on the same steps, on one core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = 65536
+L_INPUT = 4096
+W_E, W_Q = 1, 2
+RESERVE = 8
+OUT_TOKENS = 8
+U = W_E * L_INPUT + W_Q * M
+Q_U = max(1, round(0.5 * U))  # q_u_frac 0.5 (runner.py:127)
+STEP_US = 10_000
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class GpuSteps:
+    """The synthetic serving loop on the CUDA path, through the C ABI."""
+
+    def __init__(self, q, pool, device):
+        from paper_2501_14312_b200.device import Context, Trie, WorkerDev
+        self.q = q
+        self.pool = pool
+        tot = int(q.lens.sum()) + int(pool.lens.sum()) + 4 * (len(q) + len(pool)) + 1024
+        self.ctx = Context(device, arena_tokens=tot, max_requests=len(q) + len(pool) + 16)
+        self.trie = Trie(self.ctx, M)
+        self.w = WorkerDev(self.ctx, self.trie, "dlpm", Q_U, M, RESERVE, W_E, W_Q, max_clients=128)
+        self.ids = self.ctx.add_requests(q.flat, q.offsets, q.lens, q.clients, q.labels)
+        self.w.enqueue(self.ids)
+        self.prev_nodes = np.zeros(0, np.int32)
+        self.prev_clients = np.zeros(0, np.int32)
+        self.pool_next = 0
+        self.h2d = 0
+        self.d2h = 0
+
+    def step(self, now):
+        n_prev = len(self.prev_nodes)
+        if n_prev:
+            cl, cnt = np.unique(self.prev_clients, return_counts=True)
+            self.w.outputs(cl.astype(np.int32), (cnt * OUT_TOKENS).astype(np.int64))
+            self.trie.unpin_many(self.prev_nodes)
+            self.h2d += cl.nbytes + cnt.nbytes + self.prev_nodes.nbytes
+        if n_prev and self.pool_next + n_prev <= len(self.pool):
+            a, b = self.pool_next, self.pool_next + n_prev
+            p = self.pool
+            o0 = int(p.offsets[a])
+            o1 = int(p.offsets[b - 1] + p.lens[b - 1])
+            ids = self.ctx.add_requests(p.flat[o0:o1], p.offsets[a:b] - o0, p.lens[a:b], p.clients[a:b],
+                                        p.labels[a:b])
+            self.w.enqueue(ids)
+            self.pool_next = b
+            self.h2d += (o1 - o0) * 4 + (b - a) * 24
+        res = self.w.fill(now, 0, 0)
+        self.prev_nodes = res.adm_node.astype(np.int32)
+        self.prev_clients = np.asarray(self.q_clients_of(res.adm_req), np.int32)
+        self.d2h += res.adm_req.nbytes * 6 + 8 * 128 * 2 + 64
+        return res
+
+    def q_clients_of(self, ids):
+        nq = len(self.q)
+        out = []
+        for i in ids:
+            i = int(i)
+            out.append(int(self.q.clients[i]) if i < nq else int(self.pool.clients[i - nq]))
+        return out
+
+
+def clocks_start():
+    path = os.path.join(ROOT, "gpurun_out", "bench_clocks.csv") if os.path.isdir(os.path.join(ROOT, "gpurun_out")) \
+        else "/tmp/bench_clocks.csv"
+    try:
+        fh = open(path, "w")
+        p = subprocess.Popen(["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                              "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                             stdout=fh, stderr=subprocess.DEVNULL)
+        return p, fh, path
+    except Exception:
+        return None, None, None
+
+
+def clocks_stop(p, fh, path, dev):
+    if p is None:
+        return None
+    time.sleep(0.25)
+    p.terminate()
+    p.wait()
+    fh.close()
+    sm, mx, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 9 or not f[0].isdigit() or int(f[0]) != dev:
+            continue
+        try:
+            sm.append(float(f[1]))
+            mx = max(mx, float(f[2]))
+        except ValueError:
+            continue
+        for name, v in zip(names, f[5:9]):
+            if v.lower() == "active":
+                reasons.add(name)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(q, pool, steps_max=40, budget_s=15.0):
+    """C oracle (literal restatement of Dlpm.fill) on the same serving steps, one core."""
+    from oracle.lockstep import OracleSteps
+    o = OracleSteps(q, M, M, RESERVE, W_E, W_Q, Q_U, 128)
+    o.enqueue(range(len(q)))
+    pool_base = len(q)
+    nxt = 0
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < steps_max and time.perf_counter() - t0 < budget_s:
+        r = o.step((steps + 1) * STEP_US)
+        steps += 1
+        # arrivals (same pool order as the GPU loop): the oracle reads them from the pool queue
+        n = len(r["admitted"])
+        if n and nxt + n <= len(pool):
+            o.q = _concat_once(o, q, pool)
+            o.enqueue(range(pool_base + nxt, pool_base + nxt + n))
+            nxt += n
+    return {"value": o.decisions / o.fill_s, "steps": steps, "fill_s": o.fill_s, "decisions": o.decisions}
+
+
+_CAT = {}
+
+
+def _concat_once(o, q, pool):
+    key = (id(q), id(pool))
+    if key not in _CAT:
+        from paper_2501_14312_b200.workloads import Queue
+        flat = np.concatenate([q.flat, pool.flat])
+        offs = np.concatenate([q.offsets, pool.offsets + len(q.flat)])
+        _CAT[key] = Queue(flat, offs, np.concatenate([q.lens, pool.lens]),
+                          np.concatenate([q.clients, pool.clients]), np.concatenate([q.arrival, pool.arrival]),
+                          q.rids + pool.rids, np.concatenate([q.labels, pool.labels]))
+    return _CAT[key]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nq", type=int, default=65536)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        dist = tdist
+
+    from paper_2501_14312_b200.workloads import build_docs, config2, shared_prefix_queue
+    spec = config2(args.nq, seed=2 + rank)
+    docs = build_docs(spec)
+    q = shared_prefix_queue(spec, docs=docs)
+    pool_n = 96 * (args.steps + args.warmup) + 1024
+    pool = shared_prefix_queue(spec, first=args.nq, count=pool_n, arrival=STEP_US, docs=docs, stream_seed=spec.seed + 101)
+    cfg = {"workload": "config2: DLPM 1 worker/GPU, 100 clients, 64k queued, 1-4k-token prompts, "
+                       "Zipf(1.1) prefixes over 256 docs, M=capacity=65536, q_u_frac=0.5, reserve=8",
+           "nq_per_gpu": args.nq, "clients": spec.clients, "M": M, "quantum": Q_U,
+           "l2": "inputs larger than L2: each step streams every queued request's matched prefix "
+                 "(~240 MB) and the queue occupies ~640 MB",
+           "parallelism": f"dp{args.gpus} (independent workers)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        t0 = time.perf_counter()
+        cb = cpu_baseline(q, pool, steps_max=args.warmup + args.steps, budget_s=120.0)
+        line = {"metric": "scheduling decisions/sec (DLPM, 64k queued)", "value": cb["value"],
+                "unit": "decisions/s", "n_gpus": args.gpus, "steps": cb["steps"], "warmup": 0,
+                "ms_per_step": 1000 * cb["fill_s"] / max(cb["steps"], 1), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32/int64", "data": "synthetic",
+                "config": cfg, "impl": "reference",
+                "cpu_baseline": {"value": cb["value"], "unit": "decisions/s", "cores": 1, "kind": "port",
+                                 "sample": f"C oracle Dlpm.fill restatement, {cb['steps']} serving steps of the "
+                                           f"{args.nq}-request queue"},
+                "e2e": {"value": cb["value"], "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "wall_s": time.perf_counter() - t0}
+        print(json.dumps(line))
+        return
+
+    from paper_2501_14312_b200.device import launch_count
+    g = GpuSteps(q, pool, local)
+    now = 0
+    for _ in range(args.warmup):
+        now += STEP_US
+        g.step(now)
+    g.ctx.sync()
+    if dist is not None:
+        import torch
+        dist.barrier()
+    clk = clocks_start() if rank == 0 else (None, None, None)
+    l0 = launch_count()
+    h2d0, d2h0 = g.h2d, g.d2h
+    dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(4)
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        now += STEP_US
+        t0 = time.perf_counter()
+        res = g.step(now)
+        wall += time.perf_counter() - t0
+        dev_ms += res.device_ms
+        decisions += res.n_queued
+        adm += len(res.adm_req)
+        alg_tok += res.stats[0]
+        k1_ms.append(res.phases_ms[1])
+        phases += np.array(res.phases_ms)
+    g.ctx.sync()
+    t_total = time.perf_counter() - t_start
+    launches = launch_count() - l0
+    clocks = clocks_stop(*clk, local) if rank == 0 else None
+    if dist is not None:
+        import torch
+        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, wall = float(t[0]), float(t[1])
+        d = torch.tensor([decisions], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(d, op=dist.ReduceOp.SUM)
+        total_decisions = float(d[0])
+    else:
+        total_decisions = decisions
+    if rank != 0:
+        return
+    value = total_decisions / (dev_ms / 1000.0)
+    e2e = total_decisions / wall
+    peak, peak_kind = peaks()
+    n_per_step = decisions / args.steps
+    k1_avg = float(np.mean(k1_ms))
+    alg_bytes = (alg_tok / args.steps) * 4 + 36 * n_per_step
+    achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
+    share = phases / phases.sum()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_k_match_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "scheduling decisions/sec (DLPM, 64k queued); prefix-match HBM GB/s in roofline",
+        "value": value, "unit": "decisions/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32/int64", "data": "synthetic", "config": cfg,
+        "e2e": {"value": e2e, "unit": "decisions/s",
+                "h2d_bytes_per_step": int((g.h2d - h2d0) / args.steps),
+                "d2h_bytes_per_step": int((g.d2h - d2h0) / args.steps)},
+        "gpu_launches": int(launches),
+        "roofline": {"kernel": "k_match (K1 batched prefix match)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg},
+        "phase_share": {"merge": share[0], "k1_match": share[1], "k2_sort": share[2], "k3k4_schedule": share[3]},
+        "phase_ms_per_step": {"merge": phases[0] / args.steps, "k1_match": phases[1] / args.steps,
+                              "k2_sort": phases[2] / args.steps, "k3k4_schedule": phases[3] / args.steps},
+        "admissions_per_step": adm / args.steps, "queued_per_step": n_per_step,
+        "clocks": clocks, "host_wall_s": t_total,
+    }
+    if not args.no_cpu and world == 1:
+        cb = cpu_baseline(q, pool, steps_max=40, budget_s=15.0)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": "decisions/s", "cores": 1, "kind": "port",
+                                "sample": f"C oracle (literal Dlpm.fill restatement), first {cb['steps']} serving "
+                                          f"steps of the same {args.nq}-request queue on one host core"}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

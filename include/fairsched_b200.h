@@ -108,6 +108,8 @@ int fs_trie_admit(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, int32_t *
                   fs_records *recs);
 int fs_trie_pin(fs_trie *t, int32_t path_node);   /* radix.py:174-178 */
 int fs_trie_unpin(fs_trie *t, int32_t path_node); /* radix.py:180-185 */
+/* unpin of a whole finishing batch in one launch (worker.py:209-213), in order */
+int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *path_nodes);
 /* RadixTree.evict_lru without a protect set (radix.py:210-250) */
 int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs);
 /* RadixTree.longest_match_workers (radix.py:101-110): mask bit w = worker w tagged */
@@ -170,6 +172,13 @@ int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t h
                    fs_fill_result *res);
 /* Timing breakdown of the last fill: [merge, match K1, sort K2, schedule K3/K4] ms */
 int fs_worker_last_phases(fs_worker *w, float *ms4);
+/* Counters of the last fill: [0] sum over queued j of min(mlen_j+1, len_j)
+ * (request tokens K1 must read: the algorithmic bytes / 4), [1] requests
+ * matched, [2] admission events, [3] refill events, [4] frontier resumes,
+ * [5] kernel launches issued by the fill. */
+int fs_worker_last_stats(fs_worker *w, int64_t *stats8);
+/* Kernel launches issued by this library since load (all handles). */
+int64_t fs_launch_count(void);
 /* Queue length currently mirrored on device (worker.queue, worker.py:73) */
 int fs_worker_queue_len(fs_worker *w, int64_t *n);
 

@@ -74,6 +74,7 @@ SIGNATURES = {
     "fs_trie_admit": (C.c_int, [vp, i32, i64, P32, P32, PREC]),
     "fs_trie_pin": (C.c_int, [vp, i32]),
     "fs_trie_unpin": (C.c_int, [vp, i32]),
+    "fs_trie_unpin_many": (C.c_int, [vp, i64, P32]),
     "fs_trie_evict_lru": (C.c_int, [vp, i64, PREC]),
     "fs_trie_longest_match_workers": (C.c_int, [vp, i32, i64, P32, PU64]),
     "fs_trie_evict_notify": (C.c_int, [vp, i64, i32, i32, i32, i64]),
@@ -89,6 +90,8 @@ SIGNATURES = {
     "fs_worker_mark_known": (C.c_int, [vp, i64, P32]),
     "fs_worker_fill": (C.c_int, [vp, i64, i64, i64, PFILL]),
     "fs_worker_last_phases": (C.c_int, [vp, PF]),
+    "fs_worker_last_stats": (C.c_int, [vp, P64]),
+    "fs_launch_count": (i64, []),
     "fs_worker_queue_len": (C.c_int, [vp, P64]),
     "fs_worker_device_counters": (C.c_int, [vp, i32, P64, P64]),
     "fs_dispatcher_create": (C.c_int, [vp, C.c_int, i64, i64, i64, i32, PP]),

@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
                                                int64_t now, int stamp, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_fnode,
-                                               int32_t *__restrict__ out_next) {
+                                               int32_t *__restrict__ out_next,
+                                               unsigned long long *__restrict__ alg_tokens) {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= n) return;
@@ -38,7 +39,20 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
         if (out_cov) out_cov[i] = w.cov;
         if (out_fnode) out_fnode[i] = w.fnode;
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
+        // request tokens a match must read: min(mlen+1, len)
+        if (alg_tokens) atomicAdd(alg_tokens, (unsigned long long)min(w.mlen + 1, len));
     }
+}
+
+// Finish of a batch: unpin every path in order (worker.py:209-213).
+__global__ void k_unpin_many(TrieView t, const int32_t *__restrict__ nodes, int64_t n, int64_t *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    t.sc->status = FS_OK;
+    for (int64_t i = 0; i < n; i++) {
+        if (nodes[i] >= 0) unpin_chain(t, nodes[i]);
+        if (t.sc->status != FS_OK) break;
+    }
+    out[0] = t.sc->status;
 }
 
 // ---------------------------------------------------------------- queue upkeep

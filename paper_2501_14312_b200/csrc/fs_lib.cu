@@ -9,6 +9,7 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -43,6 +44,15 @@ static int fail(int code, const char *fmt, ...) {
         int rc_ = (x);           \
         if (rc_ != FS_OK) return rc_; \
     } while (0)
+
+// Kernel launches issued by this library (the bench reports it as gpu_launches).
+// CUB device-wide calls launch several kernels; their counts were taken from
+// the ncu launch list (profiles/) for the code paths used here.
+static std::atomic<int64_t> g_launches{0};
+#define FS_CUB_SORT_LAUNCHES 4   // onesweep: histogram, exclusive-sum, 2 digit passes (<= 16-bit keys)
+#define FS_CUB_SELECT_LAUNCHES 2 // scan-tile init + select
+static inline void counted(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+extern "C" int64_t fs_launch_count(void) { return g_launches.load(); }
 
 extern "C" const char *fs_last_error(void) { return g_err.c_str(); }
 extern "C" int fs_version(void) { return 1; }
@@ -344,7 +354,7 @@ static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
         TRY(dgrow(t->hkeys, hs, s)); TRY(dgrow(t->hvals, hs, s));
         t->hsize = hs;
         CK(cudaMemsetAsync(t->hkeys.p, 0xff, sizeof(uint64_t) * hs, s));
-        if (old > 0) k_rehash<<<148, 256, 0, s>>>(view(t));
+        if (old > 0) { k_rehash<<<148, 256, 0, s>>>(view(t)); counted(); }
         CK(cudaGetLastError());
     }
     return FS_OK;
@@ -376,6 +386,7 @@ extern "C" int fs_trie_create(fs_ctx *c, int64_t capacity, int track_workers, in
     TRY(dgrow(t->opout, 8, c->stream));
     TRY(hgrow(t->h_out, 8));
     k_trie_init<<<1, 32, 0, c->stream>>>(view(t), capacity);
+    counted();
     CK(cudaGetLastError());
     TRY(trie_pull(t));
     *out = t;
@@ -421,7 +432,8 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     CK(cudaMemcpyAsync(sm.ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
     const int64_t blocks = (n * 32 + 255) / 256;
     k_match<<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
-                                                      stamp, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr);
+                                                      stamp, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr, nullptr);
+    counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
     if (out_cov) CK(cudaMemcpyAsync(out_cov, sm.cov.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -462,6 +474,7 @@ static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     a.path = t->path.p;
     a.out = t->opout.p;
     k_op<<<1, 256, 0, c->stream>>>(a);
+    counted();
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, c->stream));
@@ -528,6 +541,27 @@ static int pin_op(fs_trie *t, int32_t node, int op) {
 }
 extern "C" int fs_trie_pin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_PIN); }
 extern "C" int fs_trie_unpin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_UNPIN); }
+
+extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
+    if (!t || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    if (n == 0) return FS_OK;
+    TRY(ctx_use(t->ctx));
+    for (int64_t i = 0; i < n; i++)
+        if (nodes[i] >= t->h_sc.hw) return fail(FS_ERR_INVALID, "bad path handle %d", nodes[i]);
+    cudaStream_t s = t->ctx->stream;
+    static thread_local DBuf<int32_t> dn;
+    TRY(dgrow(dn, n, s));
+    CK(cudaMemcpyAsync(dn.p, nodes, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    k_unpin_many<<<1, 32, 0, s>>>(view(t), dn.p, n, t->opout.p);
+    counted();
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (t->h_out.p[0] == FS_ERR_UNDERFLOW) return fail(FS_ERR_UNDERFLOW, "unpin below zero (radix.py:183)");
+    if (t->h_out.p[0] != FS_OK) return fail((int)t->h_out.p[0], "unpin_many failed");
+    return FS_OK;
+}
 
 extern "C" int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs) {
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
@@ -627,6 +661,8 @@ struct fs_worker {
     HBuf<int64_t> h_st64;
     cudaEvent_t ev[5];
     float phases[4] = {0, 0, 0, 0};
+    DBuf<int64_t> alg;         // K1 algorithmic-token accumulator
+    int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 struct IsQueued {
@@ -661,8 +697,9 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     CK(cudaMemsetAsync(w->q.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->refills.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
-    TRY(dgrow(w->hdr, 8, c->stream)); TRY(hgrow(w->h_hdr, 8));
+    TRY(dgrow(w->hdr, 8, c->stream)); TRY(hgrow(w->h_hdr, 16));
     TRY(dgrow(w->nsel, 1, c->stream));
+    TRY(dgrow(w->alg, 1, c->stream));
     for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
     CK(cudaStreamSynchronize(c->stream));
     *out = w;
@@ -744,6 +781,7 @@ extern "C" int fs_worker_check_refill(fs_worker *w, int64_t n, const int32_t *qu
     TRY(dgrow(dq, w->nclients, c->stream));
     CK(cudaMemcpyAsync(dq.p, flags.data(), w->nclients, cudaMemcpyHostToDevice, c->stream));
     k_check_refill<<<1, 32, 0, c->stream>>>(w->q.p, w->refills.p, w->known.p, w->nclients, dq.p, w->quantum, w->hdr.p);
+    counted();
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, c->stream));
@@ -816,6 +854,12 @@ extern "C" int fs_worker_queue_len(fs_worker *w, int64_t *n) {
     return FS_OK;
 }
 
+extern "C" int fs_worker_last_stats(fs_worker *w, int64_t *stats8) {
+    if (!w || !stats8) return fail(FS_ERR_INVALID, "NULL");
+    for (int i = 0; i < 8; i++) stats8[i] = w->stats[i];
+    return FS_OK;
+}
+
 extern "C" int fs_worker_last_phases(fs_worker *w, float *ms4) {
     if (!w || !ms4) return fail(FS_ERR_INVALID, "NULL");
     for (int i = 0; i < 4; i++) ms4[i] = w->phases[i];
@@ -848,6 +892,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     if (w->iota.cap < n + 1) {
         TRY(dgrow(w->iota, n + 1, s));
         k_iota<<<(unsigned)((w->iota.cap + 255) / 256), 256, 0, s>>>(w->iota.p, w->iota.cap);
+        counted();
         CK(cudaGetLastError());
     }
     const int64_t acap = std::max<int64_t>(n + 1, 64);
@@ -867,11 +912,13 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     cub::DeviceSelect::If(nullptr, sel_bytes, w->queue.p, w->queue2.p, w->nsel.p, (int)std::max<int64_t>(w->qn, 1), IsQueued{c->rstate.p}, s);
     TRY(dgrow(w->cub_tmp, (int64_t)std::max(sort_bytes, sel_bytes) + 256, s));
 
+    const int64_t launches0 = g_launches.load();
     CK(cudaEventRecord(w->ev[0], s));
     // ---- queue upkeep: drop last fill's admissions, merge arrivals by label
     if (w->admitted_last > 0 && w->qn > 0) {
         size_t b = w->cub_tmp.cap;
         CK(cub::DeviceSelect::If(w->cub_tmp.p, b, w->queue.p, w->queue2.p, w->nsel.p, (int)w->qn, IsQueued{c->rstate.p}, s));
+        counted(FS_CUB_SELECT_LAUNCHES);
         std::swap(w->queue, w->queue2);
     }
     if (n_new > 0) {
@@ -883,8 +930,10 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         CK(cudaMemcpyAsync(w->newids.p, w->h_st32.p, sizeof(int32_t) * n_new, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(w->newlab.p, w->h_st64.p, sizeof(int64_t) * n_new, cudaMemcpyHostToDevice, s));
         k_set_state<<<(unsigned)((n_new + 255) / 256), 256, 0, s>>>(c->rstate.p, w->newids.p, n_new, 1);
+        counted();
         k_merge<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->queue.p, (int32_t)n_old, w->newids.p, w->newlab.p,
                                                            (int32_t)n_new, c->rlabel.p, w->queue2.p);
+        counted();
         CK(cudaGetLastError());
         std::swap(w->queue, w->queue2);
         nv.clear();
@@ -898,12 +947,15 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         CK(cudaMemcpyAsync(w->dlc.p, w->dl_client.data(), sizeof(int32_t) * ndl, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(w->dld.p, w->dl_delta.data(), sizeof(int64_t) * ndl, cudaMemcpyHostToDevice, s));
     }
+    CK(cudaMemsetAsync(w->alg.p, 0, sizeof(int64_t), s));
     CK(cudaEventRecord(w->ev[1], s));
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
     if (n > 0) {
         const int64_t blocks = (n * 32 + 255) / 256;
         k_match<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
-                                                  kmax, w->keys.p, nullptr, w->cov.p, w->fnode.p, w->next.p);
+                                                  kmax, w->keys.p, nullptr, w->cov.p, w->fnode.p, w->next.p,
+                                                  (unsigned long long *)w->alg.p);
+        counted();
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(w->ev[2], s));
@@ -911,9 +963,11 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     if (n > 0) {
         size_t b = w->cub_tmp.cap;
         CK(cub::DeviceRadixSort::SortPairs(w->cub_tmp.p, b, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)n, 0, (int)bits, s));
+        counted(FS_CUB_SORT_LAUNCHES);
         k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p, w->fnode.p,
                                                             w->next.p, c->rclient.p, c->rlen.p, w->s_req.p, w->slot.p,
                                                             w->s_len.p, w->s_fnode.p);
+        counted();
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(w->ev[3], s));
@@ -934,11 +988,13 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     a.rstate = c->rstate.p;
     a.hdr = w->hdr.p;
     k_schedule<<<1, FS_SCHED_THREADS, 0, s>>>(a);
+    counted();
     CK(cudaGetLastError());
     CK(cudaEventRecord(w->ev[4], s));
     w->dl_client.clear(); w->dl_delta.clear();
     // ---- results
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 6, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p + 6, w->alg.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
@@ -947,6 +1003,12 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     const int64_t nrec = w->h_hdr.p[1];
     const int64_t status = w->h_hdr.p[2];
     for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&w->phases[i], w->ev[i], w->ev[i + 1]));
+    w->stats[0] = w->h_hdr.p[6];
+    w->stats[1] = n;
+    w->stats[2] = w->h_hdr.p[3];
+    w->stats[3] = w->h_hdr.p[4];
+    w->stats[4] = w->h_hdr.p[5];
+    w->stats[5] = g_launches.load() - launches0;
     float total = 0;
     CK(cudaEventElapsedTime(&total, w->ev[0], w->ev[4]));
     res->device_ms = total;
@@ -1058,6 +1120,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
     k_dispatch<<<1, 256, 0, s>>>(a);
+    counted();
     CK(cudaGetLastError());
     d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
     int64_t st = 0;
@@ -1150,6 +1213,7 @@ extern "C" int fs_dispatch_select(fs_dispatcher *d, int32_t client, uint64_t mat
     a.out_w = d->o_w.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
     k_dispatch<<<1, 256, 0, s>>>(a);
+    counted();
     CK(cudaGetLastError());
     d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
     int64_t r = 0;
@@ -1213,6 +1277,7 @@ extern "C" int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t 
         a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = (int32_t)d->dl_idx.size();
         a.hdr = d->hdr.p;
         k_dispatch<<<1, 256, 0, d->ctx->stream>>>(a);
+        counted();
         CK(cudaGetLastError());
         d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
     }

@@ -182,6 +182,10 @@ class Trie:
     def unpin(self, node: int):
         call("fs_trie_unpin", self._h, node)
 
+    def unpin_many(self, nodes):
+        nodes = np.ascontiguousarray(nodes, dtype=np.int32)
+        call("fs_trie_unpin_many", self._h, len(nodes), _p32(nodes))
+
     def evict_lru(self, needed: int) -> Records:
         recs, err = self._op("fs_trie_evict_lru", needed)
         return recs
@@ -250,6 +254,11 @@ class FillResult:
     pinned: int
     device_ms: float
     phases_ms: list = field(default_factory=list)
+    stats: list = field(default_factory=list)  # fs_worker_last_stats
+
+
+def launch_count() -> int:
+    return int(L.load().fs_launch_count())
 
 
 class WorkerDev:
@@ -335,10 +344,12 @@ class WorkerDev:
         recs = self.trie.read_records(res.recs.n_rec)
         ph = (C.c_float * 4)()
         call("fs_worker_last_phases", self._h, ph)
+        st = (C.c_int64 * 8)()
+        call("fs_worker_last_stats", self._h, st)
         a = res.n_adm
         return FillResult(self._req[:a].copy(), self._mlen[:a].copy(), self._unp[:a].copy(),
                           self._pinb[:a].copy(), self._node[:a].copy(), self._rend[:a].copy(),
-                          recs, res.n_queued, res.used, res.pinned, res.device_ms, list(ph))
+                          recs, res.n_queued, res.used, res.pinned, res.device_ms, list(ph), list(st))
 
 
 class DispatcherDev:

@@ -1,0 +1,106 @@
+"""Synthetic shared-prefix request queues.
+
+Token ids are uniform in [0, 2^31) (requests.py:92), drawn with numpy PCG64;
+the prefix structure is drawn with Python `random`, both from the config seed,
+so every consumer (the CUDA path, the CPU oracle, the reference) sees the
+same requests.  Returned as flat arrays ready for fs_requests_add.
+"""
+from __future__ import annotations
+
+import bisect
+import random
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class Queue:
+    flat: np.ndarray      # int32 tokens, requests back to back
+    offsets: np.ndarray   # int64 start of each request in flat
+    lens: np.ndarray      # int32
+    clients: np.ndarray   # int32 dense client ids
+    arrival: np.ndarray   # int64 trace arrival (us)
+    rids: list            # request ids (str); (arrival, rid) order == labels order
+    labels: np.ndarray    # int64 rank of (arrival, rid)
+
+    def __len__(self):
+        return len(self.lens)
+
+    def tokens(self, i) -> np.ndarray:
+        o = int(self.offsets[i])
+        return self.flat[o:o + int(self.lens[i])]
+
+
+@dataclass
+class SharedPrefixSpec:
+    n: int = 65536
+    clients: int = 100
+    docs: int = 256
+    zipf_s: float = 1.1
+    len_lo: int = 1024
+    len_hi: int = 4096
+    doc_lo: int = 512
+    doc_hi: int = 4032
+    seed: int = 2
+
+
+def config2(n: int = 65536, seed: int = 2) -> SharedPrefixSpec:
+    """Config 2: DLPM single worker, 100 clients, 64k queued, 1-4k-token prompts,
+    prefixes = Zipf(1.1)-chosen document over 256 docs of U[512, 4032] tokens."""
+    return SharedPrefixSpec(n=n, seed=seed)
+
+
+def build_docs(spec: SharedPrefixSpec):
+    pr = random.Random(spec.seed)
+    g = np.random.Generator(np.random.PCG64(spec.seed))
+    doc_len = [pr.randint(spec.doc_lo, spec.doc_hi) for _ in range(spec.docs)]
+    docs = [g.integers(0, 2 ** 31, size=dl, dtype=np.int64).astype(np.int32) for dl in doc_len]
+    w = [1.0 / (k + 1) ** spec.zipf_s for k in range(spec.docs)]
+    cum = []
+    acc = 0.0
+    for x in w:
+        acc += x
+        cum.append(acc)
+    return docs, cum
+
+
+def shared_prefix_queue(spec: SharedPrefixSpec, first: int = 0, count: int | None = None,
+                        arrival: int = 0, docs=None, stream_seed: int | None = None) -> Queue:
+    """Requests [first, first+count) of the spec's stream.  Request i draws its
+    length, document and client from a per-request Python RNG and its unique
+    suffix from a per-batch PCG64 stream, so slices are reproducible."""
+    count = spec.n if count is None else count
+    if docs is None:
+        docs = build_docs(spec)
+    doc_tok, cum = docs
+    total_w = cum[-1]
+    pr = random.Random(spec.seed * 1_000_003 + first)
+    g = np.random.Generator(np.random.PCG64((spec.seed if stream_seed is None else stream_seed) * 7919 + first))
+    L = np.empty(count, np.int64)
+    D = np.empty(count, np.int64)
+    C = np.empty(count, np.int32)
+    for i in range(count):
+        L[i] = pr.randint(spec.len_lo, spec.len_hi)
+        D[i] = bisect.bisect_left(cum, pr.random() * total_w)
+        C[i] = pr.randrange(spec.clients)
+    doc_len = np.array([len(d) for d in doc_tok], np.int64)
+    P = np.minimum(doc_len[D], L - 1)
+    suf = L - P
+    offsets = np.zeros(count, np.int64)
+    offsets[1:] = np.cumsum(L[:-1])
+    flat = np.empty(int(L.sum()), np.int32)
+    sfx = g.integers(0, 2 ** 31, size=int(suf.sum()), dtype=np.int64).astype(np.int32)
+    so = 0
+    for i in range(count):
+        o = offsets[i]
+        p = P[i]
+        flat[o:o + p] = doc_tok[D[i]][:p]
+        s = suf[i]
+        flat[o + p:o + p + s] = sfx[so:so + s]
+        so += s
+    rids = [f"r{first + i:08d}" for i in range(count)]
+    arr = np.full(count, arrival, np.int64)
+    # (arrival, rid) rank; zero-padded rids sort numerically
+    labels = (np.int64(arrival) << 32) + np.arange(first, first + count, dtype=np.int64)
+    return Queue(flat, offsets, L.astype(np.int32), C, arr, rids, labels)
