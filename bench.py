@@ -208,7 +208,7 @@ def main():
     spec = config2(args.nq, seed=2 + rank)
     docs = build_docs(spec)
     q = shared_prefix_queue(spec, docs=docs)
-    pool_n = 96 * (args.steps + args.warmup) + 1024
+    pool_n = 800 * (args.steps + args.warmup) + 1024
     pool = shared_prefix_queue(spec, first=args.nq, count=pool_n, arrival=STEP_US, docs=docs, stream_seed=spec.seed + 101)
     cfg = {"workload": "config2: DLPM 1 worker/GPU, 100 clients, 64k queued, 1-4k-token prompts, "
                        "Zipf(1.1) prefixes over 256 docs, M=capacity=65536, q_u_frac=0.5, reserve=8",
@@ -249,6 +249,7 @@ def main():
     l0 = launch_count()
     h2d0, d2h0 = g.h2d, g.d2h
     dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(4)
+    sched = np.zeros(8)
     t_start = time.perf_counter()
     for _ in range(args.steps):
         now += STEP_US
@@ -261,6 +262,7 @@ def main():
         alg_tok += res.stats[0]
         k1_ms.append(res.phases_ms[1])
         phases += np.array(res.phases_ms)
+        sched += np.array(res.stats[8:16], dtype=np.float64)
     g.ctx.sync()
     t_total = time.perf_counter() - t_start
     launches = launch_count() - l0
@@ -308,6 +310,10 @@ def main():
         "phase_ms_per_step": {"merge": phases[0] / args.steps, "k1_match": phases[1] / args.steps,
                               "k2_sort": phases[2] / args.steps, "k3k4_schedule": phases[3] / args.steps},
         "admissions_per_step": adm / args.steps, "queued_per_step": n_per_step,
+        "sched_profile_per_step": {"find_cyc": sched[0] / args.steps, "walk_cyc": sched[1] / args.steps,
+                                   "evict_cyc": sched[2] / args.steps, "tail_cyc": sched[3] / args.steps,
+                                   "chunks": sched[4] / args.steps, "evict_pops": sched[5] / args.steps,
+                                   "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }
     if not args.no_cpu and world == 1:

@@ -276,6 +276,7 @@ struct EvictSmem {
     int32_t nd[32];
     int64_t freed;
     int32_t best;
+    int64_t pops;
 };
 
 __device__ inline void block_evict(const TrieView &t, int64_t needed, EvictSmem *sm) {
@@ -314,6 +315,7 @@ __device__ inline void block_evict(const TrieView &t, int64_t needed, EvictSmem 
             }
             sm->best = b;
             if (b >= 0) {
+                sm->pops++;
                 const int32_t plen = t.end[b];  // len(full_path): the node's root-path length
                 const int64_t remaining = needed - sm->freed;
                 const int32_t el = elen(t, b);
@@ -341,6 +343,7 @@ struct InsertSmem {
     EvictSmem ev;
     int32_t np, mlen, new_len, deepest, last, status, cov, fnode;
     int64_t needed, unpinned;
+    int64_t *prof;  // optional cycle counters: [1] walk, [2] evict, [5] evict pops
 };
 
 // RadixTree.insert (radix.py:128-162) by one CTA (warp 0 walks).  `path` is a
@@ -351,6 +354,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                                     int32_t worker, int32_t *path, InsertSmem *sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t *rq = t.arena + req_off;
+    const long long c0 = clock64();
     if (warp == 0) {
         const WalkOut w = warp_walk(t, rq, len, lane, false, 0, path);
         if (lane == 0) {
@@ -374,8 +378,11 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         }
     }
     __syncthreads();
+    const long long c1 = clock64();
+    if (tid == 0 && sm->prof) sm->prof[1] += c1 - c0;
     if (sm->needed > 0) {
         block_evict(t, sm->needed, &sm->ev);
+        if (tid == 0 && sm->prof) sm->prof[2] += clock64() - c1;
         if (tid == 0) {
             for (int32_t i = 0; i < sm->np; i++) t.flags[path[i]] &= ~FS_PROTECT;
             if (t.sc->used + sm->new_len > t.sc->capacity) sm->status = FS_ERR_CACHE_FULL;

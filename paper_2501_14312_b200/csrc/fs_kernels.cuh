@@ -44,15 +44,25 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
     }
 }
 
-// Finish of a batch: unpin every path in order (worker.py:209-213).
+// Finish of a batch: unpin every finished path (worker.py:209-213).  The
+// decrements commute, so each path's chain is walked by its own thread with
+// atomics; a node whose count reaches zero releases its edge from
+// pinned_tokens exactly once (radix.py:180-185).  Underflow is reported.
 __global__ void k_unpin_many(TrieView t, const int32_t *__restrict__ nodes, int64_t n, int64_t *out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    t.sc->status = FS_OK;
-    for (int64_t i = 0; i < n; i++) {
-        if (nodes[i] >= 0) unpin_chain(t, nodes[i]);
-        if (t.sc->status != FS_OK) break;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        int32_t nd = nodes[i];
+        long long freed = 0;
+        bool under = false;
+        while (nd > 0) {
+            const int32_t old = atomicSub(&t.ref[nd], 1);
+            if (old <= 0) { under = true; break; }
+            if (old == 1) freed += elen(t, nd);
+            nd = t.parent[nd];
+        }
+        if (freed) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)(-freed));
+        if (under) { t.sc->status = FS_ERR_UNDERFLOW; out[0] = FS_ERR_UNDERFLOW; }
     }
-    out[0] = t.sc->status;
 }
 
 // ---------------------------------------------------------------- queue upkeep
@@ -128,6 +138,7 @@ struct SchedSmem {
     int32_t cursor, progress, epoch, npos, nadm, stop, j;
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
+    int64_t prof[8];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops
 };
 
 __device__ __forceinline__ int64_t sched_slack(const FillArgs &a, int64_t headroom) {
@@ -239,7 +250,7 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int32_t epoch = sm->epoch;
     for (int32_t base = from; base < until; base += FS_CHUNK) {
-        if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; }
+        if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; sm->prof[4]++; }
         __syncthreads();
         int32_t mine = FS_NONE;
 #pragma unroll
@@ -323,6 +334,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     if (tid == 0) pinb = t.sc->pinned;
     __syncthreads();
     block_insert(t, off, len, a.now, -1, a.path, &sm->ins);
+    const long long ct = clock64();
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
         if (in.status != FS_OK) {
@@ -364,6 +376,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             sm->progress = 1;
             if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
         }
+        sm->prof[3] += clock64() - ct;
     }
     __syncthreads();
 }
@@ -378,7 +391,11 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         a.hdr[2] = FS_OK;
         sm.cursor = 0; sm.progress = 0; sm.epoch = 0; sm.nadm = 0; sm.stop = 0;
         sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0;
+        for (int i = 0; i < 8; i++) sm.prof[i] = 0;
+        sm.ins.prof = sm.prof;
+        sm.ins.ev.pops = 0;
     }
+    const long long t_start = clock64();
     for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.pend_cnt[c] = 0;
     __syncthreads();
     for (int32_t p = tid; p < a.n; p += blockDim.x) atomicAdd(&a.pend_cnt[a.slot[p].x], 1);
@@ -397,7 +414,9 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         const int64_t slack = sched_slack(a, sm.headroom);
         const int32_t cur = sm.cursor;
         __syncthreads();
+        const long long cf = clock64();
         int32_t j = block_find(a, &sm, cur, a.n, ptrue, slack);
+        if (tid == 0) sm.prof[0] += clock64() - cf;
         if (j == FS_NONE) {
             if (sm.progress) {
                 __syncthreads();
@@ -427,6 +446,9 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         a.hdr[3] = sm.epoch;
         a.hdr[4] = sm.refill_events;
         a.hdr[5] = sm.resumes;
+        sm.prof[5] = sm.ins.ev.pops;
+        sm.prof[7] = clock64() - t_start;
+        for (int i = 0; i < 8; i++) a.hdr[8 + i] = sm.prof[i];
     }
 }
 
@@ -452,7 +474,7 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     __shared__ InsertSmem ins;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;
-    if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; }
+    if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.ev.pops = 0; }
     __syncthreads();
     const int32_t *rq = t.arena + a.req_off;
     switch (a.op) {
@@ -541,6 +563,8 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             else a.qsize[a.dl_w[i]] += a.dl_q[i];
         }
         t.sc->status = FS_OK;
+        ins.prof = nullptr;
+        ins.ev.pops = 0;
     }
     __syncthreads();
     if (a.select_only) {
