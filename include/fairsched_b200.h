@@ -175,10 +175,10 @@ int fs_worker_last_phases(fs_worker *w, float *ms4);
 /* Counters of the last fill: [0] sum over queued j of min(mlen_j+1, len_j)
  * (request tokens K1 must read: the algorithmic bytes / 4), [1] requests
  * matched, [2] admission events, [3] refill events, [4] frontier resumes,
- * [5] kernel launches issued by the fill, [8..15] scheduler-kernel SM cycles:
+ * [5] kernel launches issued by the fill, [6] trie hops in K1, [8..15] scheduler-kernel SM cycles:
  * [8] candidate search, [9] admission walks, [10] LRU eviction, [11] admission
  * tail (pin, counters, records), [12] search chunks, [13] eviction pops,
- * [15] total. */
+ * [14] trie hops in admission walks, [15] total. */
 int fs_worker_last_stats(fs_worker *w, int64_t *stats16);
 /* Kernel launches issued by this library since load (all handles). */
 int64_t fs_launch_count(void);

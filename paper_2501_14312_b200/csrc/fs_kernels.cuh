@@ -40,7 +40,10 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
         if (out_fnode) out_fnode[i] = w.fnode;
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
         // request tokens a match must read: min(mlen+1, len)
-        if (alg_tokens) atomicAdd(alg_tokens, (unsigned long long)min(w.mlen + 1, len));
+        if (alg_tokens) {
+            atomicAdd(alg_tokens, (unsigned long long)min(w.mlen + 1, len));
+            atomicAdd(alg_tokens + 1, (unsigned long long)w.npath);  // trie hops
+        }
     }
 }
 
@@ -377,6 +380,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
         }
         sm->prof[3] += clock64() - ct;
+        sm->prof[6] += sm->ins.np;
     }
     __syncthreads();
 }

@@ -700,7 +700,7 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
     TRY(dgrow(w->hdr, 16, c->stream)); TRY(hgrow(w->h_hdr, 24));
     TRY(dgrow(w->nsel, 1, c->stream));
-    TRY(dgrow(w->alg, 1, c->stream));
+    TRY(dgrow(w->alg, 2, c->stream));
     for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
     CK(cudaStreamSynchronize(c->stream));
     *out = w;
@@ -948,7 +948,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         CK(cudaMemcpyAsync(w->dlc.p, w->dl_client.data(), sizeof(int32_t) * ndl, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(w->dld.p, w->dl_delta.data(), sizeof(int64_t) * ndl, cudaMemcpyHostToDevice, s));
     }
-    CK(cudaMemsetAsync(w->alg.p, 0, sizeof(int64_t), s));
+    CK(cudaMemsetAsync(w->alg.p, 0, 2 * sizeof(int64_t), s));
     CK(cudaEventRecord(w->ev[1], s));
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
     if (n > 0) {
@@ -995,7 +995,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     w->dl_client.clear(); w->dl_delta.clear();
     // ---- results
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_hdr.p + 16, w->alg.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p + 16, w->alg.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
@@ -1005,6 +1005,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     const int64_t status = w->h_hdr.p[2];
     for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&w->phases[i], w->ev[i], w->ev[i + 1]));
     w->stats[0] = w->h_hdr.p[16];
+    w->stats[6] = w->h_hdr.p[17];
     for (int i = 8; i < 16; i++) w->stats[i] = w->h_hdr.p[i];
     w->stats[1] = n;
     w->stats[2] = w->h_hdr.p[3];
