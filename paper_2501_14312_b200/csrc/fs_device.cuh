@@ -4,15 +4,31 @@
 // Data model (HBM):
 //   * token arena: every request's int32 tokens, uploaded once, 16-B aligned.
 //   * radix trie (one per RadixTree, radix.py:48): SoA node table.  A node does
-//     not own tokens: its root path is arena[src : src+end] (a prefix of the
-//     request that created it) and its edge is arena[src+start : src+end].
-//     Splits and partial evictions only move start/end -- no token copies.
-//   * children: one open-addressing hash (parent, first token) -> child,
-//     linear probing with backward-shift deletion (no tombstones).
+//     not own tokens: its root path is arena[src : src+end] -- a prefix of the
+//     request that created it (its "source chain") -- and its edge is
+//     arena[src+start : src+end].  Splits and partial evictions only move
+//     start/end; no token is ever copied.
+//   * position shadow pos[arena offset]: for every token position p of a
+//     source chain S that is cached in this trie, pos[S+p] is the node covering
+//     depth p.  A walk therefore compares a request against a whole source
+//     chain in one contiguous, coalesced stream and finds the node it stops in
+//     with one lookup -- the cost is per source chain crossed, not per node.
+//     (The reference trees of configs 2/5 hold hundreds of split nodes along
+//     one document chain.)
+//   * children: one open-addressing hash (parent, first token) -> child, with
+//     key and value packed in one 16-byte slot (one load per probe), linear
+//     probing, backward-shift deletion.
+//   * last_access is stored lazily: la[n] holds the stamps of paths that
+//     *ended* at n; the reference value is the maximum over n's subtree (every
+//     stamp in radix.py:86-90,107-109,158-159 covers a whole root path).  A
+//     detached leaf pushes its la up to its parent, so leaves -- the only nodes
+//     LRU eviction compares (radix.py:196-219) -- always hold their exact value.
+//   * ref counts stay exact per node; pin/unpin touch every node of a path,
+//     enumerated block-parallel from the source-chain segments of the walk.
 //
-// All structural edits are done by a single thread of a single CTA (the
-// reference is single-writer); token compares are warp-wide
-// (32 lanes x 4 tokens per step, ballot + ffs for the first mismatch).
+// Structural edits are made by one thread of one CTA (the reference is
+// single-writer); compares are warp-wide, bulk per-position and
+// per-path-node updates are block-parallel.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -46,20 +62,20 @@ struct TrieScalars {
 
 struct TrieView {
     const int32_t *arena;
+    int32_t *pos;      // position shadow over the arena
     int64_t *src;
-    int32_t *start, *end, *parent, *nchild, *ref, *first;
+    int32_t *start, *end, *slen, *parent, *nchild, *ref, *first;
     int64_t *la, *seq;
     uint8_t *flags;
-    uint64_t *wmask;  // nullptr unless track_workers
-    int64_t *wtime;   // [node * nw + w]
+    uint64_t *wmask;   // nullptr unless track_workers
+    int64_t *wtime;    // [node * nw + w]
     int32_t nw;
-    uint64_t *hkeys;
-    int32_t *hvals;
+    ulonglong2 *hslot; // {key, child}
     uint32_t hmask;
     int32_t *freest;
     int32_t ncap;
     TrieScalars *sc;
-    int64_t *rsrc;  // eviction-record sink
+    int64_t *rsrc;     // eviction-record sink
     int32_t *rlen, *rkeep;
     int64_t rcap;
 };
@@ -79,9 +95,9 @@ __device__ __forceinline__ int32_t h_find(const TrieView &t, int32_t p, int32_t 
     const uint64_t key = fs_hkey(p, tok);
     uint32_t i = fs_hmix(key) & t.hmask;
     while (true) {
-        const uint64_t k = t.hkeys[i];
-        if (k == key) return t.hvals[i];
-        if (k == FS_HEMPTY) return -1;
+        const ulonglong2 s = t.hslot[i];
+        if (s.x == key) return (int32_t)s.y;
+        if (s.x == FS_HEMPTY) return -1;
         i = (i + 1) & t.hmask;
     }
 }
@@ -90,8 +106,8 @@ __device__ inline void h_put(const TrieView &t, int32_t p, int32_t tok, int32_t 
     const uint64_t key = fs_hkey(p, tok);
     uint32_t i = fs_hmix(key) & t.hmask;
     while (true) {
-        const uint64_t k = t.hkeys[i];
-        if (k == key || k == FS_HEMPTY) { t.hkeys[i] = key; t.hvals[i] = child; return; }
+        const uint64_t k = t.hslot[i].x;
+        if (k == key || k == FS_HEMPTY) { t.hslot[i] = make_ulonglong2(key, (unsigned long long)(uint32_t)child); return; }
         i = (i + 1) & t.hmask;
     }
 }
@@ -99,32 +115,33 @@ __device__ inline void h_put(const TrieView &t, int32_t p, int32_t tok, int32_t 
 __device__ inline void h_del(const TrieView &t, int32_t p, int32_t tok) {
     const uint64_t key = fs_hkey(p, tok);
     uint32_t i = fs_hmix(key) & t.hmask;
-    while (t.hkeys[i] != key) {
-        if (t.hkeys[i] == FS_HEMPTY) return;
+    while (t.hslot[i].x != key) {
+        if (t.hslot[i].x == FS_HEMPTY) return;
         i = (i + 1) & t.hmask;
     }
     uint32_t j = i;
     while (true) {
         j = (j + 1) & t.hmask;
-        const uint64_t kj = t.hkeys[j];
-        if (kj == FS_HEMPTY) break;
-        const uint32_t h = fs_hmix(kj) & t.hmask;
+        const ulonglong2 sj = t.hslot[j];
+        if (sj.x == FS_HEMPTY) break;
+        const uint32_t h = fs_hmix(sj.x) & t.hmask;
         const bool stay = (i <= j) ? (i < h && h <= j) : (i < h || h <= j);
         if (stay) continue;
-        t.hkeys[i] = kj; t.hvals[i] = t.hvals[j];
+        t.hslot[i] = sj;
         i = j;
     }
-    t.hkeys[i] = FS_HEMPTY;
+    t.hslot[i] = make_ulonglong2(FS_HEMPTY, 0ull);
 }
 
 // ---------------------------------------------------------------- nodes
 // RadixNode(...) with seq = self._seq; self._seq += 1  (radix.py:117-118, 153-154)
-__device__ inline int32_t node_new(const TrieView &t, int64_t src, int32_t start, int32_t end, int32_t parent) {
+__device__ inline int32_t node_new(const TrieView &t, int64_t src, int32_t start, int32_t end, int32_t slen,
+                                   int32_t parent) {
     int32_t n;
     if (t.sc->nfree > 0) n = t.freest[--t.sc->nfree];
     else if (t.sc->hw < t.ncap) n = t.sc->hw++;
     else { t.sc->status = FS_ERR_NOMEM; return -1; }
-    t.src[n] = src; t.start[n] = start; t.end[n] = end; t.parent[n] = parent;
+    t.src[n] = src; t.start[n] = start; t.end[n] = end; t.slen[n] = slen; t.parent[n] = parent;
     t.nchild[n] = 0; t.ref[n] = 0; t.la[n] = 0;
     t.seq[n] = t.sc->next_seq++;
     t.first[n] = t.arena[src + start];
@@ -142,13 +159,14 @@ __device__ inline void node_free(const TrieView &t, int32_t n) {
 __device__ __forceinline__ int32_t elen(const TrieView &t, int32_t n) { return t.end[n] - t.start[n]; }
 
 // RadixTree._split (radix.py:114-126): top gets a new seq, copies ref /
-// last_access / workers; the bottom keeps its identity (and seq).
+// last_access / workers; the bottom keeps its identity (and seq).  The caller
+// re-points pos[] for the top's depth range [start, start+k) (block_repoint).
 __device__ inline int32_t trie_split(const TrieView &t, int32_t node, int32_t k) {
     const int32_t P = t.parent[node];
-    const int32_t top = node_new(t, t.src[node], t.start[node], t.start[node] + k, P);
+    const int32_t top = node_new(t, t.src[node], t.start[node], t.start[node] + k, t.slen[node], P);
     if (top < 0) return -1;
     t.ref[top] = t.ref[node];
-    t.la[top] = t.la[node];
+    t.la[top] = 0;  // lazy: the top's value is the max over its subtree (the bottom)
     if (t.wmask) {
         t.wmask[top] = t.wmask[node];
         for (int w = 0; w < t.nw; w++) t.wtime[(int64_t)top * t.nw + w] = t.wtime[(int64_t)node * t.nw + w];
@@ -162,11 +180,13 @@ __device__ inline int32_t trie_split(const TrieView &t, int32_t node, int32_t k)
     return top;
 }
 
-// RadixTree._detach (radix.py:206-208)
+// RadixTree._detach (radix.py:206-208); the leaf's last_access moves to its
+// parent so the parent's subtree maximum is unchanged.
 __device__ inline void trie_detach(const TrieView &t, int32_t n) {
     const int32_t P = t.parent[n];
     h_del(t, P, t.first[n]);
     t.nchild[P]--;
+    if (P > 0 && t.la[n] > t.la[P]) t.la[P] = t.la[n];
     t.sc->used -= elen(t, n);
     node_free(t, n);
 }
@@ -176,28 +196,9 @@ __device__ inline void push_record(const TrieView &t, int64_t src, int32_t len, 
     if (i < t.rcap) { t.rsrc[i] = src; t.rlen[i] = len; t.rkeep[i] = keep; }
 }
 
-// pin / unpin via _chain (radix.py:164-185): deepest node up to the root
-__device__ inline void pin_chain(const TrieView &t, int32_t n) {
-    while (n > 0) {
-        if (t.ref[n] == 0) t.sc->pinned += elen(t, n);
-        t.ref[n]++;
-        n = t.parent[n];
-    }
-}
-__device__ inline void unpin_chain(const TrieView &t, int32_t n) {
-    while (n > 0) {
-        t.ref[n]--;
-        if (t.ref[n] < 0) { t.sc->status = FS_ERR_UNDERFLOW; t.ref[n] = 0; return; }
-        if (t.ref[n] == 0) t.sc->pinned -= elen(t, n);
-        n = t.parent[n];
-    }
-}
-
 // ---------------------------------------------------------------- compare
 // LCP of a[0:n) and b[0:n) by one warp: 128 tokens per step, first mismatch
 // by ballot + ffs (common_prefix_len, _speedups.pyx:11-22, at warp width).
-// `a` is trie edge data (hot, read-only path), `b` the request stream (read
-// once: streaming loads so it does not evict the trie from L1/L2).
 __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
                                             int32_t n, int lane) {
     int32_t k = 0;
@@ -206,7 +207,7 @@ __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int32_t p = k + u * 32 + lane;
-            bad[u] = (p < n) && (__ldg(a + p) != __ldcs(b + p));
+            bad[u] = (p < n) && (__ldg(a + p) != __ldg(b + p));
         }
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -218,58 +219,160 @@ __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const
     return n;
 }
 
-struct WalkOut {
-    int32_t mlen;       // match length
-    int32_t last_full;  // deepest fully matched node, -1 if none
-    int32_t partial;    // partially matched child, -1 if none
-    int32_t plen;       // tokens matched inside partial
-    int32_t cov;        // matched tokens inside pinned nodes (pinned coverage B)
-    int32_t fnode;      // node holding depth `cov` (0 = root)
-    int32_t npath;      // nodes written to `path` (full nodes + partial)
-    int64_t unpinned;   // probe()'s matched-unpinned count (radix.py:96-98)
+// Is node y the cached node covering depth d of source chain S?
+__device__ __forceinline__ bool pos_valid(const TrieView &t, int32_t y, int64_t S, int32_t d) {
+    return y > 0 && y < t.sc->hw && (t.flags[y] & FS_ALIVE) && t.src[y] == S && t.start[y] <= d && d < t.end[y];
+}
+
+// Deepest cached node of chain S covering a depth in [lo, hi] (depth lo is
+// known cached).  A chain is cached on a contiguous depth range (only its
+// bottom can be evicted or truncated), so validity is monotone.
+__device__ inline int32_t chain_lookup(const TrieView &t, int64_t S, int32_t lo, int32_t hi) {
+    int32_t y = t.pos[S + hi];
+    if (pos_valid(t, y, S, hi)) return y;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi + 1) >> 1;
+        if (pos_valid(t, t.pos[S + mid], S, mid)) lo = mid; else hi = mid - 1;
+    }
+    return t.pos[S + lo];
+}
+
+struct Seg {
+    int64_t S;
+    int32_t a, b;  // depths [a, b) of chain S on the path
 };
 
-// RadixTree._walk (radix.py:60-81) by one warp, optionally stamping
-// last_access = now on every full node and the partial node (radix.py:86-90).
-// All lanes return the same WalkOut; lane 0 writes stamps / path entries.
-__device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
-                                    bool stamp, int64_t now, int32_t *path) {
+struct WalkOut {
+    int32_t mlen;      // match length
+    int32_t last;      // deepest node the match reaches (partial or last full); -1 if none
+    int32_t plen;      // if partial: tokens matched inside `last`; 0 when `last` is fully matched
+    int32_t nseg;      // source-chain segments of the path
+    int32_t cov;       // matched tokens inside pinned nodes (pinned coverage B)
+    int64_t unpinned;  // probe()'s matched-unpinned count (radix.py:96-98)
+};
+
+// RadixTree._walk (radix.py:60-81) by one warp, chain by chain.  on_seg(S, a, b)
+// is called warp-uniformly for every source-chain segment of the path, in
+// order.  All lanes return the same WalkOut.  With want_cov, also computes the
+// pinned coverage: ref counts never increase with depth along a root path, so
+// it is one binary search per chain.
+template <typename SegFn>
+__device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
+                                       bool want_cov, SegFn on_seg) {
     WalkOut o;
-    o.mlen = 0; o.last_full = -1; o.partial = -1; o.plen = 0; o.cov = 0; o.fnode = 0; o.npath = 0; o.unpinned = 0;
+    o.mlen = 0; o.last = -1; o.plen = 0; o.nseg = 0; o.cov = 0; o.unpinned = 0;
     int32_t node = 0, idx = 0;
-    bool pinrun = true;
+    bool pinrun = want_cov;
     while (idx < len) {
-        const int32_t c = h_find(t, node, __ldcs(rq + idx));
+        const int32_t c = h_find(t, node, rq[idx]);
         if (c < 0) break;
-        const int32_t cs = t.start[c];
-        const int32_t el = t.end[c] - cs;
-        const int32_t n = min(el, len - idx);
-        const int32_t k = 1 + warp_lcp(t.arena + t.src[c] + cs + 1, rq + idx + 1, n - 1, lane);
-        const int32_t r = t.ref[c];
+        const int64_t S = t.src[c];
+        const int32_t bound = min(len, t.slen[c]);
+        const int32_t k = 1 + warp_lcp(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane);
+        const int32_t D = idx + k;  // request == chain S on [idx, D)
+        const int32_t y = chain_lookup(t, S, idx, D - 1);
+        const int32_t e = t.end[y];
+        const int32_t b = min(D, e);
+        on_seg(S, idx, b, o.nseg);
+        o.nseg++;
         if (pinrun) {
-            if (r > 0) { o.cov = idx + k; o.fnode = c; } else pinrun = false;
+            // pinned coverage inside [idx, b): first node with ref == 0
+            if (t.ref[y] > 0) {
+                o.cov = b;
+            } else {
+                int32_t lo = idx, hi = b;  // first depth in an unpinned node
+                if (t.ref[t.pos[S + lo]] == 0) {
+                    hi = lo;
+                } else {
+                    while (hi - lo > 1) {
+                        const int32_t mid = (lo + hi) >> 1;
+                        if (t.ref[t.pos[S + mid]] > 0) lo = mid; else hi = mid;
+                    }
+                }
+                o.cov = t.start[t.pos[S + hi]];
+                pinrun = false;
+            }
         }
-        if (r == 0) o.unpinned += k;
-        if (lane == 0) {
-            if (stamp && t.la[c] != now) t.la[c] = now;
-            if (path) path[o.npath] = c;
-        }
-        o.npath++;
-        idx += k;
-        if (k < el) { o.partial = c; o.plen = k; break; }
-        o.last_full = c;
-        node = c;
+        o.last = y;
+        if (D < e) { o.plen = D - t.start[y]; idx = D; break; }  // diverged inside y (or request ended)
+        idx = e;
+        node = y;
     }
     o.mlen = idx;
+    if (want_cov) o.unpinned = o.mlen - o.cov;
     return o;
 }
 
+// warp_walk_cb storing the segments (lane 0) when segs != nullptr.
+__device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
+                                    Seg *segs, bool want_cov) {
+    return warp_walk_cb(t, rq, len, lane, want_cov, [&](int64_t S, int32_t a, int32_t b, int32_t i) {
+        if (lane == 0 && segs) { segs[i].S = S; segs[i].a = a; segs[i].b = b; }
+    });
+}
+
+// unpin (radix.py:180-185) of the cached root path arena[src : src+plen] by one
+// warp: every node on it loses one reference; nodes reaching zero release
+// their edge from pinned_tokens.  Warps unpinning different paths commute.
+__device__ inline void warp_unpin_path(const TrieView &t, int64_t src, int32_t plen, int lane) {
+    long long acc = 0;
+    bool under = false;
+    warp_walk_cb(t, t.arena + src, plen, lane, false, [&](int64_t S, int32_t a, int32_t b, int32_t) {
+        for (int32_t d = a + lane; d < b; d += 32) {
+            const int32_t n = t.pos[S + d];
+            if (t.start[n] != d) continue;
+            const int32_t old = atomicSub(&t.ref[n], 1);
+            if (old <= 0) under = true;
+            else if (old == 1) acc -= elen(t, n);
+        }
+    });
+    if (acc) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)acc);
+    if (under) t.sc->status = FS_ERR_UNDERFLOW;
+}
+
+// ---------------------------------------------------------------- path nodes
+// Call fn(node) once for every node of the path described by segs (each node
+// is visited at its first depth).  Block-parallel; segs must be visible.
+template <typename F>
+__device__ inline void block_path_nodes(const TrieView &t, const Seg *segs, int32_t nseg, F fn) {
+    for (int32_t s = 0; s < nseg; s++) {
+        const int64_t S = segs[s].S;
+        const int32_t a = segs[s].a, b = segs[s].b;
+        for (int32_t d = a + (int32_t)threadIdx.x; d < b; d += blockDim.x) {
+            const int32_t n = t.pos[S + d];
+            if (t.start[n] == d) fn(n);
+        }
+    }
+}
+
+// pos[S + d] = n for d in [a, b)
+__device__ inline void block_repoint(const TrieView &t, int64_t S, int32_t a, int32_t b, int32_t n) {
+    for (int32_t d = a + (int32_t)threadIdx.x; d < b; d += blockDim.x) t.pos[S + d] = n;
+}
+
+// pin / unpin of a whole path (radix.py:164-185): ref +-1 on every node;
+// pinned_tokens follows the 0 <-> 1 transitions.
+__device__ inline void block_pin_path(const TrieView &t, const Seg *segs, int32_t nseg, int delta) {
+    long long acc = 0;
+    bool under = false;
+    block_path_nodes(t, segs, nseg, [&](int32_t n) {
+        const int32_t old = atomicAdd(&t.ref[n], delta);
+        if (delta > 0 && old == 0) acc += elen(t, n);
+        if (delta < 0) {
+            if (old <= 0) under = true;
+            else if (old == 1) acc -= elen(t, n);
+        }
+    });
+    if (acc) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)acc);
+    if (under) t.sc->status = FS_ERR_UNDERFLOW;
+}
+
 // ---------------------------------------------------------------- eviction
-// RadixTree.evict_lru (radix.py:210-250) by one CTA.  The candidate set of the
-// reference (unprotected ref==0 leaves, parents re-added as they become leaves)
-// is exactly "every current evictable leaf", so each pop is a block-wide
-// argmin of (last_access, seq) over the node table; thread 0 detaches or
-// truncates the winner and appends the record.  Protect set = FS_PROTECT flag.
+// RadixTree.evict_lru (radix.py:210-250) by one CTA.  The reference's candidate
+// set (unprotected ref==0 leaves, parents re-added as they become leaves) is
+// exactly "every current evictable leaf", so each pop is a block-wide argmin
+// of (last_access, seq) over the node table; thread 0 detaches or truncates
+// the winner and appends the record.  Protect set = FS_PROTECT flag.
 struct EvictSmem {
     int64_t la[32];
     int64_t sq[32];
@@ -341,126 +444,160 @@ __device__ inline void block_evict(const TrieView &t, int64_t needed, EvictSmem 
 // ---------------------------------------------------------------- insert
 struct InsertSmem {
     EvictSmem ev;
-    int32_t np, mlen, new_len, deepest, last, status, cov, fnode;
+    int32_t nseg, mlen, new_len, deepest, last, status, cov, split_top;
     int64_t needed, unpinned;
     int64_t *prof;  // optional cycle counters: [1] walk, [2] evict, [5] evict pops
 };
 
-// RadixTree.insert (radix.py:128-162) by one CTA (warp 0 walks).  `path` is a
-// global scratch of >= len+2 entries.  Leaves in sm: mlen (idx before the new
-// leaf), unpinned/cov of the pre-insert walk (== probe()), deepest path node,
-// status (FS_ERR_CACHE_FULL after performing the evictions, like the reference).
+// RadixTree.insert (radix.py:128-162) by one CTA (warp 0 walks).  `segs` is a
+// global scratch of >= len+2 entries; on return it holds the whole path
+// (including the new leaf) so the caller can pin it.  Leaves in sm: mlen (the
+// match before the new leaf == probe()'s), unpinned/cov of that walk, deepest
+// path node, status (FS_ERR_CACHE_FULL after performing the evictions, like
+// the reference).
 __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now,
-                                    int32_t worker, int32_t *path, InsertSmem *sm) {
+                                    int32_t worker, Seg *segs, InsertSmem *sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t *rq = t.arena + req_off;
     const long long c0 = clock64();
     if (warp == 0) {
-        const WalkOut w = warp_walk(t, rq, len, lane, false, 0, path);
+        const WalkOut w = warp_walk(t, rq, len, lane, segs, true);
         if (lane == 0) {
-            int32_t np = w.npath;
-            int32_t last = np ? path[np - 1] : 0;
-            if (w.partial >= 0) {
-                const int32_t top = trie_split(t, w.partial, w.plen);
-                path[np - 1] = top;
+            int32_t last = w.last >= 0 ? w.last : 0;
+            sm->split_top = -1;
+            if (w.plen > 0) {
+                const int32_t top = trie_split(t, w.last, w.plen);
+                sm->split_top = top;
                 last = top;
             }
-            sm->np = np; sm->mlen = w.mlen; sm->unpinned = w.unpinned; sm->cov = w.cov; sm->fnode = w.fnode;
+            sm->nseg = w.nseg; sm->mlen = w.mlen; sm->unpinned = w.unpinned; sm->cov = w.cov;
             sm->new_len = len - w.mlen;
             sm->last = last;
             sm->status = t.sc->status;
             sm->needed = 0;
             const int64_t cap = t.sc->capacity;
             if (cap >= 0 && t.sc->used + sm->new_len > cap) {
-                for (int32_t i = 0; i < np; i++) t.flags[path[i]] |= FS_PROTECT;
+                // only the path's deepest node can be a leaf: every other path
+                // node has its path child below it (radix.py:149 protect=path)
+                if (last > 0) t.flags[last] |= FS_PROTECT;
                 sm->needed = t.sc->used + sm->new_len - cap;
             }
         }
     }
     __syncthreads();
+    if (sm->split_top >= 0)
+        block_repoint(t, t.src[sm->split_top], t.start[sm->split_top], t.end[sm->split_top], sm->split_top);
     const long long c1 = clock64();
     if (tid == 0 && sm->prof) sm->prof[1] += c1 - c0;
     if (sm->needed > 0) {
         block_evict(t, sm->needed, &sm->ev);
         if (tid == 0 && sm->prof) sm->prof[2] += clock64() - c1;
         if (tid == 0) {
-            for (int32_t i = 0; i < sm->np; i++) t.flags[path[i]] &= ~FS_PROTECT;
+            if (sm->last > 0) t.flags[sm->last] &= ~FS_PROTECT;
             if (t.sc->used + sm->new_len > t.sc->capacity) sm->status = FS_ERR_CACHE_FULL;
         }
         __syncthreads();
     }
     if (tid == 0) {
-        int32_t np = sm->np;
-        if (sm->status == FS_OK) {
-            if (sm->new_len > 0) {
-                const int32_t leaf = node_new(t, req_off, sm->mlen, len, sm->last);
-                if (leaf < 0) {
-                    sm->status = FS_ERR_NOMEM;
-                } else {
-                    h_put(t, sm->last, rq[sm->mlen], leaf);
-                    t.nchild[sm->last]++;
-                    t.sc->used += sm->new_len;
-                    path[np++] = leaf;
-                }
-            }
-            for (int32_t i = 0; i < np; i++) {
-                const int32_t n = path[i];
-                t.la[n] = now;
-                if (t.wmask && worker >= 0) {
-                    t.wmask[n] |= (1ull << worker);
-                    t.wtime[(int64_t)n * t.nw + worker] = now;
-                }
+        int32_t deepest = sm->mlen > 0 ? sm->last : -1;
+        if (sm->status == FS_OK && sm->new_len > 0) {
+            const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last);
+            if (leaf < 0) {
+                sm->status = FS_ERR_NOMEM;
+            } else {
+                h_put(t, sm->last, rq[sm->mlen], leaf);
+                t.nchild[sm->last]++;
+                t.sc->used += sm->new_len;
+                segs[sm->nseg].S = req_off; segs[sm->nseg].a = sm->mlen; segs[sm->nseg].b = len;
+                sm->nseg++;
+                deepest = leaf;
             }
         }
-        sm->np = np;
-        sm->deepest = np ? path[np - 1] : -1;
+        if (sm->status == FS_OK && deepest > 0) t.la[deepest] = now;  // stamps the whole path (lazy)
+        sm->deepest = deepest;
         if (sm->status != FS_OK && t.sc->status == FS_OK && sm->status != FS_ERR_CACHE_FULL) t.sc->status = sm->status;
+    }
+    __syncthreads();
+    if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0)
+        block_repoint(t, req_off, sm->mlen, len, sm->deepest);
+    __syncthreads();
+    if (sm->status == FS_OK && t.wmask && worker >= 0) {
+        // n.workers[worker] = now on every path node (radix.py:160-161)
+        block_path_nodes(t, segs, sm->nseg, [&](int32_t n) {
+            t.wmask[n] |= (1ull << worker);
+            t.wtime[(int64_t)n * t.nw + worker] = now;
+        });
+        __syncthreads();
+    }
+}
+
+// Segments of an existing root path arena[src : src+plen] (every node on it is
+// cached): the walk of the handle's own path.  Block-level (warp 0 walks).
+__device__ inline void block_path_of(const TrieView &t, int64_t src, int32_t plen, Seg *segs, int32_t *nseg_out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        const WalkOut w = warp_walk(t, t.arena + src, plen, lane, segs, false);
+        if (lane == 0) *nseg_out = w.nseg;
     }
     __syncthreads();
 }
 
 // ---------------------------------------------------------------- evict_notify
-// RadixTree.evict_notify + _prune_up (radix.py:254-302), single thread for the
-// structure edits, warp for the compares.  `scratch` holds >= 2*(plen+2) ints.
-__device__ inline void warp_evict_notify(const TrieView &t, const int32_t *pth, int32_t plen, int32_t worker,
-                                         int32_t keep, int64_t notice, int32_t *scratch) {
-    const int lane = threadIdx.x & 31;
-    int32_t *fnode = scratch;
-    int32_t *fstart = scratch + plen + 2;
-    int32_t nf = 0;
-    int32_t node = 0, idx = 0;
-    while (idx < plen) {
-        const int32_t c = h_find(t, node, pth[idx]);
-        if (c < 0) break;
-        const int32_t el = elen(t, c);
-        const int32_t n = min(el, plen - idx);
-        const int32_t k = 1 + warp_lcp(t.arena + t.src[c] + t.start[c] + 1, pth + idx + 1, n - 1, lane);
-        if (k < el) {
-            if (k > 0 && idx + k > keep) { fnode[nf] = c; fstart[nf] = idx; nf++; }
-            break;
-        }
-        fnode[nf] = c; fstart[nf] = idx; nf++;
-        idx += k;
-        node = c;
+// RadixTree.evict_notify + _prune_up (radix.py:254-302).  The nodes the
+// reference touches are the path nodes intersecting depths [keep, mlen) of the
+// walk of `pth`; they are collected in path order and edited by thread 0.
+struct NotifySmem {
+    int32_t nseg, mlen, nf;
+};
+
+__device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32_t plen, int32_t worker,
+                                          int32_t keep, int64_t notice, Seg *segs, int32_t *found,
+                                          NotifySmem *sm) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) {
+        const WalkOut w = warp_walk(t, t.arena + psrc, plen, lane, segs, false);
+        if (lane == 0) { sm->nseg = w.nseg; sm->mlen = w.mlen; sm->nf = 0; }
     }
-    __syncwarp();
-    if (lane == 0) {
+    __syncthreads();
+    const int32_t mlen = sm->mlen;
+    if (keep < mlen) {
+        // nodes covering a depth in [keep, mlen): the node holding `keep` (visited
+        // at depth keep) and every node starting inside the range
+        for (int32_t s = 0; s < sm->nseg; s++) {
+            const int64_t S = segs[s].S;
+            const int32_t a = max(segs[s].a, keep), b = segs[s].b;
+            for (int32_t d = a + tid; d < b; d += blockDim.x) {
+                const int32_t n = t.pos[S + d];
+                if (t.start[n] == d || d == keep) found[atomicAdd(&sm->nf, 1)] = n;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int32_t nf = sm->nf;
+        // path order == increasing start depth
+        for (int32_t i = 1; i < nf; i++) {
+            const int32_t x = found[i];
+            int32_t j = i - 1;
+            while (j >= 0 && t.start[found[j]] > t.start[x]) { found[j + 1] = found[j]; j--; }
+            found[j + 1] = x;
+        }
         int32_t nt = 0;
-        int32_t *touched = fstart;  // reuse: entry i consumed before slot i is written
         for (int32_t i = 0; i < nf; i++) {
-            const int32_t nd = fnode[i];
-            const int32_t s = fstart[i];
-            const int32_t e = s + elen(t, nd);
-            if (e <= keep) continue;
-            if (s < keep) trie_split(t, nd, keep - s);  // top survives with the tag
+            const int32_t nd = found[i];
+            const int32_t s = t.start[nd];
+            if (s < keep) {
+                const int32_t top = trie_split(t, nd, keep - s);  // top survives with the tag
+                if (top >= 0) for (int32_t d = t.start[top]; d < t.end[top]; d++) t.pos[t.src[top] + d] = top;
+            }
             if (worker >= 0 && worker < 64 && ((t.wmask[nd] >> worker) & 1ull) &&
                 t.wtime[(int64_t)nd * t.nw + worker] <= notice) {
                 t.wmask[nd] &= ~(1ull << worker);
-                touched[nt++] = nd;
+                found[nt++] = nd;  // touched (slot i already consumed)
             }
         }
         for (int32_t i = 0; i < nt; i++) {
-            int32_t n = touched[i];
+            int32_t n = found[i];
             while (n > 0 && t.nchild[n] == 0 && t.wmask[n] == 0 && t.ref[n] == 0) {
                 const int32_t P = t.parent[n];
                 if (P < 0) break;
@@ -469,5 +606,5 @@ __device__ inline void warp_evict_notify(const TrieView &t, const int32_t *pth, 
             }
         }
     }
-    __syncwarp();
+    __syncthreads();
 }

@@ -1,13 +1,15 @@
 // fs_kernels.cuh -- kernels of the decision path.
 //
 //   K1  k_match      warp-per-request longest-prefix match of the whole queue
-//                    against the device trie, stamping last_access, emitting
-//                    (mlen, pinned coverage, frontier node, next token).
-//   K2  (CUB radix sort of the 14-16-bit (L - mlen) key, stable => ties stay in
-//        (arrival, rid) label order the queue is kept in)
+//                    against the device trie (chain-jumping walk), stamping
+//                    last_access, emitting (mlen key, pinned coverage B, the
+//                    token after B).
+//   K2  (CUB radix sort of the 13-16-bit (L - mlen) key, stable => ties stay in
+//        the (arrival, rid) label order the queue is kept in)
 //   K3+K4 k_schedule one persistent CTA: deficit-gated first-admissible search
 //                    with the closed-form refill and budget test, and each
 //                    admission's radix insert / split / LRU evict / pin.
+//   k_unpin_many     batch completion: warp per finished path.
 //   k_op / k_dispatch single-CTA tree operations and D2LPM dispatch chains.
 #pragma once
 #include "fs_device.cuh"
@@ -23,8 +25,7 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
                                                int64_t now, int stamp, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
-                                               int32_t *__restrict__ out_cov, int32_t *__restrict__ out_fnode,
-                                               int32_t *__restrict__ out_next,
+                                               int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
                                                unsigned long long *__restrict__ alg_tokens) {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -32,40 +33,33 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
     const int32_t r = ids[i];
     const int32_t len = rlen[r];
     const int32_t *rq = t.arena + roff[r];
-    const WalkOut w = warp_walk(t, rq, len, lane, stamp != 0, now, nullptr);
+    const WalkOut w = warp_walk(t, rq, len, lane, nullptr, true);
     if (lane == 0) {
+        // match_prefix stamps every matched node (radix.py:86-90): lazily, at the deepest
+        if (stamp && w.last > 0 && t.la[w.last] != now) t.la[w.last] = now;
         if (out_key) out_key[i] = kmax - (uint32_t)w.mlen;
         if (out_mlen) out_mlen[i] = w.mlen;
         if (out_cov) out_cov[i] = w.cov;
-        if (out_fnode) out_fnode[i] = w.fnode;
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
         // request tokens a match must read: min(mlen+1, len)
         if (alg_tokens) {
             atomicAdd(alg_tokens, (unsigned long long)min(w.mlen + 1, len));
-            atomicAdd(alg_tokens + 1, (unsigned long long)w.npath);  // trie hops
+            atomicAdd(alg_tokens + 1, (unsigned long long)w.nseg);  // source chains crossed
         }
     }
 }
 
-// Finish of a batch: unpin every finished path (worker.py:209-213).  The
-// decrements commute, so each path's chain is walked by its own thread with
-// atomics; a node whose count reaches zero releases its edge from
-// pinned_tokens exactly once (radix.py:180-185).  Underflow is reported.
+// Batch completion: unpin every finished path (worker.py:209-213), one warp
+// per path.  The decrements commute; each node releases its edge from
+// pinned_tokens when its count reaches zero (radix.py:180-185).
 __global__ void k_unpin_many(TrieView t, const int32_t *__restrict__ nodes, int64_t n, int64_t *out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        int32_t nd = nodes[i];
-        long long freed = 0;
-        bool under = false;
-        while (nd > 0) {
-            const int32_t old = atomicSub(&t.ref[nd], 1);
-            if (old <= 0) { under = true; break; }
-            if (old == 1) freed += elen(t, nd);
-            nd = t.parent[nd];
-        }
-        if (freed) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)(-freed));
-        if (under) { t.sc->status = FS_ERR_UNDERFLOW; out[0] = FS_ERR_UNDERFLOW; }
-    }
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int32_t nd = nodes[i];
+    if (nd <= 0) return;
+    warp_unpin_path(t, t.src[nd], t.end[nd], lane);
+    if (lane == 0 && t.sc->status == FS_ERR_UNDERFLOW) out[0] = FS_ERR_UNDERFLOW;
 }
 
 // ---------------------------------------------------------------- queue upkeep
@@ -90,17 +84,15 @@ __global__ void k_merge(const int32_t *__restrict__ a, int32_t na, const int32_t
 
 // Gather per-sorted-position scheduler slots: {client, cov, next token, state}.
 __global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__restrict__ queue, int32_t n,
-                         const int32_t *__restrict__ cov, const int32_t *__restrict__ fnode,
-                         const int32_t *__restrict__ next, const int32_t *__restrict__ rclient,
-                         const int32_t *__restrict__ rlen, int32_t *__restrict__ s_req, int4 *__restrict__ slot,
-                         int32_t *__restrict__ s_len, int32_t *__restrict__ s_fnode) {
+                         const int32_t *__restrict__ cov, const int32_t *__restrict__ next,
+                         const int32_t *__restrict__ rclient, const int32_t *__restrict__ rlen,
+                         int32_t *__restrict__ s_req, int4 *__restrict__ slot, int32_t *__restrict__ s_len) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int32_t qi = perm[p];
     const int32_t r = queue[qi];
     s_req[p] = r;
     s_len[p] = rlen[r];
-    s_fnode[p] = fnode[qi];
     slot[p] = make_int4(rclient[r], cov[qi], next[qi], 0);
 }
 
@@ -111,7 +103,6 @@ struct FillArgs {
     const int32_t *s_req;
     int4 *slot;  // {client, cov(B), next token, state: >=0 pending w/ exact-epoch, -1 admitted}
     const int32_t *s_len;
-    int32_t *s_fnode;
     const int64_t *roff;
     int64_t *q, *refills;
     const uint8_t *known;
@@ -122,12 +113,12 @@ struct FillArgs {
     int32_t ndl;
     int64_t M, R, gen_total, headroom0, w_e, quantum, now;
     int32_t lpm;
-    int32_t *path;
+    Seg *segs;
     int32_t *adm_req, *adm_mlen, *adm_node;
     int64_t *adm_unp, *adm_pinb, *adm_rec_end;
     int32_t adm_cap;
     int8_t *rstate;
-    int64_t *hdr;  // [n_adm, n_rec, status, epochs, refill_events, resumes]
+    int64_t *hdr;  // [n_adm, n_rec, status, epochs, refill_events, resumes, -, -, prof[8]]
 };
 
 struct SchedSmem {
@@ -141,7 +132,7 @@ struct SchedSmem {
     int32_t cursor, progress, epoch, npos, nadm, stop, j;
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
-    int64_t prof[8];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops
+    int64_t prof[8];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops, [6] chains
 };
 
 __device__ __forceinline__ int64_t sched_slack(const FillArgs &a, int64_t headroom) {
@@ -203,51 +194,25 @@ __device__ inline int64_t block_min_i64(int64_t v, int64_t *red) {
     return red[0];
 }
 
-// Exact pinned coverage B of a queued request, resumed from its cached frontier
-// (node holding depth B).  Pinned nodes are never freed or truncated inside a
-// fill, and a split only moves a node's start deeper, so climbing parents until
-// start < B finds the node that now holds depth B.  One warp.
+// Exact pinned coverage B of a queued request (re-walk; only reached through
+// the filter in block_find).  One warp.
 __device__ inline void warp_resume(const FillArgs &a, int32_t p, int lane) {
-    const TrieView &t = a.t;
     const int32_t r = a.s_req[p];
     const int32_t len = a.s_len[p];
-    const int32_t *rq = t.arena + a.roff[r];
-    const int32_t B = a.slot[p].y;
-    int32_t N = a.s_fnode[p];
-    while (N != 0 && t.start[N] >= B) N = t.parent[N];
-    int32_t idx = B;
-    bool boundary = true;
-    if (N != 0 && idx < t.end[N]) {
-        const int32_t n = min(t.end[N] - idx, len - idx);
-        const int32_t k = warp_lcp(t.arena + t.src[N] + idx, rq + idx, n, lane);
-        idx += k;
-        boundary = (idx == t.end[N]);
-    }
-    if (boundary) {
-        while (idx < len) {
-            const int32_t c = h_find(t, N, rq[idx]);
-            if (c < 0 || t.ref[c] == 0) break;
-            const int32_t el = elen(t, c);
-            const int32_t n = min(el, len - idx);
-            const int32_t k = 1 + warp_lcp(t.arena + t.src[c] + t.start[c] + 1, rq + idx + 1, n - 1, lane);
-            idx += k;
-            N = c;
-            if (k < el) break;
-        }
-    }
+    const int32_t *rq = a.t.arena + a.roff[r];
+    const WalkOut w = warp_walk(a.t, rq, len, lane, nullptr, true);
     if (lane == 0) {
-        a.slot[p].y = idx;
-        a.slot[p].z = idx < len ? rq[idx] : -1;
-        a.s_fnode[p] = N;
+        a.slot[p].y = w.cov;
+        a.slot[p].z = w.cov < len ? rq[w.cov] : -1;
     }
 }
 
 // First sorted position p in [from, until) that is pending and, unless
 // any_mode, passes the deficit gate (q > 0, skipped for LPM) and the budget
-// test len - B <= slack with B exact.  Stale B values (an admission happened
-// after B was last exact) are refreshed only when an admission since then had
-// the same pinned coverage and the same next token -- the only way LCP(r, a)
-// can exceed B ("exact budget test").
+// test len - B <= slack with B exact.  B only grows inside a fill, and an
+// admission `e` can raise B_p only if B_p == B_e and the request's token at
+// B_p equals the admitted one's (LCP(r_p, r_e) > B_p forces both), so a stale
+// B is re-walked only when such an admission happened since it was exact.
 __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t until, bool any_mode,
                               int64_t slack) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -325,8 +290,9 @@ __device__ void block_refill(const FillArgs &a, SchedSmem *sm) {
     __syncthreads();
 }
 
-// Worker.try_admit (worker.py:112-135) minus host bookkeeping, then the
-// policy's charge (local_policies.py:124).
+// Worker.try_admit (worker.py:112-135) minus host bookkeeping -- probe,
+// insert, pin (radix.py:187-192) -- then the policy's charge
+// (local_policies.py:124).
 __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t slack) {
     const int tid = threadIdx.x;
     const TrieView &t = a.t;
@@ -336,19 +302,22 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int64_t pinb;
     if (tid == 0) pinb = t.sc->pinned;
     __syncthreads();
-    block_insert(t, off, len, a.now, -1, a.path, &sm->ins);
+    block_insert(t, off, len, a.now, -1, a.segs, &sm->ins);
     const long long ct = clock64();
+    if (sm->ins.status == FS_OK) {
+        block_pin_path(t, a.segs, sm->ins.nseg, +1);
+        __syncthreads();
+    }
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
         if (in.status != FS_OK) {
             a.hdr[2] = in.status;
             sm->stop = 1;
         } else {
-            pin_chain(t, in.deepest);
             const int32_t mlen = in.mlen;
             const int32_t cov = in.cov;
             const int64_t need = len - cov;
-            if (need > slack || in.unpinned != (int64_t)(mlen - cov)) {
+            if (need > slack || in.unpinned != (int64_t)(mlen - cov) || t.sc->pinned != pinb + need) {
                 a.hdr[2] = FS_ERR_INTERNAL;  // closed-form budget test disagrees with can_add
                 sm->stop = 1;
             }
@@ -380,7 +349,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
         }
         sm->prof[3] += clock64() - ct;
-        sm->prof[6] += sm->ins.np;
+        sm->prof[6] += sm->ins.nseg;
     }
     __syncthreads();
 }
@@ -470,12 +439,15 @@ struct OpArgs {
     int64_t needed;
     int32_t keep;
     int64_t notice;
-    int32_t *path;
+    Seg *segs;
+    int32_t *found;
     int64_t *out;  // [status, mlen/new_len, deepest, mask, nrec]
 };
 
 __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     __shared__ InsertSmem ins;
+    __shared__ NotifySmem nsm;
+    __shared__ int32_t s_nseg;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;
     if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.ev.pops = 0; }
@@ -483,24 +455,24 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     const int32_t *rq = t.arena + a.req_off;
     switch (a.op) {
         case OP_INSERT:
-            block_insert(t, a.req_off, a.len, a.now, a.worker, a.path, &ins);
+            block_insert(t, a.req_off, a.len, a.now, a.worker, a.segs, &ins);
             if (tid == 0) { a.out[0] = ins.status; a.out[1] = ins.new_len; a.out[2] = ins.deepest; }
             break;
-        case OP_ADMIT: {
+        case OP_ADMIT:
             // probe (radix.py:189) -> insert -> pin; the probe's mlen equals the
-            // insert walk's idx (nothing changes between them)
-            block_insert(t, a.req_off, a.len, a.now, -1, a.path, &ins);
-            if (tid == 0) {
-                a.out[0] = ins.status; a.out[1] = ins.mlen; a.out[2] = ins.deepest;
-                if (ins.status == FS_OK) pin_chain(t, ins.deepest);
-            }
+            // insert walk's (nothing changes between them)
+            block_insert(t, a.req_off, a.len, a.now, -1, a.segs, &ins);
+            if (ins.status == FS_OK) block_pin_path(t, a.segs, ins.nseg, +1);
+            __syncthreads();
+            if (tid == 0) { a.out[0] = ins.status; a.out[1] = ins.mlen; a.out[2] = ins.deepest; }
             break;
-        }
         case OP_PIN:
-            if (tid == 0) { pin_chain(t, a.node); a.out[0] = t.sc->status; }
-            break;
         case OP_UNPIN:
-            if (tid == 0) { unpin_chain(t, a.node); a.out[0] = t.sc->status; }
+            // _chain from the deepest node (radix.py:164-172) == the nodes of its root path
+            block_path_of(t, t.src[a.node], t.end[a.node], a.segs, &s_nseg);
+            block_pin_path(t, a.segs, s_nseg, a.op == OP_PIN ? +1 : -1);
+            __syncthreads();
+            if (tid == 0) a.out[0] = t.sc->status;
             break;
         case OP_EVICT:
             block_evict(t, a.needed, &ins.ev);
@@ -508,17 +480,19 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
             break;
         case OP_LMW:
             if (warp == 0) {
-                const WalkOut w = warp_walk(t, rq, a.len, lane, true, a.now, nullptr);
+                const WalkOut w = warp_walk(t, rq, a.len, lane, nullptr, false);
                 if (lane == 0) {
-                    const int32_t deepest = w.plen > 0 ? w.partial : w.last_full;
+                    // deepest = partial or last full node (radix.py:104); stamps the path
+                    const int32_t deepest = w.mlen > 0 ? w.last : -1;
+                    if (deepest > 0) t.la[deepest] = a.now;
                     a.out[0] = FS_OK;
-                    a.out[1] = deepest >= 0 ? w.mlen : 0;
-                    a.out[3] = (deepest >= 0 && t.wmask) ? (int64_t)t.wmask[deepest] : 0;
+                    a.out[1] = deepest > 0 ? w.mlen : 0;
+                    a.out[3] = (deepest > 0 && t.wmask) ? (int64_t)t.wmask[deepest] : 0;
                 }
             }
             break;
         case OP_NOTIFY:
-            if (warp == 0) warp_evict_notify(t, rq, a.len, a.worker, a.keep, a.notice, a.path);
+            block_evict_notify(t, a.req_off, a.len, a.worker, a.keep, a.notice, a.segs, a.found, &nsm);
             if (tid == 0) a.out[0] = t.sc->status;
             break;
     }
@@ -539,19 +513,44 @@ struct DispArgs {
     uint8_t *qset;
     int64_t *qsize;
     int64_t quantum, w_e;
-    const int32_t *dl_idx;  // pending on_finish deltas: q index, q delta, worker
+    const int32_t *dl_idx;  // pending host-side updates (see k_dispatch)
     const int64_t *dl_q;
     const int32_t *dl_w;
     int32_t ndl;
-    int32_t *path;
+    Seg *segs;
     int32_t *out_w, *out_mlen;
     uint64_t *out_mask;
     int64_t *out_rounds;
     int64_t *hdr;
 };
 
+// D2lpm.select_worker (global_policies.py:107-114) + Dispatcher._min_queue
+// (57-58).  The refill loop adds Q_w to every worker per round: k rounds in
+// closed form.  Returns the worker; *rounds = refill rounds.
+__device__ inline int d2_select(const DispArgs &a, int32_t c, uint64_t mask, int64_t *rounds) {
+    int64_t *qr = a.q + (int64_t)c * a.D;
+    uint8_t *qs = a.qset + (int64_t)c * a.D;
+    bool any = false;
+    for (int w2 = 0; w2 < a.D; w2++) any |= qr[w2] > 0;
+    *rounds = 0;
+    if (!any) {
+        int64_t k = INT64_MAX;
+        for (int w2 = 0; w2 < a.D; w2++) k = min(k, (-qr[w2]) / a.quantum + 1);
+        for (int w2 = 0; w2 < a.D; w2++) { qr[w2] += k * a.quantum; qs[w2] = 1; }
+        *rounds = k;
+    }
+    int best = -1;
+    for (int pass = 0; pass < 2 && best < 0; pass++)
+        for (int w2 = 0; w2 < a.D; w2++) {
+            if (!(qr[w2] > 0)) continue;
+            if (pass == 0 && !((mask >> w2) & 1ull)) continue;
+            if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;
+        }
+    return best;
+}
+
 // Dispatcher.dispatch for a chain of arrivals (global_policies.py:40-46,
-// 107-124): every arrival's match sees the inserts of the ones before it.
+// 116-124): every arrival's match sees the inserts of the ones before it.
 __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
     __shared__ InsertSmem ins;
     __shared__ int32_t s_w;
@@ -573,27 +572,8 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
     __syncthreads();
     if (a.select_only) {
         if (tid == 0 && a.n > 0) {
-            const int32_t c = a.clients[0];
-            const uint64_t mask = a.out_mask[0];
-            int64_t *qr = a.q + (int64_t)c * a.D;
-            uint8_t *qs = a.qset + (int64_t)c * a.D;
-            bool any = false;
-            for (int w2 = 0; w2 < a.D; w2++) any |= qr[w2] > 0;
-            int64_t rounds = 0;
-            if (!any) {
-                int64_t k = INT64_MAX;
-                for (int w2 = 0; w2 < a.D; w2++) k = min(k, (-qr[w2]) / a.quantum + 1);
-                for (int w2 = 0; w2 < a.D; w2++) { qr[w2] += k * a.quantum; qs[w2] = 1; }
-                rounds = k;
-            }
-            int best = -1;
-            for (int pass = 0; pass < 2 && best < 0; pass++)
-                for (int w2 = 0; w2 < a.D; w2++) {
-                    if (!(qr[w2] > 0)) continue;
-                    if (pass == 0 && !((mask >> w2) & 1ull)) continue;
-                    if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;
-                }
-            a.out_w[0] = best;
+            int64_t rounds;
+            a.out_w[0] = d2_select(a, a.clients[0], a.out_mask[0], &rounds);
             a.out_rounds[0] = rounds;
             a.hdr[0] = FS_OK;
         }
@@ -606,41 +586,23 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
         const int64_t now = a.nows[i];
         if (warp == 0) {
             // RadixTree.longest_match_workers (radix.py:101-110)
-            const WalkOut w = warp_walk(t, t.arena + off, len, lane, true, now, nullptr);
+            const WalkOut w = warp_walk(t, t.arena + off, len, lane, nullptr, false);
             if (lane == 0) {
-                const int32_t deepest = w.plen > 0 ? w.partial : w.last_full;
-                const uint64_t mask = deepest >= 0 ? t.wmask[deepest] : 0ull;
-                const int32_t c = a.clients[i];
-                int64_t *qr = a.q + (int64_t)c * a.D;
-                uint8_t *qs = a.qset + (int64_t)c * a.D;
-                // D2lpm.select_worker (global_policies.py:107-114); the refill
-                // loop adds Q_w to every worker per round: k rounds in closed form
-                bool any = false;
-                for (int w2 = 0; w2 < a.D; w2++) any |= qr[w2] > 0;
-                int64_t rounds = 0;
-                if (!any) {
-                    int64_t k = INT64_MAX;
-                    for (int w2 = 0; w2 < a.D; w2++) k = min(k, (-qr[w2]) / a.quantum + 1);
-                    for (int w2 = 0; w2 < a.D; w2++) { qr[w2] += k * a.quantum; qs[w2] = 1; }
-                    rounds = k;
-                }
-                int best = -1;
-                for (int pass = 0; pass < 2 && best < 0; pass++) {
-                    for (int w2 = 0; w2 < a.D; w2++) {
-                        if (!(qr[w2] > 0)) continue;
-                        if (pass == 0 && !((mask >> w2) & 1ull)) continue;
-                        if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;  // _min_queue
-                    }
-                }
+                const int32_t deepest = w.mlen > 0 ? w.last : -1;
+                if (deepest > 0) t.la[deepest] = now;
+                const uint64_t mask = deepest > 0 ? t.wmask[deepest] : 0ull;
+                int64_t rounds;
+                const int best = d2_select(a, a.clients[i], mask, &rounds);
+                int64_t *qr = a.q + (int64_t)a.clients[i] * a.D;
                 a.qsize[best] += 1;
                 qr[best] -= a.w_e * (int64_t)len;  // after_dispatch: full input (global_policies.py:123)
-                qs[best] = 1;
-                s_w = best; s_mlen = deepest >= 0 ? w.mlen : 0; s_mask = mask;
+                a.qset[(int64_t)a.clients[i] * a.D + best] = 1;
+                s_w = best; s_mlen = deepest > 0 ? w.mlen : 0; s_mask = mask;
                 a.out_rounds[i] = rounds;
             }
         }
         __syncthreads();
-        block_insert(t, off, len, now, s_w, a.path, &ins);
+        block_insert(t, off, len, now, s_w, a.segs, &ins);
         if (tid == 0) {
             a.out_w[i] = s_w;
             a.out_mlen[i] = s_mlen;

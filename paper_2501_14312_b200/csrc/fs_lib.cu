@@ -270,14 +270,15 @@ struct fs_trie {
     int32_t ncap = 0;
     uint32_t hsize = 0;
     DBuf<int64_t> src, la, seq;
-    DBuf<int32_t> start, end, parent, nchild, ref, first, freest;
+    DBuf<int32_t> start, end, slen, parent, nchild, ref, first, freest;
     DBuf<uint8_t> flags;
     DBuf<uint64_t> wmask;
     DBuf<int64_t> wtime;
-    DBuf<uint64_t> hkeys;
-    DBuf<int32_t> hvals;
+    DBuf<ulonglong2> hslot;
     DBuf<TrieScalars> sc;
-    DBuf<int32_t> path;  // walk scratch
+    DBuf<int32_t> pos;   // position shadow over the context arena
+    DBuf<Seg> segs;      // walk scratch: path segments
+    DBuf<int32_t> found; // evict_notify scratch
     DBuf<int64_t> rsrc;
     DBuf<int32_t> rlen, rkeep;
     DBuf<int64_t> opout;
@@ -288,13 +289,14 @@ struct fs_trie {
 static TrieView view(fs_trie *t) {
     TrieView v;
     v.arena = t->ctx->arena.p;
-    v.src = t->src.p; v.start = t->start.p; v.end = t->end.p; v.parent = t->parent.p;
+    v.pos = t->pos.p;
+    v.src = t->src.p; v.start = t->start.p; v.end = t->end.p; v.slen = t->slen.p; v.parent = t->parent.p;
     v.nchild = t->nchild.p; v.ref = t->ref.p; v.first = t->first.p;
     v.la = t->la.p; v.seq = t->seq.p; v.flags = t->flags.p;
     v.wmask = t->track ? t->wmask.p : nullptr;
     v.wtime = t->track ? t->wtime.p : nullptr;
     v.nw = t->nw;
-    v.hkeys = t->hkeys.p; v.hvals = t->hvals.p; v.hmask = t->hsize - 1;
+    v.hslot = t->hslot.p; v.hmask = t->hsize - 1;
     v.freest = t->freest.p; v.ncap = t->ncap;
     v.sc = t->sc.p;
     v.rsrc = t->rsrc.p; v.rlen = t->rlen.p; v.rkeep = t->rkeep.p; v.rcap = t->rsrc.cap;
@@ -306,7 +308,7 @@ __global__ void k_trie_init(TrieView t, int64_t capacity) {
         TrieScalars &s = *t.sc;
         s.used = 0; s.pinned = 0; s.next_seq = 1; s.capacity = capacity; s.nrec = 0;
         s.hw = 1; s.nfree = 0; s.status = 0; s.live = 1;
-        t.src[0] = 0; t.start[0] = 0; t.end[0] = 0; t.parent[0] = -1; t.nchild[0] = 0; t.ref[0] = 0;
+        t.src[0] = 0; t.start[0] = 0; t.end[0] = 0; t.slen[0] = 0; t.parent[0] = -1; t.nchild[0] = 0; t.ref[0] = 0;
         t.la[0] = 0; t.seq[0] = 0; t.first[0] = -1; t.flags[0] = FS_ALIVE;
         if (t.wmask) t.wmask[0] = 0;
     }
@@ -320,8 +322,8 @@ __global__ void k_rehash(TrieView t) {
         const uint64_t key = fs_hkey(t.parent[n], t.first[n]);
         uint32_t i = fs_hmix(key) & t.hmask;
         while (true) {
-            const unsigned long long prev = atomicCAS((unsigned long long *)&t.hkeys[i], FS_HEMPTY, key);
-            if (prev == FS_HEMPTY) { t.hvals[i] = n; break; }
+            const unsigned long long prev = atomicCAS(&t.hslot[i].x, FS_HEMPTY, key);
+            if (prev == FS_HEMPTY) { t.hslot[i].y = (unsigned long long)(uint32_t)n; break; }
             i = (i + 1) & t.hmask;
         }
     }
@@ -336,7 +338,14 @@ static uint32_t pow2_at_least(int64_t x) {
 // Make room for `extra_nodes` more nodes and paths of length `max_len`.
 static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
     cudaStream_t s = t->ctx->stream;
-    TRY(dgrow(t->path, 2 * (int64_t)max_len + 16, s));
+    TRY(dgrow(t->segs, (int64_t)max_len + 16, s));
+    TRY(dgrow(t->found, (int64_t)max_len + 16, s));
+    // the position shadow covers the whole arena (grown with it; -1 = never written)
+    if (t->pos.cap < t->ctx->arena.cap) {
+        const int64_t old = t->pos.cap;
+        TRY(dgrow(t->pos, t->ctx->arena.cap, s, true, old));
+        CK(cudaMemsetAsync(t->pos.p + old, 0xff, sizeof(int32_t) * (t->pos.cap - old), s));
+    }
     const int64_t need = (int64_t)t->h_sc.hw + extra_nodes + 4;
     if (need <= t->ncap) return FS_OK;
     const int64_t old = t->ncap;
@@ -344,16 +353,17 @@ static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
     const int64_t keep = old;
     TRY(dgrow(t->src, nc, s, true, keep)); TRY(dgrow(t->la, nc, s, true, keep)); TRY(dgrow(t->seq, nc, s, true, keep));
     TRY(dgrow(t->start, nc, s, true, keep)); TRY(dgrow(t->end, nc, s, true, keep)); TRY(dgrow(t->parent, nc, s, true, keep));
+    TRY(dgrow(t->slen, nc, s, true, keep));
     TRY(dgrow(t->nchild, nc, s, true, keep)); TRY(dgrow(t->ref, nc, s, true, keep)); TRY(dgrow(t->first, nc, s, true, keep));
     TRY(dgrow(t->freest, nc, s, true, keep)); TRY(dgrow(t->flags, nc, s, true, keep));
     if (t->track) { TRY(dgrow(t->wmask, nc, s, true, keep)); TRY(dgrow(t->wtime, nc * t->nw, s, true, keep * t->nw)); }
     t->ncap = (int32_t)std::min<int64_t>(nc, t->src.cap);
     const uint32_t hs = pow2_at_least(2 * (int64_t)t->ncap);
     if (hs != t->hsize) {
-        t->hkeys.release(); t->hvals.release();
-        TRY(dgrow(t->hkeys, hs, s)); TRY(dgrow(t->hvals, hs, s));
+        t->hslot.release();
+        TRY(dgrow(t->hslot, hs, s));
         t->hsize = hs;
-        CK(cudaMemsetAsync(t->hkeys.p, 0xff, sizeof(uint64_t) * hs, s));
+        CK(cudaMemsetAsync(t->hslot.p, 0xff, sizeof(ulonglong2) * hs, s));
         if (old > 0) { k_rehash<<<148, 256, 0, s>>>(view(t)); counted(); }
         CK(cudaGetLastError());
     }
@@ -399,8 +409,9 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     cudaStreamSynchronize(t->ctx->stream);
     t->src.release(); t->la.release(); t->seq.release(); t->start.release(); t->end.release();
     t->parent.release(); t->nchild.release(); t->ref.release(); t->first.release(); t->freest.release();
-    t->flags.release(); t->wmask.release(); t->wtime.release(); t->hkeys.release(); t->hvals.release();
-    t->sc.release(); t->path.release(); t->rsrc.release(); t->rlen.release(); t->rkeep.release();
+    t->flags.release(); t->wmask.release(); t->wtime.release(); t->hslot.release(); t->slen.release();
+    t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
+    t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
     delete t;
     return FS_OK;
@@ -428,11 +439,12 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     for (int64_t i = 0; i < n; i++)
         if (req_ids[i] < 0 || req_ids[i] >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id");
     static thread_local fs_scratch_match sm;
+    TRY(trie_reserve(t, 0, c->max_len));
     TRY(dgrow(sm.ids, n, c->stream)); TRY(dgrow(sm.mlen, n, c->stream)); TRY(dgrow(sm.cov, n, c->stream));
     CK(cudaMemcpyAsync(sm.ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
     const int64_t blocks = (n * 32 + 255) / 256;
     k_match<<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
-                                                      stamp, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr, nullptr);
+                                                      stamp, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr);
     counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -471,7 +483,8 @@ extern "C" int fs_trie_read_records(fs_trie *t, int64_t first, int64_t n, int64_
 static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     fs_ctx *c = t->ctx;
     a.t = view(t);
-    a.path = t->path.p;
+    a.segs = t->segs.p;
+    a.found = t->found.p;
     a.out = t->opout.p;
     k_op<<<1, 256, 0, c->stream>>>(a);
     counted();
@@ -531,6 +544,7 @@ static int pin_op(fs_trie *t, int32_t node, int op) {
     TRY(ctx_use(t->ctx));
     if (node < 0) return FS_OK;  // empty path
     if (node >= t->h_sc.hw) return fail(FS_ERR_INVALID, "bad path handle %d", node);
+    TRY(trie_reserve(t, 0, t->ctx->max_len));
     OpArgs a{};
     a.op = op; a.node = node;
     int64_t o[5];
@@ -553,7 +567,7 @@ extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
     TRY(dgrow(dn, n, s));
     CK(cudaMemcpyAsync(dn.p, nodes, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(t->opout.p, 0, sizeof(int64_t), s));
-    k_unpin_many<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(view(t), dn.p, n, t->opout.p);
+    k_unpin_many<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(view(t), dn.p, n, t->opout.p);
     counted();
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -578,6 +592,7 @@ extern "C" int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs) {
 extern "C" int fs_trie_longest_match_workers(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, uint64_t *mask) {
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
+    TRY(trie_reserve(t, 0, t->ctx->max_len));
     OpArgs a{};
     a.op = OP_LMW; a.req_off = t->ctx->h_roff[req]; a.len = t->ctx->h_rlen[req]; a.now = now;
     int64_t o[5];
@@ -616,9 +631,24 @@ extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src,
         if (end) CK(cudaMemcpyAsync(end, t->end.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
         if (parent) CK(cudaMemcpyAsync(parent, t->parent.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
         if (ref) CK(cudaMemcpyAsync(ref, t->ref.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
-        if (last_access) CK(cudaMemcpyAsync(last_access, t->la.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
         if (wmask && t->track) CK(cudaMemcpyAsync(wmask, t->wmask.p, sizeof(uint64_t) * k, cudaMemcpyDeviceToHost, s));
         if (wmask && !t->track) std::memset(wmask, 0, sizeof(uint64_t) * k);
+    }
+    if (last_access && k > 0) {
+        // device la holds the stamps of paths ending at each node; the
+        // reference's last_access is the maximum over the node's subtree
+        std::vector<int64_t> la(hw);
+        std::vector<int32_t> par(hw), dep(hw);
+        CK(cudaMemcpyAsync(la.data(), t->la.p, sizeof(int64_t) * hw, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(par.data(), t->parent.p, sizeof(int32_t) * hw, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(dep.data(), t->end.p, sizeof(int32_t) * hw, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<int32_t> order;
+        for (int32_t i = 1; i < hw; i++) if (par[i] >= 0) order.push_back(i);
+        std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return dep[a] > dep[b]; });
+        for (int32_t i : order)
+            if (par[i] > 0 && la[i] > la[par[i]]) la[par[i]] = la[i];
+        std::memcpy(last_access, la.data(), sizeof(int64_t) * k);
     }
     CK(cudaStreamSynchronize(s));
     return FS_OK;
@@ -954,7 +984,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     if (n > 0) {
         const int64_t blocks = (n * 32 + 255) / 256;
         k_match<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
-                                                  kmax, w->keys.p, nullptr, w->cov.p, w->fnode.p, w->next.p,
+                                                  kmax, w->keys.p, nullptr, w->cov.p, w->next.p,
                                                   (unsigned long long *)w->alg.p);
         counted();
         CK(cudaGetLastError());
@@ -965,9 +995,9 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         size_t b = w->cub_tmp.cap;
         CK(cub::DeviceRadixSort::SortPairs(w->cub_tmp.p, b, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)n, 0, (int)bits, s));
         counted(FS_CUB_SORT_LAUNCHES);
-        k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p, w->fnode.p,
+        k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p,
                                                             w->next.p, c->rclient.p, c->rlen.p, w->s_req.p, w->slot.p,
-                                                            w->s_len.p, w->s_fnode.p);
+                                                            w->s_len.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -976,13 +1006,13 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     FillArgs a{};
     a.t = view(t);
     a.n = (int32_t)n;
-    a.s_req = w->s_req.p; a.slot = w->slot.p; a.s_len = w->s_len.p; a.s_fnode = w->s_fnode.p;
+    a.s_req = w->s_req.p; a.slot = w->slot.p; a.s_len = w->s_len.p;
     a.roff = c->roff.p;
     a.q = w->q.p; a.refills = w->refills.p; a.known = w->known.p; a.nclients = w->nclients; a.pend_cnt = w->pend_cnt.p;
     a.dl_client = w->dlc.p; a.dl_delta = w->dld.p; a.ndl = ndl;
     a.M = w->M; a.R = w->R; a.gen_total = generated_total; a.headroom0 = headroom; a.w_e = w->w_e;
     a.quantum = w->quantum; a.now = now; a.lpm = w->policy == 1;
-    a.path = t->path.p;
+    a.segs = t->segs.p;
     a.adm_req = w->adm_req.p; a.adm_mlen = w->adm_mlen.p; a.adm_node = w->adm_node.p;
     a.adm_unp = w->adm_unp.p; a.adm_pinb = w->adm_pinb.p; a.adm_rec_end = w->adm_rec_end.p;
     a.adm_cap = (int32_t)w->adm_req.cap;
@@ -1119,7 +1149,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     a.q = d->q.p; a.qset = d->qset.p; a.qsize = d->qsize.p;
     a.quantum = d->quantum; a.w_e = d->w_e;
     a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = ndl;
-    a.path = d->tree->path.p;
+    a.segs = d->tree->segs.p;
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
     k_dispatch<<<1, 256, 0, s>>>(a);
