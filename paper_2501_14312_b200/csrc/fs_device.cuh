@@ -18,11 +18,13 @@
 //   * children: one open-addressing hash (parent, first token) -> child, with
 //     key and value packed in one 16-byte slot (one load per probe), linear
 //     probing, backward-shift deletion.
-//   * last_access is stored lazily: la[n] holds the stamps of paths that
-//     *ended* at n; the reference value is the maximum over n's subtree (every
-//     stamp in radix.py:86-90,107-109,158-159 covers a whole root path).  A
-//     detached leaf pushes its la up to its parent, so leaves -- the only nodes
-//     LRU eviction compares (radix.py:196-219) -- always hold their exact value.
+//   * last_access is stored lazily: la[n] holds the latest stamp of a path
+//     that *ended* at n, tagged with its operation sequence number; the
+//     reference value is the most recent stamp in n's subtree (every stamp in
+//     radix.py:86-90,107-109,158-159 covers a whole root path, last write
+//     wins).  A detached leaf pushes its stamp up to its parent, so leaves --
+//     the only nodes LRU eviction compares (radix.py:196-219) -- always hold
+//     their exact value.
 //   * ref counts stay exact per node; pin/unpin touch every node of a path,
 //     enumerated block-parallel from the source-chain segments of the walk.
 //
@@ -66,6 +68,7 @@ struct TrieView {
     int64_t *src;
     int32_t *start, *end, *slen, *parent, *nchild, *ref, *first;
     int64_t *la, *seq;
+    int64_t *lseq;     // operation sequence number of la[n] (last write wins)
     uint8_t *flags;
     uint64_t *wmask;   // nullptr unless track_workers
     int64_t *wtime;    // [node * nw + w]
@@ -142,7 +145,7 @@ __device__ inline int32_t node_new(const TrieView &t, int64_t src, int32_t start
     else if (t.sc->hw < t.ncap) n = t.sc->hw++;
     else { t.sc->status = FS_ERR_NOMEM; return -1; }
     t.src[n] = src; t.start[n] = start; t.end[n] = end; t.slen[n] = slen; t.parent[n] = parent;
-    t.nchild[n] = 0; t.ref[n] = 0; t.la[n] = 0;
+    t.nchild[n] = 0; t.ref[n] = 0; t.la[n] = 0; t.lseq[n] = 0;
     t.seq[n] = t.sc->next_seq++;
     t.first[n] = t.arena[src + start];
     t.flags[n] = FS_ALIVE;
@@ -158,6 +161,13 @@ __device__ inline void node_free(const TrieView &t, int32_t n) {
 }
 __device__ __forceinline__ int32_t elen(const TrieView &t, int32_t n) { return t.end[n] - t.start[n]; }
 
+// last_access = now on every node of the root path ending at n (lazy: the
+// stamp is kept at n with its operation sequence number; a node's reference
+// value is the most recent stamp in its subtree).
+__device__ __forceinline__ void stamp_node(const TrieView &t, int32_t n, int64_t now, int64_t sq) {
+    if (t.lseq[n] != sq || t.la[n] != now) { t.la[n] = now; t.lseq[n] = sq; }
+}
+
 // RadixTree._split (radix.py:114-126): top gets a new seq, copies ref /
 // last_access / workers; the bottom keeps its identity (and seq).  The caller
 // re-points pos[] for the top's depth range [start, start+k) (block_repoint).
@@ -166,7 +176,8 @@ __device__ inline int32_t trie_split(const TrieView &t, int32_t node, int32_t k)
     const int32_t top = node_new(t, t.src[node], t.start[node], t.start[node] + k, t.slen[node], P);
     if (top < 0) return -1;
     t.ref[top] = t.ref[node];
-    t.la[top] = 0;  // lazy: the top's value is the max over its subtree (the bottom)
+    t.la[top] = 0;  // lazy: the top's value is the latest stamp in its subtree (the bottom's)
+    t.lseq[top] = 0;
     if (t.wmask) {
         t.wmask[top] = t.wmask[node];
         for (int w = 0; w < t.nw; w++) t.wtime[(int64_t)top * t.nw + w] = t.wtime[(int64_t)node * t.nw + w];
@@ -186,7 +197,7 @@ __device__ inline void trie_detach(const TrieView &t, int32_t n) {
     const int32_t P = t.parent[n];
     h_del(t, P, t.first[n]);
     t.nchild[P]--;
-    if (P > 0 && t.la[n] > t.la[P]) t.la[P] = t.la[n];
+    if (P > 0 && t.lseq[n] > t.lseq[P]) { t.la[P] = t.la[n]; t.lseq[P] = t.lseq[n]; }
     t.sc->used -= elen(t, n);
     node_free(t, n);
 }
@@ -455,7 +466,7 @@ struct InsertSmem {
 // match before the new leaf == probe()'s), unpinned/cov of that walk, deepest
 // path node, status (FS_ERR_CACHE_FULL after performing the evictions, like
 // the reference).
-__device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now,
+__device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now, int64_t sq,
                                     int32_t worker, Seg *segs, InsertSmem *sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t *rq = t.arena + req_off;
@@ -513,7 +524,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                 deepest = leaf;
             }
         }
-        if (sm->status == FS_OK && deepest > 0) t.la[deepest] = now;  // stamps the whole path (lazy)
+        if (sm->status == FS_OK && deepest > 0) stamp_node(t, deepest, now, sq);  // the whole path (lazy)
         sm->deepest = deepest;
         if (sm->status != FS_OK && t.sc->status == FS_OK && sm->status != FS_ERR_CACHE_FULL) t.sc->status = sm->status;
     }

@@ -23,7 +23,7 @@
 // ---------------------------------------------------------------- K1
 __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
-                                               int64_t now, int stamp, uint32_t kmax,
+                                               int64_t now, int stamp, int64_t sq, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
                                                unsigned long long *__restrict__ alg_tokens) {
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
     const WalkOut w = warp_walk(t, rq, len, lane, nullptr, true);
     if (lane == 0) {
         // match_prefix stamps every matched node (radix.py:86-90): lazily, at the deepest
-        if (stamp && w.last > 0 && t.la[w.last] != now) t.la[w.last] = now;
+        if (stamp && w.last > 0) stamp_node(t, w.last, now, sq);
         if (out_key) out_key[i] = kmax - (uint32_t)w.mlen;
         if (out_mlen) out_mlen[i] = w.mlen;
         if (out_cov) out_cov[i] = w.cov;
@@ -112,6 +112,7 @@ struct FillArgs {
     const int64_t *dl_delta;
     int32_t ndl;
     int64_t M, R, gen_total, headroom0, w_e, quantum, now;
+    int64_t sq_base;  // operation sequence number of admission e = sq_base + e
     int32_t lpm;
     Seg *segs;
     int32_t *adm_req, *adm_mlen, *adm_node;
@@ -302,7 +303,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int64_t pinb;
     if (tid == 0) pinb = t.sc->pinned;
     __syncthreads();
-    block_insert(t, off, len, a.now, -1, a.segs, &sm->ins);
+    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins);
     const long long ct = clock64();
     if (sm->ins.status == FS_OK) {
         block_pin_path(t, a.segs, sm->ins.nseg, +1);
@@ -439,6 +440,7 @@ struct OpArgs {
     int64_t needed;
     int32_t keep;
     int64_t notice;
+    int64_t sq;  // operation sequence number for stamps
     Seg *segs;
     int32_t *found;
     int64_t *out;  // [status, mlen/new_len, deepest, mask, nrec]
@@ -455,13 +457,13 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     const int32_t *rq = t.arena + a.req_off;
     switch (a.op) {
         case OP_INSERT:
-            block_insert(t, a.req_off, a.len, a.now, a.worker, a.segs, &ins);
+            block_insert(t, a.req_off, a.len, a.now, a.sq, a.worker, a.segs, &ins);
             if (tid == 0) { a.out[0] = ins.status; a.out[1] = ins.new_len; a.out[2] = ins.deepest; }
             break;
         case OP_ADMIT:
             // probe (radix.py:189) -> insert -> pin; the probe's mlen equals the
             // insert walk's (nothing changes between them)
-            block_insert(t, a.req_off, a.len, a.now, -1, a.segs, &ins);
+            block_insert(t, a.req_off, a.len, a.now, a.sq, -1, a.segs, &ins);
             if (ins.status == FS_OK) block_pin_path(t, a.segs, ins.nseg, +1);
             __syncthreads();
             if (tid == 0) { a.out[0] = ins.status; a.out[1] = ins.mlen; a.out[2] = ins.deepest; }
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
                 if (lane == 0) {
                     // deepest = partial or last full node (radix.py:104); stamps the path
                     const int32_t deepest = w.mlen > 0 ? w.last : -1;
-                    if (deepest > 0) t.la[deepest] = a.now;
+                    if (deepest > 0) stamp_node(t, deepest, a.now, a.sq);
                     a.out[0] = FS_OK;
                     a.out[1] = deepest > 0 ? w.mlen : 0;
                     a.out[3] = (deepest > 0 && t.wmask) ? (int64_t)t.wmask[deepest] : 0;
@@ -513,6 +515,7 @@ struct DispArgs {
     uint8_t *qset;
     int64_t *qsize;
     int64_t quantum, w_e;
+    int64_t sq_base;  // arrival i stamps with sq_base + 2i (match) and sq_base + 2i + 1 (insert)
     const int32_t *dl_idx;  // pending host-side updates (see k_dispatch)
     const int64_t *dl_q;
     const int32_t *dl_w;
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             const WalkOut w = warp_walk(t, t.arena + off, len, lane, nullptr, false);
             if (lane == 0) {
                 const int32_t deepest = w.mlen > 0 ? w.last : -1;
-                if (deepest > 0) t.la[deepest] = now;
+                if (deepest > 0) stamp_node(t, deepest, now, a.sq_base + 2 * (int64_t)i);
                 const uint64_t mask = deepest > 0 ? t.wmask[deepest] : 0ull;
                 int64_t rounds;
                 const int best = d2_select(a, a.clients[i], mask, &rounds);
@@ -602,7 +605,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             }
         }
         __syncthreads();
-        block_insert(t, off, len, now, s_w, a.segs, &ins);
+        block_insert(t, off, len, now, a.sq_base + 2 * (int64_t)i + 1, s_w, a.segs, &ins);
         if (tid == 0) {
             a.out_w[i] = s_w;
             a.out_mlen[i] = s_mlen;

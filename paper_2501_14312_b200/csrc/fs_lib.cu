@@ -269,8 +269,9 @@ struct fs_trie {
     int track = 0, nw = 0;
     int32_t ncap = 0;
     uint32_t hsize = 0;
-    DBuf<int64_t> src, la, seq;
+    DBuf<int64_t> src, la, seq, lseq;
     DBuf<int32_t> start, end, slen, parent, nchild, ref, first, freest;
+    int64_t opseq = 0;   // sequence number of the last stamping operation
     DBuf<uint8_t> flags;
     DBuf<uint64_t> wmask;
     DBuf<int64_t> wtime;
@@ -292,7 +293,7 @@ static TrieView view(fs_trie *t) {
     v.pos = t->pos.p;
     v.src = t->src.p; v.start = t->start.p; v.end = t->end.p; v.slen = t->slen.p; v.parent = t->parent.p;
     v.nchild = t->nchild.p; v.ref = t->ref.p; v.first = t->first.p;
-    v.la = t->la.p; v.seq = t->seq.p; v.flags = t->flags.p;
+    v.la = t->la.p; v.seq = t->seq.p; v.lseq = t->lseq.p; v.flags = t->flags.p;
     v.wmask = t->track ? t->wmask.p : nullptr;
     v.wtime = t->track ? t->wtime.p : nullptr;
     v.nw = t->nw;
@@ -309,7 +310,7 @@ __global__ void k_trie_init(TrieView t, int64_t capacity) {
         s.used = 0; s.pinned = 0; s.next_seq = 1; s.capacity = capacity; s.nrec = 0;
         s.hw = 1; s.nfree = 0; s.status = 0; s.live = 1;
         t.src[0] = 0; t.start[0] = 0; t.end[0] = 0; t.slen[0] = 0; t.parent[0] = -1; t.nchild[0] = 0; t.ref[0] = 0;
-        t.la[0] = 0; t.seq[0] = 0; t.first[0] = -1; t.flags[0] = FS_ALIVE;
+        t.la[0] = 0; t.seq[0] = 0; t.lseq[0] = 0; t.first[0] = -1; t.flags[0] = FS_ALIVE;
         if (t.wmask) t.wmask[0] = 0;
     }
 }
@@ -353,7 +354,7 @@ static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
     const int64_t keep = old;
     TRY(dgrow(t->src, nc, s, true, keep)); TRY(dgrow(t->la, nc, s, true, keep)); TRY(dgrow(t->seq, nc, s, true, keep));
     TRY(dgrow(t->start, nc, s, true, keep)); TRY(dgrow(t->end, nc, s, true, keep)); TRY(dgrow(t->parent, nc, s, true, keep));
-    TRY(dgrow(t->slen, nc, s, true, keep));
+    TRY(dgrow(t->slen, nc, s, true, keep)); TRY(dgrow(t->lseq, nc, s, true, keep));
     TRY(dgrow(t->nchild, nc, s, true, keep)); TRY(dgrow(t->ref, nc, s, true, keep)); TRY(dgrow(t->first, nc, s, true, keep));
     TRY(dgrow(t->freest, nc, s, true, keep)); TRY(dgrow(t->flags, nc, s, true, keep));
     if (t->track) { TRY(dgrow(t->wmask, nc, s, true, keep)); TRY(dgrow(t->wtime, nc * t->nw, s, true, keep * t->nw)); }
@@ -410,6 +411,7 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     t->src.release(); t->la.release(); t->seq.release(); t->start.release(); t->end.release();
     t->parent.release(); t->nchild.release(); t->ref.release(); t->first.release(); t->freest.release();
     t->flags.release(); t->wmask.release(); t->wtime.release(); t->hslot.release(); t->slen.release();
+    t->lseq.release();
     t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
     t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
@@ -443,8 +445,9 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     TRY(dgrow(sm.ids, n, c->stream)); TRY(dgrow(sm.mlen, n, c->stream)); TRY(dgrow(sm.cov, n, c->stream));
     CK(cudaMemcpyAsync(sm.ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
     const int64_t blocks = (n * 32 + 255) / 256;
+    const int64_t sq = stamp ? ++t->opseq : 0;
     k_match<<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
-                                                      stamp, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr);
+                                                      stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr);
     counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -486,6 +489,7 @@ static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     a.segs = t->segs.p;
     a.found = t->found.p;
     a.out = t->opout.p;
+    a.sq = ++t->opseq;
     k_op<<<1, 256, 0, c->stream>>>(a);
     counted();
     CK(cudaGetLastError());
@@ -635,11 +639,12 @@ extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src,
         if (wmask && !t->track) std::memset(wmask, 0, sizeof(uint64_t) * k);
     }
     if (last_access && k > 0) {
-        // device la holds the stamps of paths ending at each node; the
-        // reference's last_access is the maximum over the node's subtree
-        std::vector<int64_t> la(hw);
+        // device la holds the latest stamp of a path ending at each node; the
+        // reference's last_access is the most recent stamp in its subtree
+        std::vector<int64_t> la(hw), lsq(hw);
         std::vector<int32_t> par(hw), dep(hw);
         CK(cudaMemcpyAsync(la.data(), t->la.p, sizeof(int64_t) * hw, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(lsq.data(), t->lseq.p, sizeof(int64_t) * hw, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(par.data(), t->parent.p, sizeof(int32_t) * hw, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(dep.data(), t->end.p, sizeof(int32_t) * hw, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -647,7 +652,7 @@ extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src,
         for (int32_t i = 1; i < hw; i++) if (par[i] >= 0) order.push_back(i);
         std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return dep[a] > dep[b]; });
         for (int32_t i : order)
-            if (par[i] > 0 && la[i] > la[par[i]]) la[par[i]] = la[i];
+            if (par[i] > 0 && lsq[i] > lsq[par[i]]) { la[par[i]] = la[i]; lsq[par[i]] = lsq[i]; }
         std::memcpy(last_access, la.data(), sizeof(int64_t) * k);
     }
     CK(cudaStreamSynchronize(s));
@@ -984,7 +989,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     if (n > 0) {
         const int64_t blocks = (n * 32 + 255) / 256;
         k_match<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
-                                                  kmax, w->keys.p, nullptr, w->cov.p, w->next.p,
+                                                  ++t->opseq, kmax, w->keys.p, nullptr, w->cov.p, w->next.p,
                                                   (unsigned long long *)w->alg.p);
         counted();
         CK(cudaGetLastError());
@@ -1012,6 +1017,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     a.dl_client = w->dlc.p; a.dl_delta = w->dld.p; a.ndl = ndl;
     a.M = w->M; a.R = w->R; a.gen_total = generated_total; a.headroom0 = headroom; a.w_e = w->w_e;
     a.quantum = w->quantum; a.now = now; a.lpm = w->policy == 1;
+    a.sq_base = t->opseq + 1;
     a.segs = t->segs.p;
     a.adm_req = w->adm_req.p; a.adm_mlen = w->adm_mlen.p; a.adm_node = w->adm_node.p;
     a.adm_unp = w->adm_unp.p; a.adm_pinb = w->adm_pinb.p; a.adm_rec_end = w->adm_rec_end.p;
@@ -1050,6 +1056,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     res->used = t->h_sc.used;
     res->pinned = t->h_sc.pinned;
     w->admitted_last = nadm;
+    t->opseq += nadm;  // admission e stamped with sq_base + e
     if (status != FS_OK) return fail((int)status, "device fill failed (status %lld)", (long long)status);
     if (nadm > res->cap_adm) return fail(FS_ERR_INVALID, "admission buffer too small (%lld > %lld)", (long long)nadm, (long long)res->cap_adm);
     if (nadm > 0) {
@@ -1150,6 +1157,8 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     a.quantum = d->quantum; a.w_e = d->w_e;
     a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = ndl;
     a.segs = d->tree->segs.p;
+    a.sq_base = d->tree->opseq + 1;
+    d->tree->opseq += 2 * n;
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
     k_dispatch<<<1, 256, 0, s>>>(a);
