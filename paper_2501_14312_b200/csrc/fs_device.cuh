@@ -452,12 +452,127 @@ __device__ inline void block_evict(const TrieView &t, int64_t needed, EvictSmem 
     __syncthreads();
 }
 
+// ---------------------------------------------------------------- chunked LRU
+// Inside one schedule step the evictable-leaf set only loses members (pins,
+// detaches) or gains parents exposed by detaches, and no candidate's
+// (last_access, seq) key changes (the only stamps are on admission paths,
+// which are pinned).  The scheduler therefore keeps, in shared memory, the
+// minimum key of every CH-node chunk of the node table: a pop is a warp-wide
+// argmin over the chunk minima plus the rescan of the one or two chunks the
+// pop changed -- no block barrier per pop.
+#define FS_NCH 1024
+struct ChunkLRU {
+    int64_t la[FS_NCH];
+    int64_t sq[FS_NCH];
+    int32_t nd[FS_NCH];
+    int32_t ch;   // nodes per chunk (multiple of 32)
+    int32_t nch;  // chunks covering [0, hw0)
+    int32_t hw0;  // node-table size at the start of the step (later nodes are pinned)
+};
+
+__device__ __forceinline__ bool lru_candidate(const TrieView &t, int32_t n) {
+    return (t.flags[n] & FS_ALIVE) && t.nchild[n] == 0 && t.ref[n] == 0;
+}
+
+// Recompute the minimum of chunk c (one warp), leaving out node `exclude`.
+__device__ inline void warp_chunk_scan(const TrieView &t, ChunkLRU *L, int32_t c, int32_t exclude, int lane) {
+    int64_t bla = INT64_MAX, bsq = INT64_MAX;
+    int32_t bn = -1;
+    const int32_t lo = c * L->ch, hi = min(lo + L->ch, L->hw0);
+    for (int32_t n = max(lo, 1) + lane; n < hi; n += 32) {
+        if (n != exclude && lru_candidate(t, n)) {
+            const int64_t a = t.la[n], s = t.seq[n];
+            if (a < bla || (a == bla && s < bsq)) { bla = a; bsq = s; bn = n; }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const int64_t oa = __shfl_down_sync(FS_FULL, bla, off);
+        const int64_t os = __shfl_down_sync(FS_FULL, bsq, off);
+        const int32_t on = __shfl_down_sync(FS_FULL, bn, off);
+        if (on >= 0 && (bn < 0 || oa < bla || (oa == bla && os < bsq))) { bla = oa; bsq = os; bn = on; }
+    }
+    if (lane == 0) { L->la[c] = bla; L->sq[c] = bsq; L->nd[c] = bn; }
+    __syncwarp();
+}
+
+__device__ inline void block_chunk_build(const TrieView &t, ChunkLRU *L) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (threadIdx.x == 0) {
+        L->hw0 = t.sc->hw;
+        int32_t ch = (L->hw0 + FS_NCH - 1) / FS_NCH;
+        ch = max(32, (ch + 31) & ~31);
+        L->ch = ch;
+        L->nch = (L->hw0 + ch - 1) / ch;
+    }
+    __syncthreads();
+    for (int32_t c = warp; c < L->nch; c += nwarps) warp_chunk_scan(t, L, c, -1, lane);
+    __syncthreads();
+}
+
+__device__ __forceinline__ void warp_chunk_touch(const TrieView &t, ChunkLRU *L, int32_t n, int32_t exclude,
+                                                 int lane) {
+    if (n > 0 && n < L->hw0) warp_chunk_scan(t, L, n / L->ch, exclude, lane);
+}
+
+// RadixTree.evict_lru with protect set {protect} (radix.py:210-250), one warp.
+__device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t needed, int32_t protect,
+                                        EvictSmem *sm, int lane) {
+    if (protect > 0) warp_chunk_touch(t, L, protect, protect, lane);
+    int64_t freed = 0;
+    while (freed < needed) {
+        int64_t bla = INT64_MAX, bsq = INT64_MAX;
+        int32_t bn = -1;
+        for (int32_t c = lane; c < L->nch; c += 32) {
+            const int32_t on = L->nd[c];
+            if (on >= 0 && (bn < 0 || L->la[c] < bla || (L->la[c] == bla && L->sq[c] < bsq))) {
+                bla = L->la[c]; bsq = L->sq[c]; bn = on;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const int64_t oa = __shfl_down_sync(FS_FULL, bla, off);
+            const int64_t os = __shfl_down_sync(FS_FULL, bsq, off);
+            const int32_t on = __shfl_down_sync(FS_FULL, bn, off);
+            if (on >= 0 && (bn < 0 || oa < bla || (oa == bla && os < bsq))) { bla = oa; bsq = os; bn = on; }
+        }
+        const int32_t b = __shfl_sync(FS_FULL, bn, 0);
+        if (b < 0) break;
+        int32_t P = -1;
+        if (lane == 0) {
+            sm->pops++;
+            const int32_t plen = t.end[b];
+            const int64_t remaining = needed - freed;
+            const int32_t el = elen(t, b);
+            if (el <= remaining) {
+                P = t.parent[b];
+                push_record(t, t.src[b], plen, plen - el);
+                trie_detach(t, b);
+                freed += el;
+            } else {
+                push_record(t, t.src[b], plen, (int32_t)(plen - remaining));
+                t.end[b] -= (int32_t)remaining;
+                t.sc->used -= remaining;
+                freed += remaining;
+            }
+        }
+        freed = __shfl_sync(FS_FULL, freed, 0);
+        P = __shfl_sync(FS_FULL, P, 0);
+        __syncwarp();
+        warp_chunk_touch(t, L, b, protect, lane);
+        if (P > 0 && P / L->ch != b / L->ch) warp_chunk_touch(t, L, P, protect, lane);
+    }
+    if (lane == 0) sm->freed = freed;
+    __syncwarp();
+}
+
 // ---------------------------------------------------------------- insert
 struct InsertSmem {
     EvictSmem ev;
     int32_t nseg, mlen, new_len, deepest, last, status, cov, split_top;
     int64_t needed, unpinned;
     int64_t *prof;  // optional cycle counters: [1] walk, [2] evict, [5] evict pops
+    ChunkLRU *lru;  // scheduler: chunked LRU index (nullptr: block-wide scan)
 };
 
 // RadixTree.insert (radix.py:128-162) by one CTA (warp 0 walks).  `segs` is a
@@ -501,7 +616,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     const long long c1 = clock64();
     if (tid == 0 && sm->prof) sm->prof[1] += c1 - c0;
     if (sm->needed > 0) {
-        block_evict(t, sm->needed, &sm->ev);
+        if (sm->lru) {
+            if (warp == 0) warp_chunk_evict(t, sm->lru, sm->needed, sm->last, &sm->ev, lane);
+            __syncthreads();
+        } else {
+            block_evict(t, sm->needed, &sm->ev);
+        }
         if (tid == 0 && sm->prof) sm->prof[2] += clock64() - c1;
         if (tid == 0) {
             if (sm->last > 0) t.flags[sm->last] &= ~FS_PROTECT;

@@ -17,7 +17,7 @@
 #define FS_SCHED_THREADS 1024
 #define FS_ITEMS 4
 #define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
-#define FS_MAXA 2048
+#define FS_MAXA 8192
 #define FS_NONE 0x7fffffff
 
 // ---------------------------------------------------------------- K1
@@ -124,6 +124,7 @@ struct FillArgs {
 
 struct SchedSmem {
     InsertSmem ins;
+    ChunkLRU lru;
     int32_t wl[FS_CHUNK];
     int32_t aB[FS_MAXA];
     int32_t aTok[FS_MAXA];
@@ -214,10 +215,72 @@ __device__ inline void warp_resume(const FillArgs &a, int32_t p, int lane) {
 // admission `e` can raise B_p only if B_p == B_e and the request's token at
 // B_p equals the admitted one's (LCP(r_p, r_e) > B_p forces both), so a stale
 // B is re-walked only when such an admission happened since it was exact.
+#define FS_FAST 256
+// Warp-0 scan of [from, wend) in order; returns the first qualifying position
+// or FS_NONE.  Same predicate and resume rule as the block-wide scan.
+__device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t wend,
+                                           bool any_mode, int64_t slack, int lane) {
+    const int32_t epoch = sm->epoch;
+    for (int32_t base = from; base < wend; base += 32) {
+        const int32_t p = base + lane;
+        bool q = false, r = false;
+        if (p < wend) {
+            const int4 s = a.slot[p];
+            if (s.w >= 0) {
+                if (any_mode) {
+                    q = true;
+                } else if (a.lpm || a.q[s.x] > 0) {
+                    if (a.s_len[p] - s.y <= slack) {
+                        q = true;
+                    } else if (s.w < epoch) {
+                        bool maybe = false;
+                        if (s.z >= 0)
+                            for (int32_t e = s.w; e < epoch; e++)
+                                if (e >= FS_MAXA || (sm->aB[e] == s.y && sm->aTok[e] == s.z)) { maybe = true; break; }
+                        if (maybe) r = true; else a.slot[p].w = epoch;
+                    }
+                }
+            }
+        }
+        unsigned mq = __ballot_sync(FS_FULL, q), mr = __ballot_sync(FS_FULL, r);
+        while (mq | mr) {
+            const int first = __ffs(mq | mr) - 1;
+            if ((mq >> first) & 1u) return base + first;
+            const int32_t pp = base + first;
+            warp_resume(a, pp, lane);
+            __syncwarp();
+            bool ok = false;
+            if (lane == 0) {
+                a.slot[pp].w = epoch;
+                sm->resumes++;
+                ok = a.s_len[pp] - a.slot[pp].y <= slack;
+            }
+            ok = __shfl_sync(FS_FULL, ok, 0);
+            if (ok) return pp;
+            mr &= ~(1u << first);
+        }
+    }
+    return FS_NONE;
+}
+
 __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t until, bool any_mode,
                               int64_t slack) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int32_t epoch = sm->epoch;
+    {
+        // the next admissible request is usually right after the cursor: one
+        // warp checks a short window before the whole block sweeps chunks
+        const int32_t wend = min(until, from + FS_FAST);
+        if (warp == 0) {
+            const int32_t r = warp_find_window(a, sm, from, wend, any_mode, slack, lane);
+            if (lane == 0) sm->minA = r;
+        }
+        __syncthreads();
+        const int32_t r = sm->minA;
+        __syncthreads();
+        if (r != FS_NONE) return r;
+        from = wend;
+    }
     for (int32_t base = from; base < until; base += FS_CHUNK) {
         if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; sm->prof[4]++; }
         __syncthreads();
@@ -308,6 +371,10 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     if (sm->ins.status == FS_OK) {
         block_pin_path(t, a.segs, sm->ins.nseg, +1);
         __syncthreads();
+        // the matched node is pinned now (and may have gained a child): its
+        // chunk of the LRU index changes; new nodes are pinned and past hw0
+        if ((tid >> 5) == 0) warp_chunk_touch(t, &sm->lru, sm->ins.last, -1, tid & 31);
+        __syncthreads();
     }
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
@@ -356,7 +423,8 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
 }
 
 __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
-    __shared__ SchedSmem sm;
+    extern __shared__ __align__(16) unsigned char fs_smraw[];
+    SchedSmem &sm = *reinterpret_cast<SchedSmem *>(fs_smraw);
     const int tid = threadIdx.x;
     // on_outputs deltas accumulated since the last fill (local_policies.py:130-133)
     if (tid == 0) {
@@ -367,11 +435,13 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0;
         for (int i = 0; i < 8; i++) sm.prof[i] = 0;
         sm.ins.prof = sm.prof;
+        sm.ins.lru = &sm.lru;
         sm.ins.ev.pops = 0;
     }
     const long long t_start = clock64();
     for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.pend_cnt[c] = 0;
     __syncthreads();
+    block_chunk_build(a.t, &sm.lru);
     for (int32_t p = tid; p < a.n; p += blockDim.x) atomicAdd(&a.pend_cnt[a.slot[p].x], 1);
     __syncthreads();
     {
@@ -452,7 +522,7 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     __shared__ int32_t s_nseg;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;
-    if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.ev.pops = 0; }
+    if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.lru = nullptr; ins.ev.pops = 0; }
     __syncthreads();
     const int32_t *rq = t.arena + a.req_off;
     switch (a.op) {
@@ -570,6 +640,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
         }
         t.sc->status = FS_OK;
         ins.prof = nullptr;
+        ins.lru = nullptr;
         ins.ev.pops = 0;
     }
     __syncthreads();

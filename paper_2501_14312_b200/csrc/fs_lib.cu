@@ -1024,7 +1024,12 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     a.adm_cap = (int32_t)w->adm_req.cap;
     a.rstate = c->rstate.p;
     a.hdr = w->hdr.p;
-    k_schedule<<<1, FS_SCHED_THREADS, 0, s>>>(a);
+    static bool smem_set = false;
+    if (!smem_set) {
+        CK(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchedSmem)));
+        smem_set = true;
+    }
+    k_schedule<<<1, FS_SCHED_THREADS, sizeof(SchedSmem), s>>>(a);
     counted();
     CK(cudaGetLastError());
     CK(cudaEventRecord(w->ev[4], s));
