@@ -250,7 +250,7 @@ def main():
     h2d0, d2h0 = g.h2d, g.d2h
     dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(4)
     sched = np.zeros(8)
-    k1_hops = 0
+    k1_hops = resumes = refills = 0
     t_start = time.perf_counter()
     for _ in range(args.steps):
         now += STEP_US
@@ -265,6 +265,8 @@ def main():
         phases += np.array(res.phases_ms)
         sched += np.array(res.stats[8:16], dtype=np.float64)
         k1_hops += res.stats[6]
+        resumes += res.stats[4]
+        refills += res.stats[3]
     g.ctx.sync()
     t_total = time.perf_counter() - t_start
     launches = launch_count() - l0
@@ -315,7 +317,8 @@ def main():
         "sched_profile_per_step": {"find_cyc": sched[0] / args.steps, "walk_cyc": sched[1] / args.steps,
                                    "evict_cyc": sched[2] / args.steps, "tail_cyc": sched[3] / args.steps,
                                    "chunks": sched[4] / args.steps, "evict_pops": sched[5] / args.steps,
-                                   "admit_hops": sched[6] / args.steps, "k1_hops": k1_hops / args.steps,
+                                   "admit_chains": sched[6] / args.steps, "k1_chains": k1_hops / args.steps,
+                                   "resumes": resumes / args.steps, "refill_events": refills / args.steps,
                                    "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }

@@ -17,7 +17,6 @@
 #define FS_SCHED_THREADS 1024
 #define FS_ITEMS 4
 #define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
-#define FS_MAXA 8192
 #define FS_NONE 0x7fffffff
 
 // ---------------------------------------------------------------- K1
@@ -122,12 +121,50 @@ struct FillArgs {
     int64_t *hdr;  // [n_adm, n_rec, status, epochs, refill_events, resumes, -, -, prof[8]]
 };
 
+// (pinned coverage B, token at B) of every admission of this step -> latest
+// admission epoch.  An admission e can raise a queued request's B only if
+// both match (see block_find); open addressing in shared memory.
+#define FS_FSLOTS 8192
+struct AdmFilter {
+    unsigned long long key[FS_FSLOTS];
+    int32_t ep[FS_FSLOTS];
+    int32_t n;
+    int32_t saturated;  // too many distinct keys: every stale B is re-walked
+};
+
+__device__ __forceinline__ unsigned long long adm_key(int32_t B, int32_t tok) {
+    return ((unsigned long long)(uint32_t)B << 32) | (uint32_t)tok;
+}
+
+__device__ inline void adm_put(AdmFilter *f, int32_t B, int32_t tok, int32_t e) {
+    if (tok < 0) return;  // a request fully covered by pins extends nothing
+    if (f->n * 2 >= FS_FSLOTS) { f->saturated = 1; return; }
+    const unsigned long long k = adm_key(B, tok);
+    uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
+    while (f->key[i] != FS_HEMPTY && f->key[i] != k) i = (i + 1) & (FS_FSLOTS - 1);
+    if (f->key[i] == FS_HEMPTY) { f->key[i] = k; f->n++; }
+    f->ep[i] = e;
+}
+
+// true when some admission in [since, now) had the same (B, token)
+__device__ __forceinline__ bool adm_maybe(const AdmFilter *f, int32_t B, int32_t tok, int32_t since) {
+    if (tok < 0) return false;
+    if (f->saturated) return true;
+    const unsigned long long k = adm_key(B, tok);
+    uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
+    while (true) {
+        const unsigned long long x = f->key[i];
+        if (x == k) return f->ep[i] >= since;
+        if (x == FS_HEMPTY) return false;
+        i = (i + 1) & (FS_FSLOTS - 1);
+    }
+}
+
 struct SchedSmem {
     InsertSmem ins;
     ChunkLRU lru;
+    AdmFilter flt;
     int32_t wl[FS_CHUNK];
-    int32_t aB[FS_MAXA];
-    int32_t aTok[FS_MAXA];
     int64_t red64[32];
     int32_t red32[32];
     int32_t wl_n, minA, minB;
@@ -233,11 +270,7 @@ __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int
                     if (a.s_len[p] - s.y <= slack) {
                         q = true;
                     } else if (s.w < epoch) {
-                        bool maybe = false;
-                        if (s.z >= 0)
-                            for (int32_t e = s.w; e < epoch; e++)
-                                if (e >= FS_MAXA || (sm->aB[e] == s.y && sm->aTok[e] == s.z)) { maybe = true; break; }
-                        if (maybe) r = true; else a.slot[p].w = epoch;
+                        if (adm_maybe(&sm->flt, s.y, s.z, s.w)) r = true; else a.slot[p].w = epoch;
                     }
                 }
             }
@@ -296,13 +329,7 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
             const int32_t need = a.s_len[p] - s.y;
             if (need <= slack) { mine = p; continue; }
             if (s.w < epoch) {
-                bool maybe = false;
-                if (s.z >= 0) {
-                    for (int32_t e = s.w; e < epoch; e++) {
-                        if (e >= FS_MAXA || (sm->aB[e] == s.y && sm->aTok[e] == s.z)) { maybe = true; break; }
-                    }
-                }
-                if (maybe) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
+                if (adm_maybe(&sm->flt, s.y, s.z, s.w)) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
                 else a.slot[p].w = epoch;  // B is still exact
             }
         }
@@ -399,10 +426,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
                 a.adm_rec_end[e] = t.sc->nrec;
             }
             sm->nadm = e + 1;
-            if (sm->epoch < FS_MAXA) {
-                sm->aB[sm->epoch] = cov;
-                sm->aTok[sm->epoch] = cov < len ? t.arena[off + cov] : -1;
-            }
+            adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, sm->epoch);
             sm->epoch++;
             a.slot[j].w = -1;
             a.rstate[r] = 2;
@@ -440,6 +464,8 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
     }
     const long long t_start = clock64();
     for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.pend_cnt[c] = 0;
+    for (int32_t i = tid; i < FS_FSLOTS; i += blockDim.x) sm.flt.key[i] = FS_HEMPTY;
+    if (tid == 0) { sm.flt.n = 0; sm.flt.saturated = 0; }
     __syncthreads();
     block_chunk_build(a.t, &sm.lru);
     for (int32_t p = tid; p < a.n; p += blockDim.x) atomicAdd(&a.pend_cnt[a.slot[p].x], 1);
