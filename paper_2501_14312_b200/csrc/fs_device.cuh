@@ -210,22 +210,26 @@ __device__ inline void push_record(const TrieView &t, int64_t src, int32_t len, 
 // ---------------------------------------------------------------- compare
 // LCP of a[0:n) and b[0:n) by one warp: 128 tokens per step, first mismatch
 // by ballot + ffs (common_prefix_len, _speedups.pyx:11-22, at warp width).
+// U loads per lane in flight: 4 for the many-warp match kernel (bounded
+// over-read past the mismatch), 8 for the single-warp walks on the admission
+// critical path (latency-bound).
+template <int U = 4>
 __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
                                             int32_t n, int lane) {
     int32_t k = 0;
     while (k < n) {
-        bool bad[4];
+        bool bad[U];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < U; u++) {
             const int32_t p = k + u * 32 + lane;
             bad[u] = (p < n) && (__ldg(a + p) != __ldg(b + p));
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < U; u++) {
             const unsigned m = __ballot_sync(FS_FULL, bad[u]);
             if (m) return min(n, k + u * 32 + __ffs(m) - 1);
         }
-        k += 128;
+        k += 32 * U;
     }
     return n;
 }
@@ -267,7 +271,7 @@ struct WalkOut {
 // order.  All lanes return the same WalkOut.  With want_cov, also computes the
 // pinned coverage: ref counts never increase with depth along a root path, so
 // it is one binary search per chain.
-template <typename SegFn>
+template <int U = 4, typename SegFn>
 __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                        bool want_cov, SegFn on_seg) {
     WalkOut o;
@@ -279,7 +283,7 @@ __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restr
         if (c < 0) break;
         const int64_t S = t.src[c];
         const int32_t bound = min(len, t.slen[c]);
-        const int32_t k = 1 + warp_lcp(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane);
+        const int32_t k = 1 + warp_lcp<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane);
         const int32_t D = idx + k;  // request == chain S on [idx, D)
         const int32_t y = chain_lookup(t, S, idx, D - 1);
         const int32_t e = t.end[y];
@@ -315,9 +319,10 @@ __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restr
 }
 
 // warp_walk_cb storing the segments (lane 0) when segs != nullptr.
+template <int U = 4>
 __device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                     Seg *segs, bool want_cov) {
-    return warp_walk_cb(t, rq, len, lane, want_cov, [&](int64_t S, int32_t a, int32_t b, int32_t i) {
+    return warp_walk_cb<U>(t, rq, len, lane, want_cov, [&](int64_t S, int32_t a, int32_t b, int32_t i) {
         if (lane == 0 && segs) { segs[i].S = S; segs[i].a = a; segs[i].b = b; }
     });
 }
@@ -587,7 +592,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     const int32_t *rq = t.arena + req_off;
     const long long c0 = clock64();
     if (warp == 0) {
-        const WalkOut w = warp_walk(t, rq, len, lane, segs, true);
+        const WalkOut w = warp_walk<8>(t, rq, len, lane, segs, true);
         if (lane == 0) {
             int32_t last = w.last >= 0 ? w.last : 0;
             sm->split_top = -1;

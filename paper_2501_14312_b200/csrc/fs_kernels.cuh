@@ -239,7 +239,7 @@ __device__ inline void warp_resume(const FillArgs &a, int32_t p, int lane) {
     const int32_t r = a.s_req[p];
     const int32_t len = a.s_len[p];
     const int32_t *rq = a.t.arena + a.roff[r];
-    const WalkOut w = warp_walk(a.t, rq, len, lane, nullptr, true);
+    const WalkOut w = warp_walk<8>(a.t, rq, len, lane, nullptr, true);
     if (lane == 0) {
         a.slot[p].y = w.cov;
         a.slot[p].z = w.cov < len ? rq[w.cov] : -1;
@@ -275,22 +275,13 @@ __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int
                 }
             }
         }
-        unsigned mq = __ballot_sync(FS_FULL, q), mr = __ballot_sync(FS_FULL, r);
-        while (mq | mr) {
+        const unsigned mq = __ballot_sync(FS_FULL, q), mr = __ballot_sync(FS_FULL, r);
+        if (mq | mr) {
             const int first = __ffs(mq | mr) - 1;
             if ((mq >> first) & 1u) return base + first;
-            const int32_t pp = base + first;
-            warp_resume(a, pp, lane);
-            __syncwarp();
-            bool ok = false;
-            if (lane == 0) {
-                a.slot[pp].w = epoch;
-                sm->resumes++;
-                ok = a.s_len[pp] - a.slot[pp].y <= slack;
-            }
-            ok = __shfl_sync(FS_FULL, ok, 0);
-            if (ok) return pp;
-            mr &= ~(1u << first);
+            // a stale coverage must be re-walked first: hand the rest of the
+            // search to the block, whose 32 warps re-walk in parallel
+            return -(base + first) - 2;
         }
     }
     return FS_NONE;
@@ -311,8 +302,8 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
         __syncthreads();
         const int32_t r = sm->minA;
         __syncthreads();
-        if (r != FS_NONE) return r;
-        from = wend;
+        if (r >= 0 && r != FS_NONE) return r;
+        from = r == FS_NONE ? wend : -(r + 2);
     }
     for (int32_t base = from; base < until; base += FS_CHUNK) {
         if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; sm->prof[4]++; }
