@@ -295,16 +295,29 @@ __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restr
             if (t.ref[y] > 0) {
                 o.cov = b;
             } else {
-                int32_t lo = idx, hi = b;  // first depth in an unpinned node
-                if (t.ref[t.pos[S + lo]] == 0) {
-                    hi = lo;
-                } else {
-                    while (hi - lo > 1) {
-                        const int32_t mid = (lo + hi) >> 1;
-                        if (t.ref[t.pos[S + mid]] > 0) lo = mid; else hi = mid;
+                // first depth of [idx, b) in an unpinned node: 32-ary search
+                // (one probe per lane per round); it is a node start
+                int32_t lo = idx, hi = b;
+                while (hi - lo > 32) {
+                    const int32_t step = (hi - lo + 31) / 32;
+                    const int32_t d = min(lo + lane * step, hi - 1);
+                    const unsigned m = __ballot_sync(FS_FULL, t.ref[t.pos[S + d]] == 0);
+                    if (m == 0) {
+                        lo = min(lo + 31 * step, hi - 1) + 1;
+                    } else {
+                        const int f = __ffs(m) - 1;
+                        const int32_t df = min(lo + f * step, hi - 1);
+                        if (f == 0) { hi = lo; break; }
+                        lo = min(lo + (f - 1) * step, hi - 1) + 1;
+                        hi = df;
                     }
                 }
-                o.cov = t.start[t.pos[S + hi]];
+                if (hi - lo > 0) {
+                    const int32_t d = lo + lane;
+                    const unsigned m = __ballot_sync(FS_FULL, d < hi && t.ref[t.pos[S + d]] == 0);
+                    hi = m ? lo + __ffs(m) - 1 : hi;
+                }
+                o.cov = hi;
                 pinrun = false;
             }
         }
@@ -543,13 +556,32 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         }
         const int32_t b = __shfl_sync(FS_FULL, bn, 0);
         if (b < 0) break;
+        const int32_t el = elen(t, b);
+        const bool whole = el <= needed - freed;
+        const int32_t Pb = t.parent[b];
+        __syncwarp();
+        // b is its chunk's minimum; a detach removes it, a truncation keeps
+        // its key.  Lanes 1..31 rescan b's chunk without b (and without its
+        // parent, whose state lane 0 is changing) while lane 0 edits.
+        int64_t cla = INT64_MAX, csq = INT64_MAX;
+        int32_t cn = -1;
+        if (whole) {
+            const int32_t c = b / L->ch;
+            const int32_t lo = c * L->ch, hi = min(lo + L->ch, L->hw0);
+            if (lane > 0)
+                for (int32_t n = max(lo, 1) + lane - 1; n < hi; n += 31) {
+                    if (n != b && n != Pb && n != protect && lru_candidate(t, n)) {
+                        const int64_t x = t.la[n], s = t.seq[n];
+                        if (x < cla || (x == cla && s < csq)) { cla = x; csq = s; cn = n; }
+                    }
+                }
+        }
         int32_t P = -1;
         if (lane == 0) {
             sm->pops++;
             const int32_t plen = t.end[b];
             const int64_t remaining = needed - freed;
-            const int32_t el = elen(t, b);
-            if (el <= remaining) {
+            if (whole) {
                 P = t.parent[b];
                 push_record(t, t.src[b], plen, plen - el);
                 trie_detach(t, b);
@@ -563,9 +595,29 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         }
         freed = __shfl_sync(FS_FULL, freed, 0);
         P = __shfl_sync(FS_FULL, P, 0);
+        if (whole) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const int64_t oa = __shfl_down_sync(FS_FULL, cla, off);
+                const int64_t os = __shfl_down_sync(FS_FULL, csq, off);
+                const int32_t on = __shfl_down_sync(FS_FULL, cn, off);
+                if (on >= 0 && (cn < 0 || oa < cla || (oa == cla && os < csq))) { cla = oa; csq = os; cn = on; }
+            }
+            if (lane == 0) {
+                const int32_t c = b / L->ch;
+                L->la[c] = cla; L->sq[c] = csq; L->nd[c] = cn;
+                // the parent joins the candidates once it becomes a leaf
+                // (radix.py:231-239): its chunk minimum can only drop
+                if (P > 0 && P < L->hw0 && P != protect && lru_candidate(t, P)) {
+                    const int32_t cp = P / L->ch;
+                    const int64_t pa = t.la[P], ps = t.seq[P];
+                    if (L->nd[cp] < 0 || pa < L->la[cp] || (pa == L->la[cp] && ps < L->sq[cp])) {
+                        L->la[cp] = pa; L->sq[cp] = ps; L->nd[cp] = P;
+                    }
+                }
+            }
+        }
         __syncwarp();
-        warp_chunk_touch(t, L, b, protect, lane);
-        if (P > 0 && P / L->ch != b / L->ch) warp_chunk_touch(t, L, P, protect, lane);
     }
     if (lane == 0) sm->freed = freed;
     __syncwarp();
