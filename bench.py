@@ -249,7 +249,7 @@ def main():
     l0 = launch_count()
     h2d0, d2h0 = g.h2d, g.d2h
     dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(4)
-    sched = np.zeros(8)
+    sched = np.zeros(16)
     k1_hops = resumes = refills = 0
     t_start = time.perf_counter()
     for _ in range(args.steps):
@@ -263,7 +263,7 @@ def main():
         alg_tok += res.stats[0]
         k1_ms.append(res.phases_ms[1])
         phases += np.array(res.phases_ms)
-        sched += np.array(res.stats[8:16], dtype=np.float64)
+        sched += np.array(res.stats[8:24], dtype=np.float64)
         k1_hops += res.stats[6]
         resumes += res.stats[4]
         refills += res.stats[3]
@@ -319,6 +319,8 @@ def main():
                                    "chunks": sched[4] / args.steps, "evict_pops": sched[5] / args.steps,
                                    "admit_chains": sched[6] / args.steps, "k1_chains": k1_hops / args.steps,
                                    "resumes": resumes / args.steps, "refill_events": refills / args.steps,
+                                   "pop_argmin_cyc": sched[8] / args.steps, "pop_edit_cyc": sched[9] / args.steps,
+                                   "pop_update_cyc": sched[10] / args.steps,
                                    "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }

@@ -178,8 +178,9 @@ int fs_worker_last_phases(fs_worker *w, float *ms4);
  * [5] kernel launches issued by the fill, [6] trie hops in K1, [8..15] scheduler-kernel SM cycles:
  * [8] candidate search, [9] admission walks, [10] LRU eviction, [11] admission
  * tail (pin, counters, records), [12] search chunks, [13] eviction pops,
- * [14] trie hops in admission walks, [15] total. */
-int fs_worker_last_stats(fs_worker *w, int64_t *stats16);
+ * [14] source chains in admission walks, [15] total, [16..18] eviction-pop
+ * argmin / edit / index-update cycles.  Writes 24 entries. */
+int fs_worker_last_stats(fs_worker *w, int64_t *stats24);
 /* Kernel launches issued by this library since load (all handles). */
 int64_t fs_launch_count(void);
 /* Queue length currently mirrored on device (worker.queue, worker.py:73) */

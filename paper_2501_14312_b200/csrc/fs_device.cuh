@@ -486,6 +486,7 @@ struct ChunkLRU {
     int32_t ch;   // nodes per chunk (multiple of 32)
     int32_t nch;  // chunks covering [0, hw0)
     int32_t hw0;  // node-table size at the start of the step (later nodes are pinned)
+    int64_t prof[4];  // pop cycles: argmin, edit, chunk update
 };
 
 __device__ __forceinline__ bool lru_candidate(const TrieView &t, int32_t n) {
@@ -539,6 +540,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
     if (protect > 0) warp_chunk_touch(t, L, protect, protect, lane);
     int64_t freed = 0;
     while (freed < needed) {
+        const long long p0 = clock64();
         int64_t bla = INT64_MAX, bsq = INT64_MAX;
         int32_t bn = -1;
         for (int32_t c = lane; c < L->nch; c += 32) {
@@ -560,6 +562,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         const bool whole = el <= needed - freed;
         const int32_t Pb = t.parent[b];
         __syncwarp();
+        const long long p1 = clock64();
         // b is its chunk's minimum; a detach removes it, a truncation keeps
         // its key.  Lanes 1..31 rescan b's chunk without b (and without its
         // parent, whose state lane 0 is changing) while lane 0 edits.
@@ -595,6 +598,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         }
         freed = __shfl_sync(FS_FULL, freed, 0);
         P = __shfl_sync(FS_FULL, P, 0);
+        const long long p2 = clock64();
         if (whole) {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
@@ -618,6 +622,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
             }
         }
         __syncwarp();
+        if (lane == 0) { L->prof[0] += p1 - p0; L->prof[1] += p2 - p1; L->prof[2] += clock64() - p2; }
     }
     if (lane == 0) sm->freed = freed;
     __syncwarp();

@@ -171,7 +171,8 @@ struct SchedSmem {
     int32_t cursor, progress, epoch, npos, nadm, stop, j;
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
-    int64_t prof[8];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops, [6] chains
+    int64_t prof[16];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops,
+                       // [6] chains, [7] total, [8..10] pop argmin / edit / rescan
 };
 
 __device__ __forceinline__ int64_t sched_slack(const FillArgs &a, int64_t headroom) {
@@ -448,7 +449,8 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         a.hdr[2] = FS_OK;
         sm.cursor = 0; sm.progress = 0; sm.epoch = 0; sm.nadm = 0; sm.stop = 0;
         sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0;
-        for (int i = 0; i < 8; i++) sm.prof[i] = 0;
+        for (int i = 0; i < 16; i++) sm.prof[i] = 0;
+        for (int i = 0; i < 4; i++) sm.lru.prof[i] = 0;
         sm.ins.prof = sm.prof;
         sm.ins.lru = &sm.lru;
         sm.ins.ev.pops = 0;
@@ -509,7 +511,8 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         a.hdr[5] = sm.resumes;
         sm.prof[5] = sm.ins.ev.pops;
         sm.prof[7] = clock64() - t_start;
-        for (int i = 0; i < 8; i++) a.hdr[8 + i] = sm.prof[i];
+        for (int i = 0; i < 3; i++) sm.prof[8 + i] = sm.lru.prof[i];
+        for (int i = 0; i < 16; i++) a.hdr[8 + i] = sm.prof[i];
     }
 }
 

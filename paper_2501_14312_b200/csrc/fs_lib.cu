@@ -698,7 +698,7 @@ struct fs_worker {
     cudaEvent_t ev[5];
     float phases[4] = {0, 0, 0, 0};
     DBuf<int64_t> alg;         // K1 algorithmic-token accumulator
-    int64_t stats[16] = {0};
+    int64_t stats[24] = {0};
 };
 
 struct IsQueued {
@@ -733,7 +733,7 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     CK(cudaMemsetAsync(w->q.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->refills.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
-    TRY(dgrow(w->hdr, 16, c->stream)); TRY(hgrow(w->h_hdr, 24));
+    TRY(dgrow(w->hdr, 24, c->stream)); TRY(hgrow(w->h_hdr, 32));
     TRY(dgrow(w->nsel, 1, c->stream));
     TRY(dgrow(w->alg, 2, c->stream));
     for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
@@ -892,7 +892,7 @@ extern "C" int fs_worker_queue_len(fs_worker *w, int64_t *n) {
 
 extern "C" int fs_worker_last_stats(fs_worker *w, int64_t *stats16) {
     if (!w || !stats16) return fail(FS_ERR_INVALID, "NULL");
-    for (int i = 0; i < 16; i++) stats16[i] = w->stats[i];
+    for (int i = 0; i < 24; i++) stats16[i] = w->stats[i];
     return FS_OK;
 }
 
@@ -1035,8 +1035,8 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     CK(cudaEventRecord(w->ev[4], s));
     w->dl_client.clear(); w->dl_delta.clear();
     // ---- results
-    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_hdr.p + 16, w->alg.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 24, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p + 24, w->alg.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
@@ -1045,9 +1045,9 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     const int64_t nrec = w->h_hdr.p[1];
     const int64_t status = w->h_hdr.p[2];
     for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&w->phases[i], w->ev[i], w->ev[i + 1]));
-    w->stats[0] = w->h_hdr.p[16];
-    w->stats[6] = w->h_hdr.p[17];
-    for (int i = 8; i < 16; i++) w->stats[i] = w->h_hdr.p[i];
+    w->stats[0] = w->h_hdr.p[24];
+    w->stats[6] = w->h_hdr.p[25];
+    for (int i = 8; i < 24; i++) w->stats[i] = w->h_hdr.p[i];
     w->stats[1] = n;
     w->stats[2] = w->h_hdr.p[3];
     w->stats[3] = w->h_hdr.p[4];

@@ -344,7 +344,7 @@ class WorkerDev:
         recs = self.trie.read_records(res.recs.n_rec)
         ph = (C.c_float * 4)()
         call("fs_worker_last_phases", self._h, ph)
-        st = (C.c_int64 * 16)()
+        st = (C.c_int64 * 24)()
         call("fs_worker_last_stats", self._h, st)
         a = res.n_adm
         return FillResult(self._req[:a].copy(), self._mlen[:a].copy(), self._unp[:a].copy(),
