@@ -483,6 +483,10 @@ struct ChunkLRU {
     int64_t la[FS_NCH];
     int64_t sq[FS_NCH];
     int32_t nd[FS_NCH];
+    // minima of 32-chunk groups: a pop's argmin reads one entry per lane
+    int64_t gla[FS_NCH / 32];
+    int64_t gsq[FS_NCH / 32];
+    int32_t gnd[FS_NCH / 32];
     int32_t ch;   // nodes per chunk (multiple of 32)
     int32_t nch;  // chunks covering [0, hw0)
     int32_t hw0;  // node-table size at the start of the step (later nodes are pinned)
@@ -491,6 +495,28 @@ struct ChunkLRU {
 
 __device__ __forceinline__ bool lru_candidate(const TrieView &t, int32_t n) {
     return (t.flags[n] & FS_ALIVE) && t.nchild[n] == 0 && t.ref[n] == 0;
+}
+
+// warp-wide argmin over (la, sq, nd) triples; every lane gets the result
+__device__ __forceinline__ void warp_key_min(int64_t &bla, int64_t &bsq, int32_t &bn) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const int64_t oa = __shfl_xor_sync(FS_FULL, bla, off);
+        const int64_t os = __shfl_xor_sync(FS_FULL, bsq, off);
+        const int32_t on = __shfl_xor_sync(FS_FULL, bn, off);
+        if (on >= 0 && (bn < 0 || oa < bla || (oa == bla && os < bsq))) { bla = oa; bsq = os; bn = on; }
+    }
+}
+
+// Recompute the minimum of chunk group g (one warp).
+__device__ inline void warp_group_update(ChunkLRU *L, int32_t g, int lane) {
+    const int32_t c = g * 32 + lane;
+    int64_t bla = INT64_MAX, bsq = INT64_MAX;
+    int32_t bn = -1;
+    if (c < L->nch) { bla = L->la[c]; bsq = L->sq[c]; bn = L->nd[c]; }
+    warp_key_min(bla, bsq, bn);
+    if (lane == 0) { L->gla[g] = bla; L->gsq[g] = bsq; L->gnd[g] = bn; }
+    __syncwarp();
 }
 
 // Recompute the minimum of chunk c (one warp), leaving out node `exclude`.
@@ -527,11 +553,17 @@ __device__ inline void block_chunk_build(const TrieView &t, ChunkLRU *L) {
     __syncthreads();
     for (int32_t c = warp; c < L->nch; c += nwarps) warp_chunk_scan(t, L, c, -1, lane);
     __syncthreads();
+    for (int32_t g = warp; g * 32 < L->nch; g += nwarps) warp_group_update(L, g, lane);
+    __syncthreads();
 }
 
 __device__ __forceinline__ void warp_chunk_touch(const TrieView &t, ChunkLRU *L, int32_t n, int32_t exclude,
                                                  int lane) {
-    if (n > 0 && n < L->hw0) warp_chunk_scan(t, L, n / L->ch, exclude, lane);
+    if (n > 0 && n < L->hw0) {
+        const int32_t c = n / L->ch;
+        warp_chunk_scan(t, L, c, exclude, lane);
+        warp_group_update(L, c / 32, lane);
+    }
 }
 
 // RadixTree.evict_lru with protect set {protect} (radix.py:210-250), one warp.
@@ -539,24 +571,14 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
                                         EvictSmem *sm, int lane) {
     if (protect > 0) warp_chunk_touch(t, L, protect, protect, lane);
     int64_t freed = 0;
+    const int32_t ngroups = (L->nch + 31) / 32;
     while (freed < needed) {
         const long long p0 = clock64();
         int64_t bla = INT64_MAX, bsq = INT64_MAX;
         int32_t bn = -1;
-        for (int32_t c = lane; c < L->nch; c += 32) {
-            const int32_t on = L->nd[c];
-            if (on >= 0 && (bn < 0 || L->la[c] < bla || (L->la[c] == bla && L->sq[c] < bsq))) {
-                bla = L->la[c]; bsq = L->sq[c]; bn = on;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const int64_t oa = __shfl_down_sync(FS_FULL, bla, off);
-            const int64_t os = __shfl_down_sync(FS_FULL, bsq, off);
-            const int32_t on = __shfl_down_sync(FS_FULL, bn, off);
-            if (on >= 0 && (bn < 0 || oa < bla || (oa == bla && os < bsq))) { bla = oa; bsq = os; bn = on; }
-        }
-        const int32_t b = __shfl_sync(FS_FULL, bn, 0);
+        if (lane < ngroups) { bla = L->gla[lane]; bsq = L->gsq[lane]; bn = L->gnd[lane]; }
+        warp_key_min(bla, bsq, bn);
+        const int32_t b = bn;
         if (b < 0) break;
         const int32_t el = elen(t, b);
         const bool whole = el <= needed - freed;
@@ -600,26 +622,25 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         P = __shfl_sync(FS_FULL, P, 0);
         const long long p2 = clock64();
         if (whole) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const int64_t oa = __shfl_down_sync(FS_FULL, cla, off);
-                const int64_t os = __shfl_down_sync(FS_FULL, csq, off);
-                const int32_t on = __shfl_down_sync(FS_FULL, cn, off);
-                if (on >= 0 && (cn < 0 || oa < cla || (oa == cla && os < csq))) { cla = oa; csq = os; cn = on; }
-            }
+            warp_key_min(cla, csq, cn);
+            const int32_t c = b / L->ch;
+            int32_t cp = -1;
             if (lane == 0) {
-                const int32_t c = b / L->ch;
                 L->la[c] = cla; L->sq[c] = csq; L->nd[c] = cn;
                 // the parent joins the candidates once it becomes a leaf
                 // (radix.py:231-239): its chunk minimum can only drop
                 if (P > 0 && P < L->hw0 && P != protect && lru_candidate(t, P)) {
-                    const int32_t cp = P / L->ch;
+                    cp = P / L->ch;
                     const int64_t pa = t.la[P], ps = t.seq[P];
                     if (L->nd[cp] < 0 || pa < L->la[cp] || (pa == L->la[cp] && ps < L->sq[cp])) {
                         L->la[cp] = pa; L->sq[cp] = ps; L->nd[cp] = P;
                     }
                 }
             }
+            cp = __shfl_sync(FS_FULL, cp, 0);
+            __syncwarp();
+            warp_group_update(L, c / 32, lane);
+            if (cp >= 0 && cp / 32 != c / 32) warp_group_update(L, cp / 32, lane);
         }
         __syncwarp();
         if (lane == 0) { L->prof[0] += p1 - p0; L->prof[1] += p2 - p1; L->prof[2] += clock64() - p2; }
