@@ -311,6 +311,9 @@ def main():
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg},
         "phase_share": {"merge": share[0], "k1_match": share[1], "k2_sort": share[2], "k3k4_schedule": share[3]},
+        "dominant_kernel": {"kernel": "k_schedule (K3/K4 admission chain, one CTA)", "share": share[3],
+                            "bound": "latency (serial admission chain; see sched_profile_per_step)",
+                            "avg_launch_ms": phases[3] / args.steps},
         "phase_ms_per_step": {"merge": phases[0] / args.steps, "k1_match": phases[1] / args.steps,
                               "k2_sort": phases[2] / args.steps, "k3k4_schedule": phases[3] / args.steps},
         "admissions_per_step": adm / args.steps, "queued_per_step": n_per_step,
