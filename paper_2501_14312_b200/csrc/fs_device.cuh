@@ -67,6 +67,8 @@ struct TrieView {
     int32_t *pos;      // position shadow over the arena
     int64_t *src;
     int32_t *start, *end, *slen, *parent, *nchild, *ref, *first;
+    int32_t *ctop;     // first depth of the node's source chain (its original leaf's start)
+    int32_t *cpar;     // node above the chain's topmost node (same for the whole chain)
     int64_t *la, *seq;
     int64_t *lseq;     // operation sequence number of la[n] (last write wins)
     uint8_t *flags;
@@ -145,6 +147,7 @@ __device__ inline int32_t node_new(const TrieView &t, int64_t src, int32_t start
     else if (t.sc->hw < t.ncap) n = t.sc->hw++;
     else { t.sc->status = FS_ERR_NOMEM; return -1; }
     t.src[n] = src; t.start[n] = start; t.end[n] = end; t.slen[n] = slen; t.parent[n] = parent;
+    t.ctop[n] = start; t.cpar[n] = parent;  // a new leaf starts its own chain
     t.nchild[n] = 0; t.ref[n] = 0; t.la[n] = 0; t.lseq[n] = 0;
     t.seq[n] = t.sc->next_seq++;
     t.first[n] = t.arena[src + start];
@@ -175,6 +178,8 @@ __device__ inline int32_t trie_split(const TrieView &t, int32_t node, int32_t k)
     const int32_t P = t.parent[node];
     const int32_t top = node_new(t, t.src[node], t.start[node], t.start[node] + k, t.slen[node], P);
     if (top < 0) return -1;
+    t.ctop[top] = t.ctop[node];
+    t.cpar[top] = t.cpar[node];
     t.ref[top] = t.ref[node];
     t.la[top] = 0;  // lazy: the top's value is the latest stamp in its subtree (the bottom's)
     t.lseq[top] = 0;
@@ -271,13 +276,48 @@ struct WalkOut {
 // order.  All lanes return the same WalkOut.  With want_cov, also computes the
 // pinned coverage: ref counts never increase with depth along a root path, so
 // it is one binary search per chain.
+// Pinned coverage inside segment [a, b) of chain S whose deepest node is y:
+// returns b if every node is pinned, else the first depth in an unpinned node
+// (a node start) -- 32-ary search, one probe per lane per round.  Warp-uniform.
+__device__ inline int32_t warp_seg_cov(const TrieView &t, int64_t S, int32_t a, int32_t b, int32_t y, int lane) {
+    if (t.ref[y] > 0) return b;
+    int32_t lo = a, hi = b;
+    while (hi - lo > 32) {
+        const int32_t step = (hi - lo + 31) / 32;
+        const int32_t d = min(lo + lane * step, hi - 1);
+        const unsigned m = __ballot_sync(FS_FULL, t.ref[t.pos[S + d]] == 0);
+        if (m == 0) {
+            lo = min(lo + 31 * step, hi - 1) + 1;
+        } else {
+            const int f = __ffs(m) - 1;
+            const int32_t df = min(lo + f * step, hi - 1);
+            if (f == 0) { hi = lo; break; }
+            lo = min(lo + (f - 1) * step, hi - 1) + 1;
+            hi = df;
+        }
+    }
+    if (hi - lo > 0) {
+        const int32_t d = lo + lane;
+        const unsigned m = __ballot_sync(FS_FULL, d < hi && t.ref[t.pos[S + d]] == 0);
+        hi = m ? lo + __ffs(m) - 1 : hi;
+    }
+    return hi;
+}
+
+// Walk state handed between the chain walk and its starts (root, or a
+// validated earlier match).
+struct WalkStart {
+    int32_t node, idx, nseg, last, cov;
+    bool pinrun;
+};
+
 template <int U = 4, typename SegFn>
-__device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
-                                       bool want_cov, SegFn on_seg) {
+__device__ inline WalkOut warp_walk_from(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
+                                         bool want_cov, WalkStart st, SegFn on_seg) {
     WalkOut o;
-    o.mlen = 0; o.last = -1; o.plen = 0; o.nseg = 0; o.cov = 0; o.unpinned = 0;
-    int32_t node = 0, idx = 0;
-    bool pinrun = want_cov;
+    o.mlen = 0; o.last = st.last; o.plen = 0; o.nseg = st.nseg; o.cov = st.cov; o.unpinned = 0;
+    int32_t node = st.node, idx = st.idx;
+    bool pinrun = want_cov && st.pinrun;
     while (idx < len) {
         const int32_t c = h_find(t, node, rq[idx]);
         if (c < 0) break;
@@ -291,35 +331,8 @@ __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restr
         on_seg(S, idx, b, o.nseg);
         o.nseg++;
         if (pinrun) {
-            // pinned coverage inside [idx, b): first node with ref == 0
-            if (t.ref[y] > 0) {
-                o.cov = b;
-            } else {
-                // first depth of [idx, b) in an unpinned node: 32-ary search
-                // (one probe per lane per round); it is a node start
-                int32_t lo = idx, hi = b;
-                while (hi - lo > 32) {
-                    const int32_t step = (hi - lo + 31) / 32;
-                    const int32_t d = min(lo + lane * step, hi - 1);
-                    const unsigned m = __ballot_sync(FS_FULL, t.ref[t.pos[S + d]] == 0);
-                    if (m == 0) {
-                        lo = min(lo + 31 * step, hi - 1) + 1;
-                    } else {
-                        const int f = __ffs(m) - 1;
-                        const int32_t df = min(lo + f * step, hi - 1);
-                        if (f == 0) { hi = lo; break; }
-                        lo = min(lo + (f - 1) * step, hi - 1) + 1;
-                        hi = df;
-                    }
-                }
-                if (hi - lo > 0) {
-                    const int32_t d = lo + lane;
-                    const unsigned m = __ballot_sync(FS_FULL, d < hi && t.ref[t.pos[S + d]] == 0);
-                    hi = m ? lo + __ffs(m) - 1 : hi;
-                }
-                o.cov = hi;
-                pinrun = false;
-            }
+            o.cov = warp_seg_cov(t, S, idx, b, y, lane);
+            pinrun = o.cov == b;
         }
         o.last = y;
         if (D < e) { o.plen = D - t.start[y]; idx = D; break; }  // diverged inside y (or request ended)
@@ -329,6 +342,98 @@ __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restr
     o.mlen = idx;
     if (want_cov) o.unpinned = o.mlen - o.cov;
     return o;
+}
+
+template <int U = 4, typename SegFn>
+__device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
+                                       bool want_cov, SegFn on_seg) {
+    WalkStart st;
+    st.node = 0; st.idx = 0; st.nseg = 0; st.last = -1; st.cov = 0; st.pinrun = true;
+    return warp_walk_from<U>(t, rq, len, lane, want_cov, st, on_seg);
+}
+
+// Source-chain segments of the cached root path [0, d) whose depth d-1 lies in
+// node y: chain by chain through the per-chain constants (src, ctop, cpar) --
+// one dependent load round per chain, no token compare.  Lane 0 writes segs in
+// path order; returns the count (warp-uniform).
+__device__ inline int32_t warp_path_segments(const TrieView &t, int32_t y, int32_t d, Seg *segs, int lane) {
+    int32_t ns = 0;
+    if (lane == 0) {
+        int32_t cur = y;
+        while (d > 0 && cur > 0) {
+            const int64_t S = t.src[cur];
+            const int32_t c0 = t.ctop[cur];
+            const int32_t X = t.cpar[cur];
+            segs[ns].S = S; segs[ns].a = c0; segs[ns].b = d;
+            ns++;
+            d = c0;
+            cur = X;
+        }
+        for (int32_t i = 0; i < ns / 2; i++) {
+            const Seg tmp = segs[i];
+            segs[i] = segs[ns - 1 - i];
+            segs[ns - 1 - i] = tmp;
+        }
+    }
+    ns = __shfl_sync(FS_FULL, ns, 0);
+    __syncwarp();
+    return ns;
+}
+
+// Pinned coverage of the cached root path [0, d) ending in node y, searched
+// from the deep end chain by chain (refs never increase with depth): no
+// segment storage.  Warp-uniform.
+__device__ inline int32_t warp_cov_from_deepest(const TrieView &t, int32_t y, int32_t d, int lane) {
+    int32_t cur = y;
+    while (d > 0 && cur > 0) {
+        const int64_t S = t.src[cur];
+        const int32_t c0 = t.ctop[cur];
+        const int32_t X = t.cpar[cur];
+        if (t.ref[t.pos[S + c0]] > 0) return warp_seg_cov(t, S, c0, d, t.pos[S + d - 1], lane);
+        d = c0;
+        cur = X;
+    }
+    return 0;
+}
+
+// The walk of a queued request given its match at the start of the schedule
+// step (chain S0, length m0, from K1).  Chains never grow and a cached depth
+// of a chain implies its whole root path is cached, so if depth m0-1 of S0 is
+// still cached the first m0 tokens still match without re-reading them; the
+// walk only continues from m0 when m0 ends at a node boundary (an insert of
+// this step may have added a child there).  Otherwise: full walk.
+template <int U = 8>
+__device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
+                                         Seg *segs, int64_t S0, int32_t m0) {
+    int32_t y = -1;
+    if (m0 > 0) {
+        const int32_t c = t.pos[S0 + m0 - 1];
+        if (pos_valid(t, c, S0, m0 - 1)) y = c;
+    }
+    auto store = [&](int64_t S, int32_t a, int32_t b, int32_t i) {
+        if (lane == 0) { segs[i].S = S; segs[i].a = a; segs[i].b = b; }
+    };
+    if (y < 0) return warp_walk_cb<U>(t, rq, len, lane, true, store);
+    WalkStart st;
+    st.nseg = warp_path_segments(t, y, m0, segs, lane);
+    st.cov = 0;
+    st.pinrun = true;
+    for (int32_t s = 0; s < st.nseg && st.pinrun; s++) {
+        const Seg g = segs[s];
+        const int32_t last = t.pos[g.S + g.b - 1];
+        st.cov = warp_seg_cov(t, g.S, g.a, g.b, last, lane);
+        st.pinrun = st.cov == g.b;
+    }
+    if (m0 < t.end[y]) {
+        // K1 stopped inside y: the request's token there differs from the chain
+        // (or the request ended) -- still true
+        WalkOut o;
+        o.mlen = m0; o.last = y; o.plen = m0 - t.start[y]; o.nseg = st.nseg; o.cov = st.cov;
+        o.unpinned = m0 - st.cov;
+        return o;
+    }
+    st.node = y; st.idx = m0; st.last = y;
+    return warp_walk_from<U>(t, rq, len, lane, true, st, store);
 }
 
 // warp_walk_cb storing the segments (lane 0) when segs != nullptr.
@@ -343,18 +448,25 @@ __device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict
 // unpin (radix.py:180-185) of the cached root path arena[src : src+plen] by one
 // warp: every node on it loses one reference; nodes reaching zero release
 // their edge from pinned_tokens.  Warps unpinning different paths commute.
-__device__ inline void warp_unpin_path(const TrieView &t, int64_t src, int32_t plen, int lane) {
+__device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int lane) {
     long long acc = 0;
     bool under = false;
-    warp_walk_cb(t, t.arena + src, plen, lane, false, [&](int64_t S, int32_t a, int32_t b, int32_t) {
-        for (int32_t d = a + lane; d < b; d += 32) {
-            const int32_t n = t.pos[S + d];
-            if (t.start[n] != d) continue;
+    // the path's chains, deepest first, through the per-chain constants
+    int32_t cur = deepest, d = t.end[deepest];
+    while (d > 0 && cur > 0) {
+        const int64_t S = t.src[cur];
+        const int32_t c0 = t.ctop[cur];
+        const int32_t X = t.cpar[cur];
+        for (int32_t p = c0 + lane; p < d; p += 32) {
+            const int32_t n = t.pos[S + p];
+            if (t.start[n] != p) continue;
             const int32_t old = atomicSub(&t.ref[n], 1);
             if (old <= 0) under = true;
             else if (old == 1) acc -= elen(t, n);
         }
-    });
+        d = c0;
+        cur = X;
+    }
     if (acc) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)acc);
     if (under) t.sc->status = FS_ERR_UNDERFLOW;
 }
@@ -665,12 +777,14 @@ struct InsertSmem {
 // path node, status (FS_ERR_CACHE_FULL after performing the evictions, like
 // the reference).
 __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now, int64_t sq,
-                                    int32_t worker, Seg *segs, InsertSmem *sm) {
+                                    int32_t worker, Seg *segs, InsertSmem *sm, int64_t hint_S0 = -1,
+                                    int32_t hint_m0 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t *rq = t.arena + req_off;
     const long long c0 = clock64();
     if (warp == 0) {
-        const WalkOut w = warp_walk<8>(t, rq, len, lane, segs, true);
+        const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8>(t, rq, len, lane, segs, hint_S0, hint_m0)
+                                       : warp_walk<8>(t, rq, len, lane, segs, true);
         if (lane == 0) {
             int32_t last = w.last >= 0 ? w.last : 0;
             sm->split_top = -1;
@@ -747,11 +861,11 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
 
 // Segments of an existing root path arena[src : src+plen] (every node on it is
 // cached): the walk of the handle's own path.  Block-level (warp 0 walks).
-__device__ inline void block_path_of(const TrieView &t, int64_t src, int32_t plen, Seg *segs, int32_t *nseg_out) {
+__device__ inline void block_path_of(const TrieView &t, int32_t deepest, Seg *segs, int32_t *nseg_out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp == 0) {
-        const WalkOut w = warp_walk(t, t.arena + src, plen, lane, segs, false);
-        if (lane == 0) *nseg_out = w.nseg;
+        const int32_t ns = warp_path_segments(t, deepest, t.end[deepest], segs, lane);
+        if (lane == 0) *nseg_out = ns;
     }
     __syncthreads();
 }

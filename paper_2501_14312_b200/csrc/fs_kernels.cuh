@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
                                                int64_t now, int stamp, int64_t sq, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
+                                               int64_t *__restrict__ out_s0,
                                                unsigned long long *__restrict__ alg_tokens) {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -40,6 +41,7 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
         if (out_mlen) out_mlen[i] = w.mlen;
         if (out_cov) out_cov[i] = w.cov;
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
+        if (out_s0) out_s0[i] = w.last > 0 ? t.src[w.last] : -1;  // admission-walk hint
         // request tokens a match must read: min(mlen+1, len)
         if (alg_tokens) {
             atomicAdd(alg_tokens, (unsigned long long)min(w.mlen + 1, len));
@@ -57,7 +59,7 @@ __global__ void k_unpin_many(TrieView t, const int32_t *__restrict__ nodes, int6
     if (i >= n) return;
     const int32_t nd = nodes[i];
     if (nd <= 0) return;
-    warp_unpin_path(t, t.src[nd], t.end[nd], lane);
+    warp_unpin_path(t, nd, lane);
     if (lane == 0 && t.sc->status == FS_ERR_UNDERFLOW) out[0] = FS_ERR_UNDERFLOW;
 }
 
@@ -84,8 +86,10 @@ __global__ void k_merge(const int32_t *__restrict__ a, int32_t na, const int32_t
 // Gather per-sorted-position scheduler slots: {client, cov, next token, state}.
 __global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__restrict__ queue, int32_t n,
                          const int32_t *__restrict__ cov, const int32_t *__restrict__ next,
+                         const int32_t *__restrict__ mlen, const int64_t *__restrict__ s0,
                          const int32_t *__restrict__ rclient, const int32_t *__restrict__ rlen,
-                         int32_t *__restrict__ s_req, int4 *__restrict__ slot, int32_t *__restrict__ s_len) {
+                         int32_t *__restrict__ s_req, int4 *__restrict__ slot, int32_t *__restrict__ s_len,
+                         int32_t *__restrict__ s_mlen0, int64_t *__restrict__ s_src0) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int32_t qi = perm[p];
@@ -93,6 +97,8 @@ __global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__rest
     s_req[p] = r;
     s_len[p] = rlen[r];
     slot[p] = make_int4(rclient[r], cov[qi], next[qi], 0);
+    s_mlen0[p] = mlen[qi];
+    s_src0[p] = s0[qi];
 }
 
 // ---------------------------------------------------------------- K3 + K4
@@ -102,6 +108,8 @@ struct FillArgs {
     const int32_t *s_req;
     int4 *slot;  // {client, cov(B), next token, state: >=0 pending w/ exact-epoch, -1 admitted}
     const int32_t *s_len;
+    const int32_t *s_mlen0;  // K1 match length and last chain (admission-walk hint)
+    const int64_t *s_src0;
     const int64_t *roff;
     int64_t *q, *refills;
     const uint8_t *known;
@@ -237,13 +245,34 @@ __device__ inline int64_t block_min_i64(int64_t v, int64_t *red) {
 // Exact pinned coverage B of a queued request (re-walk; only reached through
 // the filter in block_find).  One warp.
 __device__ inline void warp_resume(const FillArgs &a, int32_t p, int lane) {
+    const TrieView &t = a.t;
     const int32_t r = a.s_req[p];
     const int32_t len = a.s_len[p];
-    const int32_t *rq = a.t.arena + a.roff[r];
-    const WalkOut w = warp_walk<8>(a.t, rq, len, lane, nullptr, true);
+    const int32_t *rq = t.arena + a.roff[r];
+    const int32_t m0 = a.s_mlen0[p];
+    const int64_t S0 = a.s_src0[p];
+    int32_t cov;
+    int32_t y = -1;
+    if (m0 > 0) {
+        const int32_t c = t.pos[S0 + m0 - 1];
+        if (pos_valid(t, c, S0, m0 - 1)) y = c;
+    }
+    auto none = [](int64_t, int32_t, int32_t, int32_t) {};
+    if (y < 0) {
+        cov = warp_walk<8>(t, rq, len, lane, nullptr, true).cov;
+    } else {
+        // the step-start match still holds: coverage of its prefix from the
+        // deep end, then continue past a node boundary (inserts of this step)
+        cov = warp_cov_from_deepest(t, y, m0, lane);
+        if (cov == m0 && m0 == t.end[y] && m0 < len) {
+            WalkStart st;
+            st.node = y; st.idx = m0; st.nseg = 0; st.last = y; st.cov = cov; st.pinrun = true;
+            cov = warp_walk_from<8>(t, rq, len, lane, true, st, none).cov;
+        }
+    }
     if (lane == 0) {
-        a.slot[p].y = w.cov;
-        a.slot[p].z = w.cov < len ? rq[w.cov] : -1;
+        a.slot[p].y = cov;
+        a.slot[p].z = cov < len ? rq[cov] : -1;
     }
 }
 
@@ -385,7 +414,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int64_t pinb;
     if (tid == 0) pinb = t.sc->pinned;
     __syncthreads();
-    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins);
+    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j]);
     const long long ct = clock64();
     if (sm->ins.status == FS_OK) {
         block_pin_path(t, a.segs, sm->ins.nseg, +1);
@@ -561,7 +590,7 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
         case OP_PIN:
         case OP_UNPIN:
             // _chain from the deepest node (radix.py:164-172) == the nodes of its root path
-            block_path_of(t, t.src[a.node], t.end[a.node], a.segs, &s_nseg);
+            block_path_of(t, a.node, a.segs, &s_nseg);
             block_pin_path(t, a.segs, s_nseg, a.op == OP_PIN ? +1 : -1);
             __syncthreads();
             if (tid == 0) a.out[0] = t.sc->status;

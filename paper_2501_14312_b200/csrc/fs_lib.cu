@@ -270,7 +270,7 @@ struct fs_trie {
     int32_t ncap = 0;
     uint32_t hsize = 0;
     DBuf<int64_t> src, la, seq, lseq;
-    DBuf<int32_t> start, end, slen, parent, nchild, ref, first, freest;
+    DBuf<int32_t> start, end, slen, parent, nchild, ref, first, freest, ctop, cpar;
     int64_t opseq = 0;   // sequence number of the last stamping operation
     DBuf<uint8_t> flags;
     DBuf<uint64_t> wmask;
@@ -293,6 +293,7 @@ static TrieView view(fs_trie *t) {
     v.pos = t->pos.p;
     v.src = t->src.p; v.start = t->start.p; v.end = t->end.p; v.slen = t->slen.p; v.parent = t->parent.p;
     v.nchild = t->nchild.p; v.ref = t->ref.p; v.first = t->first.p;
+    v.ctop = t->ctop.p; v.cpar = t->cpar.p;
     v.la = t->la.p; v.seq = t->seq.p; v.lseq = t->lseq.p; v.flags = t->flags.p;
     v.wmask = t->track ? t->wmask.p : nullptr;
     v.wtime = t->track ? t->wtime.p : nullptr;
@@ -310,6 +311,7 @@ __global__ void k_trie_init(TrieView t, int64_t capacity) {
         s.used = 0; s.pinned = 0; s.next_seq = 1; s.capacity = capacity; s.nrec = 0;
         s.hw = 1; s.nfree = 0; s.status = 0; s.live = 1;
         t.src[0] = 0; t.start[0] = 0; t.end[0] = 0; t.slen[0] = 0; t.parent[0] = -1; t.nchild[0] = 0; t.ref[0] = 0;
+        t.ctop[0] = 0; t.cpar[0] = -1;
         t.la[0] = 0; t.seq[0] = 0; t.lseq[0] = 0; t.first[0] = -1; t.flags[0] = FS_ALIVE;
         if (t.wmask) t.wmask[0] = 0;
     }
@@ -355,6 +357,7 @@ static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
     TRY(dgrow(t->src, nc, s, true, keep)); TRY(dgrow(t->la, nc, s, true, keep)); TRY(dgrow(t->seq, nc, s, true, keep));
     TRY(dgrow(t->start, nc, s, true, keep)); TRY(dgrow(t->end, nc, s, true, keep)); TRY(dgrow(t->parent, nc, s, true, keep));
     TRY(dgrow(t->slen, nc, s, true, keep)); TRY(dgrow(t->lseq, nc, s, true, keep));
+    TRY(dgrow(t->ctop, nc, s, true, keep)); TRY(dgrow(t->cpar, nc, s, true, keep));
     TRY(dgrow(t->nchild, nc, s, true, keep)); TRY(dgrow(t->ref, nc, s, true, keep)); TRY(dgrow(t->first, nc, s, true, keep));
     TRY(dgrow(t->freest, nc, s, true, keep)); TRY(dgrow(t->flags, nc, s, true, keep));
     if (t->track) { TRY(dgrow(t->wmask, nc, s, true, keep)); TRY(dgrow(t->wtime, nc * t->nw, s, true, keep * t->nw)); }
@@ -411,7 +414,7 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     t->src.release(); t->la.release(); t->seq.release(); t->start.release(); t->end.release();
     t->parent.release(); t->nchild.release(); t->ref.release(); t->first.release(); t->freest.release();
     t->flags.release(); t->wmask.release(); t->wtime.release(); t->hslot.release(); t->slen.release();
-    t->lseq.release();
+    t->lseq.release(); t->ctop.release(); t->cpar.release();
     t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
     t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
@@ -447,7 +450,8 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     const int64_t blocks = (n * 32 + 255) / 256;
     const int64_t sq = stamp ? ++t->opseq : 0;
     k_match<<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
-                                                      stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr);
+                                                      stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr,
+                                                      nullptr);
     counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -683,7 +687,8 @@ struct fs_worker {
     DBuf<int64_t> newlab;
     DBuf<uint32_t> keys, keys2;
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
-    DBuf<int32_t> s_req, s_len, s_fnode;
+    DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0;
+    DBuf<int64_t> s0, s_src0;
     DBuf<int4> slot;
     DBuf<uint8_t> cub_tmp;
     DBuf<int32_t> nsel;
@@ -925,6 +930,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     TRY(dgrow(w->mlen, n + 1, s)); TRY(dgrow(w->cov, n + 1, s)); TRY(dgrow(w->fnode, n + 1, s));
     TRY(dgrow(w->next, n + 1, s)); TRY(dgrow(w->s_req, n + 1, s)); TRY(dgrow(w->s_len, n + 1, s));
     TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
+    TRY(dgrow(w->s_mlen0, n + 1, s)); TRY(dgrow(w->s0, n + 1, s)); TRY(dgrow(w->s_src0, n + 1, s));
     if (w->iota.cap < n + 1) {
         TRY(dgrow(w->iota, n + 1, s));
         k_iota<<<(unsigned)((w->iota.cap + 255) / 256), 256, 0, s>>>(w->iota.p, w->iota.cap);
@@ -989,8 +995,8 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     if (n > 0) {
         const int64_t blocks = (n * 32 + 255) / 256;
         k_match<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
-                                                  ++t->opseq, kmax, w->keys.p, nullptr, w->cov.p, w->next.p,
-                                                  (unsigned long long *)w->alg.p);
+                                                  ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
+                                                  w->s0.p, (unsigned long long *)w->alg.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -1001,8 +1007,9 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         CK(cub::DeviceRadixSort::SortPairs(w->cub_tmp.p, b, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)n, 0, (int)bits, s));
         counted(FS_CUB_SORT_LAUNCHES);
         k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p,
-                                                            w->next.p, c->rclient.p, c->rlen.p, w->s_req.p, w->slot.p,
-                                                            w->s_len.p);
+                                                            w->next.p, w->mlen.p, w->s0.p, c->rclient.p, c->rlen.p,
+                                                            w->s_req.p, w->slot.p, w->s_len.p, w->s_mlen0.p,
+                                                            w->s_src0.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -1012,6 +1019,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     a.t = view(t);
     a.n = (int32_t)n;
     a.s_req = w->s_req.p; a.slot = w->slot.p; a.s_len = w->s_len.p;
+    a.s_mlen0 = w->s_mlen0.p; a.s_src0 = w->s_src0.p;
     a.roff = c->roff.p;
     a.q = w->q.p; a.refills = w->refills.p; a.known = w->known.p; a.nclients = w->nclients; a.pend_cnt = w->pend_cnt.p;
     a.dl_client = w->dlc.p; a.dl_delta = w->dld.p; a.ndl = ndl;
