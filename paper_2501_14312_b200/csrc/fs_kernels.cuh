@@ -467,10 +467,21 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
+__global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     extern __shared__ __align__(16) unsigned char fs_smraw[];
     SchedSmem &sm = *reinterpret_cast<SchedSmem *>(fs_smraw);
+    // the trie's scalars (used/pinned/seq/free stack/records) live in shared
+    // memory for the whole step: every serial edit touches several of them
+    __shared__ FillArgs a_sh;
+    __shared__ TrieScalars sc_sh;
     const int tid = threadIdx.x;
+    if (tid == 0) {
+        a_sh = ap;
+        sc_sh = *ap.t.sc;
+        a_sh.t.sc = &sc_sh;
+    }
+    __syncthreads();
+    const FillArgs &a = a_sh;
     // on_outputs deltas accumulated since the last fill (local_policies.py:130-133)
     if (tid == 0) {
         for (int32_t i = 0; i < a.ndl; i++) a.q[a.dl_client[i]] += a.dl_delta[i];
@@ -542,6 +553,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs a) {
         sm.prof[7] = clock64() - t_start;
         for (int i = 0; i < 3; i++) sm.prof[8 + i] = sm.lru.prof[i];
         for (int i = 0; i < 16; i++) a.hdr[8 + i] = sm.prof[i];
+        *ap.t.sc = sc_sh;
     }
 }
 
