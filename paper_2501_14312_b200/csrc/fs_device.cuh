@@ -37,6 +37,7 @@
 
 #define FS_FULL 0xffffffffu
 #define FS_HEMPTY 0xffffffffffffffffull
+#define FS_HTOMB 0xfffffffffffffffeull  // deleted slot (real keys are < 2^63)
 
 #define FS_OK 0
 #define FS_ERR_INVALID 1
@@ -60,6 +61,8 @@ struct TrieScalars {
     int32_t nfree;     // free-stack depth
     int32_t status;    // sticky device error
     int32_t live;      // live nodes (incl. root)
+    int32_t tombs;     // deleted child-hash slots
+    int32_t pad_;
 };
 
 struct TrieView {
@@ -99,43 +102,46 @@ __device__ __forceinline__ uint32_t fs_hmix(uint64_t k) {
 __device__ __forceinline__ int32_t h_find(const TrieView &t, int32_t p, int32_t tok) {
     const uint64_t key = fs_hkey(p, tok);
     uint32_t i = fs_hmix(key) & t.hmask;
-    while (true) {
+    for (uint32_t probes = 0; probes <= t.hmask; probes++) {
         const ulonglong2 s = t.hslot[i];
         if (s.x == key) return (int32_t)s.y;
         if (s.x == FS_HEMPTY) return -1;
         i = (i + 1) & t.hmask;
     }
+    return -1;
 }
-// children[tok] = child
+// children[tok] = child (update in place, else the first free or deleted slot)
 __device__ inline void h_put(const TrieView &t, int32_t p, int32_t tok, int32_t child) {
     const uint64_t key = fs_hkey(p, tok);
     uint32_t i = fs_hmix(key) & t.hmask;
+    int64_t tomb = -1;
+    uint32_t probes = 0;
     while (true) {
         const uint64_t k = t.hslot[i].x;
-        if (k == key || k == FS_HEMPTY) { t.hslot[i] = make_ulonglong2(key, (unsigned long long)(uint32_t)child); return; }
+        if (k == key) break;
+        if (k == FS_HEMPTY || probes++ > t.hmask) {
+            if (tomb >= 0) { i = (uint32_t)tomb; t.sc->tombs--; }
+            else if (k != FS_HEMPTY) { t.sc->status = FS_ERR_NOMEM; return; }  // table full
+            break;
+        }
+        if (k == FS_HTOMB && tomb < 0) tomb = i;
         i = (i + 1) & t.hmask;
     }
+    t.hslot[i] = make_ulonglong2(key, (unsigned long long)(uint32_t)child);
 }
-// del children[tok] -- backward-shift deletion keeps probe chains intact
+// del children[tok] -- tombstone (one store); the host rebuilds the table when
+// tombstones pass a quarter of it (fs_lib.cu trie_maintain)
 __device__ inline void h_del(const TrieView &t, int32_t p, int32_t tok) {
     const uint64_t key = fs_hkey(p, tok);
     uint32_t i = fs_hmix(key) & t.hmask;
-    while (t.hslot[i].x != key) {
-        if (t.hslot[i].x == FS_HEMPTY) return;
+    for (uint32_t probes = 0;; probes++) {
+        const uint64_t k = t.hslot[i].x;
+        if (k == key) break;
+        if (k == FS_HEMPTY || probes > t.hmask) return;
         i = (i + 1) & t.hmask;
     }
-    uint32_t j = i;
-    while (true) {
-        j = (j + 1) & t.hmask;
-        const ulonglong2 sj = t.hslot[j];
-        if (sj.x == FS_HEMPTY) break;
-        const uint32_t h = fs_hmix(sj.x) & t.hmask;
-        const bool stay = (i <= j) ? (i < h && h <= j) : (i < h || h <= j);
-        if (stay) continue;
-        t.hslot[i] = sj;
-        i = j;
-    }
-    t.hslot[i] = make_ulonglong2(FS_HEMPTY, 0ull);
+    t.hslot[i].x = FS_HTOMB;
+    t.sc->tombs++;
 }
 
 // ---------------------------------------------------------------- nodes
@@ -714,15 +720,40 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
                 }
         }
         int32_t P = -1;
+        bool pcand = false;
+        int64_t pla = 0, pseq = 0;
         if (lane == 0) {
             sm->pops++;
             const int32_t plen = t.end[b];
             const int64_t remaining = needed - freed;
             if (whole) {
-                P = t.parent[b];
-                push_record(t, t.src[b], plen, plen - el);
-                trie_detach(t, b);
+                // push_record + trie_detach (radix.py:206-208, 226-230) with every
+                // load issued before the first store: two dependent rounds
+                P = Pb;
+                const int64_t srcb = t.src[b];
+                const int32_t firstb = t.first[b];
+                const int64_t lab = t.la[b], lsb = t.lseq[b];
+                const int32_t ncP = t.nchild[P], refP = t.ref[P];
+                const uint8_t flP = t.flags[P];
+                const int64_t laP = t.la[P], lsP = t.lseq[P], sqP = t.seq[P];
+                const uint64_t key = fs_hkey(P, firstb);
+                uint32_t hi = fs_hmix(key) & t.hmask;
+                ulonglong2 hs = t.hslot[hi];
+                for (uint32_t probes = 0; hs.x != key && hs.x != FS_HEMPTY && probes <= t.hmask; probes++) {
+                    hi = (hi + 1) & t.hmask;
+                    hs = t.hslot[hi];
+                }
+                push_record(t, srcb, plen, plen - el);
+                if (hs.x == key) { t.hslot[hi].x = FS_HTOMB; t.sc->tombs++; }
+                t.nchild[P] = ncP - 1;
+                int64_t newla = laP;
+                if (P > 0 && lsb > lsP) { t.la[P] = lab; t.lseq[P] = lsb; newla = lab; }
+                t.sc->used -= el;
+                node_free(t, b);
                 freed += el;
+                pcand = (flP & FS_ALIVE) && ncP - 1 == 0 && refP == 0;
+                pla = newla;
+                pseq = sqP;
             } else {
                 push_record(t, t.src[b], plen, (int32_t)(plen - remaining));
                 t.end[b] -= (int32_t)remaining;
@@ -741,9 +772,9 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
                 L->la[c] = cla; L->sq[c] = csq; L->nd[c] = cn;
                 // the parent joins the candidates once it becomes a leaf
                 // (radix.py:231-239): its chunk minimum can only drop
-                if (P > 0 && P < L->hw0 && P != protect && lru_candidate(t, P)) {
+                if (P > 0 && P < L->hw0 && P != protect && pcand) {
                     cp = P / L->ch;
-                    const int64_t pa = t.la[P], ps = t.seq[P];
+                    const int64_t pa = pla, ps = pseq;
                     if (L->nd[cp] < 0 || pa < L->la[cp] || (pa == L->la[cp] && ps < L->sq[cp])) {
                         L->la[cp] = pa; L->sq[cp] = ps; L->nd[cp] = P;
                     }

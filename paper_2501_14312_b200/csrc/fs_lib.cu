@@ -309,7 +309,7 @@ __global__ void k_trie_init(TrieView t, int64_t capacity) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         TrieScalars &s = *t.sc;
         s.used = 0; s.pinned = 0; s.next_seq = 1; s.capacity = capacity; s.nrec = 0;
-        s.hw = 1; s.nfree = 0; s.status = 0; s.live = 1;
+        s.hw = 1; s.nfree = 0; s.status = 0; s.live = 1; s.tombs = 0; s.pad_ = 0;
         t.src[0] = 0; t.start[0] = 0; t.end[0] = 0; t.slen[0] = 0; t.parent[0] = -1; t.nchild[0] = 0; t.ref[0] = 0;
         t.ctop[0] = 0; t.cpar[0] = -1;
         t.la[0] = 0; t.seq[0] = 0; t.lseq[0] = 0; t.first[0] = -1; t.flags[0] = FS_ALIVE;
@@ -318,8 +318,10 @@ __global__ void k_trie_init(TrieView t, int64_t capacity) {
 }
 
 __global__ void k_rehash(TrieView t) {
-    // rebuild the child hash from the node table after a resize
+    // rebuild the child hash from the node table (after a resize, or to drop
+    // tombstones); the table was reset to empty by the host
     const int32_t hw = t.sc->hw;
+    if (blockIdx.x == 0 && threadIdx.x == 0) t.sc->tombs = 0;
     for (int32_t n = 1 + blockIdx.x * blockDim.x + threadIdx.x; n < hw; n += gridDim.x * blockDim.x) {
         if (!(t.flags[n] & FS_ALIVE)) continue;
         const uint64_t key = fs_hkey(t.parent[n], t.first[n]);
@@ -350,6 +352,14 @@ static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
         CK(cudaMemsetAsync(t->pos.p + old, 0xff, sizeof(int32_t) * (t->pos.cap - old), s));
     }
     const int64_t need = (int64_t)t->h_sc.hw + extra_nodes + 4;
+    if (t->hsize > 0 && (int64_t)t->h_sc.tombs * 4 > (int64_t)t->hsize) {
+        // too many deleted slots lengthen probes: rebuild from the node table
+        CK(cudaMemsetAsync(t->hslot.p, 0xff, sizeof(ulonglong2) * t->hsize, s));
+        k_rehash<<<148, 256, 0, s>>>(view(t));
+        counted();
+        CK(cudaGetLastError());
+        t->h_sc.tombs = 0;
+    }
     if (need <= t->ncap) return FS_OK;
     const int64_t old = t->ncap;
     const int64_t nc = std::max<int64_t>(need, old * 2);
