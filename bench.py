@@ -204,11 +204,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    dev = local
+    tdev = "cpu"
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(local)
-        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        ngpu = torch.cuda.device_count() if args.impl == "ours" else 0
+        # one process per GPU over NCCL; ranks sharing a GPU (tests on a
+        # single-GPU box) fall back to gloo for the timing plumbing
+        if ngpu >= world:
+            torch.cuda.set_device(local)
+            tdist.init_process_group("nccl")
+            tdev = f"cuda:{local}"
+        else:
+            tdist.init_process_group("gloo")
+            dev = local % max(ngpu, 1)
         dist = tdist
 
     from paper_2501_14312_b200.workloads import build_docs, config2, shared_prefix_queue
@@ -243,7 +253,7 @@ def main():
         return
 
     from paper_2501_14312_b200.device import launch_count
-    g = GpuSteps(q, pool, local)
+    g = GpuSteps(q, pool, dev)
     now = 0
     for _ in range(args.warmup):
         now += STEP_US
@@ -277,13 +287,13 @@ def main():
     g.ctx.sync()
     t_total = time.perf_counter() - t_start
     launches = launch_count() - l0
-    clocks = clocks_stop(*clk, local) if rank == 0 else None
+    clocks = clocks_stop(*clk, dev) if rank == 0 else None
     if dist is not None:
         import torch
-        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms, wall = float(t[0]), float(t[1])
-        d = torch.tensor([decisions], dtype=torch.float64, device=f"cuda:{local}")
+        d = torch.tensor([decisions], dtype=torch.float64, device=tdev)
         dist.all_reduce(d, op=dist.ReduceOp.SUM)
         total_decisions = float(d[0])
     else:
