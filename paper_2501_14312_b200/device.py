@@ -33,7 +33,9 @@ def _pu8(a):
 class Context:
     """One CUDA device: token arena + request table (fs_ctx)."""
 
-    def __init__(self, device: int = 0, arena_tokens: int = 1 << 22, max_requests: int = 1 << 16):
+    def __init__(self, device: int | str = 0, arena_tokens: int = 1 << 22, max_requests: int = 1 << 16):
+        if isinstance(device, str):  # "cuda:N" / "cuda"
+            device = int(device.split(":")[1]) if ":" in device else 0
         L.load()
         h = C.c_void_p()
         call("fs_ctx_create", device, arena_tokens, max_requests, C.byref(h))
