@@ -36,15 +36,115 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M = 65536
-L_INPUT = 4096
 W_E, W_Q = 1, 2
-RESERVE = 8
-OUT_TOKENS = 8
-U = W_E * L_INPUT + W_Q * M
-Q_U = max(1, round(0.5 * U))  # q_u_frac 0.5 (runner.py:127)
 STEP_US = 10_000
-METRIC = "scheduling decisions/sec (DLPM schedule steps over a 64k-request queue)"
+DEFAULT_WORKLOAD = "c2"
+METRIC = "scheduling decisions/sec (DLPM schedule steps over the resident request queue)"
+
+
+class Workload:
+    """One BASELINE.json configuration: serving parameters, the initial queue
+    (put on the device untimed) and the pool of later arrivals (host tokens,
+    uploaded inside the timed steps)."""
+    name = ""
+    out_tokens = 8
+    reserve = 8
+
+    def quantum(self):
+        return max(1, round(0.5 * (W_E * self.L_INPUT + W_Q * self.M)))  # q_u_frac 0.5 (runner.py:127)
+
+
+class Config2(Workload):
+    """configs[1]: one worker, 100 clients, 64k queued 1-4k-token prompts with a
+    Zipf(1.1) shared-prefix tree over 256 documents."""
+    name = "c2"
+    M = CAP = 65536
+    L_INPUT = 4096
+    clients = 100
+
+    def __init__(self, nq, rank, steps):
+        from paper_2501_14312_b200.workloads import build_docs, config2, shared_prefix_queue
+        self.nq = nq
+        self.spec = config2(nq, seed=2 + rank)
+        docs = build_docs(self.spec)
+        self.q = shared_prefix_queue(self.spec, docs=docs)
+        pool_n = 800 * steps + 1024
+        self.pool = shared_prefix_queue(self.spec, first=nq, count=pool_n, arrival=STEP_US, docs=docs,
+                                        stream_seed=self.spec.seed + 101)
+        self.queue_tokens = int(self.q.lens.sum())
+        self.desc = ("config2: DLPM 1 worker/GPU, 100 clients, %d queued, 1-4k-token prompts, Zipf(1.1) prefixes "
+                     "over 256 docs, M=capacity=65536, q_u_frac=0.5, reserve=8" % nq)
+        self.l2 = ("inputs larger than L2: each step streams every queued request's matched prefix (~240 MB) "
+                   "and the queue occupies ~640 MB")
+
+    def put_initial(self, ctx):
+        ids = ctx.add_requests(self.q.flat, self.q.offsets, self.q.lens, self.q.clients, self.q.labels)
+        return ids, self.q.clients.astype(np.int32)
+
+    def cpu_sample(self, device):
+        return self.q, self.pool, len(self.q)
+
+
+class Config5(Workload):
+    """configs[4] at D=1: 1M queued 8k-token requests over a branching-4, depth-6
+    prefix tree of 1024-token levels (+ a unique 2048-token tail), 200 clients,
+    M = capacity = 262144.  Tokens are the reference's own universe
+    (expand_tokens, requests.py:89-102) generated on the device."""
+    name = "c5"
+    M = CAP = 262144
+    L_INPUT = 8192
+    clients = 200
+    CPU_NQ = 65536
+
+    def __init__(self, nq, rank, steps, device=0):
+        from paper_2501_14312_b200.workloads import config5
+        self.nq = nq
+        self.spec = config5(nq, seed=5 + rank)
+        self.pool_n = 160 * steps + 512
+        self.pool = self._host_queue(device, stream=1, first=0, count=self.pool_n, arrival=STEP_US)
+        self.queue_tokens = nq * self.spec.length
+        self.desc = ("config5 at D=1: DLPM, 200 clients, %d queued 8192-token prompts, branching-4 depth-6 prefix "
+                     "tree of 1024-token levels + unique 2048-token tail, M=capacity=262144, q_u_frac=0.5, "
+                     "reserve=8; tokens = expand_tokens (sha256) generated on device" % nq)
+        self.l2 = "inputs larger than L2: the queue occupies %.1f GB; each step streams every queued request's " \
+                  "matched prefix" % (self.queue_tokens * 4 / 1e9)
+
+    def _host_queue(self, device, stream, first, count, arrival):
+        """Materialize on the device, read back: host token buffers for arrivals / the CPU oracle."""
+        from paper_2501_14312_b200.device import Context
+        from paper_2501_14312_b200.trace import add_segments
+        from paper_2501_14312_b200.workloads import Queue, deep_tree_segments
+        segs, clients, labels = deep_tree_segments(self.spec, first=first, count=count, stream=stream)
+        lens = segs.lens()
+        tmp = Context(device, arena_tokens=int(lens.sum()) + 4 * count + 1024, max_requests=count + 16)
+        try:
+            ids = add_segments(tmp, segs, clients, labels)
+            off0, _ = tmp.request_info(int(ids[0]))
+            offl, lnl = tmp.request_info(int(ids[-1]))
+            raw = tmp.arena_read(off0, offl + lnl - off0)
+            offs = np.array([tmp.request_info(int(i))[0] - off0 for i in ids], np.int64)
+        finally:
+            tmp.close()
+        rids = [f"c5r{stream}.{first + i:08d}" for i in range(count)]
+        return Queue(raw, offs, lens.astype(np.int32), clients, np.full(count, arrival, np.int64), rids, labels)
+
+    def put_initial(self, ctx):
+        from paper_2501_14312_b200.trace import add_segments
+        from paper_2501_14312_b200.workloads import deep_tree_segments
+        segs, clients, labels = deep_tree_segments(self.spec, first=0, count=self.nq, stream=0)
+        return add_segments(ctx, segs, clients, labels), clients
+
+    def cpu_sample(self, device):
+        n = min(self.nq, self.CPU_NQ)
+        return self._host_queue(device, stream=0, first=0, count=n, arrival=0), self.pool, n
+
+
+def make_workload(name, nq, rank, steps):
+    if name == "c2":
+        return Config2(nq or 65536, rank, steps)
+    if name == "c5":
+        return Config5(nq or (1 << 20), rank, steps)
+    raise SystemExit(f"unknown workload {name}")
 
 
 def peaks():
@@ -59,15 +159,17 @@ def peaks():
 class GpuSteps:
     """The synthetic serving loop on the CUDA path, through the C ABI."""
 
-    def __init__(self, q, pool, device):
+    def __init__(self, wl, device):
         from paper_2501_14312_b200.device import Context, Trie, WorkerDev
-        self.q = q
-        self.pool = pool
-        tot = int(q.lens.sum()) + int(pool.lens.sum()) + 4 * (len(q) + len(pool)) + 1024
-        self.ctx = Context(device, arena_tokens=tot, max_requests=len(q) + len(pool) + 16)
-        self.trie = Trie(self.ctx, M)
-        self.w = WorkerDev(self.ctx, self.trie, "dlpm", Q_U, M, RESERVE, W_E, W_Q, max_clients=128)
-        self.ids = self.ctx.add_requests(q.flat, q.offsets, q.lens, q.clients, q.labels)
+        self.wl = wl
+        self.pool = wl.pool
+        tot = wl.queue_tokens + int(self.pool.lens.sum()) + 4 * (wl.nq + len(self.pool)) + 1024
+        self.ctx = Context(device, arena_tokens=tot, max_requests=wl.nq + len(self.pool) + 16)
+        self.trie = Trie(self.ctx, wl.CAP)
+        self.w = WorkerDev(self.ctx, self.trie, "dlpm", wl.quantum(), wl.M, wl.reserve, W_E, W_Q,
+                           max_clients=max(128, wl.clients))
+        self.ids, self.clients = wl.put_initial(self.ctx)
+        self.clients = list(np.asarray(self.clients, np.int32))
         self.w.enqueue(self.ids)
         self.prev_nodes = np.zeros(0, np.int32)
         self.prev_clients = np.zeros(0, np.int32)
@@ -79,7 +181,7 @@ class GpuSteps:
         n_prev = len(self.prev_nodes)
         if n_prev:
             cl, cnt = np.unique(self.prev_clients, return_counts=True)
-            self.w.outputs(cl.astype(np.int32), (cnt * OUT_TOKENS).astype(np.int64))
+            self.w.outputs(cl.astype(np.int32), (cnt * self.wl.out_tokens).astype(np.int64))
             self.trie.unpin_many(self.prev_nodes)
             self.h2d += cl.nbytes + cnt.nbytes + self.prev_nodes.nbytes
         if n_prev and self.pool_next + n_prev <= len(self.pool):
@@ -89,22 +191,20 @@ class GpuSteps:
             o1 = int(p.offsets[b - 1] + p.lens[b - 1])
             ids = self.ctx.add_requests(p.flat[o0:o1], p.offsets[a:b] - o0, p.lens[a:b], p.clients[a:b],
                                         p.labels[a:b])
+            self.clients.extend(int(c) for c in p.clients[a:b])
             self.w.enqueue(ids)
             self.pool_next = b
             self.h2d += (o1 - o0) * 4 + (b - a) * 24
         res = self.w.fill(now, 0, 0)
         self.prev_nodes = res.adm_node.astype(np.int32)
-        self.prev_clients = np.asarray(self.q_clients_of(res.adm_req), np.int32)
+        self.prev_clients = np.asarray([self.clients[int(i)] for i in res.adm_req], np.int32)
         self.d2h += res.adm_req.nbytes * 6 + 8 * 128 * 2 + 64
         return res
 
-    def q_clients_of(self, ids):
-        nq = len(self.q)
-        out = []
-        for i in ids:
-            i = int(i)
-            out.append(int(self.q.clients[i]) if i < nq else int(self.pool.clients[i - nq]))
-        return out
+    def close(self):
+        self.w.close()
+        self.trie.close()
+        self.ctx.close()
 
 
 def clocks_start():
@@ -148,12 +248,13 @@ def clocks_stop(p, fh, path, dev):
     return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(q, pool, warmup=5, steps_max=40, budget_s=15.0):
+def cpu_baseline(wl, q, pool, warmup=5, steps_max=40, budget_s=15.0):
     """C oracle (literal restatement of Dlpm.fill) on the same serving steps as
     the GPU loop, one core: `warmup` untimed steps, then timed steps until
     steps_max or the time budget."""
     from oracle.lockstep import OracleSteps
-    o = OracleSteps(_concat_once(None, q, pool), M, M, RESERVE, W_E, W_Q, Q_U, 128)
+    o = OracleSteps(_concat_once(None, q, pool), wl.CAP, wl.M, wl.reserve, W_E, W_Q, wl.quantum(),
+                    max(128, wl.clients), out_tokens=wl.out_tokens)
     o.enqueue(range(len(q)))
     pool_base = len(q)
     nxt = 0
@@ -196,7 +297,9 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--nq", type=int, default=65536)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["c2", "c5"],
+                    help="c2 = configs[1] (64k queue), c5 = configs[4] at D=1 (1M queue, 8k prompts)")
+    ap.add_argument("--nq", type=int, default=0, help="queued requests per GPU (default: the config's)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
 
@@ -221,24 +324,16 @@ def main():
             dev = local % max(ngpu, 1)
         dist = tdist
 
-    from paper_2501_14312_b200.workloads import build_docs, config2, shared_prefix_queue
-    spec = config2(args.nq, seed=2 + rank)
-    docs = build_docs(spec)
-    q = shared_prefix_queue(spec, docs=docs)
-    pool_n = 800 * (args.steps + args.warmup) + 1024
-    pool = shared_prefix_queue(spec, first=args.nq, count=pool_n, arrival=STEP_US, docs=docs, stream_seed=spec.seed + 101)
-    cfg = {"workload": "config2: DLPM 1 worker/GPU, 100 clients, 64k queued, 1-4k-token prompts, "
-                       "Zipf(1.1) prefixes over 256 docs, M=capacity=65536, q_u_frac=0.5, reserve=8",
-           "nq_per_gpu": args.nq, "clients": spec.clients, "M": M, "quantum": Q_U,
-           "l2": "inputs larger than L2: each step streams every queued request's matched prefix "
-                 "(~240 MB) and the queue occupies ~640 MB",
-           "parallelism": f"dp{args.gpus} (independent workers)"}
+    wl = make_workload(args.workload, args.nq, rank, args.steps + args.warmup)
+    cfg = {"workload": wl.desc, "nq_per_gpu": wl.nq, "clients": wl.clients, "M": wl.M, "capacity": wl.CAP,
+           "quantum": wl.quantum(), "l2": wl.l2, "parallelism": f"dp{args.gpus} (independent workers)"}
 
     if args.impl == "reference":
         if rank != 0:
             return
         t0 = time.perf_counter()
-        cb = cpu_baseline(q, pool, warmup=args.warmup, steps_max=args.steps, budget_s=120.0)
+        q, pool, ncpu = wl.cpu_sample(dev)
+        cb = cpu_baseline(wl, q, pool, warmup=args.warmup, steps_max=args.steps, budget_s=120.0)
         line = {"metric": METRIC, "value": cb["value"],
                 "unit": "decisions/s", "n_gpus": args.gpus, "steps": cb["steps"], "warmup": 0,
                 "ms_per_step": 1000 * cb["fill_s"] / max(cb["steps"], 1), "higher_is_better": True,
@@ -246,14 +341,14 @@ def main():
                 "config": cfg, "impl": "reference",
                 "cpu_baseline": {"value": cb["value"], "unit": "decisions/s", "cores": 1, "kind": "port",
                                  "sample": f"C oracle Dlpm.fill restatement, {cb['steps']} timed serving steps (after {args.warmup} "
-                                           f"untimed) of the {args.nq}-request queue, one core"},
+                                           f"untimed) of the {ncpu}-request queue of the same config, one core"},
                 "e2e": {"value": cb["value"], "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "wall_s": time.perf_counter() - t0}
         print(json.dumps(line))
         return
 
     from paper_2501_14312_b200.device import launch_count
-    g = GpuSteps(q, pool, dev)
+    g = GpuSteps(wl, dev)
     now = 0
     for _ in range(args.warmup):
         now += STEP_US
@@ -345,10 +440,12 @@ def main():
         "clocks": clocks, "host_wall_s": t_total,
     }
     if not args.no_cpu and world == 1:
-        cb = cpu_baseline(q, pool, warmup=args.warmup, steps_max=args.steps, budget_s=20.0)
+        g.close()
+        q, pool, ncpu = wl.cpu_sample(dev)
+        cb = cpu_baseline(wl, q, pool, warmup=args.warmup, steps_max=args.steps, budget_s=20.0)
         line["cpu_baseline"] = {"value": cb["value"], "unit": "decisions/s", "cores": 1, "kind": "port",
                                 "sample": f"C oracle (literal Dlpm.fill restatement), {cb['steps']} timed serving steps "
-                                          f"(after {args.warmup} untimed) of the same {args.nq}-request queue, one host core"}
+                                          f"(after {args.warmup} untimed) of a {ncpu}-request queue of the same config, one host core"}
     print(json.dumps(line))
 
 

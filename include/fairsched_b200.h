@@ -60,6 +60,18 @@ int fs_ctx_sync(fs_ctx *ctx);
 int fs_requests_add(fs_ctx *ctx, int64_t n, const int32_t *tokens, const int64_t *offsets,
                     const int32_t *lens, const int32_t *clients, const int64_t *labels,
                     int32_t *out_ids);
+/* Trace.materialize / expand_tokens / _token_block (requests.py:89-102, 134-161)
+ * on the device: append n requests whose tokens are generated in the arena.
+ * Request i is the concatenation of segments [seg_first[i], seg_first[i+1]);
+ * segment s is expand_tokens(ns, seg_len[s]) for namespace ns = seg_ns[s],
+ * i.e. blocks sha256(f"{ns}#{b}") -> 8 big-endian words % 2^31.  Namespace k
+ * is the UTF-8 string ns_bytes[ns_off[k] : ns_off[k]+ns_len[k]].  A "req:<rid>"
+ * prefix is passed as the parent's leading segments (every segment starts at
+ * block 0 of its namespace).  clients/labels as in fs_requests_add. */
+int fs_requests_add_expanded(fs_ctx *ctx, int64_t n, const int64_t *seg_first, const int32_t *seg_ns,
+                             const int32_t *seg_len, int64_t n_ns, const uint8_t *ns_bytes,
+                             const int64_t *ns_off, const int32_t *ns_len, const int32_t *clients,
+                             const int64_t *labels, int32_t *out_ids);
 /* Relabel requests (the order-maintenance labels ran out of gaps). */
 int fs_requests_set_labels(fs_ctx *ctx, int64_t n, const int32_t *ids, const int64_t *labels);
 int fs_requests_count(fs_ctx *ctx, int64_t *n);

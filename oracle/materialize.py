@@ -1,0 +1,61 @@
+"""TEST INFRASTRUCTURE ONLY -- CPU restatement of the reference's token universe.
+
+Restates, with hashlib, the three functions that turn a trace into token ids
+(`fairsched/requests.py`, arXiv 2501.14312):
+
+* `token_block`   -- `_token_block`  requests.py:89-92
+* `expand_tokens` -- `expand_tokens` requests.py:95-102
+* `materialize`   -- `Trace.materialize` requests.py:134-161 (tokens and
+  output lengths; no Request objects)
+
+Pinned by tests/test_materialize.py against tests/golden/tokens.json, which
+tests/golden/make_golden_tokens.py recorded from the real reference.  Only
+tests/ and bench.py's CPU leg use this module; the product materializes on the
+device (paper_2501_14312_b200/trace.py -> fs_requests_add_expanded).
+"""
+from __future__ import annotations
+
+import hashlib
+
+
+def token_block(namespace: str, block: int) -> tuple:
+    # requests.py:89-92: sha256(f"{namespace}#{block}") -> 8 big-endian words % 2^31
+    d = hashlib.sha256(f"{namespace}#{block}".encode()).digest()
+    return tuple(int.from_bytes(d[i:i + 4], "big") % (1 << 31) for i in range(0, 32, 4))
+
+
+def expand_tokens(namespace: str, length: int) -> tuple:
+    # requests.py:95-102: blocks 0, 1, ... until >= length, then out[:length]
+    out = []
+    b = 0
+    while len(out) < length:
+        out.extend(token_block(namespace, b))
+        b += 1
+    return tuple(out[:length])
+
+
+def materialize(records) -> tuple:
+    """requests.py:134-161 over records exposing rid, shared_prefix_id,
+    prefix_len, input_token_count, true_output_len (objects or dicts).
+    Returns ({rid: tokens} in record order, {rid: true_output_len})."""
+    inputs = {}
+    out_lens = {}
+    order = []
+    for rec in records:
+        g = rec.get if isinstance(rec, dict) else (lambda k, r=rec: getattr(r, k))
+        rid, spid, plen = g("rid"), g("shared_prefix_id"), g("prefix_len")
+        if spid.startswith("req:"):
+            base = inputs[spid[4:]]
+            if plen > len(base):
+                raise ValueError(f"{rid}: prefix_len exceeds parent input")
+            prefix = base[:plen]
+        else:
+            prefix = expand_tokens(spid, plen)
+        suffix_len = g("input_token_count") - plen
+        if suffix_len < 0:
+            raise ValueError(f"{rid}: prefix_len exceeds input_token_count")
+        toks = prefix + expand_tokens(f"sfx:{rid}", suffix_len)
+        inputs[rid] = toks
+        out_lens[rid] = g("true_output_len")
+        order.append((rid, toks))
+    return order, out_lens

@@ -89,15 +89,20 @@ __global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__rest
                          const int32_t *__restrict__ mlen, const int64_t *__restrict__ s0,
                          const int32_t *__restrict__ rclient, const int32_t *__restrict__ rlen,
                          int32_t *__restrict__ s_req, int4 *__restrict__ slot, int32_t *__restrict__ s_len,
-                         int32_t *__restrict__ s_mlen0, int64_t *__restrict__ s_src0) {
+                         int32_t *__restrict__ s_mlen0, int64_t *__restrict__ s_src0,
+                         const int32_t *__restrict__ arena, const int64_t *__restrict__ roff,
+                         int32_t *__restrict__ s_tok0) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int32_t qi = perm[p];
     const int32_t r = queue[qi];
+    const int32_t len = rlen[r];
+    const int32_t m0 = mlen[qi];
     s_req[p] = r;
-    s_len[p] = rlen[r];
+    s_len[p] = len;
     slot[p] = make_int4(rclient[r], cov[qi], next[qi], 0);
-    s_mlen0[p] = mlen[qi];
+    s_mlen0[p] = m0;
+    s_tok0[p] = m0 < len ? arena[roff[r] + m0] : -1;  // first token the step-start trie misses
     s_src0[p] = s0[qi];
 }
 
@@ -109,6 +114,7 @@ struct FillArgs {
     int4 *slot;  // {client, cov(B), next token, state: >=0 pending w/ exact-epoch, -1 admitted}
     const int32_t *s_len;
     const int32_t *s_mlen0;  // K1 match length and last chain (admission-walk hint)
+    const int32_t *s_tok0;   // token at s_mlen0 (-1 when fully matched): the miss key
     const int64_t *s_src0;
     const int64_t *roff;
     int64_t *q, *refills;
@@ -144,21 +150,34 @@ __device__ __forceinline__ unsigned long long adm_key(int32_t B, int32_t tok) {
     return ((unsigned long long)(uint32_t)B << 32) | (uint32_t)tok;
 }
 
-__device__ inline void adm_put(AdmFilter *f, int32_t B, int32_t tok, int32_t e) {
-    if (tok < 0) return;  // a request fully covered by pins extends nothing
+// Miss keys share the table, tagged by bit 63 (depths are < 2^31).
+// Upper bound on any queued request's coverage during a fill: the trie at any
+// point of the fill holds only strings that were in it at step start or are
+// prefixes of requests admitted since, so B_p <= mlen_p <= max(mlen0_p,
+// max_e LCP(p, e)).  LCP(p, e) > mlen0_p needs p[:mlen0_p+1] == e[:mlen0_p+1];
+// that string was absent at step start while p[:mlen0_p] was present, so e's
+// own step-start match ended at the same depth: mlen0_e == mlen0_p and
+// tok0_e == tok0_p.  With no admission carrying p's miss key, B_p <= mlen0_p.
+__device__ __forceinline__ unsigned long long miss_key(int32_t m0, int32_t tok) {
+    return ((unsigned long long)((uint32_t)m0 | 0x80000000u) << 32) | (uint32_t)tok;
+}
+
+__device__ inline void adm_put_key(AdmFilter *f, unsigned long long k, int32_t e) {
     if (f->n * 2 >= FS_FSLOTS) { f->saturated = 1; return; }
-    const unsigned long long k = adm_key(B, tok);
     uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
     while (f->key[i] != FS_HEMPTY && f->key[i] != k) i = (i + 1) & (FS_FSLOTS - 1);
     if (f->key[i] == FS_HEMPTY) { f->key[i] = k; f->n++; }
     f->ep[i] = e;
 }
 
-// true when some admission in [since, now) had the same (B, token)
-__device__ __forceinline__ bool adm_maybe(const AdmFilter *f, int32_t B, int32_t tok, int32_t since) {
-    if (tok < 0) return false;
+__device__ inline void adm_put(AdmFilter *f, int32_t B, int32_t tok, int32_t m0, int32_t tok0, int32_t e) {
+    if (tok >= 0) adm_put_key(f, adm_key(B, tok), e);  // a request fully covered by pins extends nothing
+    if (tok0 >= 0) adm_put_key(f, miss_key(m0, tok0), e);
+}
+
+// true when some admission in [since, now) had key k
+__device__ __forceinline__ bool adm_maybe_key(const AdmFilter *f, unsigned long long k, int32_t since) {
     if (f->saturated) return true;
-    const unsigned long long k = adm_key(B, tok);
     uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
     while (true) {
         const unsigned long long x = f->key[i];
@@ -166,6 +185,22 @@ __device__ __forceinline__ bool adm_maybe(const AdmFilter *f, int32_t B, int32_t
         if (x == FS_HEMPTY) return false;
         i = (i + 1) & (FS_FSLOTS - 1);
     }
+}
+
+// true when some admission in [since, now) had the same (B, token)
+__device__ __forceinline__ bool adm_maybe(const AdmFilter *f, int32_t B, int32_t tok, int32_t since) {
+    if (tok < 0) return false;
+    return adm_maybe_key(f, adm_key(B, tok), since);
+}
+
+// Can position p's exact coverage reach len - slack at all this fill?  False
+// only when the miss-key bound (above) rules it out; slack never grows within
+// a fill, so such a request needs no re-walk until its miss key is admitted.
+__device__ __forceinline__ bool cov_may_reach(const FillArgs &a, const AdmFilter *f, int32_t p, int64_t slack) {
+    const int32_t m0 = a.s_mlen0[p];
+    if (a.s_len[p] - m0 <= slack) return true;
+    const int32_t t0 = a.s_tok0[p];
+    return t0 >= 0 && adm_maybe_key(f, miss_key(m0, t0), 0);
 }
 
 struct SchedSmem {
@@ -300,7 +335,8 @@ __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int
                     if (a.s_len[p] - s.y <= slack) {
                         q = true;
                     } else if (s.w < epoch) {
-                        if (adm_maybe(&sm->flt, s.y, s.z, s.w)) r = true; else a.slot[p].w = epoch;
+                        if (!adm_maybe(&sm->flt, s.y, s.z, s.w)) a.slot[p].w = epoch;
+                        else if (cov_may_reach(a, &sm->flt, p, slack)) r = true;
                     }
                 }
             }
@@ -350,8 +386,8 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
             const int32_t need = a.s_len[p] - s.y;
             if (need <= slack) { mine = p; continue; }
             if (s.w < epoch) {
-                if (adm_maybe(&sm->flt, s.y, s.z, s.w)) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
-                else a.slot[p].w = epoch;  // B is still exact
+                if (!adm_maybe(&sm->flt, s.y, s.z, s.w)) a.slot[p].w = epoch;  // B is still exact
+                else if (cov_may_reach(a, &sm->flt, p, slack)) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
             }
         }
         const int32_t minA = block_min_i32(mine, sm->red32);
@@ -447,7 +483,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
                 a.adm_rec_end[e] = t.sc->nrec;
             }
             sm->nadm = e + 1;
-            adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, sm->epoch);
+            adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, a.s_mlen0[j], a.s_tok0[j], sm->epoch);
             sm->epoch++;
             a.slot[j].w = -1;
             a.rstate[r] = 2;

@@ -19,6 +19,7 @@
 
 #include "../../include/fairsched_b200.h"
 #include "fs_kernels.cuh"
+#include "fs_materialize.cuh"
 
 // ---------------------------------------------------------------- errors
 static thread_local std::string g_err;
@@ -118,6 +119,10 @@ struct fs_ctx {
     HBuf<int32_t> stage_tok;
     HBuf<int64_t> stage64;
     HBuf<int32_t> stage32;
+    // fs_requests_add_expanded scratch
+    DBuf<int64_t> x_dst, x_nsoff;
+    DBuf<int32_t> x_len, x_ns, x_nslen;
+    DBuf<uint8_t> x_bytes;
 };
 
 static int ctx_use(fs_ctx *c) {
@@ -156,6 +161,8 @@ extern "C" int fs_ctx_destroy(fs_ctx *c) {
     c->arena.release(); c->roff.release(); c->rlen.release(); c->rclient.release();
     c->rlabel.release(); c->rstate.release();
     c->stage_tok.release(); c->stage64.release(); c->stage32.release();
+    c->x_dst.release(); c->x_nsoff.release(); c->x_len.release(); c->x_ns.release(); c->x_nslen.release();
+    c->x_bytes.release();
     cudaStreamDestroy(c->stream);
     delete c;
     return FS_OK;
@@ -163,6 +170,37 @@ extern "C" int fs_ctx_destroy(fs_ctx *c) {
 
 extern "C" int fs_ctx_sync(fs_ctx *c) {
     TRY(ctx_use(c));
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+// Request-table rows for n requests already placed at place[i] in the arena.
+static int append_request_meta(fs_ctx *c, int64_t n, const int64_t *place, const int32_t *lens,
+                               const int32_t *clients, const int64_t *labels, int32_t *out_ids) {
+    const int64_t base_id = (int64_t)c->h_roff.size();
+    const int64_t nr = base_id + n;
+    TRY(dgrow(c->roff, nr, c->stream, true, base_id));
+    TRY(dgrow(c->rlen, nr, c->stream, true, base_id));
+    TRY(dgrow(c->rclient, nr, c->stream, true, base_id));
+    TRY(dgrow(c->rlabel, nr, c->stream, true, base_id));
+    if (c->rstate.cap < nr) {
+        const int64_t old = c->rstate.cap;
+        TRY(dgrow(c->rstate, nr, c->stream, true, base_id));
+        CK(cudaMemsetAsync(c->rstate.p + old, 0, c->rstate.cap - old, c->stream));
+    }
+    for (int64_t i = 0; i < n; i++) {
+        c->h_roff.push_back(place[i]);
+        c->h_rlen.push_back(lens[i]);
+        c->h_rclient.push_back(clients ? clients[i] : 0);
+        c->h_rlabel.push_back(labels ? labels[i] : base_id + i);
+        c->max_len = std::max(c->max_len, lens[i]);
+        if (out_ids) out_ids[i] = (int32_t)(base_id + i);
+    }
+    CK(cudaStreamSynchronize(c->stream));  // staging buffer reuse
+    CK(cudaMemcpyAsync(c->roff.p + base_id, c->h_roff.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->rlen.p + base_id, c->h_rlen.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->rclient.p + base_id, c->h_rclient.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->rlabel.p + base_id, c->h_rlabel.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return FS_OK;
 }
@@ -196,30 +234,72 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
     }
     if (total) CK(cudaMemcpyAsync(c->arena.p + c->arena_used, c->stage_tok.p, sizeof(int32_t) * total,
                                   cudaMemcpyHostToDevice, c->stream));
-    const int64_t nr = base_id + n;
-    TRY(dgrow(c->roff, nr, c->stream, true, base_id));
-    TRY(dgrow(c->rlen, nr, c->stream, true, base_id));
-    TRY(dgrow(c->rclient, nr, c->stream, true, base_id));
-    TRY(dgrow(c->rlabel, nr, c->stream, true, base_id));
-    if (c->rstate.cap < nr) {
-        const int64_t old = c->rstate.cap;
-        TRY(dgrow(c->rstate, nr, c->stream, true, base_id));
-        CK(cudaMemsetAsync(c->rstate.p + old, 0, c->rstate.cap - old, c->stream));
+    TRY(append_request_meta(c, n, place.data(), lens, clients, labels, out_ids));
+    c->arena_used += total;
+    return FS_OK;
+}
+
+extern "C" int fs_requests_add_expanded(fs_ctx *c, int64_t n, const int64_t *seg_first, const int32_t *seg_ns,
+                                        const int32_t *seg_len, int64_t n_ns, const uint8_t *ns_bytes,
+                                        const int64_t *ns_off, const int32_t *ns_len, const int32_t *clients,
+                                        const int64_t *labels, int32_t *out_ids) {
+    if (!c || n < 0 || n_ns < 0 || (n > 0 && (!seg_first || !clients)) || (n_ns > 0 && (!ns_off || !ns_len)))
+        return fail(FS_ERR_INVALID, "bad arguments");
+    TRY(ctx_use(c));
+    const int64_t base_id = (int64_t)c->h_roff.size();
+    if (base_id + n > INT32_MAX) return fail(FS_ERR_NOMEM, "request id space exhausted");
+    if (n == 0) return FS_OK;
+    if (seg_first[0] != 0) return fail(FS_ERR_INVALID, "seg_first[0] must be 0");
+    const int64_t nseg = seg_first[n];
+    int64_t nbytes = 0;
+    for (int64_t k = 0; k < n_ns; k++) {
+        if (ns_len[k] < 0 || ns_off[k] < 0) return fail(FS_ERR_INVALID, "bad namespace %lld", (long long)k);
+        nbytes = std::max<int64_t>(nbytes, ns_off[k] + ns_len[k]);
     }
+    std::vector<int64_t> place(n), dst(std::max<int64_t>(nseg, 1));
+    std::vector<int32_t> lens(n);
+    int64_t total = 0;
     for (int64_t i = 0; i < n; i++) {
-        c->h_roff.push_back(place[i]);
-        c->h_rlen.push_back(lens[i]);
-        c->h_rclient.push_back(clients ? clients[i] : 0);
-        c->h_rlabel.push_back(labels ? labels[i] : base_id + i);
-        c->max_len = std::max(c->max_len, lens[i]);
-        if (out_ids) out_ids[i] = (int32_t)(base_id + i);
+        if (seg_first[i + 1] < seg_first[i]) return fail(FS_ERR_INVALID, "seg_first not monotone");
+        place[i] = c->arena_used + total;
+        int64_t L = 0;
+        for (int64_t s = seg_first[i]; s < seg_first[i + 1]; s++) {
+            if (seg_len[s] < 0 || seg_ns[s] < 0 || seg_ns[s] >= n_ns)
+                return fail(FS_ERR_INVALID, "bad segment %lld", (long long)s);
+            dst[s] = place[i] + L;
+            L += seg_len[s];
+        }
+        if (L > INT32_MAX) return fail(FS_ERR_INVALID, "request %lld longer than 2^31 tokens", (long long)i);
+        lens[i] = (int32_t)L;
+        total += (L + 3) & ~3LL;
     }
-    CK(cudaStreamSynchronize(c->stream));  // staging buffer reuse
-    CK(cudaMemcpyAsync(c->roff.p + base_id, c->h_roff.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->rlen.p + base_id, c->h_rlen.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->rclient.p + base_id, c->h_rclient.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->rlabel.p + base_id, c->h_rlabel.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
+    TRY(dgrow(c->x_dst, nseg + 1, c->stream)); TRY(dgrow(c->x_len, nseg + 1, c->stream));
+    TRY(dgrow(c->x_ns, nseg + 1, c->stream));
+    TRY(dgrow(c->x_nsoff, n_ns + 1, c->stream)); TRY(dgrow(c->x_nslen, n_ns + 1, c->stream));
+    TRY(dgrow(c->x_bytes, nbytes + 16, c->stream));
+    // pad tails of 16-B slots stay zero, like fs_requests_add
+    CK(cudaMemsetAsync(c->arena.p + c->arena_used, 0, sizeof(int32_t) * total, c->stream));
+    if (nseg) {
+        CK(cudaMemcpyAsync(c->x_dst.p, dst.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_len.p, seg_len, sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_ns.p, seg_ns, sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, c->stream));
+    }
+    if (n_ns) {
+        CK(cudaMemcpyAsync(c->x_nsoff.p, ns_off, sizeof(int64_t) * n_ns, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_nslen.p, ns_len, sizeof(int32_t) * n_ns, cudaMemcpyHostToDevice, c->stream));
+    }
+    if (nbytes) CK(cudaMemcpyAsync(c->x_bytes.p, ns_bytes, nbytes, cudaMemcpyHostToDevice, c->stream));
+    if (nseg) {
+        ExpandArgs a;
+        a.arena = c->arena.p; a.seg_dst = c->x_dst.p; a.seg_len = c->x_len.p; a.seg_ns = c->x_ns.p;
+        a.ns_bytes = c->x_bytes.p; a.ns_off = c->x_nsoff.p; a.ns_len = c->x_nslen.p; a.nseg = nseg;
+        const int64_t blocks = std::min<int64_t>((nseg + 7) / 8, 148LL * 16);
+        k_expand<<<(int)std::max<int64_t>(blocks, 1), 256, 0, c->stream>>>(a);
+        counted();
+        CK(cudaGetLastError());
+    }
+    TRY(append_request_meta(c, n, place.data(), lens.data(), clients, labels, out_ids));
     c->arena_used += total;
     return FS_OK;
 }
@@ -697,7 +777,7 @@ struct fs_worker {
     DBuf<int64_t> newlab;
     DBuf<uint32_t> keys, keys2;
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
-    DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0;
+    DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
     DBuf<int64_t> s0, s_src0;
     DBuf<int4> slot;
     DBuf<uint8_t> cub_tmp;
@@ -765,7 +845,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -939,7 +1019,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     TRY(dgrow(w->keys, n + 1, s)); TRY(dgrow(w->keys2, n + 1, s)); TRY(dgrow(w->perm, n + 1, s));
     TRY(dgrow(w->mlen, n + 1, s)); TRY(dgrow(w->cov, n + 1, s)); TRY(dgrow(w->fnode, n + 1, s));
     TRY(dgrow(w->next, n + 1, s)); TRY(dgrow(w->s_req, n + 1, s)); TRY(dgrow(w->s_len, n + 1, s));
-    TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
+    TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->s_tok0, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
     TRY(dgrow(w->s_mlen0, n + 1, s)); TRY(dgrow(w->s0, n + 1, s)); TRY(dgrow(w->s_src0, n + 1, s));
     if (w->iota.cap < n + 1) {
         TRY(dgrow(w->iota, n + 1, s));
@@ -1019,7 +1099,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p,
                                                             w->next.p, w->mlen.p, w->s0.p, c->rclient.p, c->rlen.p,
                                                             w->s_req.p, w->slot.p, w->s_len.p, w->s_mlen0.p,
-                                                            w->s_src0.p);
+                                                            w->s_src0.p, c->arena.p, c->roff.p, w->s_tok0.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -1029,7 +1109,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     a.t = view(t);
     a.n = (int32_t)n;
     a.s_req = w->s_req.p; a.slot = w->slot.p; a.s_len = w->s_len.p;
-    a.s_mlen0 = w->s_mlen0.p; a.s_src0 = w->s_src0.p;
+    a.s_mlen0 = w->s_mlen0.p; a.s_src0 = w->s_src0.p; a.s_tok0 = w->s_tok0.p;
     a.roff = c->roff.p;
     a.q = w->q.p; a.refills = w->refills.p; a.known = w->known.p; a.nclients = w->nclients; a.pend_cnt = w->pend_cnt.p;
     a.dl_client = w->dlc.p; a.dl_delta = w->dld.p; a.ndl = ndl;

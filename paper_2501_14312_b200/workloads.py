@@ -104,3 +104,72 @@ def shared_prefix_queue(spec: SharedPrefixSpec, first: int = 0, count: int | Non
     # (arrival, rid) rank; zero-padded rids sort numerically
     labels = (np.int64(arrival) << 32) + np.arange(first, first + count, dtype=np.int64)
     return Queue(flat, offsets, L.astype(np.int32), C, arr, rids, labels)
+
+
+# ---------------------------------------------------------------------------
+# Config 5: 1M queued 8k-token requests over a deep prefix tree.
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DeepTreeSpec:
+    n: int = 1 << 20
+    clients: int = 200
+    branching: int = 4
+    depth: int = 6
+    level_tokens: int = 1024
+    length: int = 8192
+    seed: int = 5
+
+
+def config5(n: int = 1 << 20, seed: int = 5) -> DeepTreeSpec:
+    """Config 5: branching-4, depth-6 prefix tree of 1024-token levels, a unique
+    tail to 8192 tokens, 200 clients, seed 5."""
+    return DeepTreeSpec(n=n, seed=seed)
+
+
+def deep_tree_segments(spec: DeepTreeSpec, first: int = 0, count: int | None = None, stream: int = 0):
+    """Requests [first, first+count) of the config-5 stream as device segments.
+
+    Request i walks a random root-to-depth path of the tree; level l of node k
+    (heap numbering, root 0) is expand_tokens(f"c5n:{k}", level_tokens) and the
+    tail is expand_tokens(f"sfx:c5r{stream}.{i:08d}", length - depth*level_tokens),
+    i.e. the reference's own token universe (requests.py:89-102).
+    Returns (Segments, clients int32, labels int64)."""
+    from .trace import Segments
+    count = spec.n - first if count is None else count
+    g = np.random.Generator(np.random.PCG64(spec.seed * 7919 + first + 1_000_003 * stream))
+    digits = g.integers(0, spec.branching, size=(count, spec.depth), dtype=np.int64)
+    clients = g.integers(0, spec.clients, size=count, dtype=np.int64).astype(np.int32)
+    n_nodes = sum(spec.branching ** l for l in range(spec.depth + 1))
+    node_ns = [f"c5n:{k}".encode() for k in range(n_nodes)]
+    tail_ns = ("".join(f"sfx:c5r{stream}.{first + i:08d}" for i in range(count))).encode()
+    tail_w = len(f"sfx:c5r{stream}.{0:08d}")
+    node_off = np.zeros(n_nodes, np.int64)
+    node_len = np.array([len(b) for b in node_ns], np.int32)
+    node_off[1:] = np.cumsum(node_len[:-1])
+    node_bytes = b"".join(node_ns)
+    ns_bytes = np.frombuffer(node_bytes + tail_ns, np.uint8).copy()
+    ns_off = np.concatenate([node_off, len(node_bytes) + tail_w * np.arange(count, dtype=np.int64)])
+    ns_len = np.concatenate([node_len, np.full(count, tail_w, np.int32)])
+    tail = spec.length - spec.depth * spec.level_tokens
+    per = spec.depth + (1 if tail > 0 else 0)
+    seg_ns = np.empty((count, per), np.int32)
+    seg_len = np.empty((count, per), np.int32)
+    node = np.zeros(count, np.int64)
+    for l in range(spec.depth):
+        node = node * spec.branching + digits[:, l] + 1
+        seg_ns[:, l] = node
+        seg_len[:, l] = spec.level_tokens
+    if tail > 0:
+        seg_ns[:, spec.depth] = n_nodes + np.arange(count)
+        seg_len[:, spec.depth] = tail
+    segs = Segments(np.arange(count + 1, dtype=np.int64) * per, seg_ns.reshape(-1), seg_len.reshape(-1),
+                    ns_bytes, ns_off, ns_len)
+    labels = (np.int64(stream) << 40) + np.arange(first, first + count, dtype=np.int64)
+    return segs, clients, labels
+
+
+def segments_namespaces(segs) -> list:
+    """Decode the namespace string of every segment (tests / oracle side)."""
+    b = segs.ns_bytes.tobytes()
+    return [b[int(segs.ns_off[k]):int(segs.ns_off[k]) + int(segs.ns_len[k])].decode() for k in segs.seg_ns]

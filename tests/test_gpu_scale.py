@@ -1,5 +1,6 @@
-"""Scale parity: the CUDA path against the CPU oracle on the config-2 serving
-loop (Zipf shared-prefix queue, 100 clients) at sizes the golden traces do not
+"""Scale parity: the CUDA path against the CPU oracle on the bench's serving
+loops (config 2: Zipf shared-prefix queue, 100 clients; config 5: deep prefix
+tree of 8k-token prompts, 200 clients) at sizes the golden traces do not
 reach -- every step's admissions, admission-time match lengths, deficit
 counters, refill counts, eviction records and tree usage must be identical."""
 import numpy as np
@@ -8,20 +9,18 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(nq, steps, seed):
+def _run_wl(wl, steps):
     import bench
     from oracle.lockstep import OracleSteps
-    from paper_2501_14312_b200.workloads import build_docs, config2, shared_prefix_queue
 
-    spec = config2(nq, seed=seed)
-    docs = build_docs(spec)
-    q = shared_prefix_queue(spec, docs=docs)
-    pool = shared_prefix_queue(spec, first=nq, count=96 * steps + 64, arrival=bench.STEP_US, docs=docs,
-                               stream_seed=seed + 101)
-    g = bench.GpuSteps(q, pool, 0)
-    o = OracleSteps(bench._concat_once(None, q, pool), bench.M, bench.M, bench.RESERVE, bench.W_E, bench.W_Q,
-                    bench.Q_U, 128)
-    o.enqueue(range(nq))
+    q, pool, n = wl.cpu_sample(0)
+    assert n == wl.nq
+    g = bench.GpuSteps(wl, 0)
+    o = OracleSteps(bench._concat_once(None, q, pool), wl.CAP, wl.M, wl.reserve, bench.W_E, bench.W_Q,
+                    wl.quantum(), max(128, wl.clients), out_tokens=wl.out_tokens)
+    o.enqueue(range(len(q)))
+    nq = len(q)
+    nc = max(128, wl.clients)
     nxt = 0
     total_adm = 0
     for k in range(steps):
@@ -30,9 +29,9 @@ def _run(nq, steps, seed):
         ro = o.step(now)
         assert [int(x) for x in rg.adm_req] == ro["admitted"], f"step {k}: admissions differ"
         assert [int(x) for x in rg.adm_mlen] == ro["mlen"], f"step {k}: match lengths differ"
-        qg, rfg, _ = g.w.counters(128)
-        assert (qg == ro["q"][:128]).all(), f"step {k}: deficit counters differ"
-        assert (rfg == ro["refills"][:128]).all(), f"step {k}: refill counts differ"
+        qg, rfg, _ = g.w.counters(nc)
+        assert (qg == ro["q"][:nc]).all(), f"step {k}: deficit counters differ"
+        assert (rfg == ro["refills"][:nc]).all(), f"step {k}: refill counts differ"
         assert (rg.used, rg.pinned) == (ro["used"], ro["pinned"]), f"step {k}: used/pinned differ"
         recs_g = [(tuple(g.ctx.arena_read(int(s), int(n))), int(kp))
                   for s, n, kp in zip(rg.records.src, rg.records.length, rg.records.keep)]
@@ -44,13 +43,22 @@ def _run(nq, steps, seed):
             nxt += n
         total_adm += n
     assert total_adm > steps  # the loop really admits and evicts
-    g.ctx.close()
+    g.close()
     return total_adm
 
 
 def test_scale_8k():
-    _run(8192, 12, 11)
+    import bench
+    _run_wl(bench.Config2(8192, 9, 12), 12)
 
 
 def test_scale_64k():
-    _run(65536, 6, 2)
+    import bench
+    _run_wl(bench.Config2(65536, 0, 6), 6)
+
+
+def test_scale_config5_64k():
+    """Config 5 (deep prefix tree, 8k-token prompts, device-generated sha256
+    tokens) at 64k queued requests against the oracle on the same tokens."""
+    import bench
+    _run_wl(bench.Config5(65536, 0, 10), 10)
