@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 
 W_E, W_Q = 1, 2
 STEP_US = 10_000
-DEFAULT_WORKLOAD = "c2"
+DEFAULT_WORKLOAD = "c5"
 METRIC = "scheduling decisions/sec (DLPM schedule steps over the resident request queue)"
 
 

@@ -20,6 +20,7 @@
 #define FS_NONE 0x7fffffff
 
 // ---------------------------------------------------------------- K1
+template <int U>
 __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
                                                int64_t now, int stamp, int64_t sq, uint32_t kmax,
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
     const int32_t r = ids[i];
     const int32_t len = rlen[r];
     const int32_t *rq = t.arena + roff[r];
-    const WalkOut w = warp_walk(t, rq, len, lane, nullptr, true);
+    const WalkOut w = warp_walk<U>(t, rq, len, lane, nullptr, true);
     if (lane == 0) {
         // match_prefix stamps every matched node (radix.py:86-90): lazily, at the deepest
         if (stamp && w.last > 0) stamp_node(t, w.last, now, sq);
@@ -133,7 +134,30 @@ struct FillArgs {
     int32_t adm_cap;
     int8_t *rstate;
     int64_t *hdr;  // [n_adm, n_rec, status, epochs, refill_events, resumes, -, -, prof[8]]
+    // grid sweep (see k_schedule): helper CTAs 1..nhelp, control block, filter mirror
+    struct SweepCtl *ctl;
+    unsigned long long *gkey;
+    int32_t *gep;
+    int32_t nhelp;
 };
+
+// Control block of one fill's grid sweeps, written by the leader CTA and read
+// by the helpers (release/acquire at gpu scope; reset by the host per fill).
+struct SweepCtl {
+    int32_t seq;       // sweep number; -1 releases the helpers
+    int32_t from, until, any_mode, epoch, result, done, saturated;
+    int64_t slack, resumes, chunks, pad_;
+    TrieScalars sc;    // the leader's trie scalars at the sweep
+};
+
+__device__ __forceinline__ int32_t ld_acquire_i32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int32_t *p, int32_t v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // (pinned coverage B, token at B) of every admission of this step -> latest
 // admission epoch.  An admission e can raise a queued request's B only if
@@ -162,33 +186,47 @@ __device__ __forceinline__ unsigned long long miss_key(int32_t m0, int32_t tok) 
     return ((unsigned long long)((uint32_t)m0 | 0x80000000u) << 32) | (uint32_t)tok;
 }
 
-__device__ inline void adm_put_key(AdmFilter *f, unsigned long long k, int32_t e) {
+// Read-only view of the filter: the leader's shared-memory table, or its
+// global mirror for the helper CTAs of a grid sweep.
+struct FiltView {
+    const unsigned long long *key;
+    const int32_t *ep;
+    int32_t saturated;
+};
+
+__device__ __forceinline__ FiltView filt_view(const AdmFilter *f) { return FiltView{f->key, f->ep, f->saturated}; }
+
+__device__ inline void adm_put_key(AdmFilter *f, unsigned long long k, int32_t e, unsigned long long *gkey,
+                                   int32_t *gep) {
     if (f->n * 2 >= FS_FSLOTS) { f->saturated = 1; return; }
     uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
     while (f->key[i] != FS_HEMPTY && f->key[i] != k) i = (i + 1) & (FS_FSLOTS - 1);
-    if (f->key[i] == FS_HEMPTY) { f->key[i] = k; f->n++; }
+    if (f->key[i] == FS_HEMPTY) { f->key[i] = k; f->n++; if (gkey) gkey[i] = k; }
     f->ep[i] = e;
+    if (gep) gep[i] = e;
 }
 
-__device__ inline void adm_put(AdmFilter *f, int32_t B, int32_t tok, int32_t m0, int32_t tok0, int32_t e) {
-    if (tok >= 0) adm_put_key(f, adm_key(B, tok), e);  // a request fully covered by pins extends nothing
-    if (tok0 >= 0) adm_put_key(f, miss_key(m0, tok0), e);
+__device__ inline void adm_put(AdmFilter *f, int32_t B, int32_t tok, int32_t m0, int32_t tok0, int32_t e,
+                               unsigned long long *gkey, int32_t *gep) {
+    // a request fully covered by pins extends nothing
+    if (tok >= 0) adm_put_key(f, adm_key(B, tok), e, gkey, gep);
+    if (tok0 >= 0) adm_put_key(f, miss_key(m0, tok0), e, gkey, gep);
 }
 
 // true when some admission in [since, now) had key k
-__device__ __forceinline__ bool adm_maybe_key(const AdmFilter *f, unsigned long long k, int32_t since) {
-    if (f->saturated) return true;
+__device__ __forceinline__ bool adm_maybe_key(const FiltView &f, unsigned long long k, int32_t since) {
+    if (f.saturated) return true;
     uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
     while (true) {
-        const unsigned long long x = f->key[i];
-        if (x == k) return f->ep[i] >= since;
+        const unsigned long long x = f.key[i];
+        if (x == k) return f.ep[i] >= since;
         if (x == FS_HEMPTY) return false;
         i = (i + 1) & (FS_FSLOTS - 1);
     }
 }
 
 // true when some admission in [since, now) had the same (B, token)
-__device__ __forceinline__ bool adm_maybe(const AdmFilter *f, int32_t B, int32_t tok, int32_t since) {
+__device__ __forceinline__ bool adm_maybe(const FiltView &f, int32_t B, int32_t tok, int32_t since) {
     if (tok < 0) return false;
     return adm_maybe_key(f, adm_key(B, tok), since);
 }
@@ -196,7 +234,7 @@ __device__ __forceinline__ bool adm_maybe(const AdmFilter *f, int32_t B, int32_t
 // Can position p's exact coverage reach len - slack at all this fill?  False
 // only when the miss-key bound (above) rules it out; slack never grows within
 // a fill, so such a request needs no re-walk until its miss key is admitted.
-__device__ __forceinline__ bool cov_may_reach(const FillArgs &a, const AdmFilter *f, int32_t p, int64_t slack) {
+__device__ __forceinline__ bool cov_may_reach(const FillArgs &a, const FiltView &f, int32_t p, int64_t slack) {
     const int32_t m0 = a.s_mlen0[p];
     if (a.s_len[p] - m0 <= slack) return true;
     const int32_t t0 = a.s_tok0[p];
@@ -211,7 +249,7 @@ struct SchedSmem {
     int64_t red64[32];
     int32_t red32[32];
     int32_t wl_n, minA, minB;
-    int32_t cursor, progress, epoch, npos, nadm, stop, j;
+    int32_t cursor, progress, epoch, npos, nadm, stop, j, cursor_seq;
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
     int64_t prof[16];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops,
@@ -335,8 +373,9 @@ __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int
                     if (a.s_len[p] - s.y <= slack) {
                         q = true;
                     } else if (s.w < epoch) {
-                        if (!adm_maybe(&sm->flt, s.y, s.z, s.w)) a.slot[p].w = epoch;
-                        else if (cov_may_reach(a, &sm->flt, p, slack)) r = true;
+                        const FiltView fv = filt_view(&sm->flt);
+                        if (!adm_maybe(fv, s.y, s.z, s.w)) a.slot[p].w = epoch;
+                        else if (cov_may_reach(a, fv, p, slack)) r = true;
                     }
                 }
             }
@@ -353,10 +392,135 @@ __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int
     return FS_NONE;
 }
 
+// One FS_CHUNK-position chunk [base, min(base+FS_CHUNK, until)) by the whole
+// block: the first qualifying position, after re-walking the stale coverages
+// that precede the chunk's first plain hit.  `sm` supplies the block's scratch
+// (wl, red32, minB); the leader and the helper CTAs both run this.
+__device__ int32_t chunk_scan(const FillArgs &a, SchedSmem *sm, const FiltView &fv, int32_t base, int32_t until,
+                              bool any_mode, int64_t slack, int32_t epoch, unsigned long long *resumes) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; }
+    __syncthreads();
+    int32_t mine = FS_NONE;
+#pragma unroll
+    for (int u = 0; u < FS_ITEMS; u++) {
+        const int32_t p = base + u * FS_SCHED_THREADS + tid;
+        if (p >= until || mine != FS_NONE) continue;
+        const int4 s = a.slot[p];
+        if (s.w < 0) continue;
+        if (any_mode) { mine = p; continue; }
+        if (!a.lpm && a.q[s.x] <= 0) continue;
+        const int32_t need = a.s_len[p] - s.y;
+        if (need <= slack) { mine = p; continue; }
+        if (s.w < epoch) {
+            if (!adm_maybe(fv, s.y, s.z, s.w)) a.slot[p].w = epoch;  // B is still exact
+            else if (cov_may_reach(a, fv, p, slack)) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
+        }
+    }
+    const int32_t minA = block_min_i32(mine, sm->red32);
+    if (sm->wl_n > 0) {
+        for (int32_t i = warp; i < sm->wl_n; i += nwarps) {
+            const int32_t p = sm->wl[i];
+            if (p >= minA) continue;
+            warp_resume(a, p, lane);
+            __syncwarp();
+            if (lane == 0) {
+                a.slot[p].w = epoch;
+                if (a.s_len[p] - a.slot[p].y <= slack) atomicMin(&sm->minB, p);
+                atomicAdd(resumes, 1ull);
+            }
+        }
+        __syncthreads();
+    }
+    const int32_t best = min(minA, sm->minB);
+    __syncthreads();
+    return best;
+}
+
+// Leader side of a grid sweep: publish the search, wait for the helpers,
+// return the first qualifying position in [from, until) (FS_NONE if none).
+__device__ int32_t grid_sweep(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t until, bool any_mode,
+                              int64_t slack) {
+    SweepCtl *c = a.ctl;
+    __threadfence();  // this thread's trie / slot / counter writes, before the release
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sm->cursor_seq++;
+        c->from = from; c->until = until; c->any_mode = any_mode; c->epoch = sm->epoch;
+        c->slack = slack; c->result = FS_NONE; c->done = 0; c->saturated = sm->flt.saturated;
+        c->sc = *a.t.sc;
+        __threadfence();
+        st_release_i32(&c->seq, sm->cursor_seq);
+        while (ld_acquire_i32(&c->done) < a.nhelp) __nanosleep(64);
+        sm->minA = ld_acquire_i32(&c->result);
+    }
+    __syncthreads();
+    (void)ld_acquire_i32(&c->done);  // every thread: drop L1 lines the helpers made stale
+    const int32_t r = sm->minA;
+    __syncthreads();
+    return r;
+}
+
+// Helper CTA: serve grid sweeps until the leader releases it.  Chunks are
+// dealt round-robin; a helper stops at chunks past the best position found so
+// far (the minimum over the grid is the sequential scan's first hit, because
+// each position's verdict depends only on the state the leader published).
+__device__ void helper_loop(const FillArgs &ap, SchedSmem *sm) {
+    __shared__ FillArgs a;
+    __shared__ TrieScalars sc;
+    __shared__ int32_t seq_sh;
+    SweepCtl *c = ap.ctl;
+    const int tid = threadIdx.x;
+    const int32_t h = blockIdx.x - 1;
+    int32_t last = 0;
+    if (tid == 0) { a = ap; a.t.sc = &sc; }
+    while (true) {
+        if (tid == 0) {
+            int32_t v;
+            while ((v = ld_acquire_i32(&c->seq)) == last) __nanosleep(128);
+            seq_sh = v;
+        }
+        __syncthreads();
+        const int32_t v = seq_sh;
+        if (v < 0) return;
+        last = v;
+        (void)ld_acquire_i32(&c->seq);  // every thread: fresh view of the leader's writes
+        if (tid < (int)(sizeof(TrieScalars) / 8))
+            reinterpret_cast<int64_t *>(&sc)[tid] = reinterpret_cast<volatile int64_t *>(&c->sc)[tid];
+        __syncthreads();
+        const int32_t from = c->from, until = c->until, epoch = c->epoch;
+        const bool any_mode = c->any_mode;
+        const int64_t slack = c->slack;
+        const FiltView fv{a.gkey, a.gep, c->saturated};
+        int32_t best = FS_NONE;
+        int64_t nch = 0;
+        for (int64_t base = from + (int64_t)h * FS_CHUNK; base < until; base += (int64_t)a.nhelp * FS_CHUNK) {
+            if (tid == 0) sm->minA = *(volatile int32_t *)&c->result;
+            __syncthreads();
+            const bool skip = sm->minA <= base;
+            __syncthreads();
+            if (skip) break;
+            nch++;
+            best = chunk_scan(a, sm, fv, (int32_t)base, until, any_mode, slack, epoch,
+                              (unsigned long long *)&c->resumes);
+            if (best != FS_NONE) {
+                if (tid == 0) atomicMin(&c->result, best);
+                break;
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            atomicAdd((unsigned long long *)&c->chunks, (unsigned long long)nch);
+            __threadfence();
+            atomicAdd(&c->done, 1);
+        }
+    }
+}
+
 __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t until, bool any_mode,
                               int64_t slack) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int32_t epoch = sm->epoch;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     {
         // the next admissible request is usually right after the cursor: one
         // warp checks a short window before the whole block sweeps chunks
@@ -371,42 +535,12 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
         if (r >= 0 && r != FS_NONE) return r;
         from = r == FS_NONE ? wend : -(r + 2);
     }
+    if (a.nhelp > 0 && until - from > FS_CHUNK) return grid_sweep(a, sm, from, until, any_mode, slack);
+    const FiltView fv = filt_view(&sm->flt);
     for (int32_t base = from; base < until; base += FS_CHUNK) {
-        if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; sm->prof[4]++; }
-        __syncthreads();
-        int32_t mine = FS_NONE;
-#pragma unroll
-        for (int u = 0; u < FS_ITEMS; u++) {
-            const int32_t p = base + u * FS_SCHED_THREADS + tid;
-            if (p >= until || mine != FS_NONE) continue;
-            const int4 s = a.slot[p];
-            if (s.w < 0) continue;
-            if (any_mode) { mine = p; continue; }
-            if (!a.lpm && a.q[s.x] <= 0) continue;
-            const int32_t need = a.s_len[p] - s.y;
-            if (need <= slack) { mine = p; continue; }
-            if (s.w < epoch) {
-                if (!adm_maybe(&sm->flt, s.y, s.z, s.w)) a.slot[p].w = epoch;  // B is still exact
-                else if (cov_may_reach(a, &sm->flt, p, slack)) sm->wl[atomicAdd(&sm->wl_n, 1)] = p;
-            }
-        }
-        const int32_t minA = block_min_i32(mine, sm->red32);
-        if (sm->wl_n > 0) {
-            for (int32_t i = warp; i < sm->wl_n; i += nwarps) {
-                const int32_t p = sm->wl[i];
-                if (p >= minA) continue;
-                warp_resume(a, p, lane);
-                __syncwarp();
-                if (lane == 0) {
-                    a.slot[p].w = epoch;
-                    if (a.s_len[p] - a.slot[p].y <= slack) atomicMin(&sm->minB, p);
-                    atomicAdd((unsigned long long *)&sm->resumes, 1ull);
-                }
-            }
-            __syncthreads();
-        }
-        const int32_t best = min(minA, sm->minB);
-        __syncthreads();
+        if (tid == 0) sm->prof[4]++;
+        const int32_t best = chunk_scan(a, sm, fv, base, until, any_mode, slack, sm->epoch,
+                                        (unsigned long long *)&sm->resumes);
         if (best != FS_NONE) return best;
     }
     return FS_NONE;
@@ -483,7 +617,8 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
                 a.adm_rec_end[e] = t.sc->nrec;
             }
             sm->nadm = e + 1;
-            adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, a.s_mlen0[j], a.s_tok0[j], sm->epoch);
+            adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, a.s_mlen0[j], a.s_tok0[j], sm->epoch,
+                    a.gkey, a.gep);
             sm->epoch++;
             a.slot[j].w = -1;
             a.rstate[r] = 2;
@@ -506,6 +641,9 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
 __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     extern __shared__ __align__(16) unsigned char fs_smraw[];
     SchedSmem &sm = *reinterpret_cast<SchedSmem *>(fs_smraw);
+    // CTAs 1..nhelp (cooperative launch, co-resident) only serve the leader's
+    // grid sweeps of the queue; CTA 0 runs the fill
+    if (blockIdx.x > 0) { helper_loop(ap, &sm); return; }
     // the trie's scalars (used/pinned/seq/free stack/records) live in shared
     // memory for the whole step: every serial edit touches several of them
     __shared__ FillArgs a_sh;
@@ -524,7 +662,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         a.t.sc->nrec = 0;
         a.hdr[2] = FS_OK;
         sm.cursor = 0; sm.progress = 0; sm.epoch = 0; sm.nadm = 0; sm.stop = 0;
-        sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0;
+        sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0; sm.cursor_seq = 0;
         for (int i = 0; i < 16; i++) sm.prof[i] = 0;
         for (int i = 0; i < 4; i++) sm.lru.prof[i] = 0;
         sm.ins.prof = sm.prof;
@@ -533,7 +671,10 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     }
     const long long t_start = clock64();
     for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.pend_cnt[c] = 0;
-    for (int32_t i = tid; i < FS_FSLOTS; i += blockDim.x) sm.flt.key[i] = FS_HEMPTY;
+    for (int32_t i = tid; i < FS_FSLOTS; i += blockDim.x) {
+        sm.flt.key[i] = FS_HEMPTY;
+        if (a.gkey) a.gkey[i] = FS_HEMPTY;
+    }
     if (tid == 0) { sm.flt.n = 0; sm.flt.saturated = 0; }
     __syncthreads();
     block_chunk_build(a.t, &sm.lru);
@@ -579,6 +720,16 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         if (sm.stop) break;
     }
     __syncthreads();
+    if (a.nhelp > 0) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            st_release_i32(&a.ctl->seq, -1);  // release the helpers
+            sm.resumes += *(volatile int64_t *)&a.ctl->resumes;
+            sm.prof[4] += *(volatile int64_t *)&a.ctl->chunks;
+        }
+        __syncthreads();
+    }
     if (tid == 0) {
         a.hdr[0] = sm.nadm;
         a.hdr[1] = a.t.sc->nrec;

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -539,7 +540,7 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     CK(cudaMemcpyAsync(sm.ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
     const int64_t blocks = (n * 32 + 255) / 256;
     const int64_t sq = stamp ? ++t->opseq : 0;
-    k_match<<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
+    k_match<4><<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
                                                       stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr,
                                                       nullptr);
     counted();
@@ -778,6 +779,10 @@ struct fs_worker {
     DBuf<uint32_t> keys, keys2;
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
+    DBuf<SweepCtl> ctl;
+    DBuf<unsigned long long> gkey;
+    DBuf<int32_t> gep;
+    int nhelp = -1;  // helper CTAs of the grid sweep (-1: not yet sized)
     DBuf<int64_t> s0, s_src0;
     DBuf<int4> slot;
     DBuf<uint8_t> cub_tmp;
@@ -845,7 +850,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1084,9 +1089,11 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
     if (n > 0) {
         const int64_t blocks = (n * 32 + 255) / 256;
-        k_match<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
-                                                  ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
-                                                  w->s0.p, (unsigned long long *)w->alg.p);
+        static const int k1u = [] { const char *e = getenv("FS_K1_UNROLL"); return e ? atoi(e) : 8; }();
+        auto k1 = k1u >= 16 ? k_match<16> : k1u >= 8 ? k_match<8> : k_match<4>;
+        k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
+                                            ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
+                                            w->s0.p, (unsigned long long *)w->alg.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -1127,7 +1134,29 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         CK(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchedSmem)));
         smem_set = true;
     }
-    k_schedule<<<1, FS_SCHED_THREADS, sizeof(SchedSmem), s>>>(a);
+    if (w->nhelp < 0) {
+        // one co-resident helper CTA per remaining SM (cooperative launch);
+        // FS_SCHED_HELPERS overrides (0 = the leader sweeps alone)
+        int nsm = 0, per = 0, coop = 0;
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+        CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_schedule, FS_SCHED_THREADS, sizeof(SchedSmem)));
+        int nh = coop ? std::max(0, per * nsm - 1) : 0;
+        if (const char *e = getenv("FS_SCHED_HELPERS")) nh = std::min(nh, std::max(0, atoi(e)));
+        w->nhelp = nh;
+        TRY(dgrow(w->ctl, 1, s));
+        TRY(dgrow(w->gkey, FS_FSLOTS, s));
+        TRY(dgrow(w->gep, FS_FSLOTS, s));
+    }
+    a.ctl = w->ctl.p; a.gkey = w->gkey.p; a.gep = w->gep.p; a.nhelp = w->nhelp;
+    CK(cudaMemsetAsync(w->ctl.p, 0, sizeof(SweepCtl), s));
+    if (w->nhelp > 0) {
+        void *args[] = {&a};
+        CK(cudaLaunchCooperativeKernel((const void *)k_schedule, dim3(1 + w->nhelp), dim3(FS_SCHED_THREADS), args,
+                                       sizeof(SchedSmem), s));
+    } else {
+        k_schedule<<<1, FS_SCHED_THREADS, sizeof(SchedSmem), s>>>(a);
+    }
     counted();
     CK(cudaGetLastError());
     CK(cudaEventRecord(w->ev[4], s));

@@ -62,3 +62,12 @@ def test_scale_config5_64k():
     tokens) at 64k queued requests against the oracle on the same tokens."""
     import bench
     _run_wl(bench.Config5(65536, 0, 10), 10)
+
+
+def test_scale_leader_only_sweeps(monkeypatch):
+    """The same parity with the grid sweep disabled (the leader CTA scans the
+    queue alone): both search paths must make identical decisions."""
+    import bench
+    monkeypatch.setenv("FS_SCHED_HELPERS", "0")
+    _run_wl(bench.Config2(8192, 9, 12), 12)
+    _run_wl(bench.Config5(16384, 0, 6), 6)
