@@ -435,7 +435,7 @@ def main():
                                    "admit_chains": sched[6] / args.steps, "k1_chains": k1_hops / args.steps,
                                    "resumes": resumes / args.steps, "refill_events": refills / args.steps,
                                    "pop_argmin_cyc": sched[8] / args.steps, "pop_edit_cyc": sched[9] / args.steps,
-                                   "pop_update_cyc": sched[10] / args.steps,
+                                   "pop_update_cyc": sched[10] / args.steps, "setup_cyc": sched[11] / args.steps,
                                    "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }

@@ -224,6 +224,14 @@ __device__ inline void push_record(const TrieView &t, int64_t src, int32_t len, 
 // U loads per lane in flight: 4 for the many-warp match kernel (bounded
 // over-read past the mismatch), 8 for the single-warp walks on the admission
 // critical path (latency-bound).
+// Request tokens are read once per match: keep them out of L1 so the trie's
+// hot chains (compared by every warp of the SM) stay resident there.
+__device__ __forceinline__ int32_t ld_stream(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 template <int U = 4>
 __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
                                             int32_t n, int lane) {
@@ -233,7 +241,7 @@ __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int32_t p = k + u * 32 + lane;
-            bad[u] = (p < n) && (__ldg(a + p) != __ldg(b + p));
+            bad[u] = (p < n) && (__ldg(a + p) != ld_stream(b + p));
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -241,6 +249,40 @@ __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const
             if (m) return min(n, k + u * 32 + __ffs(m) - 1);
         }
         k += 32 * U;
+    }
+    return n;
+}
+
+// Software-pipelined LCP for the many-warp match kernel (K1): the next
+// 32*U-token block of both sequences is in flight while the current one is
+// compared, so a warp keeps 2*U*128 B of request tokens outstanding (read
+// once: streaming loads); over-reads at most one block past the mismatch.
+template <int U = 8>
+__device__ __forceinline__ int32_t warp_lcp_pipe(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
+                                                 int32_t n, int lane) {
+    int32_t av[U], bv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const int32_t p = u * 32 + lane;
+        av[u] = p < n ? __ldg(a + p) : 0;
+        bv[u] = p < n ? __ldcs(b + p) : 0;
+    }
+    for (int32_t k = 0; k < n; k += 32 * U) {
+        int32_t an[U], bn[U];
+        const int32_t k2 = k + 32 * U;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int32_t p = k2 + u * 32 + lane;
+            an[u] = p < n ? __ldg(a + p) : 0;
+            bn[u] = p < n ? __ldcs(b + p) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const unsigned m = __ballot_sync(FS_FULL, av[u] != bv[u]);
+            if (m) return min(n, k + u * 32 + __ffs(m) - 1);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) { av[u] = an[u]; bv[u] = bn[u]; }
     }
     return n;
 }
@@ -317,7 +359,7 @@ struct WalkStart {
     bool pinrun;
 };
 
-template <int U = 4, typename SegFn>
+template <int U = 4, typename SegFn, bool PIPE = false>
 __device__ inline WalkOut warp_walk_from(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                          bool want_cov, WalkStart st, SegFn on_seg) {
     WalkOut o;
@@ -329,7 +371,8 @@ __device__ inline WalkOut warp_walk_from(const TrieView &t, const int32_t *__res
         if (c < 0) break;
         const int64_t S = t.src[c];
         const int32_t bound = min(len, t.slen[c]);
-        const int32_t k = 1 + warp_lcp<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane);
+        const int32_t k = 1 + (PIPE ? warp_lcp_pipe<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane)
+                                    : warp_lcp<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane));
         const int32_t D = idx + k;  // request == chain S on [idx, D)
         const int32_t y = chain_lookup(t, S, idx, D - 1);
         const int32_t e = t.end[y];
@@ -350,12 +393,12 @@ __device__ inline WalkOut warp_walk_from(const TrieView &t, const int32_t *__res
     return o;
 }
 
-template <int U = 4, typename SegFn>
+template <int U = 4, typename SegFn, bool PIPE = false>
 __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                        bool want_cov, SegFn on_seg) {
     WalkStart st;
     st.node = 0; st.idx = 0; st.nseg = 0; st.last = -1; st.cov = 0; st.pinrun = true;
-    return warp_walk_from<U>(t, rq, len, lane, want_cov, st, on_seg);
+    return warp_walk_from<U, SegFn, PIPE>(t, rq, len, lane, want_cov, st, on_seg);
 }
 
 // Source-chain segments of the cached root path [0, d) whose depth d-1 lies in
@@ -443,12 +486,13 @@ __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__res
 }
 
 // warp_walk_cb storing the segments (lane 0) when segs != nullptr.
-template <int U = 4>
+template <int U = 4, bool PIPE = false>
 __device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                     Seg *segs, bool want_cov) {
-    return warp_walk_cb<U>(t, rq, len, lane, want_cov, [&](int64_t S, int32_t a, int32_t b, int32_t i) {
+    auto store = [&](int64_t S, int32_t a, int32_t b, int32_t i) {
         if (lane == 0 && segs) { segs[i].S = S; segs[i].a = a; segs[i].b = b; }
-    });
+    };
+    return warp_walk_cb<U, decltype(store), PIPE>(t, rq, len, lane, want_cov, store);
 }
 
 // unpin (radix.py:180-185) of the cached root path arena[src : src+plen] by one

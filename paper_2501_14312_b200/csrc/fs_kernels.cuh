@@ -20,22 +20,36 @@
 #define FS_NONE 0x7fffffff
 
 // ---------------------------------------------------------------- K1
-template <int U>
+template <int U, bool PIPE>
 __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
                                                int64_t now, int stamp, int64_t sq, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
                                                int64_t *__restrict__ out_s0,
-                                               unsigned long long *__restrict__ alg_tokens) {
+                                               unsigned long long *__restrict__ alg_tokens,
+                                               int32_t *__restrict__ hint) {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= n) return;
     const int32_t r = ids[i];
     const int32_t len = rlen[r];
     const int32_t *rq = t.arena + roff[r];
-    const WalkOut w = warp_walk<U>(t, rq, len, lane, nullptr, true);
+    if (hint) {
+        // The request tokens this match will read are known up to the previous
+        // step's match length: hand them to the TMA engine as L2 bulk prefetches
+        // (4 KB per lane) so the DRAM fetch overlaps the trie hops below.
+        const int32_t want = min(len, hint[r] + 32);
+        const int32_t nb = (want * 4 + 4095) >> 12;
+        if (lane < nb) {
+            const int32_t b0 = lane << 10;
+            const uint32_t bytes = (uint32_t)(((min(want, b0 + 1024) - b0) * 4 + 15) & ~15);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rq + b0), "r"(bytes) : "memory");
+        }
+    }
+    const WalkOut w = warp_walk<U, PIPE>(t, rq, len, lane, nullptr, true);
     if (lane == 0) {
+        if (hint) hint[r] = w.mlen;
         // match_prefix stamps every matched node (radix.py:86-90): lazily, at the deepest
         if (stamp && w.last > 0) stamp_node(t, w.last, now, sq);
         if (out_key) out_key[i] = kmax - (uint32_t)w.mlen;
@@ -43,10 +57,12 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
         if (out_cov) out_cov[i] = w.cov;
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
         if (out_s0) out_s0[i] = w.last > 0 ? t.src[w.last] : -1;  // admission-walk hint
-        // request tokens a match must read: min(mlen+1, len)
+        // request tokens a match must read: min(mlen+1, len); the
+        // counters are spread over 64 slot pairs (summed by the host)
         if (alg_tokens) {
-            atomicAdd(alg_tokens, (unsigned long long)min(w.mlen + 1, len));
-            atomicAdd(alg_tokens + 1, (unsigned long long)w.nseg);  // source chains crossed
+            unsigned long long *slot = alg_tokens + 2 * (blockIdx.x & 63);
+            atomicAdd(slot, (unsigned long long)min(w.mlen + 1, len));
+            atomicAdd(slot + 1, (unsigned long long)w.nseg);  // source chains crossed
         }
     }
 }
@@ -253,7 +269,7 @@ struct SchedSmem {
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
     int64_t prof[16];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops,
-                       // [6] chains, [7] total, [8..10] pop argmin / edit / rescan
+                       // [6] chains, [7] total, [8..10] pop argmin / edit / rescan, [11] setup
 };
 
 __device__ __forceinline__ int64_t sched_slack(const FillArgs &a, int64_t headroom) {
@@ -670,7 +686,8 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         sm.ins.ev.pops = 0;
     }
     const long long t_start = clock64();
-    for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.pend_cnt[c] = 0;
+    // pend_cnt (pending requests per client) is maintained across fills:
+    // +1 per arrival (k_enqueue_state), -1 per admission (block_admit)
     for (int32_t i = tid; i < FS_FSLOTS; i += blockDim.x) {
         sm.flt.key[i] = FS_HEMPTY;
         if (a.gkey) a.gkey[i] = FS_HEMPTY;
@@ -678,7 +695,6 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     if (tid == 0) { sm.flt.n = 0; sm.flt.saturated = 0; }
     __syncthreads();
     block_chunk_build(a.t, &sm.lru);
-    for (int32_t p = tid; p < a.n; p += blockDim.x) atomicAdd(&a.pend_cnt[a.slot[p].x], 1);
     __syncthreads();
     {
         int64_t cnt = 0;
@@ -687,6 +703,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         if (tid == 0) sm.npos = (int32_t)cnt;
     }
     __syncthreads();
+    if (tid == 0) sm.prof[11] = clock64() - t_start;  // setup: LRU index, filter, counters
     // Dlpm.fill pass structure (local_policies.py:112-128): repeat passes over
     // the sorted snapshot until a whole pass admits nothing.
     while (true) {

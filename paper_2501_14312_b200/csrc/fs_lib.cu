@@ -114,6 +114,7 @@ struct fs_ctx {
     DBuf<int32_t> rlen, rclient;
     DBuf<int64_t> rlabel;
     DBuf<int8_t> rstate;  // 0 none, 1 queued, 2 admitted
+    DBuf<int32_t> rhint;  // last K1 match length per request (L2 prefetch extent)
     std::vector<int64_t> h_roff, h_rlabel;
     std::vector<int32_t> h_rlen, h_rclient;
     int32_t max_len = 1;
@@ -160,7 +161,7 @@ extern "C" int fs_ctx_destroy(fs_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->arena.release(); c->roff.release(); c->rlen.release(); c->rclient.release();
-    c->rlabel.release(); c->rstate.release();
+    c->rlabel.release(); c->rstate.release(); c->rhint.release();
     c->stage_tok.release(); c->stage64.release(); c->stage32.release();
     c->x_dst.release(); c->x_nsoff.release(); c->x_len.release(); c->x_ns.release(); c->x_nslen.release();
     c->x_bytes.release();
@@ -188,6 +189,11 @@ static int append_request_meta(fs_ctx *c, int64_t n, const int64_t *place, const
         const int64_t old = c->rstate.cap;
         TRY(dgrow(c->rstate, nr, c->stream, true, base_id));
         CK(cudaMemsetAsync(c->rstate.p + old, 0, c->rstate.cap - old, c->stream));
+    }
+    if (c->rhint.cap < nr) {
+        const int64_t old = c->rhint.cap;
+        TRY(dgrow(c->rhint, nr, c->stream, true, old));
+        CK(cudaMemsetAsync(c->rhint.p + old, 0, sizeof(int32_t) * (c->rhint.cap - old), c->stream));
     }
     for (int64_t i = 0; i < n; i++) {
         c->h_roff.push_back(place[i]);
@@ -540,9 +546,9 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     CK(cudaMemcpyAsync(sm.ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
     const int64_t blocks = (n * 32 + 255) / 256;
     const int64_t sq = stamp ? ++t->opseq : 0;
-    k_match<4><<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
+    k_match<4, false><<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
                                                       stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr,
-                                                      nullptr);
+                                                      nullptr, nullptr);
     counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -811,6 +817,15 @@ __global__ void k_iota(int32_t *p, int64_t n) {
     if (i < n) p[i] = (int32_t)i;
 }
 
+// Arrivals join the queue: state 1 and one more pending request for their client.
+__global__ void k_enqueue_state(int8_t *st, const int32_t *ids, int64_t n, const int32_t *rclient, int32_t *pend_cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        st[ids[i]] = 1;
+        atomicAdd(&pend_cnt[rclient[ids[i]]], 1);
+    }
+}
+
 __global__ void k_set_state(int8_t *st, const int32_t *ids, int64_t n, int8_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) st[ids[i]] = v;
@@ -833,9 +848,10 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     CK(cudaMemsetAsync(w->q.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->refills.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
-    TRY(dgrow(w->hdr, 24, c->stream)); TRY(hgrow(w->h_hdr, 32));
+    CK(cudaMemsetAsync(w->pend_cnt.p, 0, sizeof(int32_t) * max_clients, c->stream));
+    TRY(dgrow(w->hdr, 24, c->stream)); TRY(hgrow(w->h_hdr, 24 + 128));
     TRY(dgrow(w->nsel, 1, c->stream));
-    TRY(dgrow(w->alg, 2, c->stream));
+    TRY(dgrow(w->alg, 128, c->stream));
     for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
     CK(cudaStreamSynchronize(c->stream));
     *out = w;
@@ -955,7 +971,8 @@ extern "C" int fs_worker_reserve_clients(fs_worker *w, int32_t max_clients) {
     const int32_t old = w->nclients;
     const int32_t nc = std::max(max_clients, old * 2);
     TRY(dgrow(w->q, nc, s, true, old)); TRY(dgrow(w->refills, nc, s, true, old));
-    TRY(dgrow(w->known, nc, s, true, old)); TRY(dgrow(w->pend_cnt, nc, s));
+    TRY(dgrow(w->known, nc, s, true, old)); TRY(dgrow(w->pend_cnt, nc, s, true, old));
+    CK(cudaMemsetAsync(w->pend_cnt.p + old, 0, sizeof(int32_t) * (nc - old), s));
     CK(cudaMemsetAsync(w->q.p + old, 0, sizeof(int64_t) * (nc - old), s));
     CK(cudaMemsetAsync(w->refills.p + old, 0, sizeof(int64_t) * (nc - old), s));
     CK(cudaMemsetAsync(w->known.p + old, 0, nc - old, s));
@@ -1066,7 +1083,8 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         TRY(dgrow(w->newids, n_new, s)); TRY(dgrow(w->newlab, n_new, s));
         CK(cudaMemcpyAsync(w->newids.p, w->h_st32.p, sizeof(int32_t) * n_new, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(w->newlab.p, w->h_st64.p, sizeof(int64_t) * n_new, cudaMemcpyHostToDevice, s));
-        k_set_state<<<(unsigned)((n_new + 255) / 256), 256, 0, s>>>(c->rstate.p, w->newids.p, n_new, 1);
+        k_enqueue_state<<<(unsigned)((n_new + 255) / 256), 256, 0, s>>>(c->rstate.p, w->newids.p, n_new, c->rclient.p,
+                                                                   w->pend_cnt.p);
         counted();
         k_merge<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->queue.p, (int32_t)n_old, w->newids.p, w->newlab.p,
                                                            (int32_t)n_new, c->rlabel.p, w->queue2.p);
@@ -1084,16 +1102,29 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         CK(cudaMemcpyAsync(w->dlc.p, w->dl_client.data(), sizeof(int32_t) * ndl, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(w->dld.p, w->dl_delta.data(), sizeof(int64_t) * ndl, cudaMemcpyHostToDevice, s));
     }
-    CK(cudaMemsetAsync(w->alg.p, 0, 2 * sizeof(int64_t), s));
+    CK(cudaMemsetAsync(w->alg.p, 0, 128 * sizeof(int64_t), s));
     CK(cudaEventRecord(w->ev[1], s));
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
     if (n > 0) {
+        static int k1_blocks = 0;
+        if (!k1_blocks) {
+            int nsm = 0, per = 0;
+            CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_match<8, false>, 256, 0));
+            k1_blocks = std::max(1, nsm * per);
+        }
+        // one request per warp measured faster than persistent warps (k1_blocks
+        // cap) on config 5: keep the full grid
         const int64_t blocks = (n * 32 + 255) / 256;
+        (void)k1_blocks;
         static const int k1u = [] { const char *e = getenv("FS_K1_UNROLL"); return e ? atoi(e) : 8; }();
-        auto k1 = k1u >= 16 ? k_match<16> : k1u >= 8 ? k_match<8> : k_match<4>;
+        // FS_K1_UNROLL: 4 / 8 / 16 plain, 104 / 108 = pipelined 4 / 8
+        auto k1 = k1u == 104 ? k_match<4, true> : k1u == 108 ? k_match<8, true> : k1u >= 16 ? k_match<16, false>
+                : k1u >= 8 ? k_match<8, false> : k_match<4, false>;
         k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
                                             ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
-                                            w->s0.p, (unsigned long long *)w->alg.p);
+                                            w->s0.p, (unsigned long long *)w->alg.p,
+                                            getenv("FS_K1_NOPREFETCH") ? nullptr : c->rhint.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -1163,7 +1194,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     w->dl_client.clear(); w->dl_delta.clear();
     // ---- results
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 24, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_hdr.p + 24, w->alg.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p + 24, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
@@ -1172,8 +1203,9 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     const int64_t nrec = w->h_hdr.p[1];
     const int64_t status = w->h_hdr.p[2];
     for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&w->phases[i], w->ev[i], w->ev[i + 1]));
-    w->stats[0] = w->h_hdr.p[24];
-    w->stats[6] = w->h_hdr.p[25];
+    w->stats[0] = 0;
+    w->stats[6] = 0;
+    for (int k = 0; k < 64; k++) { w->stats[0] += w->h_hdr.p[24 + 2 * k]; w->stats[6] += w->h_hdr.p[25 + 2 * k]; }
     for (int i = 8; i < 24; i++) w->stats[i] = w->h_hdr.p[i];
     w->stats[1] = n;
     w->stats[2] = w->h_hdr.p[3];
