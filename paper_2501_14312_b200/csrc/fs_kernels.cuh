@@ -856,6 +856,8 @@ struct DispArgs {
     const int32_t *dl_w;
     int32_t ndl;
     Seg *segs;
+    const int32_t *m0;  // batch-start match of every arrival (k_match pre-pass, no stamp)
+    const int64_t *s0;
     int32_t *out_w, *out_mlen;
     uint64_t *out_mask;
     int64_t *out_rounds;
@@ -924,8 +926,11 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
         const int64_t off = a.roff[r];
         const int64_t now = a.nows[i];
         if (warp == 0) {
-            // RadixTree.longest_match_workers (radix.py:101-110)
-            const WalkOut w = warp_walk(t, t.arena + off, len, lane, nullptr, false);
+            // RadixTree.longest_match_workers (radix.py:101-110).  The index only
+            // gains prefixes of this batch's earlier arrivals (no capacity, no
+            // eviction inside a batch), so the batch-start match is still a
+            // prefix of the current one: resume from it (warp_walk_hint).
+            const WalkOut w = warp_walk_hint<8>(t, t.arena + off, len, lane, a.segs, a.s0[i], a.m0[i]);
             if (lane == 0) {
                 const int32_t deepest = w.mlen > 0 ? w.last : -1;
                 if (deepest > 0) stamp_node(t, deepest, now, a.sq_base + 2 * (int64_t)i);
@@ -941,7 +946,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             }
         }
         __syncthreads();
-        block_insert(t, off, len, now, a.sq_base + 2 * (int64_t)i + 1, s_w, a.segs, &ins);
+        block_insert(t, off, len, now, a.sq_base + 2 * (int64_t)i + 1, s_w, a.segs, &ins, a.s0[i], a.m0[i]);
         if (tid == 0) {
             a.out_w[i] = s_w;
             a.out_mlen[i] = s_mlen;

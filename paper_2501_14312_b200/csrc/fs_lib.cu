@@ -1249,8 +1249,8 @@ struct fs_dispatcher {
     std::vector<int64_t> dl_q;
     DBuf<int64_t> q, qsize;
     DBuf<uint8_t> qset;
-    DBuf<int32_t> ids, clients, dli, dlw, o_w, o_mlen;
-    DBuf<int64_t> nows, dlq, o_rounds, hdr;
+    DBuf<int32_t> ids, clients, dli, dlw, o_w, o_mlen, m0;
+    DBuf<int64_t> nows, dlq, o_rounds, hdr, s0;
     DBuf<uint64_t> o_mask;
 };
 
@@ -1286,6 +1286,7 @@ extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
     d->q.release(); d->qsize.release(); d->qset.release(); d->ids.release(); d->clients.release();
     d->dli.release(); d->dlw.release(); d->o_w.release(); d->o_mlen.release(); d->nows.release();
     d->dlq.release(); d->o_rounds.release(); d->hdr.release(); d->o_mask.release();
+    d->m0.release(); d->s0.release();
     delete d;
     return FS_OK;
 }
@@ -1323,6 +1324,17 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     a.segs = d->tree->segs.p;
     a.sq_base = d->tree->opseq + 1;
     d->tree->opseq += 2 * n;
+    {
+        // batch-start matches of every arrival, in parallel (K1, no stamping):
+        // the serial chain below resumes each walk from them
+        TRY(dgrow(d->m0, n, s)); TRY(dgrow(d->s0, n, s));
+        k_match<8, false><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+            view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, 0, 0, 0, 0u, nullptr, d->m0.p, nullptr,
+            nullptr, d->s0.p, nullptr, nullptr);
+        counted();
+        CK(cudaGetLastError());
+        a.m0 = d->m0.p; a.s0 = d->s0.p;
+    }
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
     k_dispatch<<<1, 256, 0, s>>>(a);
