@@ -227,6 +227,10 @@ int fs_dispatch_set_counter(fs_dispatcher *d, int32_t client, int32_t worker, in
 int fs_dispatch_set_queue_size(fs_dispatcher *d, int32_t worker, int64_t size);
 int fs_dispatcher_reserve_clients(fs_dispatcher *d, int32_t max_clients);
 /* Device-side copy of the counters (tests compare it with the host mirror). */
+/* SM-cycle profile of the last fs_dispatch chain: [0] match + select, [1] insert
+ * walk, [2] evict, [12] leaf + stamp, [13] position repoint, [14] worker tags,
+ * [15] total.  Writes 16 entries. */
+int fs_dispatch_last_profile(fs_dispatcher *d, int64_t *prof16);
 int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t *q, uint8_t *present, int64_t *qsize);
 int fs_worker_device_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills);
 

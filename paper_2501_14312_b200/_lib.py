@@ -106,6 +106,7 @@ SIGNATURES = {
     "fs_dispatch_set_counter": (C.c_int, [vp, i32, i32, i64]),
     "fs_dispatch_set_queue_size": (C.c_int, [vp, i32, i64]),
     "fs_dispatcher_reserve_clients": (C.c_int, [vp, i32]),
+    "fs_dispatch_last_profile": (C.c_int, [vp, P64]),
     "fs_dispatch_device_counters": (C.c_int, [vp, i64, P64, PU8, P64]),
 }
 

@@ -524,14 +524,28 @@ __device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int l
 // ---------------------------------------------------------------- path nodes
 // Call fn(node) once for every node of the path described by segs (each node
 // is visited at its first depth).  Block-parallel; segs must be visible.
+// Each thread batches K depths: all K pos loads, then all K start loads, then
+// the callbacks -- two memory round trips per K*blockDim depths instead of two
+// per depth (fn's stores would otherwise pin every load behind them).
 template <typename F>
 __device__ inline void block_path_nodes(const TrieView &t, const Seg *segs, int32_t nseg, F fn) {
+    constexpr int K = 8;
+    const int32_t nt = (int32_t)blockDim.x;
     for (int32_t s = 0; s < nseg; s++) {
         const int64_t S = segs[s].S;
         const int32_t a = segs[s].a, b = segs[s].b;
-        for (int32_t d = a + (int32_t)threadIdx.x; d < b; d += blockDim.x) {
-            const int32_t n = t.pos[S + d];
-            if (t.start[n] == d) fn(n);
+        for (int32_t d0 = a + (int32_t)threadIdx.x; d0 < b; d0 += K * nt) {
+            int32_t nd[K], st[K];
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                const int32_t d = d0 + k * nt;
+                nd[k] = d < b ? t.pos[S + d] : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < K; k++) st[k] = nd[k] >= 0 ? t.start[nd[k]] : -1;
+#pragma unroll
+            for (int k = 0; k < K; k++)
+                if (nd[k] >= 0 && st[k] == d0 + k * nt) fn(nd[k]);
         }
     }
 }
@@ -921,9 +935,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         if (sm->status != FS_OK && t.sc->status == FS_OK && sm->status != FS_ERR_CACHE_FULL) t.sc->status = sm->status;
     }
     __syncthreads();
+    const long long c2 = clock64();
     if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0)
         block_repoint(t, req_off, sm->mlen, len, sm->deepest);
     __syncthreads();
+    const long long c3 = clock64();
+    if (tid == 0 && sm->prof) { sm->prof[12] += c2 - c1; sm->prof[13] += c3 - c2; }
     if (sm->status == FS_OK && t.wmask && worker >= 0) {
         // n.workers[worker] = now on every path node (radix.py:160-161)
         block_path_nodes(t, segs, sm->nseg, [&](int32_t n) {
@@ -931,6 +948,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             t.wtime[(int64_t)n * t.nw + worker] = now;
         });
         __syncthreads();
+        if (tid == 0 && sm->prof) sm->prof[14] += clock64() - c3;
     }
 }
 

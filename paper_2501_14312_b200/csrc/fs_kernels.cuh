@@ -896,6 +896,9 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
     __shared__ int32_t s_w;
     __shared__ int32_t s_mlen;
     __shared__ uint64_t s_mask;
+    // cycle profile: [0] lmw walk + select, [1] insert walk, [2] evict, [12] leaf+stamp,
+    // [13] repoint, [14] worker tags, [15] total
+    __shared__ int64_t prof[16];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;
     if (tid == 0) {
@@ -906,11 +909,13 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             else a.qsize[a.dl_w[i]] += a.dl_q[i];
         }
         t.sc->status = FS_OK;
-        ins.prof = nullptr;
+        for (int i = 0; i < 16; i++) prof[i] = 0;
+        ins.prof = prof;
         ins.lru = nullptr;
         ins.ev.pops = 0;
     }
     __syncthreads();
+    const long long t0 = clock64();
     if (a.select_only) {
         if (tid == 0 && a.n > 0) {
             int64_t rounds;
@@ -925,6 +930,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
         const int32_t len = a.rlen[r];
         const int64_t off = a.roff[r];
         const int64_t now = a.nows[i];
+        const long long cw = clock64();
         if (warp == 0) {
             // RadixTree.longest_match_workers (radix.py:101-110).  The index only
             // gains prefixes of this batch's earlier arrivals (no capacity, no
@@ -946,6 +952,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             }
         }
         __syncthreads();
+        if (tid == 0) prof[0] += clock64() - cw;
         block_insert(t, off, len, now, a.sq_base + 2 * (int64_t)i + 1, s_w, a.segs, &ins, a.s0[i], a.m0[i]);
         if (tid == 0) {
             a.out_w[i] = s_w;
@@ -954,7 +961,11 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
         }
         __syncthreads();
     }
-    if (tid == 0) a.hdr[0] = t.sc->status;
+    if (tid == 0) {
+        a.hdr[0] = t.sc->status;
+        prof[15] = clock64() - t0;
+        for (int i = 0; i < 16; i++) a.hdr[4 + i] = prof[i];
+    }
 }
 
 // Dlpm.check_refill (local_policies.py:94-106) on an explicit queued set.

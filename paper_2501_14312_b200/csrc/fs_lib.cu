@@ -1272,7 +1272,7 @@ extern "C" int fs_dispatcher_create(fs_ctx *c, int D, int64_t quantum, int64_t w
     CK(cudaMemsetAsync(d->q.p, 0, sizeof(int64_t) * nq, c->stream));
     CK(cudaMemsetAsync(d->qset.p, 0, nq, c->stream));
     CK(cudaMemsetAsync(d->qsize.p, 0, sizeof(int64_t) * D, c->stream));
-    TRY(dgrow(d->hdr, 4, c->stream));
+    TRY(dgrow(d->hdr, 24, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     *out = d;
     return FS_OK;
@@ -1292,6 +1292,14 @@ extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
 }
 
 extern "C" fs_trie *fs_dispatcher_tree(fs_dispatcher *d) { return d ? d->tree : nullptr; }
+
+extern "C" int fs_dispatch_last_profile(fs_dispatcher *d, int64_t *prof16) {
+    if (!d || !prof16) return fail(FS_ERR_INVALID, "NULL argument");
+    TRY(ctx_use(d->ctx));
+    CK(cudaMemcpyAsync(prof16, d->hdr.p + 4, 16 * sizeof(int64_t), cudaMemcpyDeviceToHost, d->ctx->stream));
+    CK(cudaStreamSynchronize(d->ctx->stream));
+    return FS_OK;
+}
 
 extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
                            const int64_t *now, int32_t *out_worker, int32_t *out_mlen, uint64_t *out_mask,

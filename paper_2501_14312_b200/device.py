@@ -386,6 +386,12 @@ class DispatcherDev:
         call("fs_dispatch", self._h, n, _p32(ids), _p32(cl), _p64(nw), _p32(w), _p32(m), _pu64(mk), _p64(rd))
         return w[:n], m[:n], mk[:n], rd[:n]
 
+    def last_profile(self) -> np.ndarray:
+        """SM cycles of the last dispatch chain (fs_dispatch_last_profile)."""
+        p = np.zeros(16, np.int64)
+        call("fs_dispatch_last_profile", self._h, _p64(p))
+        return p
+
     def select(self, client: int, mask: int):
         w = C.c_int32(); r = C.c_int64()
         call("fs_dispatch_select", self._h, client, mask, C.byref(w), C.byref(r))
