@@ -139,11 +139,11 @@ class Config5(Workload):
         return self._host_queue(device, stream=0, first=0, count=n, arrival=0), self.pool, n
 
 
-def make_workload(name, nq, rank, steps):
+def make_workload(name, nq, rank, steps, device=0, world=1):
     if name == "c2":
-        return Config2(nq or 65536, rank, steps)
+        return Config2(nq or 65536, rank, steps * world)
     if name == "c5":
-        return Config5(nq or (1 << 20), rank, steps)
+        return Config5(nq or (1 << 20), rank, steps * world, device=device)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -291,6 +291,92 @@ def _concat_once(o, q, pool):
     return _CAT[key]
 
 
+def run_cluster(args, wl, rank, world, dev, tdev, dist):
+    """N>1: D2LPM across GPUs (paper_2501_14312_b200.cluster): one worker per
+    rank, a dispatcher replica on every rank, one NCCL all-gather of finishes
+    and eviction notices per round.  The workload's queue is dispatched once
+    by D2LPM at t=0 (untimed), so each worker holds ~Nq/N (strong scaling);
+    every round then completes the previous batch, exchanges, dispatches the
+    round's arrivals on every replica and runs one DLPM fill per worker."""
+    import torch
+    from paper_2501_14312_b200.cluster import ClusterRank, GpuStreamRank, LocalComm, TorchComm
+    from paper_2501_14312_b200.device import launch_count
+    U = W_E * wl.L_INPUT + W_Q * wl.M
+    q_w = max(1, round(0.5 * U))  # q_w_frac 0.5 (runner.py:131)
+    be = GpuStreamRank(rank, dev, wl, world, W_E, W_Q, q_w, max(128, wl.clients))
+    comm = TorchComm(tdev) if dist is not None else LocalComm()
+    cr = ClusterRank(be, comm, out_tokens=wl.out_tokens, max_arrivals=args.arrivals if args.arrivals > 0 else None,
+                     pipelined=True)
+    t0 = time.perf_counter()
+    cr.seed(list(range(wl.nq)), 0)
+    seed_s = time.perf_counter() - t0
+    n_seed = wl.nq
+    now = 0
+    for _ in range(args.warmup):
+        now += STEP_US
+        cr.round(now, be.arrival_stream)
+    be.ctx.sync()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks_start() if rank == 0 else (None, None, None)
+    be.fill_ms = 0.0
+    be.n_queued = be.n_dispatched = 0
+    be.h2d = 0
+    cr.t_exchange = cr.t_apply = cr.t_dispatch = cr.t_fill = cr.t_overlap = 0.0
+    l0 = launch_count()
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        now += STEP_US
+        cr.round(now, be.arrival_stream)
+    be.ctx.sync()
+    wall = time.perf_counter() - t_start
+    launches = launch_count() - l0
+    clocks = clocks_stop(*clk, dev) if rank == 0 else None
+    # the dispatcher side (apply + dispatch) overlaps the fill; a round's busy
+    # time is the exchange plus the longer of the two
+    busy_s = cr.t_exchange + cr.t_overlap
+    local = torch.tensor([busy_s, wall, float(be.n_queued), float(be.fill_ms), cr.t_exchange, cr.t_apply,
+                          cr.t_dispatch, cr.t_fill], dtype=torch.float64, device=tdev)
+    if dist is not None:
+        mx = local.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = local.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    else:
+        mx = sm = local
+    if rank != 0:
+        return
+    decisions = float(sm[2]) + be.n_dispatched  # local decisions on every worker + dispatches (replicated: once)
+    busy, wall_max = float(mx[0]), float(mx[1])
+    line = {
+        "metric": METRIC, "value": decisions / busy, "unit": "decisions/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * busy / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32/int64",
+        "data": "synthetic",
+        "config": {"workload": wl.desc.replace("at D=1: DLPM", f"D2LPM D={world}"), "nq_total": wl.nq,
+                   "clients": wl.clients, "M": wl.M, "capacity": wl.CAP, "quantum_local": wl.quantum(),
+                   "quantum_global": q_w, "l2": wl.l2,
+                   "parallelism": f"D2LPM dp{world}: one worker per GPU, replicated dispatcher, NCCL all-gather "
+                                  "of finishes + eviction notices per round",
+                   "arrivals_per_round": (f"min({args.arrivals}, cluster admissions of the previous round)"
+                                          if args.arrivals > 0 else "cluster admissions of the previous round")
+                   + ", dispatched on every replica while the workers fill (pipelined: they join the next "
+                     "round's queues)"},
+        "e2e": {"value": decisions / wall_max, "unit": "decisions/s",
+                "h2d_bytes_per_step": int(be.h2d / args.steps), "d2h_bytes_per_step": None},
+        "gpu_launches": int(launches),
+        "cluster_ms_per_step": {"fill_device": float(mx[3]) / args.steps,
+                                "exchange": 1000 * float(mx[4]) / args.steps,
+                                "apply": 1000 * float(mx[5]) / args.steps,
+                                "dispatch": 1000 * float(mx[6]) / args.steps,
+                                "fill_host_wall": 1000 * float(mx[7]) / args.steps},
+        "local_decisions_per_step": float(sm[2]) / args.steps, "dispatches_per_step": be.n_dispatched / args.steps,
+        "seed_dispatch": {"arrivals": n_seed, "seconds": seed_s},
+        "clocks": clocks, "host_wall_s": wall_max,
+    }
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -301,6 +387,10 @@ def main():
                     help="c2 = configs[1] (64k queue), c5 = configs[4] at D=1 (1M queue, 8k prompts)")
     ap.add_argument("--nq", type=int, default=0, help="queued requests per GPU (default: the config's)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cluster", action="store_true", help="D2LPM cluster path even at N=1")
+    ap.add_argument("--arrivals", type=int, default=128,
+                    help="cluster path: arrivals per round (a fixed cluster-wide rate, the same at every N; "
+                         "0 = as many as the cluster admitted last round)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -324,7 +414,13 @@ def main():
             dev = local % max(ngpu, 1)
         dist = tdist
 
-    wl = make_workload(args.workload, args.nq, rank, args.steps + args.warmup)
+    if args.impl == "reference" and rank != 0:
+        return  # the reference arm runs on rank 0 only
+    cluster = world > 1 or args.cluster
+    # the cluster path dispatches ONE shared stream (rank-independent seed);
+    # independent workers (N=1) use their rank's seed
+    wl = make_workload(args.workload, args.nq, 0 if cluster else rank, args.steps + args.warmup, device=dev,
+                       world=world if cluster else 1)
     cfg = {"workload": wl.desc, "nq_per_gpu": wl.nq, "clients": wl.clients, "M": wl.M, "capacity": wl.CAP,
            "quantum": wl.quantum(), "l2": wl.l2, "parallelism": f"dp{args.gpus} (independent workers)"}
 
@@ -348,6 +444,8 @@ def main():
         return
 
     from paper_2501_14312_b200.device import launch_count
+    if cluster:
+        return run_cluster(args, wl, rank, world, dev, tdev, dist)
     g = GpuSteps(wl, dev)
     now = 0
     for _ in range(args.warmup):

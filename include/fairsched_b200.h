@@ -129,6 +129,10 @@ int fs_trie_longest_match_workers(fs_trie *t, int32_t req, int64_t now, int32_t 
 /* RadixTree.evict_notify (radix.py:254-302); the path is arena[path_src : path_src+path_len] */
 int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_len, int32_t worker,
                          int32_t keep_len, int64_t notice_time);
+/* n notices applied in order in one launch (the all-gathered eviction notices of
+ * a D2lpm round, global_policies.py:130-132 -> radix.py:254-302). */
+int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *path_src, const int32_t *path_len,
+                              const int32_t *worker, const int32_t *keep_len, const int64_t *notice_time);
 /* Node table export for RadixTree.dump / check (radix.py:306-340).  Writes up to
  * cap nodes (index 0 = root) and sets *n to the node-table size; dead slots have
  * parent == -2. wmask may be NULL. */
@@ -214,6 +218,9 @@ int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32
                 int64_t *out_rounds);
 /* D2lpm.on_finish (global_policies.py:126-129) */
 int fs_dispatch_finish(fs_dispatcher *d, int32_t client, int32_t worker, int64_t output_tokens);
+/* n finish records in order (the all-gathered finishes of a round) */
+int fs_dispatch_finish_many(fs_dispatcher *d, int64_t n, const int32_t *clients, const int32_t *workers,
+                            const int64_t *output_tokens);
 /* q_{i,w} row of one client (D values) and dict-key presence flags */
 int fs_dispatch_counters(fs_dispatcher *d, int32_t client, int64_t *q_row, uint8_t *present);
 int fs_dispatch_queue_sizes(fs_dispatcher *d, int64_t *sizes);

@@ -89,31 +89,51 @@ class TorchComm:
 
 class ClusterRank:
     """Protocol driver of one rank.  `backend` provides the worker and the
-    dispatcher replica (see GpuRank / the oracle backend in tests)."""
+    dispatcher replica (see GpuRank / the oracle backend in tests).
 
-    def __init__(self, backend, comm, out_tokens: int = 8):
+    pipelined: a round's arrivals are dispatched while the workers fill and
+    join the queues of the NEXT round's fill (they arrive just after this
+    round's step).  The dispatcher sees exactly the same inputs in the same
+    order; only the local enqueue moves one round later.  With a backend whose
+    dispatcher has its own CUDA stream (`concurrent_dispatch`), the dispatcher
+    side runs on a second host thread concurrently with the fill."""
+
+    def __init__(self, backend, comm, out_tokens: int = 8, max_arrivals: int | None = None,
+                 pipelined: bool = False):
         self.be = backend
+        self.max_arrivals = max_arrivals
         self.comm = comm
         self.out_tokens = out_tokens
+        self.pipelined = pipelined
+        self._pool = None
+        if pipelined and getattr(backend, "concurrent_dispatch", False):
+            from concurrent.futures import ThreadPoolExecutor
+            self._pool = ThreadPoolExecutor(1)
+        self._late = []           # pipelined arrivals routed here, enqueued at the next round
         self.prev = []            # (request index, client, path handle) admitted last round
         self.notices = np.zeros((0, NOTICE_COLS), np.int64)
-        self.last_cluster_admitted = 0
         self.next_arrival = 0
+        self.t_exchange = 0.0  # host wall seconds: all-gather, apply, dispatch
+        self.t_apply = 0.0
+        self.t_dispatch = 0.0
+        self.t_fill = 0.0     # host wall of the fill call
+        self.t_overlap = 0.0  # per round: max(fill, dispatcher side) when pipelined, else their sum
 
     def seed(self, arrivals: list, now: int) -> np.ndarray:
         """Initial burst: dispatch `arrivals` everywhere, enqueue mine."""
-        return self._dispatch(arrivals, now)
+        return self._dispatch(arrivals, now)[0]
 
-    def _dispatch(self, arrivals, now) -> np.ndarray:
+    def _dispatch(self, arrivals, now, enqueue=True):
         if not arrivals:
-            return np.zeros(0, np.int32)
+            return np.zeros(0, np.int32), []
         workers = self.be.dispatch(arrivals, now)
         mine = [a for a, w in zip(arrivals, workers) if w == self.comm.rank]
-        if mine:
+        if mine and enqueue:
             self.be.enqueue(mine)
-        return workers
+        return workers, mine
 
     def round(self, now: int, arrival_stream) -> RoundResult:
+        import time
         be, comm = self.be, self.comm
         # 1. completion of last round's batch on this worker
         fin = np.zeros((len(self.prev), FIN_COLS), np.int64)
@@ -123,27 +143,65 @@ class ClusterRank:
             fin[:, 1] = comm.rank
             fin[:, 2] = self.out_tokens
             be.complete([h for _, _, h in self.prev], clients, self.out_tokens)
-        # 2. exchange and apply in rank order (finishes, then notices)
+        # 2. exchange; every replica applies the records in rank order (finishes, then notices)
         rows = np.zeros((fin.shape[0] + self.notices.shape[0], 1 + NOTICE_COLS), np.int64)
         rows[: fin.shape[0], 0] = 0
         rows[: fin.shape[0], 1:1 + FIN_COLS] = fin
         rows[fin.shape[0]:, 0] = 1
         rows[fin.shape[0]:, 1:] = self.notices
+        t0 = time.perf_counter()
         gathered = comm.all_gather_rows(rows)
-        n_adm_cluster = 0
-        for part in gathered:
-            f = part[part[:, 0] == 0]
-            for client, worker, out in f[:, 1:1 + FIN_COLS]:
-                be.dispatcher_finish(int(client), int(worker), int(out))
-            n_adm_cluster += len(f)
-            for src, ln, keep, worker, emitted in part[part[:, 0] == 1][:, 1:]:
-                be.dispatcher_notice(int(src), int(ln), int(keep), int(worker), int(emitted))
-        # 3. arrivals, dispatched identically on every replica
-        arrivals = arrival_stream(self.next_arrival, n_adm_cluster)
+        t1 = time.perf_counter()
+        n_adm_cluster = sum(int((part[:, 0] == 0).sum()) for part in gathered)
+        n_arr = n_adm_cluster if self.max_arrivals is None else min(n_adm_cluster, self.max_arrivals)
+        arrivals = arrival_stream(self.next_arrival, n_arr)
         self.next_arrival += len(arrivals)
-        workers = self._dispatch(arrivals, now)
-        # 4. local fill
-        adm, handles, clients, notices, nq, ms = be.fill(now)
+
+        def dispatcher_side():
+            ta = time.perf_counter()
+            batched = hasattr(be, "dispatcher_apply")
+            for part in gathered:
+                f = part[part[:, 0] == 0]
+                nt = part[part[:, 0] == 1][:, 1:]
+                if batched:
+                    be.dispatcher_apply(f[:, 1:1 + FIN_COLS], nt)
+                    continue
+                for client, worker, out in f[:, 1:1 + FIN_COLS]:
+                    be.dispatcher_finish(int(client), int(worker), int(out))
+                for src, ln, keep, worker, emitted in nt:
+                    be.dispatcher_notice(int(src), int(ln), int(keep), int(worker), int(emitted))
+            tb = time.perf_counter()
+            # 3. arrivals, dispatched identically on every replica
+            ws, mine = self._dispatch(arrivals, now, enqueue=not self.pipelined)
+            return ws, mine, tb - ta, time.perf_counter() - tb
+
+        if self.pipelined:
+            if self._late:
+                be.enqueue(self._late)  # last round's arrivals join this round's queue
+            fut = self._pool.submit(dispatcher_side) if self._pool is not None else None
+            if fut is None:
+                workers, mine, ta, td = dispatcher_side()
+            # 4. local fill (concurrently with the dispatcher chain on its own stream)
+            tf = time.perf_counter()
+            adm, handles, clients, notices, nq, ms = be.fill(now)
+            tf = time.perf_counter() - tf
+            if fut is not None:
+                workers, mine, ta, td = fut.result()
+                self.t_overlap += time.perf_counter() - t1
+            else:
+                self.t_overlap += ta + td + tf
+            self._late = mine
+        else:
+            workers, mine, ta, td = dispatcher_side()
+            # 4. local fill
+            tf = time.perf_counter()
+            adm, handles, clients, notices, nq, ms = be.fill(now)
+            tf = time.perf_counter() - tf
+            self.t_overlap += ta + td + tf
+        self.t_fill += tf
+        self.t_exchange += t1 - t0
+        self.t_apply += ta
+        self.t_dispatch += td
         self.prev = list(zip(adm, clients, handles))
         self.notices = notices
         return RoundResult(adm, workers, nq, len(arrivals), ms)
@@ -152,6 +210,8 @@ class ClusterRank:
 class GpuRank:
     """CUDA backend of one rank: its worker (local trie + DLPM queue) and a
     dispatcher replica, both on this rank's GPU, through the C ABI."""
+
+    concurrent_dispatch = True  # the dispatcher replica has its own CUDA stream
 
     def __init__(self, rank, device, queue, D, M, capacity, reserve, w_e, w_q, q_u, q_w, n_clients):
         from .device import Context, DispatcherDev, Trie, WorkerDev
@@ -201,3 +261,106 @@ class GpuRank:
     def dispatcher_state(self, n_clients):
         q, present, qsize = self.d.device_counters(n_clients)
         return q, present, qsize
+
+
+class GpuStreamRank:
+    """CUDA backend of one rank for the benchmark's serving loop: the workload's
+    initial queue materialized on the device (identical order on every rank, so
+    arena offsets and eviction-notice paths agree) plus a host pool of later
+    arrivals uploaded as they arrive.  Stream index i < nq is initial request i;
+    nq + k is pool request k."""
+
+    concurrent_dispatch = True  # the dispatcher replica has its own CUDA stream
+
+    def __init__(self, rank, device, wl, D, w_e, w_q, q_w, n_clients):
+        from .device import Context, DispatcherDev, Trie, WorkerDev
+        self.rank = rank
+        self.wl = wl
+        self.pool = wl.pool
+        tot = wl.queue_tokens + int(self.pool.lens.sum()) + 4 * (wl.nq + len(self.pool)) + 1024
+        self.ctx = Context(device, arena_tokens=tot, max_requests=wl.nq + len(self.pool) + 16)
+        ids, clients = wl.put_initial(self.ctx)
+        self.ids = np.full(wl.nq + len(self.pool), -1, np.int32)
+        self.clients = np.zeros(wl.nq + len(self.pool), np.int32)
+        self.ids[:wl.nq] = ids
+        self.clients[:wl.nq] = clients
+        self.clients[wl.nq:] = self.pool.clients
+        self.uploaded = wl.nq
+        self.trie = Trie(self.ctx, wl.CAP)
+        self.w = WorkerDev(self.ctx, self.trie, "dlpm", wl.quantum(), wl.M, wl.reserve, w_e, w_q,
+                           max_clients=n_clients)
+        self.d = DispatcherDev(self.ctx, D, q_w, w_e, w_q, max_clients=n_clients)
+        self.h2d = 0
+        self.fill_ms = 0.0
+        self.disp_s = 0.0
+        self.n_queued = 0
+        self.n_dispatched = 0
+
+    def _ensure(self, upto):
+        if upto <= self.uploaded:
+            return
+        p, nq = self.pool, self.wl.nq
+        a, b = self.uploaded - nq, upto - nq
+        o0 = int(p.offsets[a])
+        o1 = int(p.offsets[b - 1] + p.lens[b - 1])
+        self.ids[self.uploaded:upto] = self.ctx.add_requests(p.flat[o0:o1], p.offsets[a:b] - o0, p.lens[a:b],
+                                                             p.clients[a:b], p.labels[a:b])
+        self.h2d += (o1 - o0) * 4 + (b - a) * 24
+        self.uploaded = upto
+
+    def arrival_stream(self, first, count):
+        nq = self.wl.nq
+        count = max(0, min(count, len(self.pool) - first))
+        return list(range(nq + first, nq + first + count))
+
+    def dispatch(self, arrivals, now, batch=1 << 16):
+        import time
+        idx = np.asarray(arrivals, np.int64)
+        self._ensure(int(idx.max()) + 1)
+        t0 = time.perf_counter()
+        out = []
+        for a in range(0, len(idx), batch):
+            j = idx[a:a + batch]
+            w, _, _, _ = self.d.dispatch(self.ids[j], self.clients[j], np.full(len(j), now, np.int64))
+            out.append(w)
+        self.disp_s += time.perf_counter() - t0
+        self.n_dispatched += len(idx)
+        return np.concatenate(out)
+
+    def enqueue(self, mine):
+        self.w.enqueue(self.ids[np.asarray(mine, np.int64)])
+
+    def complete(self, handles, clients, out_tokens):
+        cl, cnt = np.unique(np.asarray(clients, np.int32), return_counts=True)
+        self.w.outputs(cl.astype(np.int32), (cnt * out_tokens).astype(np.int64))
+        self.trie.unpin_many(np.asarray(handles, np.int32))
+        self.h2d += cl.nbytes + cnt.nbytes + 4 * len(handles)
+
+    def dispatcher_apply(self, fin, notices):
+        if len(fin):
+            self.d.finish_many(fin[:, 0], fin[:, 1], fin[:, 2])
+        if len(notices):
+            self.d.trie.evict_notify_many(notices[:, 0], notices[:, 1], notices[:, 3], notices[:, 2], notices[:, 4])
+
+    def fill(self, now):
+        r = self.w.fill(now, 0, 0)
+        self.fill_ms += r.device_ms
+        self.n_queued += r.n_queued
+        adm_ids = np.asarray(r.adm_req, np.int64)
+        # device id -> stream index (uploads are in stream order: ids are increasing)
+        adm = np.searchsorted(self.ids[:self.uploaded], adm_ids).tolist()
+        notices = np.zeros((len(r.records), NOTICE_COLS), np.int64)
+        if len(r.records):
+            notices[:, 0] = r.records.src
+            notices[:, 1] = r.records.length
+            notices[:, 2] = r.records.keep
+            notices[:, 3] = self.rank
+            notices[:, 4] = now
+        return adm, [int(x) for x in r.adm_node], [int(self.clients[i]) for i in adm], notices, r.n_queued, \
+            r.device_ms
+
+    def close(self):
+        self.w.close()
+        self.trie.close()
+        self.d.close()
+        self.ctx.close()

@@ -971,12 +971,16 @@ struct NotifySmem {
     int32_t nseg, mlen, nf;
 };
 
+// hint_m0 >= 0: the path's match against the index at the start of the notice
+// batch (chain hint_S0); notices only remove strings, so a still-valid hint is
+// the exact match (warp_walk_hint validates it and re-walks otherwise).
 __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32_t plen, int32_t worker,
                                           int32_t keep, int64_t notice, Seg *segs, int32_t *found,
-                                          NotifySmem *sm) {
+                                          NotifySmem *sm, int64_t hint_S0 = -1, int32_t hint_m0 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp == 0) {
-        const WalkOut w = warp_walk(t, t.arena + psrc, plen, lane, segs, false);
+        const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8>(t, t.arena + psrc, plen, lane, segs, hint_S0, hint_m0)
+                                       : warp_walk<8>(t, t.arena + psrc, plen, lane, segs, false);
         if (lane == 0) { sm->nseg = w.nseg; sm->mlen = w.mlen; sm->nf = 0; }
     }
     __syncthreads();

@@ -32,7 +32,9 @@ __global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__rest
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= n) return;
-    const int32_t r = ids[i];
+    // ids == nullptr: roff/rlen are the i-th sequence's arena offset and length
+    // (eviction-notice paths), not request-table columns
+    const int32_t r = ids ? ids[i] : (int32_t)i;
     const int32_t len = rlen[r];
     const int32_t *rq = t.arena + roff[r];
     if (hint) {
@@ -835,6 +837,23 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     }
     __syncthreads();
     if (tid == 0) a.out[4] = t.sc->nrec;
+}
+
+// A round's eviction notices applied in order (evict_notify, radix.py:254-302).
+__global__ void __launch_bounds__(256) k_notify_many(TrieView t, int32_t n, const int64_t *__restrict__ src,
+                                                     const int32_t *__restrict__ len, const int32_t *__restrict__ worker,
+                                                     const int32_t *__restrict__ keep, const int64_t *__restrict__ when,
+                                                     const int32_t *__restrict__ m0, const int64_t *__restrict__ s0,
+                                                     Seg *segs, int32_t *found, int64_t *out) {
+    __shared__ NotifySmem nsm;
+    if (threadIdx.x == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; }
+    __syncthreads();
+    for (int32_t i = 0; i < n; i++) {
+        block_evict_notify(t, src[i], len[i], worker[i], keep[i], when[i], segs, found, &nsm, s0[i], m0[i]);
+        __syncthreads();
+        if (t.sc->status != FS_OK) break;
+    }
+    if (threadIdx.x == 0) out[0] = t.sc->status;
 }
 
 // ---------------------------------------------------------------- D2LPM

@@ -352,6 +352,7 @@ extern "C" int fs_arena_read(fs_ctx *c, int64_t off, int64_t n, int32_t *out) {
 // ---------------------------------------------------------------- trie
 struct fs_trie {
     fs_ctx *ctx = nullptr;
+    cudaStream_t stream = nullptr;  // own stream (dispatcher index) or null = the context's
     int64_t capacity = -1;
     int track = 0, nw = 0;
     int32_t ncap = 0;
@@ -370,9 +371,16 @@ struct fs_trie {
     DBuf<int64_t> rsrc;
     DBuf<int32_t> rlen, rkeep;
     DBuf<int64_t> opout;
+    DBuf<int64_t> nt_src, nt_when, nt_s0;  // fs_trie_evict_notify_many staging
+    DBuf<int32_t> nt_len, nt_worker, nt_keep, nt_m0;
     TrieScalars h_sc{};
     HBuf<int64_t> h_out;
 };
+
+// Every entry point synchronizes its stream before returning, so calls made
+// one after another are ordered whatever stream they use; a dispatcher's index
+// has its own stream so its chain can run while a worker fills (other thread).
+static cudaStream_t tstream(fs_trie *t) { return t->stream ? t->stream : t->ctx->stream; }
 
 static TrieView view(fs_trie *t) {
     TrieView v;
@@ -429,7 +437,7 @@ static uint32_t pow2_at_least(int64_t x) {
 
 // Make room for `extra_nodes` more nodes and paths of length `max_len`.
 static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
-    cudaStream_t s = t->ctx->stream;
+    cudaStream_t s = tstream(t);
     TRY(dgrow(t->segs, (int64_t)max_len + 16, s));
     TRY(dgrow(t->found, (int64_t)max_len + 16, s));
     // the position shadow covers the whole arena (grown with it; -1 = never written)
@@ -472,8 +480,8 @@ static int trie_reserve(fs_trie *t, int64_t extra_nodes, int32_t max_len) {
 }
 
 static int trie_pull(fs_trie *t) {
-    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, t->ctx->stream));
-    CK(cudaStreamSynchronize(t->ctx->stream));
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, tstream(t)));
+    CK(cudaStreamSynchronize(tstream(t)));
     return FS_OK;
 }
 
@@ -507,7 +515,7 @@ extern "C" int fs_trie_create(fs_ctx *c, int64_t capacity, int track_workers, in
 extern "C" int fs_trie_destroy(fs_trie *t) {
     if (!t) return FS_OK;
     cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
+    cudaStreamSynchronize(tstream(t));
     t->src.release(); t->la.release(); t->seq.release(); t->start.release(); t->end.release();
     t->parent.release(); t->nchild.release(); t->ref.release(); t->first.release(); t->freest.release();
     t->flags.release(); t->wmask.release(); t->wtime.release(); t->hslot.release(); t->slen.release();
@@ -515,6 +523,8 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
     t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
+    t->nt_src.release(); t->nt_when.release(); t->nt_len.release(); t->nt_worker.release(); t->nt_keep.release();
+    t->nt_s0.release(); t->nt_m0.release();
     delete t;
     return FS_OK;
 }
@@ -563,9 +573,9 @@ static int copy_records(fs_trie *t, int64_t nrec, fs_records *recs) {
     const int64_t k = std::min(nrec, recs->rec_cap);
     if (nrec > t->rsrc.cap) return fail(FS_ERR_INTERNAL, "eviction record sink overflow (%lld)", (long long)nrec);
     if (k > 0) {
-        CK(cudaMemcpyAsync(recs->rec_src, t->rsrc.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, t->ctx->stream));
-        CK(cudaMemcpyAsync(recs->rec_len, t->rlen.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, t->ctx->stream));
-        CK(cudaMemcpyAsync(recs->rec_keep, t->rkeep.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, t->ctx->stream));
+        CK(cudaMemcpyAsync(recs->rec_src, t->rsrc.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, tstream(t)));
+        CK(cudaMemcpyAsync(recs->rec_len, t->rlen.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, tstream(t)));
+        CK(cudaMemcpyAsync(recs->rec_keep, t->rkeep.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, tstream(t)));
     }
     return FS_OK;
 }
@@ -591,15 +601,15 @@ static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     a.found = t->found.p;
     a.out = t->opout.p;
     a.sq = ++t->opseq;
-    k_op<<<1, 256, 0, c->stream>>>(a);
+    k_op<<<1, 256, 0, tstream(t)>>>(a);
     counted();
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t) * 5, cudaMemcpyDeviceToHost, tstream(t)));
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, tstream(t)));
+    CK(cudaStreamSynchronize(tstream(t)));
     for (int i = 0; i < 5; i++) out5[i] = t->h_out.p[i];
     TRY(copy_records(t, out5[4], recs));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(tstream(t)));
     return FS_OK;
 }
 
@@ -718,6 +728,48 @@ extern "C" int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_l
     int64_t o[5];
     TRY(run_op(t, a, o, nullptr));
     if (o[0] != FS_OK) return fail((int)o[0], "evict_notify failed");
+    return FS_OK;
+}
+
+extern "C" int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *path_src, const int32_t *path_len,
+                                         const int32_t *worker, const int32_t *keep_len, const int64_t *notice_time) {
+    if (!t || !t->track) return fail(FS_ERR_INVALID, "evict_notify needs a track_workers trie");
+    if (n < 0) return fail(FS_ERR_INVALID, "bad count");
+    if (n == 0) return FS_OK;
+    fs_ctx *c = t->ctx;
+    TRY(ctx_use(c));
+    int32_t maxlen = c->max_len;
+    for (int64_t i = 0; i < n; i++) {
+        if (path_src[i] < 0 || path_len[i] < 0 || path_src[i] + path_len[i] > c->arena_used)
+            return fail(FS_ERR_INVALID, "path range of notice %lld", (long long)i);
+        if (worker[i] < 0 || worker[i] >= t->nw) return fail(FS_ERR_INVALID, "worker of notice %lld", (long long)i);
+        maxlen = std::max(maxlen, path_len[i]);
+    }
+    cudaStream_t s = tstream(t);
+    TRY(trie_reserve(t, 2 * n, maxlen));
+    TRY(dgrow(t->nt_src, n, s)); TRY(dgrow(t->nt_when, n, s)); TRY(dgrow(t->nt_len, n, s));
+    TRY(dgrow(t->nt_worker, n, s)); TRY(dgrow(t->nt_keep, n, s));
+    CK(cudaMemcpyAsync(t->nt_src.p, path_src, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(t->nt_when.p, notice_time, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(t->nt_len.p, path_len, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(t->nt_worker.p, worker, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(t->nt_keep.p, keep_len, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    // batch-start matches of every path in parallel (K1 over arena ranges, no
+    // stamping); the serial chain resumes each walk from them
+    TRY(dgrow(t->nt_m0, n, s)); TRY(dgrow(t->nt_s0, n, s));
+    k_match<8, false><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+        view(t), nullptr, (int32_t)n, t->nt_src.p, t->nt_len.p, 0, 0, 0, 0u, nullptr, t->nt_m0.p, nullptr, nullptr,
+        t->nt_s0.p, nullptr, nullptr);
+    counted();
+    k_notify_many<<<1, 256, 0, s>>>(view(t), (int32_t)n, t->nt_src.p, t->nt_len.p, t->nt_worker.p, t->nt_keep.p,
+                                    t->nt_when.p, t->nt_m0.p, t->nt_s0.p, t->segs.p, t->found.p, t->opout.p);
+    counted();
+    CK(cudaGetLastError());
+    t->opseq += 1;
+    CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (t->h_out.p[0] != FS_OK) return fail((int)t->h_out.p[0], "evict_notify_many failed");
     return FS_OK;
 }
 
@@ -1166,13 +1218,15 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         smem_set = true;
     }
     if (w->nhelp < 0) {
-        // one co-resident helper CTA per remaining SM (cooperative launch);
+        // one co-resident helper CTA per SM but two (cooperative launch);
         // FS_SCHED_HELPERS overrides (0 = the leader sweeps alone)
         int nsm = 0, per = 0, coop = 0;
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
         CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_schedule, FS_SCHED_THREADS, sizeof(SchedSmem)));
-        int nh = coop ? std::max(0, per * nsm - 1) : 0;
+        // one SM stays free: a D2LPM dispatcher chain on its own stream runs
+        // concurrently with the fill (cluster rounds)
+        int nh = coop ? std::max(0, per * nsm - 2) : 0;
         if (const char *e = getenv("FS_SCHED_HELPERS")) nh = std::min(nh, std::max(0, atoi(e)));
         w->nhelp = nh;
         TRY(dgrow(w->ctl, 1, s));
@@ -1266,6 +1320,13 @@ extern "C" int fs_dispatcher_create(fs_ctx *c, int D, int64_t quantum, int64_t w
     fs_dispatcher *d = new fs_dispatcher();
     d->ctx = c; d->D = D; d->quantum = quantum; d->w_e = w_e; d->w_q = w_q; d->nclients = max_clients;
     TRY(fs_trie_create(c, -1, 1, D, &d->tree));
+    {
+        // highest priority: the serial dispatch chain is the latency-critical
+        // side when it overlaps a worker's fill (cluster rounds)
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&d->tree->stream, cudaStreamNonBlocking, hi));
+    }
     const int64_t nq = (int64_t)max_clients * D;
     d->h_q.assign(nq, 0); d->h_qset.assign(nq, 0); d->h_qsize.assign(D, 0);
     TRY(dgrow(d->q, nq, c->stream)); TRY(dgrow(d->qset, nq, c->stream)); TRY(dgrow(d->qsize, D, c->stream));
@@ -1281,8 +1342,10 @@ extern "C" int fs_dispatcher_create(fs_ctx *c, int D, int64_t quantum, int64_t w
 extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
     if (!d) return FS_OK;
     cudaSetDevice(d->ctx->device);
-    cudaStreamSynchronize(d->ctx->stream);
+    cudaStream_t ds = d->tree->stream;
+    cudaStreamSynchronize(ds);
     fs_trie_destroy(d->tree);
+    if (ds) cudaStreamDestroy(ds);
     d->q.release(); d->qsize.release(); d->qset.release(); d->ids.release(); d->clients.release();
     d->dli.release(); d->dlw.release(); d->o_w.release(); d->o_mlen.release(); d->nows.release();
     d->dlq.release(); d->o_rounds.release(); d->hdr.release(); d->o_mask.release();
@@ -1296,8 +1359,8 @@ extern "C" fs_trie *fs_dispatcher_tree(fs_dispatcher *d) { return d ? d->tree : 
 extern "C" int fs_dispatch_last_profile(fs_dispatcher *d, int64_t *prof16) {
     if (!d || !prof16) return fail(FS_ERR_INVALID, "NULL argument");
     TRY(ctx_use(d->ctx));
-    CK(cudaMemcpyAsync(prof16, d->hdr.p + 4, 16 * sizeof(int64_t), cudaMemcpyDeviceToHost, d->ctx->stream));
-    CK(cudaStreamSynchronize(d->ctx->stream));
+    CK(cudaMemcpyAsync(prof16, d->hdr.p + 4, 16 * sizeof(int64_t), cudaMemcpyDeviceToHost, d->tree->stream));
+    CK(cudaStreamSynchronize(d->tree->stream));
     return FS_OK;
 }
 
@@ -1307,7 +1370,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     if (!d || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     if (n == 0) return FS_OK;
     fs_ctx *c = d->ctx;
-    cudaStream_t s = c->stream;
+    cudaStream_t s = d->tree->stream;
     TRY(ctx_use(c));
     for (int64_t i = 0; i < n; i++) {
         if (req_ids[i] < 0 || req_ids[i] >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id");
@@ -1392,6 +1455,13 @@ extern "C" int fs_dispatch_finish(fs_dispatcher *d, int32_t client, int32_t work
     return FS_OK;
 }
 
+extern "C" int fs_dispatch_finish_many(fs_dispatcher *d, int64_t n, const int32_t *clients, const int32_t *workers,
+                                       const int64_t *output_tokens) {
+    if (!d || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    for (int64_t i = 0; i < n; i++) TRY(fs_dispatch_finish(d, clients[i], workers[i], output_tokens[i]));
+    return FS_OK;
+}
+
 extern "C" int fs_dispatch_counters(fs_dispatcher *d, int32_t client, int64_t *q_row, uint8_t *present) {
     if (!d || client < 0 || client >= d->nclients) return fail(FS_ERR_INVALID, "bad arguments");
     const int64_t b = (int64_t)client * d->D;
@@ -1409,7 +1479,7 @@ extern "C" int fs_dispatch_queue_sizes(fs_dispatcher *d, int64_t *sizes) {
 // Push every host-side override (set_counter / set_queue_size) and finish delta.
 static int disp_flush(fs_dispatcher *d) {
     fs_ctx *c = d->ctx;
-    cudaStream_t s = c->stream;
+    cudaStream_t s = d->tree->stream;
     const int32_t ndl = (int32_t)d->dl_idx.size();
     if (ndl == 0) return FS_OK;
     TRY(dgrow(d->dli, ndl, s)); TRY(dgrow(d->dlw, ndl, s)); TRY(dgrow(d->dlq, ndl, s));
@@ -1423,7 +1493,7 @@ extern "C" int fs_dispatch_select(fs_dispatcher *d, int32_t client, uint64_t mat
                                   int64_t *rounds) {
     if (!d || client < 0 || client >= d->nclients || !worker) return fail(FS_ERR_INVALID, "bad arguments");
     fs_ctx *c = d->ctx;
-    cudaStream_t s = c->stream;
+    cudaStream_t s = d->tree->stream;
     TRY(ctx_use(c));
     TRY(disp_flush(d));
     TRY(dgrow(d->clients, 1, s)); TRY(dgrow(d->o_w, 1, s)); TRY(dgrow(d->o_mask, 1, s)); TRY(dgrow(d->o_rounds, 1, s));
@@ -1478,7 +1548,7 @@ extern "C" int fs_dispatcher_reserve_clients(fs_dispatcher *d, int32_t max_clien
     if (!d) return fail(FS_ERR_INVALID, "NULL dispatcher");
     if (max_clients <= d->nclients) return FS_OK;
     fs_ctx *c = d->ctx;
-    cudaStream_t s = c->stream;
+    cudaStream_t s = d->tree->stream;
     TRY(ctx_use(c));
     const int32_t nc = std::max(max_clients, d->nclients * 2);
     const int64_t old = (int64_t)d->nclients * d->D, nw = (int64_t)nc * d->D;
@@ -1502,13 +1572,13 @@ extern "C" int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t 
         a.q = d->q.p; a.qset = d->qset.p; a.qsize = d->qsize.p;
         a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = (int32_t)d->dl_idx.size();
         a.hdr = d->hdr.p;
-        k_dispatch<<<1, 256, 0, d->ctx->stream>>>(a);
+        k_dispatch<<<1, 256, 0, d->tree->stream>>>(a);
         counted();
         CK(cudaGetLastError());
         d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
     }
     const int64_t k = std::min<int64_t>(n, (int64_t)d->nclients * d->D);
-    cudaStream_t s = d->ctx->stream;
+    cudaStream_t s = d->tree->stream;
     if (q) CK(cudaMemcpyAsync(q, d->q.p, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
     if (present) CK(cudaMemcpyAsync(present, d->qset.p, k, cudaMemcpyDeviceToHost, s));
     if (qsize) CK(cudaMemcpyAsync(qsize, d->qsize.p, sizeof(int64_t) * d->D, cudaMemcpyDeviceToHost, s));

@@ -200,6 +200,18 @@ class Trie:
     def evict_notify(self, path_src: int, path_len: int, worker: int, keep_len: int, notice_time: int):
         call("fs_trie_evict_notify", self._h, path_src, path_len, worker, keep_len, notice_time)
 
+    def evict_notify_many(self, src, length, worker, keep, when):
+        """A round's notices in order, one launch (fs_trie_evict_notify_many)."""
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        n = len(src)
+        if n == 0:
+            return
+        ln = np.ascontiguousarray(length, dtype=np.int32)
+        wk = np.ascontiguousarray(worker, dtype=np.int32)
+        kp = np.ascontiguousarray(keep, dtype=np.int32)
+        wh = np.ascontiguousarray(when, dtype=np.int64)
+        call("fs_trie_evict_notify_many", self._h, n, _p64(src), _p32(ln), _p32(wk), _p32(kp), _p64(wh))
+
     def export(self):
         n = C.c_int64()
         call("fs_trie_export", self._h, 0, C.byref(n), None, None, None, None, None, None, None)
@@ -399,6 +411,14 @@ class DispatcherDev:
 
     def finish(self, client: int, worker: int, out: int):
         call("fs_dispatch_finish", self._h, client, worker, out)
+
+    def finish_many(self, clients, workers, outs):
+        cl = np.ascontiguousarray(clients, dtype=np.int32)
+        if len(cl) == 0:
+            return
+        wk = np.ascontiguousarray(workers, dtype=np.int32)
+        ot = np.ascontiguousarray(outs, dtype=np.int64)
+        call("fs_dispatch_finish_many", self._h, len(cl), _p32(cl), _p32(wk), _p64(ot))
 
     def set_counter(self, client: int, worker: int, q: int):
         call("fs_dispatch_set_counter", self._h, client, worker, q)

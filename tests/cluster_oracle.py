@@ -103,20 +103,25 @@ class OracleRank(_OracleWorkerSide):
 class SingleCluster:
     """All workers and one dispatcher in one process, same round structure."""
 
-    def __init__(self, q, D):
+    def __init__(self, q, D, pipelined=False):
         self.q = q
         self.D = D
+        self.pipelined = pipelined
+        self.late = [[] for _ in range(D)]
         self.workers = [_OracleWorkerSide(r, q) for r in range(D)]
         self.od = OracleD2lpm(D, Q_W, W_E, W_Q, SPEC.clients)
         self.prev = [[] for _ in range(D)]
         self.notices = [np.zeros((0, NOTICE_COLS), np.int64) for _ in range(D)]
         self.next_arrival = 0
 
-    def _dispatch(self, arrivals, now):
+    def _dispatch(self, arrivals, now, late=False):
         ws = []
         for i in arrivals:
             w = self.od.dispatch(self.q.tokens(i), int(self.q.clients[i]), now)[0]
-            self.workers[w].enqueue([i])
+            if late:
+                self.late[w].append(i)
+            else:
+                self.workers[w].enqueue([i])
             ws.append(w)
         return np.array(ws, np.int32)
 
@@ -139,7 +144,12 @@ class SingleCluster:
                 self.od.on_eviction(self.q.tokens(int(src))[: int(ln)], int(keep), int(worker), int(emitted))
         arrivals = take(self.next_arrival, n_adm)
         self.next_arrival += len(arrivals)
-        ws = self._dispatch(arrivals, now)
+        if self.pipelined:
+            for r, wk in enumerate(self.workers):  # last round's arrivals join now
+                if self.late[r]:
+                    wk.enqueue(self.late[r])
+                self.late[r] = []
+        ws = self._dispatch(arrivals, now, late=self.pipelined)
         out = []
         for r, wk in enumerate(self.workers):
             adm, handles, clients, notices, nq, _ = wk.fill(now)
@@ -149,9 +159,9 @@ class SingleCluster:
         return out, ws
 
 
-def run_single(D):
+def run_single(D, pipelined=False):
     q = workload()
-    c = SingleCluster(q, D)
+    c = SingleCluster(q, D, pipelined)
     take = stream(q)
     seed_ws = c.seed(list(range(N_SEED)), 0)
     rounds = []
@@ -164,11 +174,11 @@ def run_single(D):
             "n_notices": n_notices}
 
 
-def run_rank(rank, comm, backend):
+def run_rank(rank, comm, backend, pipelined=False):
     """Drive one rank through the protocol; returns its view of every round."""
     from paper_2501_14312_b200.cluster import ClusterRank
     q = backend.q
-    cr = ClusterRank(backend, comm, out_tokens=8)
+    cr = ClusterRank(backend, comm, out_tokens=8, pipelined=pipelined)
     take = stream(q)
     seed_ws = cr.seed(list(range(N_SEED)), 0)
     rounds = []
@@ -178,7 +188,7 @@ def run_rank(rank, comm, backend):
     return {"seed": np.asarray(seed_ws).tolist(), "rounds": rounds}
 
 
-def gloo_main(rank, world, port, out_dir, kind):
+def gloo_main(rank, world, port, out_dir, kind, pipelined=False):
     """Entry of one spawned rank (world size `world`, gloo on 127.0.0.1)."""
     import json
     import os
@@ -197,7 +207,7 @@ def gloo_main(rank, world, port, out_dir, kind):
             be = OracleRank(rank, q, world)
         else:
             be = make_gpu_rank(rank, q, world, "cuda:0")
-        res = run_rank(rank, TorchComm("cpu"), be)
+        res = run_rank(rank, TorchComm("cpu"), be, pipelined)
         st = be.dispatcher_state(SPEC.clients)
         res["qsize"] = [int(x) for x in st[-1]]
         with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:

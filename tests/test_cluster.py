@@ -24,6 +24,11 @@ def single():
     return {D: co.run_single(D) for D in (1, 2)}
 
 
+@pytest.fixture(scope="module")
+def single_pipe():
+    return {D: co.run_single(D, pipelined=True) for D in (1, 2)}
+
+
 def _check(rank_results, ref, D):
     assert rank_results[0]["seed"] == ref["seed"]
     for res in rank_results:
@@ -53,9 +58,9 @@ def test_local_rank_matches_single(single):
     _check([res], single[1], 1)
 
 
-def _spawn(world, kind, tmp_path):
+def _spawn(world, kind, tmp_path, pipelined=False):
     port = _free_port()
-    mp.start_processes(co.gloo_main, args=(world, port, str(tmp_path), kind), nprocs=world, join=True,
+    mp.start_processes(co.gloo_main, args=(world, port, str(tmp_path), kind, pipelined), nprocs=world, join=True,
                        start_method="spawn")
     return [json.load(open(tmp_path / f"rank{r}.json")) for r in range(world)]
 
@@ -77,3 +82,21 @@ def test_gpu_rank_single(single):
 def test_gpu_two_ranks_gloo(single, tmp_path):
     """Two ranks (both on cuda:0 here; one per GPU in deployment) over gloo."""
     _check(_spawn(2, "gpu", tmp_path), single[2], 2)
+
+
+def test_pipelined_differs_but_dispatches_alike(single, single_pipe):
+    """Pipelining moves the local enqueue one round later: the schedules differ,
+    the protocol still exercises every worker."""
+    assert single_pipe[2]["rounds"] != single[2]["rounds"]
+    ws = {w for rr in single_pipe[2]["rounds"] for w in rr["dispatched"]}
+    assert ws == {0, 1}
+
+
+def test_gloo_two_ranks_oracle_pipelined(single_pipe, tmp_path):
+    _check(_spawn(2, "oracle", tmp_path, pipelined=True), single_pipe[2], 2)
+
+
+@pytest.mark.gpu
+def test_gpu_two_ranks_gloo_pipelined(single_pipe, tmp_path):
+    """Pipelined rounds on the CUDA backend (dispatcher on its own stream)."""
+    _check(_spawn(2, "gpu", tmp_path, pipelined=True), single_pipe[2], 2)
