@@ -502,7 +502,7 @@ def main():
     achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
     share = phases / phases.sum()
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_k_match_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r01_k_match_traffic%s.json" % ("" if args.workload == "c2" else "_c5"))
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")

@@ -253,36 +253,52 @@ __device__ __forceinline__ int32_t warp_lcp(const int32_t *__restrict__ a, const
     return n;
 }
 
-// Software-pipelined LCP for the many-warp match kernel (K1): the next
-// 32*U-token block of both sequences is in flight while the current one is
-// compared, so a warp keeps 2*U*128 B of request tokens outstanding (read
-// once: streaming loads); over-reads at most one block past the mismatch.
-template <int U = 8>
-__device__ __forceinline__ int32_t warp_lcp_pipe(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
-                                                 int32_t n, int lane) {
-    int32_t av[U], bv[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-        const int32_t p = u * 32 + lane;
-        av[u] = p < n ? __ldg(a + p) : 0;
-        bv[u] = p < n ? __ldcs(b + p) : 0;
+// Vectorized LCP for the many-warp match kernel (K1).  Both sequences are
+// arena rows of 16-B aligned requests compared at the same depth, so they
+// share their alignment mod 4 tokens: after a scalar head up to the next
+// 16-B boundary, every lane compares 4 tokens with one 128-bit load per side
+// (V loads per side in flight per lane, 128*V tokens per warp step).  Reads
+// at most 3 tokens past n (inside the arena's row padding / next row).
+template <int V = 2>
+__device__ __forceinline__ int32_t warp_lcp_vec(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
+                                                int32_t n, int lane) {
+    if (n <= 0) return 0;
+    const int32_t h = min(n, (int32_t)(((16u - ((uint32_t)(uintptr_t)b & 15u)) & 15u) >> 2));
+    if ((((uintptr_t)a ^ (uintptr_t)b) & 15u) != 0) return warp_lcp<8>(a, b, n, lane);  // not co-aligned
+    if (h > 0) {
+        const unsigned m = __ballot_sync(FS_FULL, lane < h && __ldg(a + lane) != ld_stream(b + lane));
+        if (m) return __ffs(m) - 1;
     }
-    for (int32_t k = 0; k < n; k += 32 * U) {
-        int32_t an[U], bn[U];
-        const int32_t k2 = k + 32 * U;
+    for (int32_t k = h; k < n; k += 128 * V) {
+        int4 av[V], bv[V];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int32_t p = k2 + u * 32 + lane;
-            an[u] = p < n ? __ldg(a + p) : 0;
-            bn[u] = p < n ? __ldcs(b + p) : 0;
+        for (int v = 0; v < V; v++) {
+            const int32_t p = k + 128 * v + 4 * lane;
+            if (p < n) {
+                av[v] = __ldg(reinterpret_cast<const int4 *>(a + p));
+                int4 x;
+                asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(b + p));
+                bv[v] = x;
+            } else {
+                av[v] = make_int4(0, 0, 0, 0);
+                bv[v] = av[v];
+            }
         }
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const unsigned m = __ballot_sync(FS_FULL, av[u] != bv[u]);
-            if (m) return min(n, k + u * 32 + __ffs(m) - 1);
+        for (int v = 0; v < V; v++) {
+            const int32_t p = k + 128 * v + 4 * lane;
+            int f = 4;
+            if (av[v].w != bv[v].w && p + 3 < n) f = 3;
+            if (av[v].z != bv[v].z && p + 2 < n) f = 2;
+            if (av[v].y != bv[v].y && p + 1 < n) f = 1;
+            if (av[v].x != bv[v].x && p < n) f = 0;
+            const unsigned m = __ballot_sync(FS_FULL, f < 4);
+            if (m) {
+                const int L = __ffs(m) - 1;
+                return min(n, k + 128 * v + 4 * L + __shfl_sync(FS_FULL, f, L));
+            }
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) { av[u] = an[u]; bv[u] = bn[u]; }
     }
     return n;
 }
@@ -371,7 +387,7 @@ __device__ inline WalkOut warp_walk_from(const TrieView &t, const int32_t *__res
         if (c < 0) break;
         const int64_t S = t.src[c];
         const int32_t bound = min(len, t.slen[c]);
-        const int32_t k = 1 + (PIPE ? warp_lcp_pipe<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane)
+        const int32_t k = 1 + (PIPE ? warp_lcp_vec<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane)
                                     : warp_lcp<U>(t.arena + S + idx + 1, rq + idx + 1, bound - idx - 1, lane));
         const int32_t D = idx + k;  // request == chain S on [idx, D)
         const int32_t y = chain_lookup(t, S, idx, D - 1);

@@ -21,7 +21,7 @@
 
 // ---------------------------------------------------------------- K1
 template <int U, bool PIPE>
-__global__ void __launch_bounds__(256) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
+__global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
                                                int64_t now, int stamp, int64_t sq, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,

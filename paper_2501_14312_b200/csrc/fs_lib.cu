@@ -757,7 +757,7 @@ extern "C" int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *p
     // batch-start matches of every path in parallel (K1 over arena ranges, no
     // stamping); the serial chain resumes each walk from them
     TRY(dgrow(t->nt_m0, n, s)); TRY(dgrow(t->nt_s0, n, s));
-    k_match<8, false><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+    k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
         view(t), nullptr, (int32_t)n, t->nt_src.p, t->nt_len.p, 0, 0, 0, 0u, nullptr, t->nt_m0.p, nullptr, nullptr,
         t->nt_s0.p, nullptr, nullptr);
     counted();
@@ -1169,10 +1169,10 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         // cap) on config 5: keep the full grid
         const int64_t blocks = (n * 32 + 255) / 256;
         (void)k1_blocks;
-        static const int k1u = [] { const char *e = getenv("FS_K1_UNROLL"); return e ? atoi(e) : 8; }();
-        // FS_K1_UNROLL: 4 / 8 / 16 plain, 104 / 108 = pipelined 4 / 8
-        auto k1 = k1u == 104 ? k_match<4, true> : k1u == 108 ? k_match<8, true> : k1u >= 16 ? k_match<16, false>
-                : k1u >= 8 ? k_match<8, false> : k_match<4, false>;
+        static const int k1u = [] { const char *e = getenv("FS_K1_UNROLL"); return e ? atoi(e) : 101; }();
+        // FS_K1_UNROLL: 4 / 8 / 16 scalar lanes, 101 / 102 / 104 = 128-bit loads, 1 / 2 / 4 per side
+        auto k1 = k1u == 101 ? k_match<1, true> : k1u == 102 ? k_match<2, true> : k1u == 104 ? k_match<4, true>
+                : k1u >= 16 ? k_match<16, false> : k1u >= 8 ? k_match<8, false> : k_match<4, false>;
         k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
                                             ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
                                             w->s0.p, (unsigned long long *)w->alg.p,
@@ -1399,7 +1399,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
         // batch-start matches of every arrival, in parallel (K1, no stamping):
         // the serial chain below resumes each walk from them
         TRY(dgrow(d->m0, n, s)); TRY(dgrow(d->s0, n, s));
-        k_match<8, false><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+        k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
             view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, 0, 0, 0, 0u, nullptr, d->m0.p, nullptr,
             nullptr, d->s0.p, nullptr, nullptr);
         counted();
