@@ -176,6 +176,7 @@ class GpuSteps:
         self.pool_next = 0
         self.h2d = 0
         self.d2h = 0
+        self.unpin_ms = 0.0  # device time of the batch-completion unpins
 
     def step(self, now):
         n_prev = len(self.prev_nodes)
@@ -183,6 +184,7 @@ class GpuSteps:
             cl, cnt = np.unique(self.prev_clients, return_counts=True)
             self.w.outputs(cl.astype(np.int32), (cnt * self.wl.out_tokens).astype(np.int64))
             self.trie.unpin_many(self.prev_nodes)
+            self.unpin_ms += self.trie.last_ms()
             self.h2d += cl.nbytes + cnt.nbytes + self.prev_nodes.nbytes
         if n_prev and self.pool_next + n_prev <= len(self.pool):
             a, b = self.pool_next, self.pool_next + n_prev
@@ -458,21 +460,22 @@ def main():
     clk = clocks_start() if rank == 0 else (None, None, None)
     l0 = launch_count()
     h2d0, d2h0 = g.h2d, g.d2h
-    dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(4)
+    dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(5)
     sched = np.zeros(16)
     k1_hops = resumes = refills = 0
     t_start = time.perf_counter()
     for _ in range(args.steps):
         now += STEP_US
         t0 = time.perf_counter()
+        u0 = g.unpin_ms
         res = g.step(now)
         wall += time.perf_counter() - t0
-        dev_ms += res.device_ms
+        dev_ms += res.device_ms + (g.unpin_ms - u0)  # the fill plus the completion unpins
         decisions += res.n_queued
         adm += len(res.adm_req)
         alg_tok += res.stats[0]
         k1_ms.append(res.phases_ms[1])
-        phases += np.array(res.phases_ms)
+        phases += np.array(list(res.phases_ms) + [g.unpin_ms - u0])
         sched += np.array(res.stats[8:24], dtype=np.float64)
         k1_hops += res.stats[6]
         resumes += res.stats[4]
@@ -520,12 +523,14 @@ def main():
         "roofline": {"kernel": "k_match (K1 batched prefix match)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg},
-        "phase_share": {"merge": share[0], "k1_match": share[1], "k2_sort": share[2], "k3k4_schedule": share[3]},
+        "phase_share": {"merge": share[0], "k1_match": share[1], "k2_sort": share[2], "k3k4_schedule": share[3],
+                        "unpin": share[4]},
         "dominant_kernel": {"kernel": "k_schedule (K3/K4 admission chain, one CTA)", "share": share[3],
                             "bound": "latency (serial admission chain; see sched_profile_per_step)",
                             "avg_launch_ms": phases[3] / args.steps},
         "phase_ms_per_step": {"merge": phases[0] / args.steps, "k1_match": phases[1] / args.steps,
-                              "k2_sort": phases[2] / args.steps, "k3k4_schedule": phases[3] / args.steps},
+                              "k2_sort": phases[2] / args.steps, "k3k4_schedule": phases[3] / args.steps,
+                              "unpin": phases[4] / args.steps},
         "admissions_per_step": adm / args.steps, "queued_per_step": n_per_step,
         "sched_profile_per_step": {"find_cyc": sched[0] / args.steps, "walk_cyc": sched[1] / args.steps,
                                    "evict_cyc": sched[2] / args.steps, "tail_cyc": sched[3] / args.steps,
@@ -534,6 +539,8 @@ def main():
                                    "resumes": resumes / args.steps, "refill_events": refills / args.steps,
                                    "pop_argmin_cyc": sched[8] / args.steps, "pop_edit_cyc": sched[9] / args.steps,
                                    "pop_update_cyc": sched[10] / args.steps, "setup_cyc": sched[11] / args.steps,
+                                   "grid_sweeps": sched[15] / args.steps, "grid_sweep_cyc": sched[14] / args.steps,
+                                   "window_cyc": sched[13] / args.steps, "leaf_repoint_cyc": sched[12] / args.steps,
                                    "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }

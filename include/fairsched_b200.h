@@ -122,6 +122,8 @@ int fs_trie_pin(fs_trie *t, int32_t path_node);   /* radix.py:174-178 */
 int fs_trie_unpin(fs_trie *t, int32_t path_node); /* radix.py:180-185 */
 /* unpin of a whole finishing batch in one launch (worker.py:209-213), in order */
 int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *path_nodes);
+/* device time (CUDA events) of the last fs_trie_unpin_many */
+int fs_trie_last_ms(fs_trie *t, float *ms);
 /* RadixTree.evict_lru without a protect set (radix.py:210-250) */
 int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs);
 /* RadixTree.longest_match_workers (radix.py:101-110): mask bit w = worker w tagged */

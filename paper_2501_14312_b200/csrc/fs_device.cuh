@@ -956,7 +956,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         block_repoint(t, req_off, sm->mlen, len, sm->deepest);
     __syncthreads();
     const long long c3 = clock64();
-    if (tid == 0 && sm->prof) { sm->prof[12] += c2 - c1; sm->prof[13] += c3 - c2; }
+    if (tid == 0 && sm->prof) sm->prof[12] += c3 - c1;  // leaf + stamp + position repoint
     if (sm->status == FS_OK && t.wmask && worker >= 0) {
         // n.workers[worker] = now on every path node (radix.py:160-161)
         block_path_nodes(t, segs, sm->nseg, [&](int32_t n) {

@@ -157,13 +157,17 @@ struct FillArgs {
     unsigned long long *gkey;
     int32_t *gep;
     int32_t nhelp;
+    int32_t local_chunks;  // chunks the leader scans before a grid sweep
+    int32_t *rw_list;      // grid re-walk list (FS_CHUNK entries, -1 = skip)
 };
+#define FS_GRID_REWALK 96  // leader re-walk lists longer than this go to the helpers
 
 // Control block of one fill's grid sweeps, written by the leader CTA and read
 // by the helpers (release/acquire at gpu scope; reset by the host per fill).
 struct SweepCtl {
     int32_t seq;       // sweep number; -1 releases the helpers
     int32_t from, until, any_mode, epoch, result, done, saturated;
+    int32_t kind, nlist, pad2_;  // kind 0: sweep [from, until); 1: re-walk rw_list[0, nlist)
     int64_t slack, resumes, chunks, pad_;
     TrieScalars sc;    // the leader's trie scalars at the sweep
 };
@@ -374,37 +378,52 @@ __device__ inline void warp_resume(const FillArgs &a, int32_t p, int lane) {
 // B_p equals the admitted one's (LCP(r_p, r_e) > B_p forces both), so a stale
 // B is re-walked only when such an admission happened since it was exact.
 #define FS_FAST 256
+
 // Warp-0 scan of [from, wend) in order; returns the first qualifying position
 // or FS_NONE.  Same predicate and resume rule as the block-wide scan.
 __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t wend,
                                            bool any_mode, int64_t slack, int lane) {
+    // 4 x 32 positions per round: all slot loads, then all counter / length
+    // loads, then the in-order verdicts -- 2 memory round trips per 128
+    // positions instead of 2 per 32
+    constexpr int K = 4;
     const int32_t epoch = sm->epoch;
-    for (int32_t base = from; base < wend; base += 32) {
-        const int32_t p = base + lane;
-        bool q = false, r = false;
-        if (p < wend) {
-            const int4 s = a.slot[p];
-            if (s.w >= 0) {
-                if (any_mode) {
+    for (int32_t base = from; base < wend; base += 32 * K) {
+        int4 sv[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int32_t p = base + 32 * k + lane;
+            sv[k] = p < wend ? a.slot[p] : make_int4(0, 0, 0, -1);
+        }
+        bool gate[K];
+        int32_t need[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int32_t p = base + 32 * k + lane;
+            gate[k] = sv[k].w >= 0 && (any_mode || a.lpm || a.q[sv[k].x] > 0);
+            need[k] = gate[k] && !any_mode ? a.s_len[p] - sv[k].y : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int32_t p = base + 32 * k + lane;
+            bool q = false, r = false;
+            if (gate[k]) {
+                if (any_mode || need[k] <= slack) {
                     q = true;
-                } else if (a.lpm || a.q[s.x] > 0) {
-                    if (a.s_len[p] - s.y <= slack) {
-                        q = true;
-                    } else if (s.w < epoch) {
-                        const FiltView fv = filt_view(&sm->flt);
-                        if (!adm_maybe(fv, s.y, s.z, s.w)) a.slot[p].w = epoch;
-                        else if (cov_may_reach(a, fv, p, slack)) r = true;
-                    }
+                } else if (sv[k].w < epoch) {
+                    const FiltView fv = filt_view(&sm->flt);
+                    if (!adm_maybe(fv, sv[k].y, sv[k].z, sv[k].w)) a.slot[p].w = epoch;
+                    else if (cov_may_reach(a, fv, p, slack)) r = true;
                 }
             }
-        }
-        const unsigned mq = __ballot_sync(FS_FULL, q), mr = __ballot_sync(FS_FULL, r);
-        if (mq | mr) {
-            const int first = __ffs(mq | mr) - 1;
-            if ((mq >> first) & 1u) return base + first;
-            // a stale coverage must be re-walked first: hand the rest of the
-            // search to the block, whose 32 warps re-walk in parallel
-            return -(base + first) - 2;
+            const unsigned mq = __ballot_sync(FS_FULL, q), mr = __ballot_sync(FS_FULL, r);
+            if (mq | mr) {
+                const int first = __ffs(mq | mr) - 1;
+                if ((mq >> first) & 1u) return base + 32 * k + first;
+                // a stale coverage must be re-walked first: hand the rest of the
+                // search to the block, whose 32 warps re-walk in parallel
+                return -(base + 32 * k + first) - 2;
+            }
         }
     }
     return FS_NONE;
@@ -414,8 +433,11 @@ __device__ inline int32_t warp_find_window(const FillArgs &a, SchedSmem *sm, int
 // block: the first qualifying position, after re-walking the stale coverages
 // that precede the chunk's first plain hit.  `sm` supplies the block's scratch
 // (wl, red32, minB); the leader and the helper CTAs both run this.
+__device__ int32_t grid_rewalk(const FillArgs &a, SchedSmem *sm, int32_t nlist, int64_t slack);
+
 __device__ int32_t chunk_scan(const FillArgs &a, SchedSmem *sm, const FiltView &fv, int32_t base, int32_t until,
-                              bool any_mode, int64_t slack, int32_t epoch, unsigned long long *resumes) {
+                              bool any_mode, int64_t slack, int32_t epoch, unsigned long long *resumes,
+                              bool leader = false) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     if (tid == 0) { sm->wl_n = 0; sm->minB = FS_NONE; }
     __syncthreads();
@@ -436,6 +458,15 @@ __device__ int32_t chunk_scan(const FillArgs &a, SchedSmem *sm, const FiltView &
         }
     }
     const int32_t minA = block_min_i32(mine, sm->red32);
+    if (leader && a.nhelp > 0 && sm->wl_n > FS_GRID_REWALK) {
+        // many stale coverages before the first plain hit: the helper CTAs
+        // re-walk them (a warp each) instead of the leader's 32 warps
+        const int32_t nw = sm->wl_n;
+        for (int32_t i = tid; i < nw; i += blockDim.x) a.rw_list[i] = sm->wl[i] < minA ? sm->wl[i] : -1;
+        const int32_t mb = grid_rewalk(a, sm, nw, slack);
+        __syncthreads();
+        return min(minA, mb);
+    }
     if (sm->wl_n > 0) {
         for (int32_t i = warp; i < sm->wl_n; i += nwarps) {
             const int32_t p = sm->wl[i];
@@ -464,8 +495,33 @@ __device__ int32_t grid_sweep(const FillArgs &a, SchedSmem *sm, int32_t from, in
     __syncthreads();
     if (threadIdx.x == 0) {
         sm->cursor_seq++;
+        c->kind = 0;
         c->from = from; c->until = until; c->any_mode = any_mode; c->epoch = sm->epoch;
         c->slack = slack; c->result = FS_NONE; c->done = 0; c->saturated = sm->flt.saturated;
+        c->sc = *a.t.sc;
+        __threadfence();
+        st_release_i32(&c->seq, sm->cursor_seq);
+        while (ld_acquire_i32(&c->done) < a.nhelp) __nanosleep(64);
+        sm->minA = ld_acquire_i32(&c->result);
+    }
+    __syncthreads();
+    (void)ld_acquire_i32(&c->done);  // every thread: drop L1 lines the helpers made stale
+    const int32_t r = sm->minA;
+    __syncthreads();
+    return r;
+}
+
+// Leader side of a grid re-walk: the helpers' warps re-walk a.rw_list[0, n)
+// (warp_resume: exact coverage), refresh those slots and return the first
+// position that passes the budget test (FS_NONE if none).
+__device__ int32_t grid_rewalk(const FillArgs &a, SchedSmem *sm, int32_t nlist, int64_t slack) {
+    SweepCtl *c = a.ctl;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sm->cursor_seq++;
+        c->kind = 1; c->nlist = nlist; c->epoch = sm->epoch; c->slack = slack;
+        c->result = FS_NONE; c->done = 0;
         c->sc = *a.t.sc;
         __threadfence();
         st_release_i32(&c->seq, sm->cursor_seq);
@@ -512,6 +568,30 @@ __device__ void helper_loop(const FillArgs &ap, SchedSmem *sm) {
         const FiltView fv{a.gkey, a.gep, c->saturated};
         int32_t best = FS_NONE;
         int64_t nch = 0;
+        if (c->kind == 1) {
+            // re-walk list: one warp per entry
+            const int lane = tid & 31;
+            const int32_t nlist = c->nlist;
+            const int32_t gw = h * (int32_t)(blockDim.x >> 5) + (tid >> 5);
+            const int32_t nw = a.nhelp * (int32_t)(blockDim.x >> 5);
+            unsigned long long nres = 0;
+            for (int32_t i = gw; i < nlist; i += nw) {
+                const int32_t p = a.rw_list[i];
+                if (p < 0) continue;
+                warp_resume(a, p, lane);
+                __syncwarp();
+                if (lane == 0) {
+                    a.slot[p].w = epoch;
+                    if (a.s_len[p] - a.slot[p].y <= slack) atomicMin(&c->result, p);
+                    nres++;
+                }
+            }
+            if (lane == 0 && nres) atomicAdd((unsigned long long *)&c->resumes, nres);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd(&c->done, 1);
+            continue;
+        }
         for (int64_t base = from + (int64_t)h * FS_CHUNK; base < until; base += (int64_t)a.nhelp * FS_CHUNK) {
             if (tid == 0) sm->minA = *(volatile int32_t *)&c->result;
             __syncthreads();
@@ -539,6 +619,7 @@ __device__ void helper_loop(const FillArgs &ap, SchedSmem *sm) {
 __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, int32_t until, bool any_mode,
                               int64_t slack) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long cw0 = clock64();
     {
         // the next admissible request is usually right after the cursor: one
         // warp checks a short window before the whole block sweeps chunks
@@ -550,16 +631,26 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
         __syncthreads();
         const int32_t r = sm->minA;
         __syncthreads();
+        if (tid == 0) sm->prof[13] += clock64() - cw0;  // [13]: warp windows
         if (r >= 0 && r != FS_NONE) return r;
         from = r == FS_NONE ? wend : -(r + 2);
     }
-    if (a.nhelp > 0 && until - from > FS_CHUNK) return grid_sweep(a, sm, from, until, any_mode, slack);
+    // the leader scans the next FS_LOCAL_CHUNKS chunks itself (a hit is usually
+    // close), then hands the rest of the queue to the helper CTAs
     const FiltView fv = filt_view(&sm->flt);
-    for (int32_t base = from; base < until; base += FS_CHUNK) {
+    const int32_t local_end = a.nhelp > 0 ? min(until, from + a.local_chunks * FS_CHUNK) : until;
+    const int32_t grid_from = local_end;
+    for (int32_t base = from; base < local_end; base += FS_CHUNK) {
         if (tid == 0) sm->prof[4]++;
-        const int32_t best = chunk_scan(a, sm, fv, base, until, any_mode, slack, sm->epoch,
-                                        (unsigned long long *)&sm->resumes);
+        const int32_t best = chunk_scan(a, sm, fv, base, min(until, base + FS_CHUNK), any_mode, slack, sm->epoch,
+                                        (unsigned long long *)&sm->resumes, true);
         if (best != FS_NONE) return best;
+    }
+    if (grid_from < until) {
+        const long long cg = clock64();
+        const int32_t r = grid_sweep(a, sm, grid_from, until, any_mode, slack);
+        if (threadIdx.x == 0) { sm->prof[15]++; sm->prof[14] += clock64() - cg; }  // grid sweeps, cycles
+        return r;
     }
     return FS_NONE;
 }
@@ -915,8 +1006,8 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
     __shared__ int32_t s_w;
     __shared__ int32_t s_mlen;
     __shared__ uint64_t s_mask;
-    // cycle profile: [0] lmw walk + select, [1] insert walk, [2] evict, [12] leaf+stamp,
-    // [13] repoint, [14] worker tags, [15] total
+    // cycle profile: [0] lmw walk + select, [1] insert walk, [2] evict, [12] leaf + stamp +
+    // repoint, [14] worker tags, [15] total
     __shared__ int64_t prof[16];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;

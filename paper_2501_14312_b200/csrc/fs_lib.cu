@@ -375,6 +375,8 @@ struct fs_trie {
     DBuf<int32_t> nt_len, nt_worker, nt_keep, nt_m0;
     TrieScalars h_sc{};
     HBuf<int64_t> h_out;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    float last_ms = 0.f;  // device time of the last unpin_many
 };
 
 // Every entry point synchronizes its stream before returning, so calls made
@@ -523,6 +525,7 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
     t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
+    if (t->ev[0]) { cudaEventDestroy(t->ev[0]); cudaEventDestroy(t->ev[1]); }
     t->nt_src.release(); t->nt_when.release(); t->nt_len.release(); t->nt_worker.release(); t->nt_keep.release();
     t->nt_s0.release(); t->nt_m0.release();
     delete t;
@@ -682,14 +685,24 @@ extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
     TRY(dgrow(dn, n, s));
     CK(cudaMemcpyAsync(dn.p, nodes, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(t->opout.p, 0, sizeof(int64_t), s));
+    if (!t->ev[0]) { CK(cudaEventCreate(&t->ev[0])); CK(cudaEventCreate(&t->ev[1])); }
+    CK(cudaEventRecord(t->ev[0], s));
     k_unpin_many<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(view(t), dn.p, n, t->opout.p);
     counted();
     CK(cudaGetLastError());
+    CK(cudaEventRecord(t->ev[1], s));
     CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    CK(cudaEventElapsedTime(&t->last_ms, t->ev[0], t->ev[1]));
     if (t->h_out.p[0] == FS_ERR_UNDERFLOW) return fail(FS_ERR_UNDERFLOW, "unpin below zero (radix.py:183)");
     if (t->h_out.p[0] != FS_OK) return fail((int)t->h_out.p[0], "unpin_many failed");
+    return FS_OK;
+}
+
+extern "C" int fs_trie_last_ms(fs_trie *t, float *ms) {
+    if (!t || !ms) return fail(FS_ERR_INVALID, "NULL argument");
+    *ms = t->last_ms;
     return FS_OK;
 }
 
@@ -838,6 +851,7 @@ struct fs_worker {
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
     DBuf<SweepCtl> ctl;
+    DBuf<int32_t> rw_list;
     DBuf<unsigned long long> gkey;
     DBuf<int32_t> gep;
     int nhelp = -1;  // helper CTAs of the grid sweep (-1: not yet sized)
@@ -918,7 +932,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1230,10 +1244,13 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         if (const char *e = getenv("FS_SCHED_HELPERS")) nh = std::min(nh, std::max(0, atoi(e)));
         w->nhelp = nh;
         TRY(dgrow(w->ctl, 1, s));
+        TRY(dgrow(w->rw_list, FS_CHUNK, s));
         TRY(dgrow(w->gkey, FS_FSLOTS, s));
         TRY(dgrow(w->gep, FS_FSLOTS, s));
     }
-    a.ctl = w->ctl.p; a.gkey = w->gkey.p; a.gep = w->gep.p; a.nhelp = w->nhelp;
+    a.ctl = w->ctl.p; a.gkey = w->gkey.p; a.gep = w->gep.p; a.nhelp = w->nhelp; a.rw_list = w->rw_list.p;
+    static const int lch = [] { const char *e = getenv("FS_LOCAL_CHUNKS"); return e ? atoi(e) : 1; }();
+    a.local_chunks = lch;
     CK(cudaMemsetAsync(w->ctl.p, 0, sizeof(SweepCtl), s));
     if (w->nhelp > 0) {
         void *args[] = {&a};

@@ -200,6 +200,12 @@ class Trie:
     def evict_notify(self, path_src: int, path_len: int, worker: int, keep_len: int, notice_time: int):
         call("fs_trie_evict_notify", self._h, path_src, path_len, worker, keep_len, notice_time)
 
+    def last_ms(self) -> float:
+        """Device time of the last unpin_many (fs_trie_last_ms)."""
+        v = C.c_float()
+        call("fs_trie_last_ms", self._h, C.byref(v))
+        return v.value
+
     def evict_notify_many(self, src, length, worker, keep, when):
         """A round's notices in order, one launch (fs_trie_evict_notify_many)."""
         src = np.ascontiguousarray(src, dtype=np.int64)

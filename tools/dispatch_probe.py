@@ -32,8 +32,8 @@ for a in range(0, n, 4096):
     done = b
     prof = d.last_profile()
     if a == 0 or b == n:
-        print("cycles/arrival: lmw+select %.0f insert-walk %.0f leaf %.0f repoint %.0f tags %.0f total %.0f"
-              % tuple(x / (b - a) for x in (prof[0], prof[1], prof[12], prof[13], prof[14], prof[15])))
+        print("cycles/arrival: lmw+select %.0f insert-walk %.0f leaf+repoint %.0f tags %.0f total %.0f"
+              % tuple(x / (b - a) for x in (prof[0], prof[1], prof[12], prof[14], prof[15])))
     if time.perf_counter() - t0 > 60:
         break
 ctx.sync()
