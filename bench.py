@@ -96,11 +96,12 @@ class Config5(Workload):
     clients = 200
     CPU_NQ = 65536
 
-    def __init__(self, nq, rank, steps, device=0):
+    def __init__(self, nq, rank, steps, device=0, cpu_only=False):
         from paper_2501_14312_b200.workloads import config5
         self.nq = nq
         self.spec = config5(nq, seed=5 + rank)
         self.pool_n = 160 * steps + 512
+        self.cpu_only = cpu_only  # reference arm: build every token on the host (oracle/tokens.c)
         self.pool = self._host_queue(device, stream=1, first=0, count=self.pool_n, arrival=STEP_US)
         self.queue_tokens = nq * self.spec.length
         self.desc = ("config5 at D=1: DLPM, 200 clients, %d queued 8192-token prompts, branching-4 depth-6 prefix "
@@ -109,13 +110,21 @@ class Config5(Workload):
         self.l2 = "inputs larger than L2: the queue occupies %.1f GB; each step streams every queued request's " \
                   "matched prefix" % (self.queue_tokens * 4 / 1e9)
 
-    def _host_queue(self, device, stream, first, count, arrival):
-        """Materialize on the device, read back: host token buffers for arrivals / the CPU oracle."""
-        from paper_2501_14312_b200.device import Context
-        from paper_2501_14312_b200.trace import add_segments
+    def _host_queue(self, device, stream, first, count, arrival, cpu=False):
+        """Host token buffers of a slice of the stream: materialized on the device
+        and read back (the GPU arm's arrivals), or by the CPU restatement
+        oracle/tokens.c (the CPU baseline's sample, the reference arm)."""
         from paper_2501_14312_b200.workloads import Queue, deep_tree_segments
         segs, clients, labels = deep_tree_segments(self.spec, first=first, count=count, stream=stream)
         lens = segs.lens()
+        rids = [f"c5r{stream}.{first + i:08d}" for i in range(count)]
+        if cpu or self.cpu_only:
+            from oracle.materialize import expand_segments
+            flat, offs = expand_segments(segs)
+            return Queue(flat, offs[:-1].copy(), lens.astype(np.int32), clients, np.full(count, arrival, np.int64),
+                         rids, labels)
+        from paper_2501_14312_b200.device import Context
+        from paper_2501_14312_b200.trace import add_segments
         tmp = Context(device, arena_tokens=int(lens.sum()) + 4 * count + 1024, max_requests=count + 16)
         try:
             ids = add_segments(tmp, segs, clients, labels)
@@ -125,7 +134,6 @@ class Config5(Workload):
             offs = np.array([tmp.request_info(int(i))[0] - off0 for i in ids], np.int64)
         finally:
             tmp.close()
-        rids = [f"c5r{stream}.{first + i:08d}" for i in range(count)]
         return Queue(raw, offs, lens.astype(np.int32), clients, np.full(count, arrival, np.int64), rids, labels)
 
     def put_initial(self, ctx):
@@ -136,14 +144,14 @@ class Config5(Workload):
 
     def cpu_sample(self, device):
         n = min(self.nq, self.CPU_NQ)
-        return self._host_queue(device, stream=0, first=0, count=n, arrival=0), self.pool, n
+        return self._host_queue(device, stream=0, first=0, count=n, arrival=0, cpu=True), self.pool, n
 
 
-def make_workload(name, nq, rank, steps, device=0, world=1):
+def make_workload(name, nq, rank, steps, device=0, world=1, cpu_only=False):
     if name == "c2":
         return Config2(nq or 65536, rank, steps * world)
     if name == "c5":
-        return Config5(nq or (1 << 20), rank, steps * world, device=device)
+        return Config5(nq or (1 << 20), rank, steps * world, device=device, cpu_only=cpu_only)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -422,7 +430,7 @@ def main():
     # the cluster path dispatches ONE shared stream (rank-independent seed);
     # independent workers (N=1) use their rank's seed
     wl = make_workload(args.workload, args.nq, 0 if cluster else rank, args.steps + args.warmup, device=dev,
-                       world=world if cluster else 1)
+                       world=world if cluster else 1, cpu_only=args.impl == "reference")
     cfg = {"workload": wl.desc, "nq_per_gpu": wl.nq, "clients": wl.clients, "M": wl.M, "capacity": wl.CAP,
            "quantum": wl.quantum(), "l2": wl.l2, "parallelism": f"dp{args.gpus} (independent workers)"}
 

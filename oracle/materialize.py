@@ -59,3 +59,37 @@ def materialize(records) -> tuple:
         out_lens[rid] = g("true_output_len")
         order.append((rid, toks))
     return order, out_lens
+
+
+def expand_segments(segs):
+    """All requests of a paper_2501_14312_b200.trace.Segments, expanded by the C
+    restatement (oracle/tokens.c, pthreads): returns (flat int32 tokens, offsets
+    int64[n+1]).  Same tokens as expand_tokens per segment."""
+    import ctypes as C
+    import os
+    import subprocess
+
+    import numpy as np
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    lib_path = os.path.join(here, "libtokens.so")
+    src = os.path.join(here, "tokens.c")
+    if not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", here, "libtokens.so"], check=True)
+    lib = C.CDLL(lib_path)
+    fn = lib.or_expand_segments
+    fn.restype = C.c_int64
+    n = len(segs.seg_first) - 1
+    sf = np.ascontiguousarray(segs.seg_first, np.int64)
+    sn = np.ascontiguousarray(segs.seg_ns, np.int32)
+    sl = np.ascontiguousarray(segs.seg_len, np.int32)
+    nb = np.ascontiguousarray(segs.ns_bytes, np.uint8)
+    no = np.ascontiguousarray(segs.ns_off, np.int64)
+    nl = np.ascontiguousarray(segs.ns_len, np.int32)
+    total = int(sl.astype(np.int64).sum())
+    out = np.zeros(max(total, 1), np.int32)
+    offs = np.zeros(n + 1, np.int64)
+    P = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    fn(C.c_int64(n), P(sf, C.c_int64), P(sn, C.c_int32), P(sl, C.c_int32), P(nb, C.c_uint8), P(no, C.c_int64),
+       P(nl, C.c_int32), P(out, C.c_int32), P(offs, C.c_int64))
+    return out[:total], offs

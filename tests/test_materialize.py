@@ -79,6 +79,20 @@ def test_resolve_errors_match_reference():
     assert [digest(x) for x in oracle_expand_segments(segs)] == [digest(x) for _, x in order]
 
 
+def test_c_restatement_matches_hashlib():
+    """oracle/tokens.c (used for large CPU samples) == the hashlib restatement
+    == the reference goldens."""
+    for t in GOLD["traces"]:
+        segs, *_ = resolve(t["records"])
+        flat, offs = OM.expand_segments(segs)
+        got = [flat[offs[i]:offs[i + 1]] for i in range(segs.n)]
+        assert [digest(x) for x in got] == t["digests"]
+    segs, _, _ = deep_tree_segments(config5(), first=7, count=5)
+    flat, offs = OM.expand_segments(segs)
+    want = oracle_expand_segments(segs)
+    assert [list(flat[offs[i]:offs[i + 1]]) for i in range(5)] == [list(w) for w in want]
+
+
 def test_config5_structure():
     spec = config5()
     segs, clients, labels = deep_tree_segments(spec, first=100, count=64)
