@@ -74,6 +74,9 @@ int fs_requests_add_expanded(fs_ctx *ctx, int64_t n, const int64_t *seg_first, c
                              const int64_t *labels, int32_t *out_ids);
 /* Relabel requests (the order-maintenance labels ran out of gaps). */
 int fs_requests_set_labels(fs_ctx *ctx, int64_t n, const int32_t *ids, const int64_t *labels);
+/* Set the client of requests first uploaded without one (a token sequence the
+ * routing index saw before the worker enqueued it). */
+int fs_requests_set_clients(fs_ctx *ctx, int64_t n, const int32_t *ids, const int32_t *clients);
 int fs_requests_count(fs_ctx *ctx, int64_t *n);
 int fs_request_info(fs_ctx *ctx, int32_t id, int64_t *arena_off, int32_t *len);
 /* Read n arena tokens starting at arena offset off (paths of eviction records). */

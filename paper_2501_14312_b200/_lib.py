@@ -63,6 +63,7 @@ SIGNATURES = {
     "fs_requests_add": (C.c_int, [vp, i64, P32, P64, P32, P32, P64, P32]),
     "fs_requests_add_expanded": (C.c_int, [vp, i64, P64, P32, P32, i64, PU8, P64, P32, P32, P64, P32]),
     "fs_requests_set_labels": (C.c_int, [vp, i64, P32, P64]),
+    "fs_requests_set_clients": (C.c_int, [vp, i64, P32, P32]),
     "fs_requests_count": (C.c_int, [vp, P64]),
     "fs_request_info": (C.c_int, [vp, i32, P64, P32]),
     "fs_arena_read": (C.c_int, [vp, i64, i64, P32]),

@@ -226,9 +226,17 @@ __device__ inline void push_record(const TrieView &t, int64_t src, int32_t len, 
 // critical path (latency-bound).
 // Request tokens are read once per match: keep them out of L1 so the trie's
 // hot chains (compared by every warp of the SM) stay resident there.
+// They are also marked evict-first in L2: K1 streams ~10 GB per step on
+// config 5, which would otherwise flush the trie's node table, child hash and
+// position shadow out of L2 before the latency-bound scheduler runs.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ int32_t ld_stream(const int32_t *p) {
     int32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_first()));
     return v;
 }
 
@@ -263,6 +271,7 @@ template <int V = 2>
 __device__ __forceinline__ int32_t warp_lcp_vec(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
                                                 int32_t n, int lane) {
     if (n <= 0) return 0;
+    const uint64_t pol = l2_evict_first();
     const int32_t h = min(n, (int32_t)(((16u - ((uint32_t)(uintptr_t)b & 15u)) & 15u) >> 2));
     if ((((uintptr_t)a ^ (uintptr_t)b) & 15u) != 0) return warp_lcp<8>(a, b, n, lane);  // not co-aligned
     if (h > 0) {
@@ -277,8 +286,8 @@ __device__ __forceinline__ int32_t warp_lcp_vec(const int32_t *__restrict__ a, c
             if (p < n) {
                 av[v] = __ldg(reinterpret_cast<const int4 *>(a + p));
                 int4 x;
-                asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(b + p));
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(b + p), "l"(pol));
                 bv[v] = x;
             } else {
                 av[v] = make_int4(0, 0, 0, 0);
@@ -540,29 +549,41 @@ __device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int l
 // ---------------------------------------------------------------- path nodes
 // Call fn(node) once for every node of the path described by segs (each node
 // is visited at its first depth).  Block-parallel; segs must be visible.
-// Each thread batches K depths: all K pos loads, then all K start loads, then
-// the callbacks -- two memory round trips per K*blockDim depths instead of two
-// per depth (fn's stores would otherwise pin every load behind them).
+// The path's depths are flattened across its segments and each thread takes
+// K of them: all K pos loads, then all K (start, end) loads, then the callbacks
+// fn(node, start, end) -- a constant number of memory round trips per
+// K*blockDim depths whatever the number of segments (fn's stores would
+// otherwise pin every load behind them).
 template <typename F>
 __device__ inline void block_path_nodes(const TrieView &t, const Seg *segs, int32_t nseg, F fn) {
     constexpr int K = 8;
     const int32_t nt = (int32_t)blockDim.x;
-    for (int32_t s = 0; s < nseg; s++) {
-        const int64_t S = segs[s].S;
-        const int32_t a = segs[s].a, b = segs[s].b;
-        for (int32_t d0 = a + (int32_t)threadIdx.x; d0 < b; d0 += K * nt) {
-            int32_t nd[K], st[K];
+    int32_t total = 0;
+    for (int32_t s = 0; s < nseg; s++) total += segs[s].b - segs[s].a;
+    for (int32_t g0 = (int32_t)threadIdx.x; g0 < total; g0 += K * nt) {
+        int32_t nd[K], dd[K];
+        int32_t s = 0, base = 0;  // segment of depth index g (g increases with k)
 #pragma unroll
-            for (int k = 0; k < K; k++) {
-                const int32_t d = d0 + k * nt;
-                nd[k] = d < b ? t.pos[S + d] : -1;
+        for (int k = 0; k < K; k++) {
+            const int32_t g = g0 + k * nt;
+            nd[k] = -1;
+            dd[k] = -1;
+            if (g < total) {
+                while (g - base >= segs[s].b - segs[s].a) { base += segs[s].b - segs[s].a; s++; }
+                const int32_t d = segs[s].a + (g - base);
+                dd[k] = d;
+                nd[k] = t.pos[segs[s].S + d];
             }
-#pragma unroll
-            for (int k = 0; k < K; k++) st[k] = nd[k] >= 0 ? t.start[nd[k]] : -1;
-#pragma unroll
-            for (int k = 0; k < K; k++)
-                if (nd[k] >= 0 && st[k] == d0 + k * nt) fn(nd[k]);
         }
+        int32_t st[K], en[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            st[k] = nd[k] >= 0 ? t.start[nd[k]] : -1;
+            en[k] = nd[k] >= 0 ? t.end[nd[k]] : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++)
+            if (nd[k] >= 0 && st[k] == dd[k]) fn(nd[k], st[k], en[k]);
     }
 }
 
@@ -576,12 +597,12 @@ __device__ inline void block_repoint(const TrieView &t, int64_t S, int32_t a, in
 __device__ inline void block_pin_path(const TrieView &t, const Seg *segs, int32_t nseg, int delta) {
     long long acc = 0;
     bool under = false;
-    block_path_nodes(t, segs, nseg, [&](int32_t n) {
+    block_path_nodes(t, segs, nseg, [&](int32_t n, int32_t st, int32_t en) {
         const int32_t old = atomicAdd(&t.ref[n], delta);
-        if (delta > 0 && old == 0) acc += elen(t, n);
+        if (delta > 0 && old == 0) acc += en - st;
         if (delta < 0) {
             if (old <= 0) under = true;
-            else if (old == 1) acc -= elen(t, n);
+            else if (old == 1) acc -= en - st;
         }
     });
     if (acc) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)acc);
@@ -956,10 +977,10 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         block_repoint(t, req_off, sm->mlen, len, sm->deepest);
     __syncthreads();
     const long long c3 = clock64();
-    if (tid == 0 && sm->prof) sm->prof[12] += c3 - c1;  // leaf + stamp + position repoint
+    (void)c3;
     if (sm->status == FS_OK && t.wmask && worker >= 0) {
         // n.workers[worker] = now on every path node (radix.py:160-161)
-        block_path_nodes(t, segs, sm->nseg, [&](int32_t n) {
+        block_path_nodes(t, segs, sm->nseg, [&](int32_t n, int32_t, int32_t) {
             t.wmask[n] |= (1ull << worker);
             t.wtime[(int64_t)n * t.nw + worker] = now;
         });

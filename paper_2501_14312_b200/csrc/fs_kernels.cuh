@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
         if (lane < nb) {
             const int32_t b0 = lane << 10;
             const uint32_t bytes = (uint32_t)(((min(want, b0 + 1024) - b0) * 4 + 15) & ~15);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rq + b0), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(rq + b0), "r"(bytes),
+                         "l"(l2_evict_first()) : "memory");
         }
     }
     const WalkOut w = warp_walk<U, PIPE>(t, rq, len, lane, nullptr, true);
@@ -631,7 +632,7 @@ __device__ int32_t block_find(const FillArgs &a, SchedSmem *sm, int32_t from, in
         __syncthreads();
         const int32_t r = sm->minA;
         __syncthreads();
-        if (tid == 0) sm->prof[13] += clock64() - cw0;  // [13]: warp windows
+        (void)cw0;
         if (r >= 0 && r != FS_NONE) return r;
         from = r == FS_NONE ? wend : -(r + 2);
     }
@@ -698,10 +699,13 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     if (sm->ins.status == FS_OK) {
         block_pin_path(t, a.segs, sm->ins.nseg, +1);
         __syncthreads();
+        if (tid == 0) sm->prof[12] += clock64() - ct;  // TEMP: pin
+        const long long ct2 = clock64();
         // the matched node is pinned now (and may have gained a child): its
         // chunk of the LRU index changes; new nodes are pinned and past hw0
         if ((tid >> 5) == 0) warp_chunk_touch(t, &sm->lru, sm->ins.last, -1, tid & 31);
         __syncthreads();
+        if (tid == 0) sm->prof[13] += clock64() - ct2;  // TEMP: touch
     }
     if (tid == 0) {
         const InsertSmem &in = sm->ins;

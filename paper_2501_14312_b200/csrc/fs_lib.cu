@@ -328,6 +328,20 @@ extern "C" int fs_requests_set_labels(fs_ctx *c, int64_t n, const int32_t *ids, 
     return FS_OK;
 }
 
+extern "C" int fs_requests_set_clients(fs_ctx *c, int64_t n, const int32_t *ids, const int32_t *clients) {
+    if (!c || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    TRY(ctx_use(c));
+    for (int64_t i = 0; i < n; i++) {
+        if (ids[i] < 0 || ids[i] >= (int64_t)c->h_rclient.size()) return fail(FS_ERR_INVALID, "bad request id");
+        if (clients[i] < 0) return fail(FS_ERR_INVALID, "bad client id");
+        c->h_rclient[ids[i]] = clients[i];
+        CK(cudaMemcpyAsync(c->rclient.p + ids[i], c->h_rclient.data() + ids[i], sizeof(int32_t),
+                           cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
 extern "C" int fs_requests_count(fs_ctx *c, int64_t *n) {
     if (!c || !n) return fail(FS_ERR_INVALID, "NULL");
     *n = (int64_t)c->h_roff.size();

@@ -78,6 +78,11 @@ class Context:
         labels = np.ascontiguousarray(labels, dtype=np.int64)
         call("fs_requests_set_labels", self._h, len(ids), _p32(ids), _p64(labels))
 
+    def set_clients(self, ids: np.ndarray, clients: np.ndarray) -> None:
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        cl = np.ascontiguousarray(clients, dtype=np.int32)
+        call("fs_requests_set_clients", self._h, len(ids), _p32(ids), _p32(cl))
+
     def arena_read(self, off: int, n: int) -> np.ndarray:
         out = np.zeros(max(n, 1), np.int32)
         call("fs_arena_read", self._h, off, n, _p32(out))

@@ -69,6 +69,7 @@ class DeviceRuntime:
         self.ctx = Context(device, arena_tokens=1 << 22, max_requests=1 << 16)
         self._by_tuple = {}      # id(tokens) -> (device id, tokens)  (strong ref keeps id stable)
         self._key_of_id = {}     # device id -> (arrival, rid) label key
+        self._client_of = {}     # device id -> client id stored in the request table
         self.clients = {}        # client name -> dense id
         self.client_names = []
         self.labels = OrderLabels()
@@ -104,6 +105,7 @@ class DeviceRuntime:
             cid = self.client_id(client) if client is not None else 0
             did = self.ctx.add_request(np.fromiter(tokens, dtype=np.int64, count=len(tokens)), cid, lab)
             self._by_tuple[id(tokens)] = (did, tokens)
+            self._client_of[did] = cid
             if key is not None:
                 self._key_of_id[did] = key
             if relabeled is not None:
@@ -116,15 +118,18 @@ class DeviceRuntime:
                 self._push_labels()
             else:
                 self.ctx.set_labels(np.array([did], np.int32), np.array([lab], np.int64))
-            if client is not None:
-                self._set_client(did, client)
+        if client is not None:
+            self._set_client(did, client)
         return did
 
     def _set_client(self, did, client):
-        # the request table stores the client id at upload; requests first seen
-        # by the dispatcher are uploaded with their client already, so this is
-        # only a consistency guard
-        return None
+        # a token sequence first seen by a routing index (e.g. the reference's
+        # ThresholdRouter walking the device tree) was uploaded without its
+        # client; the worker's enqueue supplies it
+        cid = self.client_id(client)
+        if self._client_of.get(did) != cid:
+            self.ctx.set_clients(np.array([did], np.int32), np.array([cid], np.int32))
+            self._client_of[did] = cid
 
     def _push_labels(self):
         ids = np.fromiter(self._key_of_id.keys(), dtype=np.int32, count=len(self._key_of_id))

@@ -1,0 +1,46 @@
+"""Plugin-level parity beyond DLPM/LPM/D2LPM: with the drop-in installed every
+worker's RadixTree is the device tree, so VTC / FCFS local policies and the
+rr / per_client_rr / threshold routers (ThresholdRouter walks the device
+global index) run on the GPU through the per-call operations.  The reference's
+unchanged runner must reproduce the event-log sha256 and service-gap
+violation counts recorded from the CPU reference
+(tests/golden/make_golden_policies.py), including the config-4 style
+comparison: one bursty trace (cv=4, up to 120 clients) under dlpm / vtc / lpm /
+fcfs."""
+import gzip
+import json
+import os
+
+import pytest
+
+from refpath import import_fairsched
+
+pytestmark = pytest.mark.gpu
+
+RUNS = json.load(gzip.open(os.path.join(os.path.dirname(__file__), "golden", "policies_runs.json.gz")))["runs"]
+
+
+@pytest.fixture(scope="module")
+def fs():
+    mod = import_fairsched()
+    if mod is None:
+        pytest.skip("reference package not available (build() installs it into baseline/_ref)")
+    from paper_2501_14312_b200 import plugin
+    plugin.install()
+    yield mod
+    plugin.uninstall()
+
+
+@pytest.mark.parametrize("idx", range(len(RUNS)), ids=[r["name"] for r in RUNS])
+def test_policy_run_matches_reference(idx, fs):
+    from fairsched.requests import Trace, TraceRecord
+    from fairsched.runner import config_from_dict, run_experiment
+    from paper_2501_14312_b200.radix import DeviceRadixTree
+
+    run = RUNS[idx]
+    cfg = config_from_dict(run["config"])
+    trace = Trace([TraceRecord(**r) for r in run["trace"]])
+    result = run_experiment(cfg, trace)
+    assert all(isinstance(w.tree, DeviceRadixTree) for w in result.workers)
+    assert result.log.sha256() == run["event_sha256"]
+    assert {k: len(v) for k, v in result.violations.items()} == run["violations"]
