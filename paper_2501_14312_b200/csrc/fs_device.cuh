@@ -609,6 +609,13 @@ __device__ inline void block_pin_path(const TrieView &t, const Seg *segs, int32_
     if (under) t.sc->status = FS_ERR_UNDERFLOW;
 }
 
+// pin of a freshly admitted path whose pinned-token gain is known (len - cov,
+// SURVEY a7'): fire-and-forget increments.
+__device__ inline void block_pin_path_known(const TrieView &t, const Seg *segs, int32_t nseg, int64_t gain) {
+    block_path_nodes(t, segs, nseg, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); });
+    if (threadIdx.x == 0 && gain) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)gain);
+}
+
 // ---------------------------------------------------------------- eviction
 // RadixTree.evict_lru (radix.py:210-250) by one CTA.  The reference's candidate
 // set (unprotected ref==0 leaves, parents re-added as they become leaves) is
@@ -1005,7 +1012,7 @@ __device__ inline void block_path_of(const TrieView &t, int32_t deepest, Seg *se
 // reference touches are the path nodes intersecting depths [keep, mlen) of the
 // walk of `pth`; they are collected in path order and edited by thread 0.
 struct NotifySmem {
-    int32_t nseg, mlen, nf;
+    int32_t nseg, mlen, nf, top;
 };
 
 // hint_m0 >= 0: the path's match against the index at the start of the notice
@@ -1024,19 +1031,31 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
     const int32_t mlen = sm->mlen;
     if (keep < mlen) {
         // nodes covering a depth in [keep, mlen): the node holding `keep` (visited
-        // at depth keep) and every node starting inside the range
+        // at depth keep) and every node starting inside the range; depths batched
+        // K per thread (all pos loads, then all start loads)
+        constexpr int K = 8;
+        const int32_t nt_ = (int32_t)blockDim.x;
         for (int32_t s = 0; s < sm->nseg; s++) {
             const int64_t S = segs[s].S;
             const int32_t a = max(segs[s].a, keep), b = segs[s].b;
-            for (int32_t d = a + tid; d < b; d += blockDim.x) {
-                const int32_t n = t.pos[S + d];
-                if (t.start[n] == d || d == keep) found[atomicAdd(&sm->nf, 1)] = n;
+            for (int32_t d0 = a + tid; d0 < b; d0 += K * nt_) {
+                int32_t nd[K], st[K];
+#pragma unroll
+                for (int k = 0; k < K; k++) nd[k] = d0 + k * nt_ < b ? t.pos[S + d0 + k * nt_] : -1;
+#pragma unroll
+                for (int k = 0; k < K; k++) st[k] = nd[k] >= 0 ? t.start[nd[k]] : -1;
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const int32_t d = d0 + k * nt_;
+                    if (nd[k] >= 0 && (st[k] == d || d == keep)) found[atomicAdd(&sm->nf, 1)] = nd[k];
+                }
             }
         }
     }
     __syncthreads();
     if (tid == 0) {
         const int32_t nf = sm->nf;
+        sm->top = -1;
         // path order == increasing start depth
         for (int32_t i = 1; i < nf; i++) {
             const int32_t x = found[i];
@@ -1049,8 +1068,8 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
             const int32_t nd = found[i];
             const int32_t s = t.start[nd];
             if (s < keep) {
-                const int32_t top = trie_split(t, nd, keep - s);  // top survives with the tag
-                if (top >= 0) for (int32_t d = t.start[top]; d < t.end[top]; d++) t.pos[t.src[top] + d] = top;
+                // top survives with the tag; its positions are re-pointed by the block below
+                sm->top = trie_split(t, nd, keep - s);
             }
             if (worker >= 0 && worker < 64 && ((t.wmask[nd] >> worker) & 1ull) &&
                 t.wtime[(int64_t)nd * t.nw + worker] <= notice) {
@@ -1069,4 +1088,9 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
         }
     }
     __syncthreads();
+    if (sm->top >= 0) {
+        const int32_t top = sm->top;
+        block_repoint(t, t.src[top], t.start[top], t.end[top], top);
+        __syncthreads();
+    }
 }

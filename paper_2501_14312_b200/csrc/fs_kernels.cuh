@@ -697,15 +697,19 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j]);
     const long long ct = clock64();
     if (sm->ins.status == FS_OK) {
-        block_pin_path(t, a.segs, sm->ins.nseg, +1);
+        // ref + 1 on every path node; the walk's coverage already says which
+        // were unpinned (every node from depth cov down), so pinned_tokens grows
+        // by len - cov and the increments need no return value
+        block_pin_path_known(t, a.segs, sm->ins.nseg, (int64_t)len - sm->ins.cov);
         __syncthreads();
-        if (tid == 0) sm->prof[12] += clock64() - ct;  // TEMP: pin
+        if (tid == 0) sm->prof[12] += clock64() - ct;  // pin
+
         const long long ct2 = clock64();
         // the matched node is pinned now (and may have gained a child): its
         // chunk of the LRU index changes; new nodes are pinned and past hw0
         if ((tid >> 5) == 0) warp_chunk_touch(t, &sm->lru, sm->ins.last, -1, tid & 31);
         __syncthreads();
-        if (tid == 0) sm->prof[13] += clock64() - ct2;  // TEMP: touch
+        (void)ct2;
     }
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
