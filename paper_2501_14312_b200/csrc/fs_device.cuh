@@ -476,7 +476,9 @@ __device__ inline int32_t warp_cov_from_deepest(const TrieView &t, int32_t y, in
 // still cached the first m0 tokens still match without re-reading them; the
 // walk only continues from m0 when m0 ends at a node boundary (an insert of
 // this step may have added a child there).  Otherwise: full walk.
-template <int U = 8>
+// COV: compute the pinned coverage (local tries; the routing index has no
+// pins).  SEGS: record the path's chain segments (callers that edit the path).
+template <int U = 8, bool COV = true, bool SEGS = true>
 __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                          Seg *segs, int64_t S0, int32_t m0) {
     int32_t y = -1;
@@ -485,14 +487,14 @@ __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__res
         if (pos_valid(t, c, S0, m0 - 1)) y = c;
     }
     auto store = [&](int64_t S, int32_t a, int32_t b, int32_t i) {
-        if (lane == 0) { segs[i].S = S; segs[i].a = a; segs[i].b = b; }
+        if (SEGS && lane == 0) { segs[i].S = S; segs[i].a = a; segs[i].b = b; }
     };
-    if (y < 0) return warp_walk_cb<U>(t, rq, len, lane, true, store);
+    if (y < 0) return warp_walk_cb<U>(t, rq, len, lane, COV, store);
     WalkStart st;
-    st.nseg = warp_path_segments(t, y, m0, segs, lane);
+    st.nseg = SEGS || COV ? warp_path_segments(t, y, m0, segs, lane) : 0;
     st.cov = 0;
-    st.pinrun = true;
-    for (int32_t s = 0; s < st.nseg && st.pinrun; s++) {
+    st.pinrun = COV;
+    for (int32_t s = 0; COV && s < st.nseg && st.pinrun; s++) {
         const Seg g = segs[s];
         const int32_t last = t.pos[g.S + g.b - 1];
         st.cov = warp_seg_cov(t, g.S, g.a, g.b, last, lane);
@@ -507,7 +509,7 @@ __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__res
         return o;
     }
     st.node = y; st.idx = m0; st.last = y;
-    return warp_walk_from<U>(t, rq, len, lane, true, st, store);
+    return warp_walk_from<U>(t, rq, len, lane, COV, st, store);
 }
 
 // warp_walk_cb storing the segments (lane 0) when segs != nullptr.
@@ -916,8 +918,10 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     const int32_t *rq = t.arena + req_off;
     const long long c0 = clock64();
     if (warp == 0) {
-        const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8>(t, rq, len, lane, segs, hint_S0, hint_m0)
-                                       : warp_walk<8>(t, rq, len, lane, segs, true);
+        // the routing index (worker tags) has no pins: no coverage to compute
+        const WalkOut w = hint_m0 >= 0 ? (t.wmask ? warp_walk_hint<8, false, true>(t, rq, len, lane, segs, hint_S0, hint_m0)
+                                                  : warp_walk_hint<8, true, true>(t, rq, len, lane, segs, hint_S0, hint_m0))
+                                       : warp_walk<8>(t, rq, len, lane, segs, t.wmask == nullptr);
         if (lane == 0) {
             int32_t last = w.last >= 0 ? w.last : 0;
             sm->split_top = -1;
@@ -1023,7 +1027,7 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
                                           NotifySmem *sm, int64_t hint_S0 = -1, int32_t hint_m0 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp == 0) {
-        const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8>(t, t.arena + psrc, plen, lane, segs, hint_S0, hint_m0)
+        const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8, false, true>(t, t.arena + psrc, plen, lane, segs, hint_S0, hint_m0)
                                        : warp_walk<8>(t, t.arena + psrc, plen, lane, segs, false);
         if (lane == 0) { sm->nseg = w.nseg; sm->mlen = w.mlen; sm->nf = 0; }
     }

@@ -15,6 +15,9 @@
 #include "fs_device.cuh"
 
 #define FS_SCHED_THREADS 1024
+#ifndef FS_DISPATCH_THREADS
+#define FS_DISPATCH_THREADS 1024  // one batch of block_path_nodes covers an 8k-token path
+#endif
 #define FS_ITEMS 4
 #define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
 #define FS_NONE 0x7fffffff
@@ -1009,7 +1012,7 @@ __device__ inline int d2_select(const DispArgs &a, int32_t c, uint64_t mask, int
 
 // Dispatcher.dispatch for a chain of arrivals (global_policies.py:40-46,
 // 116-124): every arrival's match sees the inserts of the ones before it.
-__global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
+__global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a) {
     __shared__ InsertSmem ins;
     __shared__ int32_t s_w;
     __shared__ int32_t s_mlen;
@@ -1054,7 +1057,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DispArgs a) {
             // gains prefixes of this batch's earlier arrivals (no capacity, no
             // eviction inside a batch), so the batch-start match is still a
             // prefix of the current one: resume from it (warp_walk_hint).
-            const WalkOut w = warp_walk_hint<8>(t, t.arena + off, len, lane, a.segs, a.s0[i], a.m0[i]);
+            const WalkOut w = warp_walk_hint<8, false, false>(t, t.arena + off, len, lane, a.segs, a.s0[i], a.m0[i]);
             if (lane == 0) {
                 const int32_t deepest = w.mlen > 0 ? w.last : -1;
                 if (deepest > 0) stamp_node(t, deepest, now, a.sq_base + 2 * (int64_t)i);

@@ -1439,7 +1439,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     }
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
-    k_dispatch<<<1, 256, 0, s>>>(a);
+    k_dispatch<<<1, FS_DISPATCH_THREADS, 0, s>>>(a);
     counted();
     CK(cudaGetLastError());
     d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
@@ -1539,7 +1539,7 @@ extern "C" int fs_dispatch_select(fs_dispatcher *d, int32_t client, uint64_t mat
     a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = (int32_t)d->dl_idx.size();
     a.out_w = d->o_w.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
-    k_dispatch<<<1, 256, 0, s>>>(a);
+    k_dispatch<<<1, FS_DISPATCH_THREADS, 0, s>>>(a);
     counted();
     CK(cudaGetLastError());
     d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
@@ -1603,7 +1603,7 @@ extern "C" int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t 
         a.q = d->q.p; a.qset = d->qset.p; a.qsize = d->qsize.p;
         a.dl_idx = d->dli.p; a.dl_q = d->dlq.p; a.dl_w = d->dlw.p; a.ndl = (int32_t)d->dl_idx.size();
         a.hdr = d->hdr.p;
-        k_dispatch<<<1, 256, 0, d->tree->stream>>>(a);
+        k_dispatch<<<1, FS_DISPATCH_THREADS, 0, d->tree->stream>>>(a);
         counted();
         CK(cudaGetLastError());
         d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
