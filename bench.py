@@ -177,6 +177,11 @@ class GpuSteps:
         self.w = WorkerDev(self.ctx, self.trie, "dlpm", wl.quantum(), wl.M, wl.reserve, W_E, W_Q,
                            max_clients=max(128, wl.clients))
         self.ids, self.clients = wl.put_initial(self.ctx)
+        # arrivals are uploaded from page-locked host memory (DMA), like a
+        # serving frontend's pinned receive buffers
+        from paper_2501_14312_b200.device import host_register
+        self.pool.flat = np.ascontiguousarray(self.pool.flat, dtype=np.int32)
+        host_register(self.pool.flat)
         self.clients = list(np.asarray(self.clients, np.int32))
         self.w.enqueue(self.ids)
         self.prev_nodes = np.zeros(0, np.int32)
@@ -212,6 +217,8 @@ class GpuSteps:
         return res
 
     def close(self):
+        from paper_2501_14312_b200.device import host_unregister
+        host_unregister(self.pool.flat)
         self.w.close()
         self.trie.close()
         self.ctx.close()

@@ -52,11 +52,17 @@ int fs_device_count(int *count);
  * Trace.materialize requests.py:134-161): tokens are uploaded once per request
  * into a device arena and referenced by request id from then on.            */
 int fs_ctx_create(int device, int64_t arena_tokens, int64_t max_requests, fs_ctx **out);
+/* Page-lock a caller buffer (cudaHostRegister) so fs_requests_add uploads from
+ * it by DMA; unregister before freeing it. */
+int fs_host_register(void *ptr, int64_t bytes);
+int fs_host_unregister(void *ptr);
 int fs_ctx_destroy(fs_ctx *ctx);
 int fs_ctx_sync(fs_ctx *ctx);
 /* Append n requests.  tokens: concatenated ids, offsets[i]/lens[i] index them;
  * clients: dense client ids; labels: order key of (arrival, rid) used as the
- * LPM tie-break (local_policies.py:17).  Writes the new request ids. */
+ * LPM tie-break (local_policies.py:17).  Writes the new request ids.  When the
+ * requests are back to back in `tokens` the block is copied in one transfer and
+ * range-checked on the device (FS_ERR_TOKEN_RANGE leaves nothing appended). */
 int fs_requests_add(fs_ctx *ctx, int64_t n, const int32_t *tokens, const int64_t *offsets,
                     const int32_t *lens, const int32_t *clients, const int64_t *labels,
                     int32_t *out_ids);

@@ -57,6 +57,8 @@ SIGNATURES = {
     "fs_last_error": (C.c_char_p, []),
     "fs_version": (C.c_int, []),
     "fs_device_count": (C.c_int, [PI]),
+    "fs_host_register": (C.c_int, [vp, i64]),
+    "fs_host_unregister": (C.c_int, [vp]),
     "fs_ctx_create": (C.c_int, [C.c_int, i64, i64, PP]),
     "fs_ctx_destroy": (C.c_int, [vp]),
     "fs_ctx_sync": (C.c_int, [vp]),

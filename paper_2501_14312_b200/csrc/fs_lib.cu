@@ -9,6 +9,7 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -104,6 +105,26 @@ static int hgrow(HBuf<T> &b, int64_t n) {
     return FS_OK;
 }
 
+// ---------------------------------------------------------------- uploads
+// Request i: src[soff[i] : soff[i]+len[i]) -> arena[dst[i] ...], zero-padded to
+// a 16-B row; any id outside [0, 2^31) sets *bad.
+__global__ void k_scatter_rows(const int32_t *__restrict__ src, const int64_t *__restrict__ soff,
+                               const int64_t *__restrict__ dst, const int32_t *__restrict__ len,
+                               int32_t *__restrict__ arena, int32_t *bad) {
+    const int64_t i = blockIdx.x;
+    const int32_t n = len[i];
+    const int32_t padded = (n + 3) & ~3;
+    const int32_t *s = src + soff[i];
+    int32_t *d = arena + dst[i];
+    bool neg = false;
+    for (int32_t k = threadIdx.x; k < padded; k += blockDim.x) {
+        const int32_t v = k < n ? s[k] : 0;
+        neg |= v < 0;
+        d[k] = v;
+    }
+    if (__syncthreads_or(neg) && threadIdx.x == 0) *bad = 1;
+}
+
 // ---------------------------------------------------------------- context
 struct fs_ctx {
     int device = 0;
@@ -125,10 +146,23 @@ struct fs_ctx {
     DBuf<int64_t> x_dst, x_nsoff;
     DBuf<int32_t> x_len, x_ns, x_nslen;
     DBuf<uint8_t> x_bytes;
+    DBuf<int32_t> x_tok, x_flag;  // fs_requests_add contiguous fast path
 };
 
 static int ctx_use(fs_ctx *c) {
     CK(cudaSetDevice(c->device));
+    return FS_OK;
+}
+
+extern "C" int fs_host_register(void *ptr, int64_t bytes) {
+    if (!ptr || bytes <= 0) return fail(FS_ERR_INVALID, "bad host range");
+    CK(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault));
+    return FS_OK;
+}
+
+extern "C" int fs_host_unregister(void *ptr) {
+    if (!ptr) return fail(FS_ERR_INVALID, "NULL");
+    CK(cudaHostUnregister(ptr));
     return FS_OK;
 }
 
@@ -164,7 +198,7 @@ extern "C" int fs_ctx_destroy(fs_ctx *c) {
     c->rlabel.release(); c->rstate.release(); c->rhint.release();
     c->stage_tok.release(); c->stage64.release(); c->stage32.release();
     c->x_dst.release(); c->x_nsoff.release(); c->x_len.release(); c->x_ns.release(); c->x_nslen.release();
-    c->x_bytes.release();
+    c->x_bytes.release(); c->x_tok.release(); c->x_flag.release();
     cudaStreamDestroy(c->stream);
     delete c;
     return FS_OK;
@@ -226,6 +260,41 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         if (lens[i] < 0) return fail(FS_ERR_INVALID, "negative length");
         place[i] = c->arena_used + total;
         total += (lens[i] + 3) & ~3LL;
+    }
+    bool contiguous = n > 0;
+    for (int64_t i = 0; i + 1 < n && contiguous; i++) contiguous = offsets[i + 1] == offsets[i] + lens[i];
+    if (contiguous) {
+        // one H2D of the caller's token block (a DMA when the caller registered it,
+        // fs_host_register), then a scatter kernel into the 16-B aligned arena
+        // rows that also checks the id range -- no host pass over the tokens
+        const int64_t src_total = offsets[n - 1] + lens[n - 1] - offsets[0];
+        TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
+        TRY(dgrow(c->x_tok, src_total + 4, c->stream));
+        TRY(dgrow(c->x_dst, n + 1, c->stream)); TRY(dgrow(c->x_nsoff, n + 1, c->stream));
+        TRY(dgrow(c->x_len, n + 1, c->stream)); TRY(dgrow(c->x_flag, 1, c->stream));
+        TRY(hgrow(c->stage64, 2 * n + 2)); TRY(hgrow(c->stage32, n + 2));
+        for (int64_t i = 0; i < n; i++) {
+            c->stage64.p[i] = place[i];
+            c->stage64.p[n + i] = offsets[i] - offsets[0];
+            c->stage32.p[i] = lens[i];
+        }
+        if (src_total) CK(cudaMemcpyAsync(c->x_tok.p, tokens + offsets[0], sizeof(int32_t) * src_total,
+                                          cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_dst.p, c->stage64.p, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_nsoff.p, c->stage64.p + n, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_len.p, c->stage32.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemsetAsync(c->x_flag.p, 0, sizeof(int32_t), c->stream));
+        k_scatter_rows<<<(unsigned)n, 256, 0, c->stream>>>(c->x_tok.p, c->x_nsoff.p, c->x_dst.p, c->x_len.p,
+                                                           c->arena.p, c->x_flag.p);
+        counted();
+        CK(cudaGetLastError());
+        int32_t bad = 0;
+        CK(cudaMemcpyAsync(&bad, c->x_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (bad) return fail(FS_ERR_TOKEN_RANGE, "a token id is outside [0, 2^31)");  // nothing committed
+        TRY(append_request_meta(c, n, place.data(), lens, clients, labels, out_ids));
+        c->arena_used += total;
+        return FS_OK;
     }
     for (int64_t i = 0; i < n; i++) {
         const int32_t *tk = tokens + offsets[i];
@@ -1108,6 +1177,8 @@ static uint32_t key_bits(int32_t max_len) {
 extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom,
                               fs_fill_result *res) {
     if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
+    static const bool hprof = getenv("FS_HOST_PROFILE") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
     fs_ctx *c = w->ctx;
     fs_trie *t = w->tree;
     cudaStream_t s = c->stream;
@@ -1147,6 +1218,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     TRY(dgrow(w->cub_tmp, (int64_t)std::max(sort_bytes, sel_bytes) + 256, s));
 
     const int64_t launches0 = g_launches.load();
+    const auto h1 = std::chrono::steady_clock::now();
     CK(cudaEventRecord(w->ev[0], s));
     // ---- queue upkeep: drop last fill's admissions, merge arrivals by label
     if (w->admitted_last > 0 && w->qn > 0) {
@@ -1276,6 +1348,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     counted();
     CK(cudaGetLastError());
     CK(cudaEventRecord(w->ev[4], s));
+    const auto h2 = std::chrono::steady_clock::now();
     w->dl_client.clear(); w->dl_delta.clear();
     // ---- results
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 24, cudaMemcpyDeviceToHost, s));
@@ -1318,6 +1391,12 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     }
     TRY(copy_records(t, nrec, &res->recs));
     CK(cudaStreamSynchronize(s));
+    if (hprof) {
+        const auto h3 = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        fprintf(stderr, "fill host: prologue %.0f us, launches %.0f us, wait+results %.0f us, device %.0f us\n",
+                us(h0, h1), us(h1, h2), us(h2, h3), 1000.0 * total);
+    }
     return FS_OK;
 }
 

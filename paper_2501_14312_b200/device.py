@@ -30,6 +30,17 @@ def _pu8(a):
     return a.ctypes.data_as(PU8)
 
 
+def host_register(arr: np.ndarray) -> None:
+    """Page-lock a numpy buffer for DMA uploads (fs_host_register); keep the
+    array alive and call host_unregister before it is freed."""
+    L.load()
+    call("fs_host_register", arr.ctypes.data_as(C.c_void_p), arr.nbytes)
+
+
+def host_unregister(arr: np.ndarray) -> None:
+    call("fs_host_unregister", arr.ctypes.data_as(C.c_void_p))
+
+
 class Context:
     """One CUDA device: token arena + request table (fs_ctx)."""
 
