@@ -405,6 +405,8 @@ def main():
     ap.add_argument("--nq", type=int, default=0, help="queued requests per GPU (default: the config's)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cluster", action="store_true", help="D2LPM cluster path even at N=1")
+    ap.add_argument("--k1-full-steps", type=int, default=3,
+                    help="untimed steps after the timed region with the full re-match (scan roofline)")
     ap.add_argument("--arrivals", type=int, default=128,
                     help="cluster path: arrivals per round (a fixed cluster-wide rate, the same at every N; "
                          "0 = as many as the cluster admitted last round)")
@@ -499,6 +501,19 @@ def main():
     t_total = time.perf_counter() - t_start
     launches = launch_count() - l0
     clocks = clocks_stop(*clk, dev) if rank == 0 else None
+    # ablation after the timed region: the same serving steps with every queued
+    # request re-matched from the root (the full streaming scan the incremental
+    # match avoids); identical decisions -- reported as the scan kernel's roofline
+    full_k1, full_tok = [], 0
+    if args.k1_full_steps > 0:
+        g.w.set_k1_full(True)
+        for _ in range(args.k1_full_steps):
+            now += STEP_US
+            r = g.step(now)
+            full_k1.append(r.phases_ms[1])
+            full_tok += r.stats[0]
+            full_n = r.n_queued
+        g.w.set_k1_full(False)
     if dist is not None:
         import torch
         t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=tdev)
@@ -516,14 +531,28 @@ def main():
     peak, peak_kind = peaks()
     n_per_step = decisions / args.steps
     k1_avg = float(np.mean(k1_ms))
-    alg_bytes = (alg_tok / args.steps) * 4 + 36 * n_per_step
+    # incremental K1: request tokens actually needed beyond each request's still-
+    # valid previous match, plus per-request metadata (queue entry, row offset and
+    # length, hint in/out, outputs: 88 B)
+    alg_bytes = (alg_tok / args.steps) * 4 + 88 * n_per_step
     achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
+    full_roof = None
+    if full_k1:
+        fk = float(np.mean(full_k1))
+        fb = (full_tok / len(full_k1)) * 4 + 36 * full_n  # 4*min(mlen+1, L) + 36 per request
+        full_roof = {"kernel": "k_match with FS_OPT_K1_FULL (every request re-matched from the root)",
+                     "bound": "hbm", "achieved": fb / (fk / 1000.0) / 1e9, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": fb / (fk / 1000.0) / 1e9 / peak, "alg_bytes_per_launch": fb,
+                     "avg_launch_ms": fk, "steps": len(full_k1), "traffic": None}
     share = phases / phases.sum()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "r01_k_match_traffic%s.json" % ("" if args.workload == "c2" else "_c5"))
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            traffic = tj.get("dram_bytes_per_launch")
+            if full_roof is not None:
+                full_roof["traffic"] = tj.get("full_scan_dram_bytes_per_launch")
         except Exception:
             traffic = None
     line = {
@@ -535,9 +564,13 @@ def main():
                 "h2d_bytes_per_step": int((g.h2d - h2d0) / args.steps),
                 "d2h_bytes_per_step": int((g.d2h - d2h0) / args.steps)},
         "gpu_launches": int(launches),
-        "roofline": {"kernel": "k_match (K1 batched prefix match)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": "k_match (K1 incremental prefix match)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg},
+                     "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg,
+                     "note": "resumes each request from its still-valid previous match; reads only the tokens "
+                             "past it, so it is latency- not bandwidth-bound; see k1_full_match_roofline for the "
+                             "streaming scan"},
+        "k1_full_match_roofline": full_roof,
         "phase_share": {"merge": share[0], "k1_match": share[1], "k2_sort": share[2], "k3k4_schedule": share[3],
                         "unpin": share[4]},
         "dominant_kernel": {"kernel": "k_schedule (K3/K4 admission chain, one CTA)", "share": share[3],

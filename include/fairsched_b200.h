@@ -208,6 +208,11 @@ int fs_worker_last_phases(fs_worker *w, float *ms4);
  * [14] source chains in admission walks, [15] total, [16..18] eviction-pop
  * argmin / edit / index-update cycles.  Writes 24 entries. */
 int fs_worker_last_stats(fs_worker *w, int64_t *stats24);
+/* Worker options.  FS_OPT_K1_FULL (1): value != 0 makes every fill re-match
+ * every queued request from the root instead of resuming from its previous
+ * match (same decisions; the incremental match is the default). */
+#define FS_OPT_K1_FULL 1
+int fs_worker_set_option(fs_worker *w, int option, int64_t value);
 /* Kernel launches issued by this library since load (all handles). */
 int64_t fs_launch_count(void);
 /* Queue length currently mirrored on device (worker.queue, worker.py:73) */

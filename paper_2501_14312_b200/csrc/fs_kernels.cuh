@@ -21,8 +21,42 @@
 #define FS_ITEMS 4
 #define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
 #define FS_NONE 0x7fffffff
+#define FS_FSLOTS 8192  // admission filter slots (shared memory + global mirror)
+#define FS_MKEY_SLOTS FS_FSLOTS
 
 // ---------------------------------------------------------------- K1
+// Per-request match hints kept across fills (incremental K1).  Between two
+// fills of a worker the trie changes only through that fill's admissions
+// (when no per-call operation touched the tree since -- the host checks a
+// structural version), so a queued request's previous match p[:m] is still
+// the exact match when (i) its deepest node is still cached -- one pos lookup
+// (pos_valid), because a cached depth of a chain implies its whole root path is
+// cached -- and (ii) no admission of that fill had the request's miss key
+// (m, p[m]): an insert can extend p's match only if it shares p[:m+1], which
+// forces its own step-start match to stop at the same depth with the same
+// token (k_schedule's miss-key argument).  Otherwise the walk resumes at m, or
+// starts from the root when the hint is gone.
+struct K1Hints {
+    int32_t *owner;                   // worker the hint belongs to (-1: none)
+    int32_t *m;                       // match length (also the L2 prefetch extent)
+    int64_t *S0;                      // chain (arena row) of the deepest matched node
+    int32_t *tok0;                    // token at m, -1 when fully matched
+    const unsigned long long *mkeys;  // the last fill's admission filter (global mirror)
+    int32_t wid;
+    int32_t use;                      // hints are valid for this fill
+};
+
+__device__ __forceinline__ bool mkey_hit(const unsigned long long *keys, int32_t m, int32_t tok) {
+    const unsigned long long k = ((unsigned long long)((uint32_t)m | 0x80000000u) << 32) | (uint32_t)tok;
+    uint32_t i = fs_hmix(k) & (FS_MKEY_SLOTS - 1);
+    while (true) {
+        const unsigned long long x = keys[i];
+        if (x == k) return true;
+        if (x == FS_HEMPTY) return false;
+        i = (i + 1) & (FS_MKEY_SLOTS - 1);
+    }
+}
+
 template <int U, bool PIPE>
 __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
@@ -31,7 +65,7 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
                                                int64_t *__restrict__ out_s0,
                                                unsigned long long *__restrict__ alg_tokens,
-                                               int32_t *__restrict__ hint) {
+                                               K1Hints hints) {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= n) return;
@@ -40,34 +74,72 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
     const int32_t r = ids ? ids[i] : (int32_t)i;
     const int32_t len = rlen[r];
     const int32_t *rq = t.arena + roff[r];
-    if (hint) {
+    int32_t hy = -1, hm = -1, htok = -1;
+    bool stream = true;
+    if (hints.use && hints.owner[r] == hints.wid) {
+        hm = hints.m[r];
+        htok = hints.tok0[r];
+        if (hm > 0) {
+            const int64_t S0 = hints.S0[r];
+            const int32_t c = t.pos[S0 + hm - 1];
+            if (pos_valid(t, c, S0, hm - 1)) hy = c;
+        }
+        if (hy > 0) stream = htok >= 0 && mkey_hit(hints.mkeys, hm, htok);
+    }
+    if (stream && hints.m) {
         // The request tokens this match will read are known up to the previous
         // step's match length: hand them to the TMA engine as L2 bulk prefetches
         // (4 KB per lane) so the DRAM fetch overlaps the trie hops below.
-        const int32_t want = min(len, hint[r] + 32);
-        const int32_t nb = (want * 4 + 4095) >> 12;
+        const int32_t b_lo = hy > 0 ? hm : 0;
+        const int32_t want = min(len, hints.m[r] + 32);
+        const int32_t nb = (max(0, want - (b_lo & ~1023)) * 4 + 4095) >> 12;
         if (lane < nb) {
-            const int32_t b0 = lane << 10;
+            const int32_t b0 = (b_lo & ~1023) + (lane << 10);
             const uint32_t bytes = (uint32_t)(((min(want, b0 + 1024) - b0) * 4 + 15) & ~15);
             asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(rq + b0), "r"(bytes),
                          "l"(l2_evict_first()) : "memory");
         }
     }
-    const WalkOut w = warp_walk<U, PIPE>(t, rq, len, lane, nullptr, true);
+    WalkOut w;
+    int32_t read_from = 0;
+    if (hy > 0) {
+        // the previous match still holds: coverage from the deep end; the walk
+        // continues only if an admission of the last fill shared the miss key
+        const int32_t cov0 = warp_cov_from_deepest(t, hy, hm, lane);
+        if (!stream || hm < t.end[hy]) {
+            w.mlen = hm; w.last = hy; w.plen = 0; w.nseg = 0; w.cov = cov0; w.unpinned = hm - cov0;
+            read_from = hm + 1;  // nothing to read
+        } else {
+            WalkStart st;
+            st.node = hy; st.idx = hm; st.nseg = 0; st.last = hy; st.cov = cov0; st.pinrun = cov0 == hm;
+            auto none = [](int64_t, int32_t, int32_t, int32_t) {};
+            w = warp_walk_from<8>(t, rq, len, lane, true, st, none);
+            read_from = hm;
+        }
+    } else {
+        w = warp_walk<U, PIPE>(t, rq, len, lane, nullptr, true);
+    }
     if (lane == 0) {
-        if (hint) hint[r] = w.mlen;
         // match_prefix stamps every matched node (radix.py:86-90): lazily, at the deepest
         if (stamp && w.last > 0) stamp_node(t, w.last, now, sq);
         if (out_key) out_key[i] = kmax - (uint32_t)w.mlen;
         if (out_mlen) out_mlen[i] = w.mlen;
         if (out_cov) out_cov[i] = w.cov;
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
-        if (out_s0) out_s0[i] = w.last > 0 ? t.src[w.last] : -1;  // admission-walk hint
-        // request tokens a match must read: min(mlen+1, len); the
-        // counters are spread over 64 slot pairs (summed by the host)
+        const int64_t s0 = w.last > 0 ? t.src[w.last] : -1;
+        if (out_s0) out_s0[i] = s0;  // admission-walk hint
+        if (hints.owner) {
+            hints.owner[r] = hints.wid;
+            hints.S0[r] = s0;
+            if (w.mlen != hm || hy <= 0) hints.tok0[r] = w.mlen < len ? rq[w.mlen] : -1;
+        }
+        if (hints.m) hints.m[r] = w.mlen;
+        // request tokens this match read: [read_from, min(mlen+1, len)) (SURVEY 8d,
+        // minus what the hint already established); the counters are spread over
+        // 64 slot pairs (summed by the host)
         if (alg_tokens) {
             unsigned long long *slot = alg_tokens + 2 * (blockIdx.x & 63);
-            atomicAdd(slot, (unsigned long long)min(w.mlen + 1, len));
+            atomicAdd(slot, (unsigned long long)max(0, min(w.mlen + 1, len) - read_from));
             atomicAdd(slot + 1, (unsigned long long)w.nseg);  // source chains crossed
         }
     }
@@ -188,7 +260,7 @@ __device__ __forceinline__ void st_release_i32(int32_t *p, int32_t v) {
 // (pinned coverage B, token at B) of every admission of this step -> latest
 // admission epoch.  An admission e can raise a queued request's B only if
 // both match (see block_find); open addressing in shared memory.
-#define FS_FSLOTS 8192
+
 struct AdmFilter {
     unsigned long long key[FS_FSLOTS];
     int32_t ep[FS_FSLOTS];
@@ -857,6 +929,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         a.hdr[3] = sm.epoch;
         a.hdr[4] = sm.refill_events;
         a.hdr[5] = sm.resumes;
+        a.hdr[6] = sm.flt.saturated;  // the next fill's K1 trusts the filter only when complete
         sm.prof[5] = sm.ins.ev.pops;
         sm.prof[7] = clock64() - t_start;
         for (int i = 0; i < 3; i++) sm.prof[8 + i] = sm.lru.prof[i];

@@ -135,7 +135,9 @@ struct fs_ctx {
     DBuf<int32_t> rlen, rclient;
     DBuf<int64_t> rlabel;
     DBuf<int8_t> rstate;  // 0 none, 1 queued, 2 admitted
-    DBuf<int32_t> rhint;  // last K1 match length per request (L2 prefetch extent)
+    DBuf<int32_t> rhint;  // last K1 match length per request (L2 prefetch extent, match hint)
+    DBuf<int32_t> h_owner, h_tok0;  // match hints (K1Hints): owning worker, token at the match
+    DBuf<int64_t> h_S0;             //   and the chain of its deepest node
     std::vector<int64_t> h_roff, h_rlabel;
     std::vector<int32_t> h_rlen, h_rclient;
     int32_t max_len = 1;
@@ -196,6 +198,7 @@ extern "C" int fs_ctx_destroy(fs_ctx *c) {
     cudaStreamSynchronize(c->stream);
     c->arena.release(); c->roff.release(); c->rlen.release(); c->rclient.release();
     c->rlabel.release(); c->rstate.release(); c->rhint.release();
+    c->h_owner.release(); c->h_tok0.release(); c->h_S0.release();
     c->stage_tok.release(); c->stage64.release(); c->stage32.release();
     c->x_dst.release(); c->x_nsoff.release(); c->x_len.release(); c->x_ns.release(); c->x_nslen.release();
     c->x_bytes.release(); c->x_tok.release(); c->x_flag.release();
@@ -228,6 +231,13 @@ static int append_request_meta(fs_ctx *c, int64_t n, const int64_t *place, const
         const int64_t old = c->rhint.cap;
         TRY(dgrow(c->rhint, nr, c->stream, true, old));
         CK(cudaMemsetAsync(c->rhint.p + old, 0, sizeof(int32_t) * (c->rhint.cap - old), c->stream));
+    }
+    if (c->h_owner.cap < nr) {
+        const int64_t old = c->h_owner.cap;
+        TRY(dgrow(c->h_owner, nr, c->stream, true, old));
+        TRY(dgrow(c->h_tok0, c->h_owner.cap, c->stream, true, old));
+        TRY(dgrow(c->h_S0, c->h_owner.cap, c->stream, true, old));
+        CK(cudaMemsetAsync(c->h_owner.p + old, 0xff, sizeof(int32_t) * (c->h_owner.cap - old), c->stream));
     }
     for (int64_t i = 0; i < n; i++) {
         c->h_roff.push_back(place[i]);
@@ -443,6 +453,7 @@ struct fs_trie {
     DBuf<int64_t> src, la, seq, lseq;
     DBuf<int32_t> start, end, slen, parent, nchild, ref, first, freest, ctop, cpar;
     int64_t opseq = 0;   // sequence number of the last stamping operation
+    int64_t version = 0; // bumped by every structural edit outside a worker fill (K1 hints)
     DBuf<uint8_t> flags;
     DBuf<uint64_t> wmask;
     DBuf<int64_t> wtime;
@@ -644,7 +655,7 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     const int64_t sq = stamp ? ++t->opseq : 0;
     k_match<4, false><<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
                                                       stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr,
-                                                      nullptr, nullptr);
+                                                      nullptr, K1Hints{});
     counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -687,6 +698,7 @@ static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     a.found = t->found.p;
     a.out = t->opout.p;
     a.sq = ++t->opseq;
+    if (a.op == OP_INSERT || a.op == OP_ADMIT || a.op == OP_EVICT || a.op == OP_NOTIFY) t->version++;
     k_op<<<1, 256, 0, tstream(t)>>>(a);
     counted();
     CK(cudaGetLastError());
@@ -855,13 +867,14 @@ extern "C" int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *p
     TRY(dgrow(t->nt_m0, n, s)); TRY(dgrow(t->nt_s0, n, s));
     k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
         view(t), nullptr, (int32_t)n, t->nt_src.p, t->nt_len.p, 0, 0, 0, 0u, nullptr, t->nt_m0.p, nullptr, nullptr,
-        t->nt_s0.p, nullptr, nullptr);
+        t->nt_s0.p, nullptr, K1Hints{});
     counted();
     k_notify_many<<<1, 256, 0, s>>>(view(t), (int32_t)n, t->nt_src.p, t->nt_len.p, t->nt_worker.p, t->nt_keep.p,
                                     t->nt_when.p, t->nt_m0.p, t->nt_s0.p, t->segs.p, t->found.p, t->opout.p);
     counted();
     CK(cudaGetLastError());
     t->opseq += 1;
+    t->version++;
     CK(cudaMemcpyAsync(t->h_out.p, t->opout.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -912,6 +925,10 @@ extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src,
 struct fs_worker {
     fs_ctx *ctx = nullptr;
     fs_trie *tree = nullptr;
+    int32_t wid = 0;                 // unique id (owner of K1 match hints)
+    int64_t hint_version = -1;       // tree version at the end of the last fill
+    bool hints_ok = false;           // last fill completed with a complete admission filter
+    bool k1_full = false;            // fs_worker_set_option(FS_OPT_K1_FULL): ignore match hints
     int policy = 0;
     int64_t quantum = 1, M = 0, R = 0, w_e = 1, w_q = 2;
     int32_t nclients = 0;
@@ -989,6 +1006,8 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     if (max_clients <= 0) return fail(FS_ERR_INVALID, "max_clients must be positive");
     TRY(ctx_use(c));
     fs_worker *w = new fs_worker();
+    static std::atomic<int32_t> next_wid{0};
+    w->wid = next_wid.fetch_add(1);
     w->ctx = c; w->tree = tree; w->policy = policy; w->quantum = quantum > 0 ? quantum : 1;
     w->M = M; w->R = output_reserve; w->w_e = w_e; w->w_q = w_q; w->nclients = max_clients;
     w->h_q.assign(max_clients, 0); w->h_refills.assign(max_clients, 0); w->h_known.assign(max_clients, 0);
@@ -1156,6 +1175,14 @@ extern "C" int fs_worker_queue_len(fs_worker *w, int64_t *n) {
     return FS_OK;
 }
 
+extern "C" int fs_worker_set_option(fs_worker *w, int option, int64_t value) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL worker");
+    switch (option) {
+        case 1: w->k1_full = value != 0; return FS_OK;  // FS_OPT_K1_FULL
+        default: return fail(FS_ERR_INVALID, "unknown option %d", option);
+    }
+}
+
 extern "C" int fs_worker_last_stats(fs_worker *w, int64_t *stats16) {
     if (!w || !stats16) return fail(FS_ERR_INVALID, "NULL");
     for (int i = 0; i < 24; i++) stats16[i] = w->stats[i];
@@ -1273,10 +1300,14 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         // FS_K1_UNROLL: 4 / 8 / 16 scalar lanes, 101 / 102 / 104 = 128-bit loads, 1 / 2 / 4 per side
         auto k1 = k1u == 101 ? k_match<1, true> : k1u == 102 ? k_match<2, true> : k1u == 104 ? k_match<4, true>
                 : k1u >= 16 ? k_match<16, false> : k1u >= 8 ? k_match<8, false> : k_match<4, false>;
+        static const bool no_hints = getenv("FS_K1_FULL") != nullptr;  // ablation: full re-match every fill
+        K1Hints h{};
+        h.owner = c->h_owner.p; h.m = c->rhint.p; h.S0 = c->h_S0.p; h.tok0 = c->h_tok0.p;
+        h.mkeys = w->gkey.p; h.wid = w->wid;
+        h.use = !no_hints && !w->k1_full && w->hints_ok && w->gkey.p && w->hint_version == t->version;
         k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
                                             ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
-                                            w->s0.p, (unsigned long long *)w->alg.p,
-                                            getenv("FS_K1_NOPREFETCH") ? nullptr : c->rhint.p);
+                                            w->s0.p, (unsigned long long *)w->alg.p, h);
         counted();
         CK(cudaGetLastError());
     }
@@ -1379,6 +1410,8 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     res->pinned = t->h_sc.pinned;
     w->admitted_last = nadm;
     t->opseq += nadm;  // admission e stamped with sq_base + e
+    w->hint_version = t->version;
+    w->hints_ok = status == FS_OK && w->h_hdr.p[6] == 0;
     if (status != FS_OK) return fail((int)status, "device fill failed (status %lld)", (long long)status);
     if (nadm > res->cap_adm) return fail(FS_ERR_INVALID, "admission buffer too small (%lld > %lld)", (long long)nadm, (long long)res->cap_adm);
     if (nadm > 0) {
@@ -1505,13 +1538,14 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     a.segs = d->tree->segs.p;
     a.sq_base = d->tree->opseq + 1;
     d->tree->opseq += 2 * n;
+    d->tree->version++;
     {
         // batch-start matches of every arrival, in parallel (K1, no stamping):
         // the serial chain below resumes each walk from them
         TRY(dgrow(d->m0, n, s)); TRY(dgrow(d->s0, n, s));
         k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
             view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, 0, 0, 0, 0u, nullptr, d->m0.p, nullptr,
-            nullptr, d->s0.p, nullptr, nullptr);
+            nullptr, d->s0.p, nullptr, K1Hints{});
         counted();
         CK(cudaGetLastError());
         a.m0 = d->m0.p; a.s0 = d->s0.p;

@@ -361,6 +361,11 @@ class WorkerDev:
         call("fs_worker_device_counters", self._h, n, _p64(q), _p64(rf))
         return q[:n], rf[:n]
 
+    def set_k1_full(self, full: bool) -> None:
+        """Re-match every queued request from the root each fill (ablation of the
+        incremental match; identical decisions)."""
+        call("fs_worker_set_option", self._h, 1, 1 if full else 0)
+
     def queue_len(self) -> int:
         n = C.c_int64()
         call("fs_worker_queue_len", self._h, C.byref(n))
