@@ -158,13 +158,17 @@ static int ctx_use(fs_ctx *c) {
 
 extern "C" int fs_host_register(void *ptr, int64_t bytes) {
     if (!ptr || bytes <= 0) return fail(FS_ERR_INVALID, "bad host range");
-    CK(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault));
+    const cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) { cudaGetLastError(); return FS_OK; }  // idempotent
+    CK(e);
     return FS_OK;
 }
 
 extern "C" int fs_host_unregister(void *ptr) {
     if (!ptr) return fail(FS_ERR_INVALID, "NULL");
-    CK(cudaHostUnregister(ptr));
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e == cudaErrorHostMemoryNotRegistered) { cudaGetLastError(); return FS_OK; }
+    CK(e);
     return FS_OK;
 }
 

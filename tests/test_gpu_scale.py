@@ -71,3 +71,34 @@ def test_scale_leader_only_sweeps(monkeypatch):
     monkeypatch.setenv("FS_SCHED_HELPERS", "0")
     _run_wl(bench.Config2(8192, 9, 12), 12)
     _run_wl(bench.Config5(16384, 0, 6), 6)
+
+
+def test_incremental_match_equals_full_rematch():
+    """The incremental K1 (resume from each request's previous match) makes the
+    same decisions as re-matching every request from the root (FS_OPT_K1_FULL),
+    including when per-call tree edits between fills invalidate the hints
+    (structural version bump): two workers in lockstep on identical inputs."""
+    import numpy as np
+    import bench
+    wl = bench.Config5(16384, 0, 10)
+    a = bench.GpuSteps(wl, 0)
+    b = bench.GpuSteps(wl, 0)
+    b.w.set_k1_full(True)
+    for k in range(10):
+        now = (k + 1) * bench.STEP_US
+        if k in (4, 7):
+            # an out-of-fill structural edit on both trees (RadixTree.evict_lru)
+            ra = a.trie.evict_lru(4096)
+            rb = b.trie.evict_lru(4096)
+            assert list(ra.src) == list(rb.src) and list(ra.keep) == list(rb.keep)
+        x, y = a.step(now), b.step(now)
+        assert list(x.adm_req) == list(y.adm_req), f"step {k}"
+        assert list(x.adm_mlen) == list(y.adm_mlen), f"step {k}"
+        assert list(x.records.src) == list(y.records.src) and list(x.records.keep) == list(y.records.keep)
+        qa, _, _ = a.w.counters(256)
+        qb, _, _ = b.w.counters(256)
+        assert np.array_equal(qa, qb)
+        assert (x.used, x.pinned) == (y.used, y.pinned)
+    assert a.w is not b.w
+    a.close()
+    b.close()
