@@ -791,7 +791,8 @@ __device__ __forceinline__ void warp_chunk_touch(const TrieView &t, ChunkLRU *L,
 // RadixTree.evict_lru with protect set {protect} (radix.py:210-250), one warp.
 __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t needed, int32_t protect,
                                         EvictSmem *sm, int lane) {
-    if (protect > 0) warp_chunk_touch(t, L, protect, protect, lane);
+    // The protected node (the path's deepest, just stamped) is rarely the LRU
+    // minimum: it is dropped from its chunk's minimum only if it comes up.
     int64_t freed = 0;
     const int32_t ngroups = (L->nch + 31) / 32;
     while (freed < needed) {
@@ -802,6 +803,10 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         warp_key_min(bla, bsq, bn);
         const int32_t b = bn;
         if (b < 0) break;
+        if (b == protect) {
+            warp_chunk_touch(t, L, protect, protect, lane);
+            continue;
+        }
         const int32_t el = elen(t, b);
         const bool whole = el <= needed - freed;
         const int32_t Pb = t.parent[b];
