@@ -803,8 +803,11 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         warp_key_min(bla, bsq, bn);
         const int32_t b = bn;
         if (b < 0) break;
-        if (b == protect) {
-            warp_chunk_touch(t, L, protect, protect, lane);
+        // Chunk minima may also name a node an earlier admission of this fill
+        // pinned (or gave a child): block_admit leaves the index as is, and a
+        // stale minimum is rescanned here when it comes up.
+        if (b == protect || !lru_candidate(t, b)) {
+            warp_chunk_touch(t, L, b, protect, lane);
             continue;
         }
         const int32_t el = elen(t, b);

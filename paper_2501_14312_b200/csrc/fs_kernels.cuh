@@ -780,10 +780,8 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
         if (tid == 0) sm->prof[12] += clock64() - ct;  // pin
 
         const long long ct2 = clock64();
-        // the matched node is pinned now (and may have gained a child): its
-        // chunk of the LRU index changes; new nodes are pinned and past hw0
-        if ((tid >> 5) == 0) warp_chunk_touch(t, &sm->lru, sm->ins.last, -1, tid & 31);
-        __syncthreads();
+        // the matched node is pinned now (and may have gained a child): the LRU
+        // index keeps naming it until a pop finds it stale (warp_chunk_evict)
         (void)ct2;
     }
     if (tid == 0) {
