@@ -65,10 +65,16 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
                                                int64_t *__restrict__ out_s0,
                                                unsigned long long *__restrict__ alg_tokens,
-                                               K1Hints hints) {
+                                               K1Hints hints, const int32_t *__restrict__ jobs = nullptr,
+                                               const int32_t *__restrict__ njobs = nullptr) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (i >= n) return;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // jobs != nullptr: persistent warps take the queue positions k_match_fast
+    // could not settle (jobs[0, *njobs)); otherwise warp i takes position i
+    const int64_t nw = jobs ? ((int64_t)gridDim.x * blockDim.x) >> 5 : 1;
+    const int64_t nj = jobs ? *njobs : (gw < n ? gw + 1 : 0);
+    for (int64_t k = gw; k < nj; k += nw) {
+    const int64_t i = jobs ? jobs[k] : k;
     // ids == nullptr: roff/rlen are the i-th sequence's arena offset and length
     // (eviction-notice paths), not request-table columns
     const int32_t r = ids ? ids[i] : (int32_t)i;
@@ -142,6 +148,82 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
             atomicAdd(slot, (unsigned long long)max(0, min(w.mlen + 1, len) - read_from));
             atomicAdd(slot + 1, (unsigned long long)w.nseg);  // source chains crossed
         }
+    }
+    }
+}
+
+// Pinned coverage of the cached root path [0, d) ending in node y, by one
+// thread: chain by chain from the deep end (refs never increase with depth);
+// inside the chain where pinning stops, up the parent links to the deepest
+// pinned node.  Same value as warp_cov_from_deepest.
+__device__ inline int32_t thread_cov_from_deepest(const TrieView &t, int32_t y, int32_t d) {
+    int32_t cur = y;
+    while (d > 0 && cur > 0) {
+        const int64_t S = t.src[cur];
+        const int32_t c0 = t.ctop[cur];
+        const int32_t X = t.cpar[cur];
+        if (t.ref[t.pos[S + c0]] > 0) {
+            int32_t n = cur;
+            while (t.ref[n] == 0) n = t.parent[n];
+            return min(t.end[n], d);
+        }
+        d = c0;
+        cur = X;
+    }
+    return 0;
+}
+
+// K1 fast path, one thread per queued request: a request whose hint settles
+// its match (K1Hints: deepest node still cached, miss key not admitted) gets
+// every output here; the others are queued for the warp-per-request walk.
+__global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *__restrict__ ids, int32_t n,
+                                                    const int64_t *__restrict__ roff,
+                                                    const int32_t *__restrict__ rlen, int64_t now, int64_t sq,
+                                                    uint32_t kmax, uint32_t *__restrict__ out_key,
+                                                    int32_t *__restrict__ out_mlen, int32_t *__restrict__ out_cov,
+                                                    int32_t *__restrict__ out_next, int64_t *__restrict__ out_s0,
+                                                    K1Hints hints, int32_t *__restrict__ jobs,
+                                                    int32_t *__restrict__ njobs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool slow = true;
+    if (i < n) {
+        const int32_t r = ids[i];
+        if (hints.use && hints.owner[r] == hints.wid) {
+            const int32_t hm = hints.m[r];
+            const int32_t htok = hints.tok0[r];
+            const int64_t S0 = hints.S0[r];
+            int32_t y = -1;
+            bool settled = false;
+            if (hm == 0) {
+                settled = htok < 0 || !mkey_hit(hints.mkeys, 0, htok);
+            } else {
+                const int32_t c = t.pos[S0 + hm - 1];
+                if (pos_valid(t, c, S0, hm - 1)) {
+                    y = c;
+                    settled = htok < 0 || hm < t.end[c] || !mkey_hit(hints.mkeys, hm, htok);
+                }
+            }
+            if (settled) {
+                slow = false;
+                const int32_t len = rlen[r];
+                const int32_t cov = y > 0 ? thread_cov_from_deepest(t, y, hm) : 0;
+                if (y > 0) stamp_node(t, y, now, sq);
+                out_key[i] = kmax - (uint32_t)hm;
+                out_mlen[i] = hm;
+                out_cov[i] = cov;
+                out_next[i] = cov < len ? t.arena[roff[r] + cov] : -1;
+                out_s0[i] = y > 0 ? S0 : -1;
+            }
+        }
+    }
+    // warp-aggregated append of the unsettled positions
+    const unsigned m = __ballot_sync(FS_FULL, i < n && slow);
+    if (m) {
+        const int lane = threadIdx.x & 31;
+        int32_t base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(njobs, __popc(m));
+        base = __shfl_sync(FS_FULL, base, __ffs(m) - 1);
+        if (i < n && slow) jobs[base + __popc(m & ((1u << lane) - 1))] = (int32_t)i;
     }
 }
 

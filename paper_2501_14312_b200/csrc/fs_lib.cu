@@ -955,6 +955,7 @@ struct fs_worker {
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
     DBuf<SweepCtl> ctl;
+    DBuf<int32_t> k1jobs, k1njobs;  // K1 positions the fast path left to the walk
     DBuf<int32_t> rw_list;
     DBuf<unsigned long long> gkey;
     DBuf<int32_t> gep;
@@ -1038,7 +1039,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1293,13 +1294,10 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         if (!k1_blocks) {
             int nsm = 0, per = 0;
             CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_match<8, false>, 256, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_match<1, true>, 256, 0));
             k1_blocks = std::max(1, nsm * per);
         }
-        // one request per warp measured faster than persistent warps (k1_blocks
-        // cap) on config 5: keep the full grid
         const int64_t blocks = (n * 32 + 255) / 256;
-        (void)k1_blocks;
         static const int k1u = [] { const char *e = getenv("FS_K1_UNROLL"); return e ? atoi(e) : 101; }();
         // FS_K1_UNROLL: 4 / 8 / 16 scalar lanes, 101 / 102 / 104 = 128-bit loads, 1 / 2 / 4 per side
         auto k1 = k1u == 101 ? k_match<1, true> : k1u == 102 ? k_match<2, true> : k1u == 104 ? k_match<4, true>
@@ -1309,9 +1307,25 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         h.owner = c->h_owner.p; h.m = c->rhint.p; h.S0 = c->h_S0.p; h.tok0 = c->h_tok0.p;
         h.mkeys = w->gkey.p; h.wid = w->wid;
         h.use = !no_hints && !w->k1_full && w->hints_ok && w->gkey.p && w->hint_version == t->version;
-        k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
-                                            ++t->opseq, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
-                                            w->s0.p, (unsigned long long *)w->alg.p, h);
+        const int64_t sq1 = ++t->opseq;
+        if (h.use && k1u == 101) {
+            // fast path: a thread per request settles the ones whose hint holds;
+            // persistent warps walk the rest (the queue positions it appended)
+            TRY(dgrow(w->k1jobs, n + 1, s));
+            TRY(dgrow(w->k1njobs, 1, s));
+            CK(cudaMemsetAsync(w->k1njobs.p, 0, sizeof(int32_t), s));
+            k_match_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+                view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, sq1, kmax, w->keys.p, w->mlen.p,
+                w->cov.p, w->next.p, w->s0.p, h, w->k1jobs.p, w->k1njobs.p);
+            counted();
+            k1<<<(unsigned)std::min<int64_t>(blocks, k1_blocks), 256, 0, s>>>(
+                view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1, sq1, kmax, w->keys.p, w->mlen.p,
+                w->cov.p, w->next.p, w->s0.p, (unsigned long long *)w->alg.p, h, w->k1jobs.p, w->k1njobs.p);
+        } else {
+            k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
+                                                sq1, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
+                                                w->s0.p, (unsigned long long *)w->alg.p, h, nullptr, nullptr);
+        }
         counted();
         CK(cudaGetLastError());
     }
