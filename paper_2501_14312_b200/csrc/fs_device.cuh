@@ -526,23 +526,19 @@ __device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict
 // warp: every node on it loses one reference; nodes reaching zero release
 // their edge from pinned_tokens.  Warps unpinning different paths commute.
 __device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int lane) {
+    // the path's nodes are exactly the ancestors of its deepest node
+    // (RadixTree._chain walks up the parent links, radix.py:164-172): one
+    // lane follows them -- a handful of hops instead of a scan of every depth
+    if (lane != 0) return;
     long long acc = 0;
     bool under = false;
-    // the path's chains, deepest first, through the per-chain constants
-    int32_t cur = deepest, d = t.end[deepest];
-    while (d > 0 && cur > 0) {
-        const int64_t S = t.src[cur];
-        const int32_t c0 = t.ctop[cur];
-        const int32_t X = t.cpar[cur];
-        for (int32_t p = c0 + lane; p < d; p += 32) {
-            const int32_t n = t.pos[S + p];
-            if (t.start[n] != p) continue;
-            const int32_t old = atomicSub(&t.ref[n], 1);
-            if (old <= 0) under = true;
-            else if (old == 1) acc -= elen(t, n);
-        }
-        d = c0;
-        cur = X;
+    for (int32_t n = deepest; n > 0;) {
+        const int32_t P = t.parent[n];
+        const int32_t el = elen(t, n);
+        const int32_t old = atomicSub(&t.ref[n], 1);
+        if (old <= 0) under = true;
+        else if (old == 1) acc -= el;
+        n = P;
     }
     if (acc) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)acc);
     if (under) t.sc->status = FS_ERR_UNDERFLOW;

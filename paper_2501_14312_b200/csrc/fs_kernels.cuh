@@ -57,7 +57,7 @@ __device__ __forceinline__ bool mkey_hit(const unsigned long long *keys, int32_t
     }
 }
 
-template <int U, bool PIPE>
+template <int U, bool PIPE, bool JOBS = false>
 __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                const int64_t *__restrict__ roff, const int32_t *__restrict__ rlen,
                                                int64_t now, int stamp, int64_t sq, uint32_t kmax,
@@ -71,10 +71,10 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     // jobs != nullptr: persistent warps take the queue positions k_match_fast
     // could not settle (jobs[0, *njobs)); otherwise warp i takes position i
-    const int64_t nw = jobs ? ((int64_t)gridDim.x * blockDim.x) >> 5 : 1;
-    const int64_t nj = jobs ? *njobs : (gw < n ? gw + 1 : 0);
+    const int64_t nw = JOBS ? ((int64_t)gridDim.x * blockDim.x) >> 5 : 1;
+    const int64_t nj = JOBS ? *njobs : (gw < n ? gw + 1 : 0);
     for (int64_t k = gw; k < nj; k += nw) {
-    const int64_t i = jobs ? jobs[k] : k;
+    const int64_t i = JOBS ? jobs[k] : k;
     // ids == nullptr: roff/rlen are the i-th sequence's arena offset and length
     // (eviction-notice paths), not request-table columns
     const int32_t r = ids ? ids[i] : (int32_t)i;

@@ -1318,7 +1318,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
                 view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, sq1, kmax, w->keys.p, w->mlen.p,
                 w->cov.p, w->next.p, w->s0.p, h, w->k1jobs.p, w->k1njobs.p);
             counted();
-            k1<<<(unsigned)std::min<int64_t>(blocks, k1_blocks), 256, 0, s>>>(
+            k_match<1, true, true><<<(unsigned)std::min<int64_t>(blocks, k1_blocks), 256, 0, s>>>(
                 view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1, sq1, kmax, w->keys.p, w->mlen.p,
                 w->cov.p, w->next.p, w->s0.p, (unsigned long long *)w->alg.p, h, w->k1jobs.p, w->k1njobs.p);
         } else {
