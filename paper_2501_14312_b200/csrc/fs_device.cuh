@@ -553,12 +553,14 @@ __device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int l
 // K*blockDim depths whatever the number of segments (fn's stores would
 // otherwise pin every load behind them).
 template <typename F>
-__device__ inline void block_path_nodes(const TrieView &t, const Seg *segs, int32_t nseg, F fn) {
+__device__ inline void block_path_nodes(const TrieView &t, const Seg *segs, int32_t nseg, F fn, int32_t first = 0) {
+    // threads [first, blockDim) take part (the others may be busy elsewhere)
     constexpr int K = 8;
-    const int32_t nt = (int32_t)blockDim.x;
+    const int32_t nt = (int32_t)blockDim.x - first;
+    if ((int32_t)threadIdx.x < first) return;
     int32_t total = 0;
     for (int32_t s = 0; s < nseg; s++) total += segs[s].b - segs[s].a;
-    for (int32_t g0 = (int32_t)threadIdx.x; g0 < total; g0 += K * nt) {
+    for (int32_t g0 = (int32_t)threadIdx.x - first; g0 < total; g0 += K * nt) {
         int32_t nd[K], dd[K];
         int32_t s = 0, base = 0;  // segment of depth index g (g increases with k)
 #pragma unroll
@@ -915,9 +917,13 @@ struct InsertSmem {
 // match before the new leaf == probe()'s), unpinned/cov of that walk, deepest
 // path node, status (FS_ERR_CACHE_FULL after performing the evictions, like
 // the reference).
+// pin_path (scheduler admissions): ref + 1 on every node of the new path.  The
+// pre-existing path nodes are pinned by warps 1.. while warp 0 evicts (they are
+// internal nodes or the protected deepest node, never eviction candidates),
+// the new leaf when it is created.
 __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now, int64_t sq,
                                     int32_t worker, Seg *segs, InsertSmem *sm, int64_t hint_S0 = -1,
-                                    int32_t hint_m0 = -1) {
+                                    int32_t hint_m0 = -1, bool pin_path = false) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t *rq = t.arena + req_off;
     const long long c0 = clock64();
@@ -953,6 +959,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         block_repoint(t, t.src[sm->split_top], t.start[sm->split_top], t.end[sm->split_top], sm->split_top);
     const long long c1 = clock64();
     if (tid == 0 && sm->prof) sm->prof[1] += c1 - c0;
+    if (pin_path) {
+        __syncthreads();  // the split top's positions are visible
+        if (warp > 0)
+            block_path_nodes(t, segs, sm->nseg, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 32);
+        if (!(sm->needed > 0 && sm->lru)) __syncthreads();
+    }
     if (sm->needed > 0) {
         if (sm->lru) {
             if (warp == 0) warp_chunk_evict(t, sm->lru, sm->needed, sm->last, &sm->ev, lane);
@@ -976,6 +988,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             } else {
                 h_put(t, sm->last, rq[sm->mlen], leaf);
                 t.nchild[sm->last]++;
+                if (pin_path) t.ref[leaf] = 1;
                 t.sc->used += sm->new_len;
                 segs[sm->nseg].S = req_off; segs[sm->nseg].a = sm->mlen; segs[sm->nseg].b = len;
                 sm->nseg++;

@@ -851,15 +851,13 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int64_t pinb;
     if (tid == 0) pinb = t.sc->pinned;
     __syncthreads();
-    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j]);
+    // the insert pins the path (pin_path): ref + 1 on every path node; the
+    // walk's coverage already says which were unpinned (every node from depth
+    // cov down), so pinned_tokens grows by len - cov
+    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j], true);
     const long long ct = clock64();
     if (sm->ins.status == FS_OK) {
-        // ref + 1 on every path node; the walk's coverage already says which
-        // were unpinned (every node from depth cov down), so pinned_tokens grows
-        // by len - cov and the increments need no return value
-        block_pin_path_known(t, a.segs, sm->ins.nseg, (int64_t)len - sm->ins.cov);
-        __syncthreads();
-        if (tid == 0) sm->prof[12] += clock64() - ct;  // pin
+        if (tid == 0) t.sc->pinned += (int64_t)len - sm->ins.cov;
 
         const long long ct2 = clock64();
         // the matched node is pinned now (and may have gained a child): the LRU
