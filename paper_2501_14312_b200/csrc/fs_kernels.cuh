@@ -430,6 +430,7 @@ struct SchedSmem {
     int32_t red32[32];
     int32_t wl_n, minA, minB;
     int32_t cursor, progress, epoch, npos, nadm, stop, j, cursor_seq;
+    int32_t pre_j, pre_end;  // next-candidate prescan of the last admission (block_admit)
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
     int64_t prof[16];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops,
@@ -842,6 +843,12 @@ __device__ void block_refill(const FillArgs &a, SchedSmem *sm) {
 // Worker.try_admit (worker.py:112-135) minus host bookkeeping -- probe,
 // insert, pin (radix.py:187-192) -- then the policy's charge
 // (local_policies.py:124).
+// Worker.try_admit (worker.py:112-135) minus host bookkeeping -- probe,
+// insert, pin (radix.py:187-192) -- then the policy's charge
+// (local_policies.py:124).  The scheduler state this admission changes (the
+// charge, pending counts, filter keys, epoch, headroom, pinned tokens) is
+// settled as soon as the walk is done, so warp 1 can already search the next
+// window for the following candidate while warp 0 evicts and warps 2.. pin.
 __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t slack) {
     const int tid = threadIdx.x;
     const TrieView &t = a.t;
@@ -849,60 +856,71 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     const int32_t len = a.s_len[j];
     const int64_t off = a.roff[r];
     __shared__ int64_t pinb;
-    if (tid == 0) pinb = t.sc->pinned;
+    __shared__ int64_t pre_slack;
+    __shared__ int32_t pre_ok;
+    if (tid == 0) { pinb = t.sc->pinned; sm->pre_j = -1; }
     __syncthreads();
-    // the insert pins the path (pin_path): ref + 1 on every path node; the
-    // walk's coverage already says which were unpinned (every node from depth
-    // cov down), so pinned_tokens grows by len - cov
-    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j], true);
-    const long long ct = clock64();
-    if (sm->ins.status == FS_OK) {
-        if (tid == 0) t.sc->pinned += (int64_t)len - sm->ins.cov;
-
-        const long long ct2 = clock64();
-        // the matched node is pinned now (and may have gained a child): the LRU
-        // index keeps naming it until a pop finds it stale (warp_chunk_evict)
-        (void)ct2;
-    }
+    const long long ct0 = clock64();
+    auto on_walk = [&](int) {
+        // thread 0: everything the next search depends on
+        const InsertSmem &in = sm->ins;
+        pre_ok = 0;
+        if (in.status != FS_OK) return;
+        const int32_t mlen = in.mlen;
+        const int32_t cov = in.cov;
+        const int64_t need = len - cov;
+        t.sc->pinned += need;  // pinned_tokens grows by len - cov (the pin itself runs below)
+        if (need > slack || in.unpinned != (int64_t)(mlen - cov)) {
+            a.hdr[2] = FS_ERR_INTERNAL;  // closed-form budget test disagrees with can_add
+            sm->stop = 1;
+            return;
+        }
+        adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, a.s_mlen0[j], a.s_tok0[j], sm->epoch,
+                a.gkey, a.gep);
+        sm->epoch++;
+        a.slot[j].w = -1;
+        a.rstate[r] = 2;
+        const int32_t c = a.slot[j].x;
+        const bool was = a.pend_cnt[c] > 0 && a.q[c] > 0;
+        a.pend_cnt[c]--;
+        if (!a.lpm) a.q[c] -= a.w_e * (int64_t)(len - mlen);
+        const bool now_pos = a.pend_cnt[c] > 0 && a.q[c] > 0;
+        sm->npos += (int)now_pos - (int)was;
+        sm->headroom += a.R;
+        sm->progress = 1;
+        pre_slack = sched_slack(a, sm->headroom);
+        pre_ok = !(!a.lpm && sm->npos == 0);  // the next search needs no refill
+    };
+    auto on_side = [&](int lane) {
+        // warp 1: the next search's first window (no tree reads; stale
+        // coverages are reported, not re-walked)
+        if (!pre_ok) return;
+        const int32_t from = j + 1, wend = min(a.n, from + FS_FAST);
+        const int32_t rr = from < wend ? warp_find_window(a, sm, from, wend, false, pre_slack, lane) : FS_NONE;
+        if (lane == 0) { sm->pre_j = rr; sm->pre_end = wend; }
+    };
+    block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j], true,
+                 on_walk, on_side);
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
         if (in.status != FS_OK) {
             a.hdr[2] = in.status;
             sm->stop = 1;
+            sm->pre_j = -1;
         } else {
-            const int32_t mlen = in.mlen;
-            const int32_t cov = in.cov;
-            const int64_t need = len - cov;
-            if (need > slack || in.unpinned != (int64_t)(mlen - cov) || t.sc->pinned != pinb + need) {
-                a.hdr[2] = FS_ERR_INTERNAL;  // closed-form budget test disagrees with can_add
-                sm->stop = 1;
-            }
             const int32_t e = sm->nadm;
             if (e < a.adm_cap) {
                 a.adm_req[e] = r;
-                a.adm_mlen[e] = mlen;
+                a.adm_mlen[e] = in.mlen;
                 a.adm_unp[e] = in.unpinned;
                 a.adm_pinb[e] = pinb;
                 a.adm_node[e] = in.deepest;
                 a.adm_rec_end[e] = t.sc->nrec;
             }
             sm->nadm = e + 1;
-            adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, a.s_mlen0[j], a.s_tok0[j], sm->epoch,
-                    a.gkey, a.gep);
-            sm->epoch++;
-            a.slot[j].w = -1;
-            a.rstate[r] = 2;
-            const int32_t c = a.slot[j].x;
-            const bool was = a.pend_cnt[c] > 0 && a.q[c] > 0;
-            a.pend_cnt[c]--;
-            if (!a.lpm) a.q[c] -= a.w_e * (int64_t)(len - mlen);
-            const bool now_pos = a.pend_cnt[c] > 0 && a.q[c] > 0;
-            sm->npos += (int)now_pos - (int)was;
-            sm->headroom += a.R;
-            sm->progress = 1;
             if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
         }
-        sm->prof[3] += clock64() - ct;
+        sm->prof[3] += clock64() - ct0;
         sm->prof[6] += sm->ins.nseg;
     }
     __syncthreads();
@@ -933,6 +951,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         a.hdr[2] = FS_OK;
         sm.cursor = 0; sm.progress = 0; sm.epoch = 0; sm.nadm = 0; sm.stop = 0;
         sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0; sm.cursor_seq = 0;
+        sm.pre_j = -1; sm.pre_end = 0;
         for (int i = 0; i < 16; i++) sm.prof[i] = 0;
         for (int i = 0; i < 4; i++) sm.lru.prof[i] = 0;
         sm.ins.prof = sm.prof;
@@ -964,10 +983,18 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         const bool ptrue = !a.lpm && sm.npos == 0;
         const int64_t slack = sched_slack(a, sm.headroom);
         const int32_t cur = sm.cursor;
+        const int32_t pre = sm.pre_j;
         __syncthreads();
         const long long cf = clock64();
-        int32_t j = block_find(a, &sm, cur, a.n, ptrue, slack);
-        if (tid == 0) sm.prof[0] += clock64() - cf;
+        int32_t j;
+        if (pre >= 0 && pre != FS_NONE && !ptrue) {
+            j = pre;  // the last admission's prescan already found it
+        } else {
+            // a clean prescan window needs no second look
+            const int32_t from = (pre == FS_NONE && !ptrue) ? sm.pre_end : cur;
+            j = from < a.n ? block_find(a, &sm, from, a.n, ptrue, slack) : FS_NONE;
+        }
+        if (tid == 0) { sm.prof[0] += clock64() - cf; sm.pre_j = -1; }
         if (j == FS_NONE) {
             if (sm.progress) {
                 __syncthreads();
