@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfsb200.so")
+LIB_PATH = os.environ.get("FS_LIB_PATH") or os.path.join(HERE, "libfsb200.so")  # override: build experiments
 
 FS_OK = 0
 FS_ERR_INVALID = 1

@@ -14,11 +14,15 @@
 #pragma once
 #include "fs_device.cuh"
 
-#define FS_SCHED_THREADS 1024
+#ifndef FS_SCHED_THREADS
+#define FS_SCHED_THREADS 512  // 112 registers without spills (1024 threads capped them at 64)
+#endif
 #ifndef FS_DISPATCH_THREADS
 #define FS_DISPATCH_THREADS 1024  // one batch of block_path_nodes covers an 8k-token path
 #endif
-#define FS_ITEMS 4
+#ifndef FS_ITEMS
+#define FS_ITEMS 8
+#endif
 #define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
 #define FS_NONE 0x7fffffff
 #define FS_FSLOTS 8192  // admission filter slots (shared memory + global mirror)
