@@ -862,7 +862,19 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int64_t pinb;
     __shared__ int64_t pre_slack;
     __shared__ int32_t pre_ok;
-    if (tid == 0) { pinb = t.sc->pinned; sm->pre_j = -1; }
+    // thread 0's charge operands do not depend on the tree edit: load them now
+    // so they arrive while warp 0 walks
+    int32_t c_pre = 0, pend_pre = 0, tok0_pre = -1, m0_pre = 0;
+    int64_t q_pre = 0;
+    if (tid == 0) {
+        pinb = t.sc->pinned;
+        sm->pre_j = -1;
+        c_pre = a.slot[j].x;
+        pend_pre = a.pend_cnt[c_pre];
+        q_pre = a.q[c_pre];
+        m0_pre = a.s_mlen0[j];
+        tok0_pre = a.s_tok0[j];
+    }
     __syncthreads();
     const long long ct0 = clock64();
     auto on_walk = [&](int) {
@@ -879,16 +891,17 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             sm->stop = 1;
             return;
         }
-        adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, a.s_mlen0[j], a.s_tok0[j], sm->epoch,
-                a.gkey, a.gep);
+        adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, m0_pre, tok0_pre, sm->epoch, a.gkey, a.gep);
         sm->epoch++;
         a.slot[j].w = -1;
         a.rstate[r] = 2;
-        const int32_t c = a.slot[j].x;
-        const bool was = a.pend_cnt[c] > 0 && a.q[c] > 0;
-        a.pend_cnt[c]--;
-        if (!a.lpm) a.q[c] -= a.w_e * (int64_t)(len - mlen);
-        const bool now_pos = a.pend_cnt[c] > 0 && a.q[c] > 0;
+        const int32_t c = c_pre;
+        const int32_t pend = pend_pre - 1;
+        const int64_t qn = a.lpm ? q_pre : q_pre - a.w_e * (int64_t)(len - mlen);
+        a.pend_cnt[c] = pend;
+        if (!a.lpm) a.q[c] = qn;
+        const bool was = pend_pre > 0 && q_pre > 0;
+        const bool now_pos = pend > 0 && qn > 0;
         sm->npos += (int)now_pos - (int)was;
         sm->headroom += a.R;
         sm->progress = 1;
