@@ -1005,9 +1005,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                 segs[sm->nseg].S = req_off; segs[sm->nseg].a = sm->mlen; segs[sm->nseg].b = len;
                 sm->nseg++;
                 deepest = leaf;
+                t.la[leaf] = now;  // stamp of the whole path (lazy): a fresh node needs no compare
+                t.lseq[leaf] = sq;
             }
         }
-        if (sm->status == FS_OK && deepest > 0) stamp_node(t, deepest, now, sq);  // the whole path (lazy)
+        if (sm->status == FS_OK && deepest > 0 && !(sm->new_len > 0))
+            stamp_node(t, deepest, now, sq);  // the whole path (lazy); a new leaf was stamped at creation
         sm->deepest = deepest;
         if (sm->status != FS_OK && t.sc->status == FS_OK && sm->status != FS_ERR_CACHE_FULL) t.sc->status = sm->status;
     }
