@@ -526,19 +526,51 @@ __device__ inline WalkOut warp_walk(const TrieView &t, const int32_t *__restrict
 // warp: every node on it loses one reference; nodes reaching zero release
 // their edge from pinned_tokens.  Warps unpinning different paths commute.
 __device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int lane) {
-    // the path's nodes are exactly the ancestors of its deepest node
-    // (RadixTree._chain walks up the parent links, radix.py:164-172): one
-    // lane follows them -- a handful of hops instead of a scan of every depth
-    if (lane != 0) return;
+    // The path's nodes are the ancestors of its deepest node (RadixTree._chain,
+    // radix.py:164-172), grouped in source chains.  Per chain, lane 0 follows up
+    // to 8 parent links (a chain usually holds a few nodes); a chain split into
+    // more nodes (nested prefixes) is finished by the whole warp scanning the
+    // chain's remaining depths for node starts, 8 depths per lane per round.
     long long acc = 0;
     bool under = false;
-    for (int32_t n = deepest; n > 0;) {
-        const int32_t P = t.parent[n];
+    auto unpin1 = [&](int32_t n) {
         const int32_t el = elen(t, n);
         const int32_t old = atomicSub(&t.ref[n], 1);
         if (old <= 0) under = true;
         else if (old == 1) acc -= el;
-        n = P;
+    };
+    int32_t cur = deepest, d = t.end[deepest];
+    while (d > 0 && cur > 0) {
+        const int64_t S = t.src[cur];
+        const int32_t c0 = t.ctop[cur];
+        const int32_t X = t.cpar[cur];
+        int32_t rest = -1;  // chain depths [c0, rest) still to visit
+        if (lane == 0) {
+            int32_t n = cur;
+            for (int k = 0; k < 8; k++) {
+                unpin1(n);
+                const int32_t st = t.start[n];
+                if (st <= c0) { n = -1; break; }
+                n = t.parent[n];
+            }
+            rest = n < 0 ? -1 : t.end[n];  // n (not yet visited) ends where the visited part starts
+        }
+        rest = __shfl_sync(FS_FULL, rest, 0);
+        if (rest > c0) {
+            constexpr int K = 8;
+            for (int32_t p0 = c0 + lane; p0 < rest; p0 += 32 * K) {
+                int32_t nd[K], st[K];
+#pragma unroll
+                for (int k = 0; k < K; k++) nd[k] = p0 + 32 * k < rest ? t.pos[S + p0 + 32 * k] : -1;
+#pragma unroll
+                for (int k = 0; k < K; k++) st[k] = nd[k] >= 0 ? t.start[nd[k]] : -1;
+#pragma unroll
+                for (int k = 0; k < K; k++)
+                    if (nd[k] >= 0 && st[k] == p0 + 32 * k) unpin1(nd[k]);
+            }
+        }
+        d = c0;
+        cur = X;
     }
     if (acc) atomicAdd((unsigned long long *)&t.sc->pinned, (unsigned long long)acc);
     if (under) t.sc->status = FS_ERR_UNDERFLOW;
