@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
                                                int64_t now, int stamp, int64_t sq, uint32_t kmax,
                                                uint32_t *__restrict__ out_key, int32_t *__restrict__ out_mlen,
                                                int32_t *__restrict__ out_cov, int32_t *__restrict__ out_next,
-                                               int64_t *__restrict__ out_s0,
+                                               int64_t *__restrict__ out_s0, int32_t *__restrict__ out_tok0,
                                                unsigned long long *__restrict__ alg_tokens,
                                                K1Hints hints, const int32_t *__restrict__ jobs = nullptr,
                                                const int32_t *__restrict__ njobs = nullptr) {
@@ -138,10 +138,12 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
         if (out_next) out_next[i] = w.cov < len ? rq[w.cov] : -1;
         const int64_t s0 = w.last > 0 ? t.src[w.last] : -1;
         if (out_s0) out_s0[i] = s0;  // admission-walk hint
+        const int32_t tok0 = (w.mlen == hm && hy > 0) ? htok : (w.mlen < len ? rq[w.mlen] : -1);
+        if (out_tok0) out_tok0[i] = tok0;  // first token the step-start trie misses
         if (hints.owner) {
             hints.owner[r] = hints.wid;
             hints.S0[r] = s0;
-            if (w.mlen != hm || hy <= 0) hints.tok0[r] = w.mlen < len ? rq[w.mlen] : -1;
+            hints.tok0[r] = tok0;
         }
         if (hints.m) hints.m[r] = w.mlen;
         // request tokens this match read: [read_from, min(mlen+1, len)) (SURVEY 8d,
@@ -186,7 +188,8 @@ __global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *_
                                                     uint32_t kmax, uint32_t *__restrict__ out_key,
                                                     int32_t *__restrict__ out_mlen, int32_t *__restrict__ out_cov,
                                                     int32_t *__restrict__ out_next, int64_t *__restrict__ out_s0,
-                                                    K1Hints hints, int32_t *__restrict__ jobs,
+                                                    int32_t *__restrict__ out_tok0, K1Hints hints,
+                                                    int32_t *__restrict__ jobs,
                                                     int32_t *__restrict__ njobs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool slow = true;
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *_
                 out_cov[i] = cov;
                 out_next[i] = cov < len ? t.arena[roff[r] + cov] : -1;
                 out_s0[i] = y > 0 ? S0 : -1;
+                out_tok0[i] = htok;
             }
         }
     }
@@ -271,8 +275,7 @@ __global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__rest
                          const int32_t *__restrict__ rclient, const int32_t *__restrict__ rlen,
                          int32_t *__restrict__ s_req, int4 *__restrict__ slot, int32_t *__restrict__ s_len,
                          int32_t *__restrict__ s_mlen0, int64_t *__restrict__ s_src0,
-                         const int32_t *__restrict__ arena, const int64_t *__restrict__ roff,
-                         int32_t *__restrict__ s_tok0) {
+                         const int32_t *__restrict__ tok0, int32_t *__restrict__ s_tok0) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int32_t qi = perm[p];
@@ -283,7 +286,7 @@ __global__ void k_gather(const int32_t *__restrict__ perm, const int32_t *__rest
     s_len[p] = len;
     slot[p] = make_int4(rclient[r], cov[qi], next[qi], 0);
     s_mlen0[p] = m0;
-    s_tok0[p] = m0 < len ? arena[roff[r] + m0] : -1;  // first token the step-start trie misses
+    s_tok0[p] = tok0[qi];  // first token the step-start trie misses (K1)
     s_src0[p] = s0[qi];
 }
 

@@ -659,7 +659,7 @@ extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int6
     const int64_t sq = stamp ? ++t->opseq : 0;
     k_match<4, false><<<(unsigned)blocks, 256, 0, c->stream>>>(view(t), sm.ids.p, (int32_t)n, c->roff.p, c->rlen.p, now,
                                                       stamp, sq, 0u, nullptr, sm.mlen.p, sm.cov.p, nullptr, nullptr,
-                                                      nullptr, K1Hints{});
+                                                      nullptr, nullptr, K1Hints{});
     counted();
     CK(cudaGetLastError());
     if (out_mlen) CK(cudaMemcpyAsync(out_mlen, sm.mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -871,7 +871,7 @@ extern "C" int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *p
     TRY(dgrow(t->nt_m0, n, s)); TRY(dgrow(t->nt_s0, n, s));
     k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
         view(t), nullptr, (int32_t)n, t->nt_src.p, t->nt_len.p, 0, 0, 0, 0u, nullptr, t->nt_m0.p, nullptr, nullptr,
-        t->nt_s0.p, nullptr, K1Hints{});
+        t->nt_s0.p, nullptr, nullptr, K1Hints{});
     counted();
     k_notify_many<<<1, 256, 0, s>>>(view(t), (int32_t)n, t->nt_src.p, t->nt_len.p, t->nt_worker.p, t->nt_keep.p,
                                     t->nt_when.p, t->nt_m0.p, t->nt_s0.p, t->segs.p, t->found.p, t->opout.p);
@@ -956,6 +956,7 @@ struct fs_worker {
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
     DBuf<SweepCtl> ctl;
     DBuf<int32_t> k1jobs, k1njobs;  // K1 positions the fast path left to the walk
+    DBuf<int32_t> tok0q;            // K1: token at each queue position's match (miss key)
     DBuf<int32_t> rw_list;
     DBuf<unsigned long long> gkey;
     DBuf<int32_t> gep;
@@ -1039,7 +1040,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1224,7 +1225,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     TRY(dgrow(w->keys, n + 1, s)); TRY(dgrow(w->keys2, n + 1, s)); TRY(dgrow(w->perm, n + 1, s));
     TRY(dgrow(w->mlen, n + 1, s)); TRY(dgrow(w->cov, n + 1, s)); TRY(dgrow(w->fnode, n + 1, s));
     TRY(dgrow(w->next, n + 1, s)); TRY(dgrow(w->s_req, n + 1, s)); TRY(dgrow(w->s_len, n + 1, s));
-    TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->s_tok0, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
+    TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->s_tok0, n + 1, s)); TRY(dgrow(w->tok0q, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
     TRY(dgrow(w->s_mlen0, n + 1, s)); TRY(dgrow(w->s0, n + 1, s)); TRY(dgrow(w->s_src0, n + 1, s));
     if (w->iota.cap < n + 1) {
         TRY(dgrow(w->iota, n + 1, s));
@@ -1316,15 +1317,17 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
             CK(cudaMemsetAsync(w->k1njobs.p, 0, sizeof(int32_t), s));
             k_match_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                 view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, sq1, kmax, w->keys.p, w->mlen.p,
-                w->cov.p, w->next.p, w->s0.p, h, w->k1jobs.p, w->k1njobs.p);
+                w->cov.p, w->next.p, w->s0.p, w->tok0q.p, h, w->k1jobs.p, w->k1njobs.p);
             counted();
             k_match<1, true, true><<<(unsigned)std::min<int64_t>(blocks, k1_blocks), 256, 0, s>>>(
                 view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1, sq1, kmax, w->keys.p, w->mlen.p,
-                w->cov.p, w->next.p, w->s0.p, (unsigned long long *)w->alg.p, h, w->k1jobs.p, w->k1njobs.p);
+                w->cov.p, w->next.p, w->s0.p, w->tok0q.p, (unsigned long long *)w->alg.p, h, w->k1jobs.p,
+                w->k1njobs.p);
         } else {
             k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
                                                 sq1, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
-                                                w->s0.p, (unsigned long long *)w->alg.p, h, nullptr, nullptr);
+                                                w->s0.p, w->tok0q.p, (unsigned long long *)w->alg.p, h, nullptr,
+                                                nullptr);
         }
         counted();
         CK(cudaGetLastError());
@@ -1338,7 +1341,7 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
         k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p,
                                                             w->next.p, w->mlen.p, w->s0.p, c->rclient.p, c->rlen.p,
                                                             w->s_req.p, w->slot.p, w->s_len.p, w->s_mlen0.p,
-                                                            w->s_src0.p, c->arena.p, c->roff.p, w->s_tok0.p);
+                                                            w->s_src0.p, w->tok0q.p, w->s_tok0.p);
         counted();
         CK(cudaGetLastError());
     }
@@ -1563,7 +1566,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
         TRY(dgrow(d->m0, n, s)); TRY(dgrow(d->s0, n, s));
         k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
             view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, 0, 0, 0, 0u, nullptr, d->m0.p, nullptr,
-            nullptr, d->s0.p, nullptr, K1Hints{});
+            nullptr, d->s0.p, nullptr, nullptr, K1Hints{});
         counted();
         CK(cudaGetLastError());
         a.m0 = d->m0.p; a.s0 = d->s0.p;
