@@ -389,6 +389,9 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
                                 "fill_host_wall": 1000 * float(mx[7]) / args.steps},
         "local_decisions_per_step": float(sm[2]) / args.steps, "dispatches_per_step": be.n_dispatched / args.steps,
         "seed_dispatch": {"arrivals": n_seed, "seconds": seed_s},
+        "notice_cycles_per_notice": (dict(zip(["walk", "collect", "edit", "repoint"],
+                                              (getattr(be, "notice_prof", np.zeros(4)) /
+                                               max(getattr(be, "n_notices", 0), 1)).tolist()))),
         "clocks": clocks, "host_wall_s": wall_max,
     }
     print(json.dumps(line))

@@ -144,6 +144,8 @@ int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_len, int32_t
  * a D2lpm round, global_policies.py:130-132 -> radix.py:254-302). */
 int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *path_src, const int32_t *path_len,
                               const int32_t *worker, const int32_t *keep_len, const int64_t *notice_time);
+/* SM cycles of the last fs_trie_evict_notify_many: walk, collect, edit, repoint */
+int fs_trie_last_notify_profile(fs_trie *t, int64_t *prof4);
 /* Node table export for RadixTree.dump / check (radix.py:306-340).  Writes up to
  * cap nodes (index 0 = root) and sets *n to the node-table size; dead slots have
  * parent == -2. wmask may be NULL. */

@@ -84,6 +84,7 @@ SIGNATURES = {
     "fs_trie_longest_match_workers": (C.c_int, [vp, i32, i64, P32, PU64]),
     "fs_trie_evict_notify": (C.c_int, [vp, i64, i32, i32, i32, i64]),
     "fs_trie_evict_notify_many": (C.c_int, [vp, i64, P64, P32, P32, P32, P64]),
+    "fs_trie_last_notify_profile": (C.c_int, [vp, P64]),
     "fs_trie_export": (C.c_int, [vp, i64, P64, P64, P32, P32, P32, P32, P64, PU64]),
     "fs_worker_create": (C.c_int, [vp, vp, C.c_int, i64, i64, i64, i64, i64, i32, PP]),
     "fs_worker_destroy": (C.c_int, [vp]),

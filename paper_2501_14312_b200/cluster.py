@@ -341,6 +341,12 @@ class GpuStreamRank:
             self.d.finish_many(fin[:, 0], fin[:, 1], fin[:, 2])
         if len(notices):
             self.d.trie.evict_notify_many(notices[:, 0], notices[:, 1], notices[:, 3], notices[:, 2], notices[:, 4])
+            import ctypes as C
+            from ._lib import call
+            pr = np.zeros(4, np.int64)
+            call("fs_trie_last_notify_profile", self.d.trie._h, pr.ctypes.data_as(C.POINTER(C.c_int64)))
+            self.notice_prof = getattr(self, "notice_prof", np.zeros(4, np.int64)) + pr
+            self.n_notices = getattr(self, "n_notices", 0) + len(notices)
 
     def fill(self, now):
         r = self.w.fill(now, 0, 0)

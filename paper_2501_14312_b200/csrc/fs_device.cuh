@@ -1081,6 +1081,7 @@ __device__ inline void block_path_of(const TrieView &t, int32_t deepest, Seg *se
 // walk of `pth`; they are collected in path order and edited by thread 0.
 struct NotifySmem {
     int32_t nseg, mlen, nf, top;
+    long long prof[4];  // cycles: walk, collect, edit (thread 0), repoint
 };
 
 // hint_m0 >= 0: the path's match against the index at the start of the notice
@@ -1090,12 +1091,14 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
                                           int32_t keep, int64_t notice, Seg *segs, int32_t *found,
                                           NotifySmem *sm, int64_t hint_S0 = -1, int32_t hint_m0 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long q0 = clock64();
     if (warp == 0) {
         const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8, false, true>(t, t.arena + psrc, plen, lane, segs, hint_S0, hint_m0)
                                        : warp_walk<8>(t, t.arena + psrc, plen, lane, segs, false);
         if (lane == 0) { sm->nseg = w.nseg; sm->mlen = w.mlen; sm->nf = 0; }
     }
     __syncthreads();
+    const long long q1 = clock64();
     const int32_t mlen = sm->mlen;
     if (keep < mlen) {
         // nodes covering a depth in [keep, mlen): the node holding `keep` (visited
@@ -1121,6 +1124,7 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
         }
     }
     __syncthreads();
+    const long long q2 = clock64();
     if (tid == 0) {
         const int32_t nf = sm->nf;
         sm->top = -1;
@@ -1156,9 +1160,13 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
         }
     }
     __syncthreads();
+    const long long q3 = clock64();
     if (sm->top >= 0) {
         const int32_t top = sm->top;
         block_repoint(t, t.src[top], t.start[top], t.end[top], top);
         __syncthreads();
+    }
+    if (tid == 0) {
+        sm->prof[0] += q1 - q0; sm->prof[1] += q2 - q1; sm->prof[2] += q3 - q2; sm->prof[3] += clock64() - q3;
     }
 }

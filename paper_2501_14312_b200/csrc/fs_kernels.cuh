@@ -1089,7 +1089,10 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     __shared__ int32_t s_nseg;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;
-    if (tid == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.lru = nullptr; ins.ev.pops = 0; }
+    if (tid == 0) {
+        t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.lru = nullptr; ins.ev.pops = 0;
+        for (int k = 0; k < 4; k++) nsm.prof[k] = 0;
+    }
     __syncthreads();
     const int32_t *rq = t.arena + a.req_off;
     switch (a.op) {
@@ -1146,14 +1149,20 @@ __global__ void __launch_bounds__(256) k_notify_many(TrieView t, int32_t n, cons
                                                      const int32_t *__restrict__ m0, const int64_t *__restrict__ s0,
                                                      Seg *segs, int32_t *found, int64_t *out) {
     __shared__ NotifySmem nsm;
-    if (threadIdx.x == 0) { t.sc->nrec = 0; t.sc->status = FS_OK; }
+    if (threadIdx.x == 0) {
+        t.sc->nrec = 0; t.sc->status = FS_OK;
+        for (int k = 0; k < 4; k++) nsm.prof[k] = 0;
+    }
     __syncthreads();
     for (int32_t i = 0; i < n; i++) {
         block_evict_notify(t, src[i], len[i], worker[i], keep[i], when[i], segs, found, &nsm, s0[i], m0[i]);
         __syncthreads();
         if (t.sc->status != FS_OK) break;
     }
-    if (threadIdx.x == 0) out[0] = t.sc->status;
+    if (threadIdx.x == 0) {
+        out[0] = t.sc->status;
+        for (int k = 0; k < 4; k++) out[1 + k] = nsm.prof[k];  // walk, collect, edit, repoint cycles
+    }
 }
 
 // ---------------------------------------------------------------- D2LPM

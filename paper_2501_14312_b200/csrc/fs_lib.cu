@@ -886,6 +886,14 @@ extern "C" int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *p
     return FS_OK;
 }
 
+extern "C" int fs_trie_last_notify_profile(fs_trie *t, int64_t *prof4) {
+    if (!t || !prof4) return fail(FS_ERR_INVALID, "NULL argument");
+    TRY(ctx_use(t->ctx));
+    CK(cudaMemcpyAsync(prof4, t->opout.p + 1, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, tstream(t)));
+    CK(cudaStreamSynchronize(tstream(t)));
+    return FS_OK;
+}
+
 extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src, int32_t *start, int32_t *end,
                               int32_t *parent, int32_t *ref, int64_t *last_access, uint64_t *wmask) {
     if (!t || !n) return fail(FS_ERR_INVALID, "NULL argument");
