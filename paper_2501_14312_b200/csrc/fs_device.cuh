@@ -833,16 +833,18 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         warp_key_min(bla, bsq, bn);
         const int32_t b = bn;
         if (b < 0) break;
+        // one round for everything the pop needs to know about b
+        const uint8_t flb = t.flags[b];
+        const int32_t ncb = t.nchild[b], refb = t.ref[b], stb = t.start[b], enb = t.end[b], Pb = t.parent[b];
         // Chunk minima may also name a node an earlier admission of this fill
         // pinned (or gave a child): block_admit leaves the index as is, and a
         // stale minimum is rescanned here when it comes up.
-        if (b == protect || !lru_candidate(t, b)) {
+        if (b == protect || !((flb & FS_ALIVE) && ncb == 0 && refb == 0)) {
             warp_chunk_touch(t, L, b, protect, lane);
             continue;
         }
-        const int32_t el = elen(t, b);
+        const int32_t el = enb - stb;
         const bool whole = el <= needed - freed;
-        const int32_t Pb = t.parent[b];
         __syncwarp();
         const long long p1 = clock64();
         // b is its chunk's minimum; a detach removes it, a truncation keeps
@@ -866,7 +868,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
         int64_t pla = 0, pseq = 0;
         if (lane == 0) {
             sm->pops++;
-            const int32_t plen = t.end[b];
+            const int32_t plen = enb;
             const int64_t remaining = needed - freed;
             if (whole) {
                 // push_record + trie_detach (radix.py:206-208, 226-230) with every
