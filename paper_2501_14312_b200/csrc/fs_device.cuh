@@ -1081,9 +1081,14 @@ __device__ inline void block_path_of(const TrieView &t, int32_t deepest, Seg *se
 // RadixTree.evict_notify + _prune_up (radix.py:254-302).  The nodes the
 // reference touches are the path nodes intersecting depths [keep, mlen) of the
 // walk of `pth`; they are collected in path order and edited by thread 0.
+#define FS_NF_CAP 64
 struct NotifySmem {
     int32_t nseg, mlen, nf, top;
     long long prof[4];  // cycles: walk, collect, edit (thread 0), repoint
+    // the collected nodes with what the edit needs (first FS_NF_CAP of them)
+    int32_t fnode[FS_NF_CAP], fstart[FS_NF_CAP];
+    uint64_t fmask[FS_NF_CAP];
+    uint8_t fhit[FS_NF_CAP];
 };
 
 // hint_m0 >= 0: the path's match against the index at the start of the notice
@@ -1120,14 +1125,61 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int32_t d = d0 + k * nt_;
-                    if (nd[k] >= 0 && (st[k] == d || d == keep)) found[atomicAdd(&sm->nf, 1)] = nd[k];
+                    if (nd[k] >= 0 && (st[k] == d || d == keep)) {
+                        // the tag test in parallel (loads issued before the
+                        // append): the edit below only stores
+                        const uint64_t wm = t.wmask[nd[k]];
+                        const int64_t wt = worker >= 0 && worker < t.nw ? t.wtime[(int64_t)nd[k] * t.nw + worker] : 0;
+                        const int32_t slot = atomicAdd(&sm->nf, 1);
+                        found[slot] = nd[k];
+                        if (slot < FS_NF_CAP) {
+                            sm->fnode[slot] = nd[k];
+                            sm->fstart[slot] = st[k];
+                            sm->fmask[slot] = wm;
+                            sm->fhit[slot] = worker >= 0 && worker < 64 && ((wm >> worker) & 1ull) && wt <= notice;
+                        }
+                    }
                 }
             }
         }
     }
     __syncthreads();
     const long long q2 = clock64();
-    if (tid == 0) {
+    if (tid == 0 && sm->nf <= FS_NF_CAP) {
+        // the usual case: everything the edit reads was collected above
+        const int32_t nf = sm->nf;
+        sm->top = -1;
+        for (int32_t i = 1; i < nf; i++) {  // path order == increasing start depth
+            const int32_t xn = sm->fnode[i], xs = sm->fstart[i];
+            const uint64_t xm = sm->fmask[i];
+            const uint8_t xh = sm->fhit[i];
+            int32_t j = i - 1;
+            while (j >= 0 && sm->fstart[j] > xs) {
+                sm->fnode[j + 1] = sm->fnode[j]; sm->fstart[j + 1] = sm->fstart[j];
+                sm->fmask[j + 1] = sm->fmask[j]; sm->fhit[j + 1] = sm->fhit[j];
+                j--;
+            }
+            sm->fnode[j + 1] = xn; sm->fstart[j + 1] = xs; sm->fmask[j + 1] = xm; sm->fhit[j + 1] = xh;
+        }
+        int32_t nt = 0;
+        for (int32_t i = 0; i < nf; i++) {
+            const int32_t nd = sm->fnode[i];
+            if (sm->fstart[i] < keep) sm->top = trie_split(t, nd, keep - sm->fstart[i]);
+            if (sm->fhit[i]) {
+                t.wmask[nd] = sm->fmask[i] & ~(1ull << worker);
+                found[nt++] = nd;
+            }
+        }
+        for (int32_t i = 0; i < nt; i++) {
+            int32_t n = found[i];
+            while (n > 0 && t.nchild[n] == 0 && t.wmask[n] == 0 && t.ref[n] == 0) {
+                const int32_t P = t.parent[n];
+                if (P < 0) break;
+                if (h_find(t, P, t.first[n]) == n) trie_detach(t, n); else break;
+                n = P;
+            }
+        }
+    } else if (tid == 0) {
         const int32_t nf = sm->nf;
         sm->top = -1;
         // path order == increasing start depth
