@@ -176,13 +176,14 @@ class GpuSteps:
         self.trie = Trie(self.ctx, wl.CAP)
         self.w = WorkerDev(self.ctx, self.trie, "dlpm", wl.quantum(), wl.M, wl.reserve, W_E, W_Q,
                            max_clients=max(128, wl.clients))
-        self.ids, self.clients = wl.put_initial(self.ctx)
+        self.ids, clients0 = wl.put_initial(self.ctx)
+        # client of every device request id: the initial queue, then the pool in upload order
+        self.clients = np.concatenate([np.asarray(clients0, np.int32), np.asarray(self.pool.clients, np.int32)])
         # arrivals are uploaded from page-locked host memory (DMA), like a
         # serving frontend's pinned receive buffers
         from paper_2501_14312_b200.device import host_register
         self.pool.flat = np.ascontiguousarray(self.pool.flat, dtype=np.int32)
         host_register(self.pool.flat)
-        self.clients = list(np.asarray(self.clients, np.int32))
         self.w.enqueue(self.ids)
         self.prev_nodes = np.zeros(0, np.int32)
         self.prev_clients = np.zeros(0, np.int32)
@@ -206,13 +207,12 @@ class GpuSteps:
             o1 = int(p.offsets[b - 1] + p.lens[b - 1])
             ids = self.ctx.add_requests(p.flat[o0:o1], p.offsets[a:b] - o0, p.lens[a:b], p.clients[a:b],
                                         p.labels[a:b])
-            self.clients.extend(int(c) for c in p.clients[a:b])
             self.w.enqueue(ids)
             self.pool_next = b
             self.h2d += (o1 - o0) * 4 + (b - a) * 24
         res = self.w.fill(now, 0, 0)
         self.prev_nodes = res.adm_node.astype(np.int32)
-        self.prev_clients = np.asarray([self.clients[int(i)] for i in res.adm_req], np.int32)
+        self.prev_clients = self.clients[np.asarray(res.adm_req, np.int64)]
         self.d2h += res.adm_req.nbytes * 6 + 8 * 128 * 2 + 64
         return res
 
