@@ -1,6 +1,7 @@
-"""Benchmark: DLPM scheduling decisions/s on the config-2 queue (BASELINE.json
-configs[1]: one worker, 100 clients, 64k queued 1-4k-token prompts with a
-Zipf(1.1) shared-prefix tree), plus the prefix-match kernel's HBM GB/s.
+"""Benchmark: DLPM / D2LPM scheduling decisions/s (BASELINE.json metric, "at
+1M-request queue") on config 5 by default -- 1M queued 8k-token requests over a
+deep shared-prefix tree (`--workload c2` for configs[1], the 64k queue) -- plus
+the prefix-match kernel's roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -8,18 +9,22 @@ A step is one pass of the decision path over the resident queue, driven the
 way the reference's serving loop drives it:
   1. the previous step's batch completes: output charge w_q*8 per request
      (Dlpm.on_outputs) and unpin of its paths (worker.py:209-213);
-  2. as many new requests arrive as were admitted (uploaded from host memory
-     through the C ABI, Worker.enqueue -> on_request_enqueued);
+  2. as many new requests arrive as were admitted (uploaded from page-locked
+     host memory through the C ABI, Worker.enqueue -> on_request_enqueued);
   3. one schedule step over the whole queue (Dlpm.fill): K1 match + LRU stamp
      of every queued request, K2 sort, K3/K4 deficit-gated admission with
      radix insert / split / LRU evict / pin.
 Decisions per step = queued requests evaluated.  `value` is device time
 (CUDA events inside the library, inputs resident); `e2e` is host wall time of
 the same public-API calls including the H2D upload of arrivals and the D2H of
-the admission results.  N>1 (torchrun): one independent worker per GPU with
-its own 64k queue (weak scaling; the local DLPM fill has no cross-worker
-exchange).  The CPU baseline is the C oracle (a literal restatement of the
-reference's Dlpm.fill) on the same steps, on one core.
+the admission results.
+N>1 (torchrun): one DLPM worker per GPU with its own 1M queue (weak scaling;
+the local fill has no cross-worker exchange), then -- reported under
+`d2lpm_cluster` -- D2LPM across the same GPUs: one shared 1M queue dispatched
+by a replicated dispatcher, one NCCL all-gather per round (strong scaling).
+`--cluster` runs only the latter (also at N=1).
+The CPU baseline is the C oracle (a literal restatement of the reference's
+Dlpm.fill) on the same steps of a 65,536-request sample, on one core.
 """
 from __future__ import annotations
 
@@ -394,7 +399,8 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
                                                max(getattr(be, "n_notices", 0), 1)).tolist()))),
         "clocks": clocks, "host_wall_s": wall_max,
     }
-    print(json.dumps(line))
+    be.close()
+    return line
 
 
 def main():
@@ -407,7 +413,9 @@ def main():
                     help="c2 = configs[1] (64k queue), c5 = configs[4] at D=1 (1M queue, 8k prompts)")
     ap.add_argument("--nq", type=int, default=0, help="queued requests per GPU (default: the config's)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--cluster", action="store_true", help="D2LPM cluster path even at N=1")
+    ap.add_argument("--cluster", action="store_true",
+                    help="only the D2LPM cluster run (replicated dispatcher over NCCL), also at N=1")
+    ap.add_argument("--no-d2lpm", action="store_true", help="N>1: skip the D2LPM cluster run")
     ap.add_argument("--k1-full-steps", type=int, default=3,
                     help="untimed steps after the timed region with the full re-match (scan roofline)")
     ap.add_argument("--arrivals", type=int, default=128,
@@ -438,13 +446,15 @@ def main():
 
     if args.impl == "reference" and rank != 0:
         return  # the reference arm runs on rank 0 only
-    cluster = world > 1 or args.cluster
+    cluster = args.cluster
     # the cluster path dispatches ONE shared stream (rank-independent seed);
     # independent workers (N=1) use their rank's seed
     wl = make_workload(args.workload, args.nq, 0 if cluster else rank, args.steps + args.warmup, device=dev,
                        world=world if cluster else 1, cpu_only=args.impl == "reference")
     cfg = {"workload": wl.desc, "nq_per_gpu": wl.nq, "clients": wl.clients, "M": wl.M, "capacity": wl.CAP,
-           "quantum": wl.quantum(), "l2": wl.l2, "parallelism": f"dp{args.gpus} (independent workers)"}
+           "quantum": wl.quantum(), "l2": wl.l2,
+           "parallelism": f"dp{args.gpus}: one DLPM worker per GPU with its own queue (the local fill has no "
+                          "cross-worker exchange; D2LPM across the GPUs is the separate d2lpm_cluster run)"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -467,7 +477,10 @@ def main():
 
     from paper_2501_14312_b200.device import launch_count
     if cluster:
-        return run_cluster(args, wl, rank, world, dev, tdev, dist)
+        line = run_cluster(args, wl, rank, world, dev, tdev, dist)
+        if line is not None:
+            print(json.dumps(line))
+        return
     g = GpuSteps(wl, dev)
     now = 0
     for _ in range(args.warmup):
@@ -527,6 +540,15 @@ def main():
         total_decisions = float(d[0])
     else:
         total_decisions = decisions
+    if world > 1 and not args.no_d2lpm:
+        # the same GPUs then run D2LPM across them (replicated dispatcher, NCCL
+        # exchange) on ONE shared config-5 queue: a second, separately timed run
+        g.close()
+        wl2 = make_workload(args.workload, args.nq, 0, args.steps + args.warmup, device=dev, world=world)
+        d2 = run_cluster(args, wl2, rank, world, dev, tdev, dist)
+        del wl2
+    else:
+        d2 = None
     if rank != 0:
         return
     value = total_decisions / (dev_ms / 1000.0)
@@ -595,6 +617,11 @@ def main():
                                    "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }
+    if d2 is not None:
+        line["d2lpm_cluster"] = {k: d2[k] for k in ("value", "unit", "ms_per_step", "scaling", "e2e", "config",
+                                                   "cluster_ms_per_step", "local_decisions_per_step",
+                                                   "dispatches_per_step", "seed_dispatch",
+                                                   "notice_cycles_per_notice", "gpu_launches")}
     if not args.no_cpu and world == 1:
         g.close()
         q, pool, ncpu = wl.cpu_sample(dev)
