@@ -494,11 +494,39 @@ __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__res
     st.nseg = SEGS || COV ? warp_path_segments(t, y, m0, segs, lane) : 0;
     st.cov = 0;
     st.pinrun = COV;
-    for (int32_t s = 0; COV && s < st.nseg && st.pinrun; s++) {
-        const Seg g = segs[s];
-        const int32_t last = t.pos[g.S + g.b - 1];
-        st.cov = warp_seg_cov(t, g.S, g.a, g.b, last, lane);
-        st.pinrun = st.cov == g.b;
+    if (COV && st.nseg > 0 && st.nseg <= 32) {
+        // every segment's top and bottom pin state in one round per lane; pinned
+        // segments form a prefix of the path (refs never increase with depth)
+        bool top_p = false, bot_p = false;
+        int32_t botn = -1;
+        if (lane < st.nseg) {
+            const Seg g = segs[lane];
+            const int32_t topn = t.pos[g.S + g.a];
+            botn = t.pos[g.S + g.b - 1];
+            top_p = t.ref[topn] > 0;
+            bot_p = t.ref[botn] > 0;
+        }
+        const unsigned valid = st.nseg == 32 ? FS_FULL : ((1u << st.nseg) - 1u);
+        const unsigned mtop = __ballot_sync(FS_FULL, top_p) & valid;
+        const unsigned mbot = __ballot_sync(FS_FULL, bot_p) & valid;
+        const int32_t kstar = (~mtop & valid) ? __ffs(~mtop & valid) - 1 : st.nseg;  // first unpinned top
+        if (kstar == 0) {
+            st.cov = segs[0].a;
+            st.pinrun = false;
+        } else {
+            const int32_t kk = kstar - 1;
+            const Seg g = segs[kk];
+            const int32_t bk = __shfl_sync(FS_FULL, botn, kk);
+            st.cov = ((mbot >> kk) & 1u) ? g.b : warp_seg_cov(t, g.S, g.a, g.b, bk, lane);
+            st.pinrun = kk == st.nseg - 1 && st.cov == g.b;
+        }
+    } else {
+        for (int32_t s = 0; COV && s < st.nseg && st.pinrun; s++) {
+            const Seg g = segs[s];
+            const int32_t last = t.pos[g.S + g.b - 1];
+            st.cov = warp_seg_cov(t, g.S, g.a, g.b, last, lane);
+            st.pinrun = st.cov == g.b;
+        }
     }
     if (m0 < t.end[y]) {
         // K1 stopped inside y: the request's token there differs from the chain
