@@ -986,9 +986,9 @@ struct NoHook {
 // pin_path (scheduler admissions): ref + 1 on every node of the new path.  The
 // pre-existing path nodes are pinned by warps 2.. while warp 0 evicts (they are
 // internal nodes or the protected deepest node, never eviction candidates),
-// the new leaf when it is created.  Hooks (pin_path only): on_walk runs on
-// thread 0 once the walk's results are known, before the eviction; on_side
-// runs on warp 1 concurrently with the eviction and the pin.
+// the new leaf when it is created.  Hooks (pin_path only): once the walk's
+// results are known, warp 1 runs on_walk (lane 0) then on_side, concurrently
+// with warp 0's eviction and the other warps' pin.
 template <typename OnWalk = NoHook, typename OnSide = NoHook>
 __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now, int64_t sq,
                                     int32_t worker, Seg *segs, InsertSmem *sm, int64_t hint_S0 = -1,
@@ -1031,12 +1031,13 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     if (tid == 0 && sm->prof) sm->prof[1] += c1 - c0;
     if (pin_path) {
         __syncthreads();  // the split top's positions are visible
-        if (tid == 0) on_walk(0);
-        __syncthreads();
-        if (warp > 1)
+        if (warp > 1) {
             block_path_nodes(t, segs, sm->nseg, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);
-        else if (warp == 1)
+        } else if (warp == 1) {
+            if (lane == 0) on_walk(0);
+            __syncwarp();
             on_side(lane);
+        }
         if (!(sm->needed > 0 && sm->lru)) __syncthreads();
     }
     if (sm->needed > 0) {

@@ -867,12 +867,17 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int32_t pre_ok;
     // thread 0's charge operands do not depend on the tree edit: load them now
     // so they arrive while warp 0 walks
-    int32_t c_pre = 0, pend_pre = 0, tok0_pre = -1, m0_pre = 0;
+    int32_t c_pre = 0, pend_pre = 0, tok0_pre = -1, m0_pre = 0, b_pre = -1, tokb_pre = -1;
     int64_t q_pre = 0;
     if (tid == 0) {
         pinb = t.sc->pinned;
         sm->pre_j = -1;
-        c_pre = a.slot[j].x;
+    }
+    if (tid == 32) {  // on_walk runs on thread 32 (warp 1, lane 0)
+        const int4 sl = a.slot[j];
+        c_pre = sl.x;
+        b_pre = sl.y;      // the coverage the search saw, and the token there
+        tokb_pre = sl.z;
         pend_pre = a.pend_cnt[c_pre];
         q_pre = a.q[c_pre];
         m0_pre = a.s_mlen0[j];
@@ -881,7 +886,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __syncthreads();
     const long long ct0 = clock64();
     auto on_walk = [&](int) {
-        // thread 0: everything the next search depends on
+        // thread 32: everything the next search depends on
         const InsertSmem &in = sm->ins;
         pre_ok = 0;
         if (in.status != FS_OK) return;
@@ -894,7 +899,8 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             sm->stop = 1;
             return;
         }
-        adm_put(&sm->flt, cov, cov < len ? t.arena[off + cov] : -1, m0_pre, tok0_pre, sm->epoch, a.gkey, a.gep);
+        const int32_t tokc = cov >= len ? -1 : (cov == b_pre ? tokb_pre : t.arena[off + cov]);
+        adm_put(&sm->flt, cov, tokc, m0_pre, tok0_pre, sm->epoch, a.gkey, a.gep);
         sm->epoch++;
         a.slot[j].w = -1;
         a.rstate[r] = 2;
