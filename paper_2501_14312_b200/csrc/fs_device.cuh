@@ -1029,10 +1029,41 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         block_repoint(t, t.src[sm->split_top], t.start[sm->split_top], t.end[sm->split_top], sm->split_top);
     const long long c1 = clock64();
     if (tid == 0 && sm->prof) sm->prof[1] += c1 - c0;
+    int32_t nseg_path = sm->nseg;
     if (pin_path) {
-        __syncthreads();  // the split top's positions are visible
+        // The new leaf comes first: pinned from birth it is never an eviction
+        // candidate, and its sequence number does not depend on the evictions
+        // (they allocate none) -- only its node slot may differ, which nothing
+        // observes.  used_tokens counts it now; the capacity test below adjusts.
+        if (tid == 0) {
+            int32_t deepest = sm->mlen > 0 ? sm->last : -1;
+            if (sm->status == FS_OK && sm->new_len > 0) {
+                const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last);
+                if (leaf < 0) {
+                    sm->status = FS_ERR_NOMEM;
+                } else {
+                    h_put(t, sm->last, rq[sm->mlen], leaf);
+                    t.nchild[sm->last]++;
+                    t.ref[leaf] = 1;
+                    t.sc->used += sm->new_len;
+                    segs[sm->nseg].S = req_off; segs[sm->nseg].a = sm->mlen; segs[sm->nseg].b = len;
+                    sm->nseg++;
+                    deepest = leaf;
+                    t.la[leaf] = now;  // stamp of the whole path (lazy): a fresh node needs no compare
+                    t.lseq[leaf] = sq;
+                }
+            } else if (sm->status == FS_OK && deepest > 0) {
+                stamp_node(t, deepest, now, sq);
+            }
+            sm->deepest = deepest;
+        }
+        __syncthreads();  // the split top's positions and the leaf are visible
         if (warp > 1) {
-            block_path_nodes(t, segs, sm->nseg, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);
+            // pin the pre-existing path, then point the new leaf's depths at it
+            block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);
+            if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0)
+                for (int32_t d = sm->mlen + (int32_t)tid - 64; d < len; d += (int32_t)blockDim.x - 64)
+                    t.pos[req_off + d] = sm->deepest;
         } else if (warp == 1) {
             if (lane == 0) on_walk(0);
             __syncwarp();
@@ -1050,9 +1081,14 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         if (tid == 0 && sm->prof) sm->prof[2] += clock64() - c1;
         if (tid == 0) {
             if (sm->last > 0) t.flags[sm->last] &= ~FS_PROTECT;
-            if (t.sc->used + sm->new_len > t.sc->capacity) sm->status = FS_ERR_CACHE_FULL;
+            if (t.sc->used + (pin_path ? 0 : sm->new_len) > t.sc->capacity) sm->status = FS_ERR_CACHE_FULL;
         }
         __syncthreads();
+    }
+    if (pin_path) {
+        if (tid == 0 && sm->status != FS_OK && t.sc->status == FS_OK && sm->status != FS_ERR_CACHE_FULL)
+            t.sc->status = sm->status;
+        return;  // the leaf, its positions and the pins are done
     }
     if (tid == 0) {
         int32_t deepest = sm->mlen > 0 ? sm->last : -1;
