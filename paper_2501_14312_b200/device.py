@@ -317,6 +317,13 @@ class WorkerDev:
         self._req = np.zeros(cap, np.int32); self._mlen = np.zeros(cap, np.int32)
         self._unp = np.zeros(cap, np.int64); self._pinb = np.zeros(cap, np.int64)
         self._node = np.zeros(cap, np.int32); self._rend = np.zeros(cap, np.int64)
+        if not hasattr(self, "_rcap"):
+            self._rec_alloc(4096)
+
+    def _rec_alloc(self, cap):
+        # eviction records come back with the fill (one transfer set, one sync)
+        self._rcap = cap
+        self._rsrc = np.zeros(cap, np.int64); self._rlen = np.zeros(cap, np.int32); self._rkeep = np.zeros(cap, np.int32)
 
     def close(self):
         if self._h:
@@ -380,9 +387,14 @@ class WorkerDev:
         res.adm_req = _p32(self._req); res.adm_mlen = _p32(self._mlen); res.adm_unpinned = _p64(self._unp)
         res.adm_pinned_before = _p64(self._pinb); res.adm_path_node = _p32(self._node)
         res.adm_rec_end = _p64(self._rend)
-        res.recs = L.FsRecords(0, None, None, None, 0)
+        res.recs = L.FsRecords(self._rcap, _p64(self._rsrc), _p32(self._rlen), _p32(self._rkeep), 0)
         call("fs_worker_fill", self._h, now, generated_total, headroom, C.byref(res))
-        recs = self.trie.read_records(res.recs.n_rec)
+        nr = res.recs.n_rec
+        if nr <= self._rcap:
+            recs = Records(self._rsrc[:nr].copy(), self._rlen[:nr].copy(), self._rkeep[:nr].copy())
+        else:
+            recs = self.trie.read_records(nr)
+            self._rec_alloc(2 * nr)
         ph = (C.c_float * 4)()
         call("fs_worker_last_phases", self._h, ph)
         st = (C.c_int64 * 24)()
