@@ -90,6 +90,28 @@ class Config2(Workload):
         return self.q, self.pool, len(self.q)
 
 
+class Config3(Config2):
+    """configs[2]: the config-2 generator with 200 clients and 256k queued
+    requests -- the D2LPM D=8 configuration (`--workload c3 --cluster`);
+    per-worker M = capacity = 65536, q_w_frac 0.5."""
+    name = "c3"
+    clients = 200
+
+    def __init__(self, nq, rank, steps):
+        from paper_2501_14312_b200.workloads import build_docs, config3, shared_prefix_queue
+        self.nq = nq
+        self.spec = config3(nq, seed=3 + rank)
+        docs = build_docs(self.spec)
+        self.q = shared_prefix_queue(self.spec, docs=docs)
+        pool_n = 800 * steps + 1024
+        self.pool = shared_prefix_queue(self.spec, first=nq, count=pool_n, arrival=STEP_US, docs=docs,
+                                        stream_seed=self.spec.seed + 101)
+        self.queue_tokens = int(self.q.lens.sum())
+        self.desc = ("config3: 200 clients, %d queued, 1-4k-token prompts, Zipf(1.1) prefixes over 256 docs, "
+                     "per-worker M=capacity=65536, q_u_frac=q_w_frac=0.5, reserve=8" % nq)
+        self.l2 = "inputs larger than L2: the queue occupies %.1f GB" % (self.queue_tokens * 4 / 1e9)
+
+
 class Config5(Workload):
     """configs[4] at D=1: 1M queued 8k-token requests over a branching-4, depth-6
     prefix tree of 1024-token levels (+ a unique 2048-token tail), 200 clients,
@@ -155,6 +177,8 @@ class Config5(Workload):
 def make_workload(name, nq, rank, steps, device=0, world=1, cpu_only=False):
     if name == "c2":
         return Config2(nq or 65536, rank, steps * world)
+    if name == "c3":
+        return Config3(nq or 262144, rank, steps * world)
     if name == "c5":
         return Config5(nq or (1 << 20), rank, steps * world, device=device, cpu_only=cpu_only)
     raise SystemExit(f"unknown workload {name}")
@@ -409,8 +433,9 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["c2", "c5"],
-                    help="c2 = configs[1] (64k queue), c5 = configs[4] at D=1 (1M queue, 8k prompts)")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["c2", "c3", "c5"],
+                    help="c2 = configs[1] (64k queue), c3 = configs[2] (256k queue, 200 clients; with --cluster "
+                         "for D2LPM), c5 = configs[4] (1M queue, 8k prompts)")
     ap.add_argument("--nq", type=int, default=0, help="queued requests per GPU (default: the config's)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cluster", action="store_true",

@@ -51,6 +51,12 @@ def config2(n: int = 65536, seed: int = 2) -> SharedPrefixSpec:
     return SharedPrefixSpec(n=n, seed=seed)
 
 
+def config3(n: int = 262144, seed: int = 3) -> SharedPrefixSpec:
+    """Config 3: D2LPM D=8 workers, 200 clients, 256k queued -- the config-2
+    generator (1-4k-token prompts, Zipf(1.1) document prefixes)."""
+    return SharedPrefixSpec(n=n, clients=200, seed=seed)
+
+
 def build_docs(spec: SharedPrefixSpec):
     pr = random.Random(spec.seed)
     g = np.random.Generator(np.random.PCG64(spec.seed))
