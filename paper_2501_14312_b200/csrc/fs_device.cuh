@@ -1148,7 +1148,7 @@ __device__ inline void block_path_of(const TrieView &t, int32_t deepest, Seg *se
 // walk of `pth`; they are collected in path order and edited by thread 0.
 #define FS_NF_CAP 64
 struct NotifySmem {
-    int32_t nseg, mlen, nf, top;
+    int32_t nseg, mlen, nf, top, fast;
     long long prof[4];  // cycles: walk, collect, edit (thread 0), repoint
     // the collected nodes with what the edit needs (first FS_NF_CAP of them)
     int32_t fnode[FS_NF_CAP], fstart[FS_NF_CAP];
@@ -1164,7 +1164,47 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
                                           NotifySmem *sm, int64_t hint_S0 = -1, int32_t hint_m0 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long q0 = clock64();
-    if (warp == 0) {
+    // Fast path (thread 0): the batch-start match still holds and cannot be
+    // extended (it stops inside its deepest node, or covers the whole path), so
+    // the walk's answer is known, and the nodes intersecting [keep, mlen) are
+    // the deepest node's ancestors down to depth keep -- collected up the
+    // parent links with what the edit needs, no segment list or depth scan.
+    if (tid == 0) {
+        sm->fast = 0;
+        if (hint_m0 > 0) {
+            const int32_t y = t.pos[hint_S0 + hint_m0 - 1];
+            if (pos_valid(t, y, hint_S0, hint_m0 - 1) && (hint_m0 < t.end[y] || hint_m0 == plen)) {
+                int32_t nf = 0;
+                bool ok = true;
+                for (int32_t n = y; n > 0 && keep < hint_m0; n = t.parent[n]) {
+                    const int32_t st = t.start[n];
+                    if (nf == FS_NF_CAP) { ok = false; break; }
+                    const uint64_t wm = t.wmask[n];
+                    const int64_t wt = worker >= 0 && worker < t.nw ? t.wtime[(int64_t)n * t.nw + worker] : 0;
+                    sm->fnode[nf] = n; sm->fstart[nf] = st; sm->fmask[nf] = wm;
+                    sm->fhit[nf] = worker >= 0 && worker < 64 && ((wm >> worker) & 1ull) && wt <= notice;
+                    found[nf] = n;
+                    nf++;
+                    if (st <= keep) break;  // this node holds depth keep
+                }
+                if (ok) {
+                    // ancestors were collected deepest first: path order is the reverse
+                    for (int32_t i = 0; i < nf / 2; i++) {
+                        const int32_t k = nf - 1 - i;
+                        int32_t tn = sm->fnode[i]; sm->fnode[i] = sm->fnode[k]; sm->fnode[k] = tn;
+                        int32_t ts = sm->fstart[i]; sm->fstart[i] = sm->fstart[k]; sm->fstart[k] = ts;
+                        uint64_t tm = sm->fmask[i]; sm->fmask[i] = sm->fmask[k]; sm->fmask[k] = tm;
+                        uint8_t th = sm->fhit[i]; sm->fhit[i] = sm->fhit[k]; sm->fhit[k] = th;
+                    }
+                    sm->nf = nf;
+                    sm->mlen = hint_m0;
+                    sm->fast = 1;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (!sm->fast && warp == 0) {
         const WalkOut w = hint_m0 >= 0 ? warp_walk_hint<8, false, true>(t, t.arena + psrc, plen, lane, segs, hint_S0, hint_m0)
                                        : warp_walk<8>(t, t.arena + psrc, plen, lane, segs, false);
         if (lane == 0) { sm->nseg = w.nseg; sm->mlen = w.mlen; sm->nf = 0; }
@@ -1172,7 +1212,7 @@ __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32
     __syncthreads();
     const long long q1 = clock64();
     const int32_t mlen = sm->mlen;
-    if (keep < mlen) {
+    if (!sm->fast && keep < mlen) {
         // nodes covering a depth in [keep, mlen): the node holding `keep` (visited
         // at depth keep) and every node starting inside the range; depths batched
         // K per thread (all pos loads, then all start loads)
