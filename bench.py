@@ -368,7 +368,9 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
     be.fill_ms = 0.0
     be.n_queued = be.n_dispatched = 0
     be.h2d = 0
-    cr.t_exchange = cr.t_apply = cr.t_dispatch = cr.t_fill = cr.t_overlap = 0.0
+    be.disp_s = be.upload_s = 0.0
+    be.disp_prof[:] = 0
+    cr.t_exchange = cr.t_apply = cr.t_dispatch = cr.t_fill = cr.t_overlap = cr.t_upload = 0.0
     l0 = launch_count()
     t_start = time.perf_counter()
     for _ in range(args.steps):
@@ -382,7 +384,7 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
     # time is the exchange plus the longer of the two
     busy_s = cr.t_exchange + cr.t_overlap
     local = torch.tensor([busy_s, wall, float(be.n_queued), float(be.fill_ms), cr.t_exchange, cr.t_apply,
-                          cr.t_dispatch, cr.t_fill], dtype=torch.float64, device=tdev)
+                          cr.t_dispatch, cr.t_fill, cr.t_upload], dtype=torch.float64, device=tdev)
     if dist is not None:
         mx = local.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -415,7 +417,13 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
                                 "exchange": 1000 * float(mx[4]) / args.steps,
                                 "apply": 1000 * float(mx[5]) / args.steps,
                                 "dispatch": 1000 * float(mx[6]) / args.steps,
-                                "fill_host_wall": 1000 * float(mx[7]) / args.steps},
+                                "fill_host_wall": 1000 * float(mx[7]) / args.steps,
+                                "arrival_upload": 1000 * float(mx[8]) / args.steps},
+        "dispatch_detail": {"upload_ms_per_step": 1000 * be.upload_s / args.steps,
+                            "call_ms_per_step": 1000 * be.disp_s / args.steps,
+                            "kernel_cycles_per_arrival": dict(zip(
+                                ["lmw_select", "insert_walk", "evict", "leaf_stamp_repoint", "tags", "total"],
+                                (be.disp_prof[[0, 1, 2, 12, 14, 15]] / max(be.n_dispatched, 1)).tolist()))},
         "local_decisions_per_step": float(sm[2]) / args.steps, "dispatches_per_step": be.n_dispatched / args.steps,
         "seed_dispatch": {"arrivals": n_seed, "seconds": seed_s},
         "notice_cycles_per_notice": (dict(zip(["walk", "collect", "edit", "repoint"],

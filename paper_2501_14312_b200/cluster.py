@@ -117,6 +117,7 @@ class ClusterRank:
         self.t_apply = 0.0
         self.t_dispatch = 0.0
         self.t_fill = 0.0     # host wall of the fill call
+        self.t_upload = 0.0   # host wall of the arrivals' upload (pipelined, before the fill)
         self.t_overlap = 0.0  # per round: max(fill, dispatcher side) when pipelined, else their sum
 
     def seed(self, arrivals: list, now: int) -> np.ndarray:
@@ -178,6 +179,12 @@ class ClusterRank:
         if self.pipelined:
             if self._late:
                 be.enqueue(self._late)  # last round's arrivals join this round's queue
+            if arrivals and hasattr(be, "prepare"):
+                # arrival uploads go out before the fill is launched: an H2D issued
+                # while another thread waits on the fill stalls in the driver
+                tp = time.perf_counter()
+                be.prepare(arrivals)
+                self.t_upload += time.perf_counter() - tp
             fut = self._pool.submit(dispatcher_side) if self._pool is not None else None
             if fut is None:
                 workers, mine, ta, td = dispatcher_side()
@@ -290,9 +297,15 @@ class GpuStreamRank:
         self.w = WorkerDev(self.ctx, self.trie, "dlpm", wl.quantum(), wl.M, wl.reserve, w_e, w_q,
                            max_clients=n_clients)
         self.d = DispatcherDev(self.ctx, D, q_w, w_e, w_q, max_clients=n_clients)
+        # arrivals upload straight from the page-locked pool (one DMA per round)
+        from .device import host_register
+        self.pool.flat = np.ascontiguousarray(self.pool.flat, dtype=np.int32)
+        host_register(self.pool.flat)
         self.h2d = 0
         self.fill_ms = 0.0
         self.disp_s = 0.0
+        self.upload_s = 0.0
+        self.disp_prof = np.zeros(16, np.int64)
         self.n_queued = 0
         self.n_dispatched = 0
 
@@ -313,16 +326,25 @@ class GpuStreamRank:
         count = max(0, min(count, len(self.pool) - first))
         return list(range(nq + first, nq + first + count))
 
+    def prepare(self, arrivals):
+        import time
+        tu = time.perf_counter()
+        self._ensure(int(max(arrivals)) + 1)
+        self.upload_s += time.perf_counter() - tu
+
     def dispatch(self, arrivals, now, batch=1 << 16):
         import time
         idx = np.asarray(arrivals, np.int64)
+        tu = time.perf_counter()
         self._ensure(int(idx.max()) + 1)
         t0 = time.perf_counter()
+        self.upload_s += t0 - tu
         out = []
         for a in range(0, len(idx), batch):
             j = idx[a:a + batch]
             w, _, _, _ = self.d.dispatch(self.ids[j], self.clients[j], np.full(len(j), now, np.int64))
             out.append(w)
+            self.disp_prof += self.d.last_profile()
         self.disp_s += time.perf_counter() - t0
         self.n_dispatched += len(idx)
         return np.concatenate(out)
@@ -366,6 +388,8 @@ class GpuStreamRank:
             r.device_ms
 
     def close(self):
+        from .device import host_unregister
+        host_unregister(self.pool.flat)
         self.w.close()
         self.trie.close()
         self.d.close()

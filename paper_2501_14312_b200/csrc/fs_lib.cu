@@ -183,7 +183,13 @@ extern "C" int fs_ctx_create(int device, int64_t arena_tokens, int64_t max_reque
     fs_ctx *c = new fs_ctx();
     c->device = device;
     CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    {
+        // uploads are short and sit in front of the dispatch chain of a
+        // cluster round: highest priority, so they do not queue behind a fill
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+    }
     TRY(dgrow(c->arena, std::max<int64_t>(arena_tokens, 1024), c->stream));
     const int64_t mr = std::max<int64_t>(max_requests, 1024);
     TRY(dgrow(c->roff, mr, c->stream));
@@ -285,7 +291,9 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         // rows that also checks the id range -- no host pass over the tokens
         const int64_t src_total = offsets[n - 1] + lens[n - 1] - offsets[0];
         TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
-        TRY(dgrow(c->x_tok, src_total + 4, c->stream));
+        // staging for the caller's block: reserved in 16 MB steps so a stream of
+        // growing arrival batches does not reallocate (and synchronize) per call
+        TRY(dgrow(c->x_tok, std::max<int64_t>(src_total + 4, std::min<int64_t>(c->arena.cap, 1 << 22)), c->stream));
         TRY(dgrow(c->x_dst, n + 1, c->stream)); TRY(dgrow(c->x_nsoff, n + 1, c->stream));
         TRY(dgrow(c->x_len, n + 1, c->stream)); TRY(dgrow(c->x_flag, 1, c->stream));
         TRY(hgrow(c->stage64, 2 * n + 2)); TRY(hgrow(c->stage32, n + 2));
@@ -294,18 +302,24 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
             c->stage64.p[n + i] = offsets[i] - offsets[0];
             c->stage32.p[i] = lens[i];
         }
+        const auto ag = std::chrono::steady_clock::now();
         if (src_total) CK(cudaMemcpyAsync(c->x_tok.p, tokens + offsets[0], sizeof(int32_t) * src_total,
                                           cudaMemcpyHostToDevice, c->stream));
+        const auto ah = std::chrono::steady_clock::now();
         CK(cudaMemcpyAsync(c->x_dst.p, c->stage64.p, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->x_nsoff.p, c->stage64.p + n, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->x_len.p, c->stage32.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemsetAsync(c->x_flag.p, 0, sizeof(int32_t), c->stream));
+        const auto ac = std::chrono::steady_clock::now();
+        if (hprof) CK(cudaStreamSynchronize(c->stream));
+        const auto ad = std::chrono::steady_clock::now();
         k_scatter_rows<<<(unsigned)n, 256, 0, c->stream>>>(c->x_tok.p, c->x_nsoff.p, c->x_dst.p, c->x_len.p,
                                                            c->arena.p, c->x_flag.p);
         counted();
         CK(cudaGetLastError());
         int32_t bad = 0;
         CK(cudaMemcpyAsync(&bad, c->x_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        const auto aq = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(c->stream));
         if (bad) return fail(FS_ERR_TOKEN_RANGE, "a token id is outside [0, 2^31)");  // nothing committed
         const auto a1 = std::chrono::steady_clock::now();
@@ -314,8 +328,8 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         if (hprof) {
             const auto a2 = std::chrono::steady_clock::now();
             auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
-            fprintf(stderr, "requests_add: %lld rows, %lld tokens: copy+scatter %.0f us, meta %.0f us\n",
-                    (long long)n, (long long)src_total, us(a0, a1), us(a1, a2));
+            fprintf(stderr, "requests_add: %lld rows, %lld tokens: copy+scatter %.0f us (grow %.0f, tok copy %.0f, rest %.0f, copy wait %.0f, kernel %.0f), meta %.0f us\n",
+                    (long long)n, (long long)src_total, us(a0, a1), us(a0, ag), us(ag, ah), us(ah, ac), us(ac, ad), us(ad, a1), us(a1, a2));
         }
         return FS_OK;
     }
