@@ -370,7 +370,7 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
     be.h2d = 0
     be.disp_s = be.upload_s = 0.0
     be.disp_prof[:] = 0
-    cr.t_exchange = cr.t_apply = cr.t_dispatch = cr.t_fill = cr.t_overlap = cr.t_upload = 0.0
+    cr.t_exchange = cr.t_apply = cr.t_dispatch = cr.t_fill = cr.t_overlap = cr.t_upload = cr.t_complete = 0.0
     l0 = launch_count()
     t_start = time.perf_counter()
     for _ in range(args.steps):
@@ -381,10 +381,10 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
     launches = launch_count() - l0
     clocks = clocks_stop(*clk, dev) if rank == 0 else None
     # the dispatcher side (apply + dispatch) overlaps the fill; a round's busy
-    # time is the exchange plus the longer of the two
-    busy_s = cr.t_exchange + cr.t_overlap
+    # time is completion + exchange + the longer of the two
+    busy_s = cr.t_complete + cr.t_exchange + cr.t_overlap
     local = torch.tensor([busy_s, wall, float(be.n_queued), float(be.fill_ms), cr.t_exchange, cr.t_apply,
-                          cr.t_dispatch, cr.t_fill, cr.t_upload], dtype=torch.float64, device=tdev)
+                          cr.t_dispatch, cr.t_fill, cr.t_upload, cr.t_complete], dtype=torch.float64, device=tdev)
     if dist is not None:
         mx = local.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -418,7 +418,8 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
                                 "apply": 1000 * float(mx[5]) / args.steps,
                                 "dispatch": 1000 * float(mx[6]) / args.steps,
                                 "fill_host_wall": 1000 * float(mx[7]) / args.steps,
-                                "arrival_upload": 1000 * float(mx[8]) / args.steps},
+                                "arrival_upload": 1000 * float(mx[8]) / args.steps,
+                                "complete": 1000 * float(mx[9]) / args.steps},
         "dispatch_detail": {"upload_ms_per_step": 1000 * be.upload_s / args.steps,
                             "call_ms_per_step": 1000 * be.disp_s / args.steps,
                             "kernel_cycles_per_arrival": dict(zip(

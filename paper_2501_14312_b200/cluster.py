@@ -117,6 +117,7 @@ class ClusterRank:
         self.t_apply = 0.0
         self.t_dispatch = 0.0
         self.t_fill = 0.0     # host wall of the fill call
+        self.t_complete = 0.0  # host wall of step 1 (unpin + output accounting of the last batch)
         self.t_upload = 0.0   # host wall of the arrivals' upload (pipelined, before the fill)
         self.t_overlap = 0.0  # per round: max(fill, dispatcher side) when pipelined, else their sum
 
@@ -136,6 +137,7 @@ class ClusterRank:
     def round(self, now: int, arrival_stream) -> RoundResult:
         import time
         be, comm = self.be, self.comm
+        tc = time.perf_counter()
         # 1. completion of last round's batch on this worker
         fin = np.zeros((len(self.prev), FIN_COLS), np.int64)
         if self.prev:
@@ -151,6 +153,7 @@ class ClusterRank:
         rows[fin.shape[0]:, 0] = 1
         rows[fin.shape[0]:, 1:] = self.notices
         t0 = time.perf_counter()
+        self.t_complete += t0 - tc
         gathered = comm.all_gather_rows(rows)
         t1 = time.perf_counter()
         n_adm_cluster = sum(int((part[:, 0] == 0).sum()) for part in gathered)

@@ -480,7 +480,10 @@ __device__ inline int32_t warp_cov_from_deepest(const TrieView &t, int32_t y, in
 // pins).  SEGS: record the path's chain segments (callers that edit the path).
 template <int U = 8, bool COV = true, bool SEGS = true>
 __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
-                                         Seg *segs, int64_t S0, int32_t m0) {
+                                         Seg *segs, int64_t S0, int32_t m0, const Seg *pre = nullptr,
+                                         int32_t pre_n = -1) {
+    // pre / pre_n (optional, pre_n <= 32): the segments of [0, m0) recorded by
+    // a batch-start walk of this same path (k_dispatch_prematch)
     int32_t y = -1;
     if (m0 > 0) {
         const int32_t c = t.pos[S0 + m0 - 1];
@@ -491,7 +494,13 @@ __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__res
     };
     if (y < 0) return warp_walk_cb<U>(t, rq, len, lane, COV, store);
     WalkStart st;
-    st.nseg = SEGS || COV ? warp_path_segments(t, y, m0, segs, lane) : 0;
+    if ((SEGS || COV) && pre && pre_n >= 0 && pre_n <= 32) {
+        if (lane < pre_n) segs[lane] = pre[lane];
+        __syncwarp();
+        st.nseg = pre_n;
+    } else {
+        st.nseg = SEGS || COV ? warp_path_segments(t, y, m0, segs, lane) : 0;
+    }
     st.cov = 0;
     st.pinrun = COV;
     if (COV && st.nseg > 0 && st.nseg <= 32) {
@@ -612,9 +621,40 @@ __device__ inline void warp_unpin_path(const TrieView &t, int32_t deepest, int l
 // fn(node, start, end) -- a constant number of memory round trips per
 // K*blockDim depths whatever the number of segments (fn's stores would
 // otherwise pin every load behind them).
+//
+// Hop variant (FS_PATH_HOP, default): thread i owns a window of W consecutive
+// flattened depths and reports the nodes STARTING in it -- one pos load at the
+// window start, then hops node to node (pos at end[n]) until the window is
+// passed.  Paths of long nodes (config 5: 1024-token levels) cost one
+// pos + (start, end) round trip per thread instead of K of each.
+#ifndef FS_PATH_HOP
+#define FS_PATH_HOP 1
+#endif
 template <typename F>
 __device__ inline void block_path_nodes(const TrieView &t, const Seg *segs, int32_t nseg, F fn, int32_t first = 0) {
     // threads [first, blockDim) take part (the others may be busy elsewhere)
+#if FS_PATH_HOP
+    {
+        const int32_t nt = (int32_t)blockDim.x - first;
+        if ((int32_t)threadIdx.x < first) return;
+        int32_t total = 0;
+        for (int32_t s = 0; s < nseg; s++) total += segs[s].b - segs[s].a;
+        const int32_t W = (total + nt - 1) / nt;
+        int32_t g = ((int32_t)threadIdx.x - first) * W;
+        const int32_t hi = min(total, g + W);
+        int32_t s = 0, base = 0;
+        while (g < hi) {
+            while (g - base >= segs[s].b - segs[s].a) { base += segs[s].b - segs[s].a; s++; }
+            const int32_t d = segs[s].a + (g - base);
+            const int32_t n = t.pos[segs[s].S + d];
+            const int32_t st = t.start[n], en = t.end[n];
+            if (st == d) fn(n, st, en);  // else: a node started before the window
+            // next node: its first depth, clamped to the segment end
+            g = base + min(en, segs[s].b) - segs[s].a;
+        }
+        return;
+    }
+#endif
     constexpr int K = 8;
     const int32_t nt = (int32_t)blockDim.x - first;
     if ((int32_t)threadIdx.x < first) return;
@@ -993,13 +1033,17 @@ template <typename OnWalk = NoHook, typename OnSide = NoHook>
 __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now, int64_t sq,
                                     int32_t worker, Seg *segs, InsertSmem *sm, int64_t hint_S0 = -1,
                                     int32_t hint_m0 = -1, bool pin_path = false, OnWalk on_walk = OnWalk(),
-                                    OnSide on_side = OnSide()) {
+                                    OnSide on_side = OnSide(), const WalkOut *pre = nullptr) {
+    // pre (warp 0, optional): the caller's own walk of this path with segments
+    // written to segs, against the current tree (the dispatch chain's
+    // longest_match_workers walk) -- reused instead of walking again
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t *rq = t.arena + req_off;
     const long long c0 = clock64();
     if (warp == 0) {
         // the routing index (worker tags) has no pins: no coverage to compute
-        const WalkOut w = hint_m0 >= 0 ? (t.wmask ? warp_walk_hint<8, false, true>(t, rq, len, lane, segs, hint_S0, hint_m0)
+        const WalkOut w = pre ? *pre
+                        : hint_m0 >= 0 ? (t.wmask ? warp_walk_hint<8, false, true>(t, rq, len, lane, segs, hint_S0, hint_m0)
                                                   : warp_walk_hint<8, true, true>(t, rq, len, lane, segs, hint_S0, hint_m0))
                                        : warp_walk<8>(t, rq, len, lane, segs, t.wmask == nullptr);
         if (lane == 0) {

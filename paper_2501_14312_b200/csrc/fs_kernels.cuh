@@ -20,6 +20,12 @@
 #ifndef FS_DISPATCH_THREADS
 #define FS_DISPATCH_THREADS 1024  // one batch of block_path_nodes covers an 8k-token path
 #endif
+#ifndef FS_DISP_STAGE
+#define FS_DISP_STAGE 256
+#endif
+#ifndef FS_PRE_SEGS
+#define FS_PRE_SEGS 32
+#endif
 #ifndef FS_ITEMS
 #define FS_ITEMS 8
 #endif
@@ -1190,8 +1196,10 @@ struct DispArgs {
     const int32_t *dl_w;
     int32_t ndl;
     Seg *segs;
-    const int32_t *m0;  // batch-start match of every arrival (k_match pre-pass, no stamp)
+    const int32_t *m0;  // batch-start match of every arrival (k_dispatch_prematch, no stamp)
     const int64_t *s0;
+    const Seg *pre_segs;       // its source-chain segments, FS_PRE_SEGS per arrival
+    const int32_t *pre_nseg;   // -1: more than FS_PRE_SEGS (rebuilt from the chain links)
     int32_t *out_w, *out_mlen;
     uint64_t *out_mask;
     int64_t *out_rounds;
@@ -1221,6 +1229,33 @@ __device__ inline int d2_select(const DispArgs &a, int32_t c, uint64_t mask, int
             if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;
         }
     return best;
+}
+
+// Batch-start longest match of every arrival of a dispatch chain, a warp each,
+// in parallel (no stamps): match length, chain of the deepest matched node and
+// the segments of the matched path.  Inside the chain the index only gains
+// nodes (inserts and splits keep every node's source chain), so these
+// segments still describe [0, m0) when the arrival's turn comes.
+__global__ void __launch_bounds__(256) k_dispatch_prematch(TrieView t, const int32_t *__restrict__ ids, int32_t n,
+                                                           const int64_t *__restrict__ roff,
+                                                           const int32_t *__restrict__ rlen, int32_t *out_m0,
+                                                           int64_t *out_s0, Seg *out_segs, int32_t *out_nseg) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int32_t r = ids[i];
+    Seg *my = out_segs + i * FS_PRE_SEGS;
+    int64_t lastS = -1;
+    auto store = [&](int64_t S, int32_t a, int32_t b, int32_t k) {
+        if (lane == 0 && k < FS_PRE_SEGS) { my[k].S = S; my[k].a = a; my[k].b = b; }
+        lastS = S;
+    };
+    const WalkOut w = warp_walk_cb<8, decltype(store), true>(t, t.arena + roff[r], rlen[r], lane, false, store);
+    if (lane == 0) {
+        out_m0[i] = w.mlen;
+        out_s0[i] = w.mlen > 0 ? lastS : -1;
+        out_nseg[i] = w.nseg <= FS_PRE_SEGS ? w.nseg : -1;
+    }
 }
 
 // Dispatcher.dispatch for a chain of arrivals (global_policies.py:40-46,
@@ -1259,35 +1294,56 @@ __global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a)
         }
         return;
     }
+    // the chain's per-arrival scalars, staged FS_DISP_STAGE at a time so each
+    // arrival starts without a dependent ids -> (len, off) round trip
+    __shared__ int32_t s_len[FS_DISP_STAGE], s_m0[FS_DISP_STAGE], s_cl[FS_DISP_STAGE];
+    __shared__ int64_t s_off[FS_DISP_STAGE], s_now[FS_DISP_STAGE], s_s0[FS_DISP_STAGE];
     for (int32_t i = 0; i < a.n; i++) {
-        const int32_t r = a.ids[i];
-        const int32_t len = a.rlen[r];
-        const int64_t off = a.roff[r];
-        const int64_t now = a.nows[i];
+        const int32_t k = i % FS_DISP_STAGE;
+        if (k == 0) {
+            __syncthreads();
+            for (int32_t j = tid; j < FS_DISP_STAGE && i + j < a.n; j += blockDim.x) {
+                const int32_t r = a.ids[i + j];
+                s_len[j] = a.rlen[r]; s_off[j] = a.roff[r]; s_now[j] = a.nows[i + j];
+                s_s0[j] = a.s0[i + j]; s_m0[j] = a.m0[i + j]; s_cl[j] = a.clients[i + j];
+            }
+            __syncthreads();
+        }
+        const int32_t len = s_len[k];
+        const int64_t off = s_off[k];
+        const int64_t now = s_now[k];
+        const int64_t hs0 = s_s0[k];
+        const int32_t hm0 = s_m0[k];
         const long long cw = clock64();
+        WalkOut w{};
         if (warp == 0) {
             // RadixTree.longest_match_workers (radix.py:101-110).  The index only
             // gains prefixes of this batch's earlier arrivals (no capacity, no
             // eviction inside a batch), so the batch-start match is still a
             // prefix of the current one: resume from it (warp_walk_hint).
-            const WalkOut w = warp_walk_hint<8, false, false>(t, t.arena + off, len, lane, a.segs, a.s0[i], a.m0[i]);
+            // (with its segments: block_insert below reuses this walk)
+            w = warp_walk_hint<8, false, true>(t, t.arena + off, len, lane, a.segs, hs0, hm0,
+                                                a.pre_segs ? a.pre_segs + (int64_t)i * FS_PRE_SEGS : nullptr,
+                                                a.pre_nseg ? a.pre_nseg[i] : -1);
             if (lane == 0) {
                 const int32_t deepest = w.mlen > 0 ? w.last : -1;
                 if (deepest > 0) stamp_node(t, deepest, now, a.sq_base + 2 * (int64_t)i);
                 const uint64_t mask = deepest > 0 ? t.wmask[deepest] : 0ull;
                 int64_t rounds;
-                const int best = d2_select(a, a.clients[i], mask, &rounds);
-                int64_t *qr = a.q + (int64_t)a.clients[i] * a.D;
+                const int32_t cl = s_cl[k];
+                const int best = d2_select(a, cl, mask, &rounds);
+                int64_t *qr = a.q + (int64_t)cl * a.D;
                 a.qsize[best] += 1;
                 qr[best] -= a.w_e * (int64_t)len;  // after_dispatch: full input (global_policies.py:123)
-                a.qset[(int64_t)a.clients[i] * a.D + best] = 1;
+                a.qset[(int64_t)cl * a.D + best] = 1;
                 s_w = best; s_mlen = deepest > 0 ? w.mlen : 0; s_mask = mask;
                 a.out_rounds[i] = rounds;
             }
         }
         __syncthreads();
         if (tid == 0) prof[0] += clock64() - cw;
-        block_insert(t, off, len, now, a.sq_base + 2 * (int64_t)i + 1, s_w, a.segs, &ins, a.s0[i], a.m0[i]);
+        block_insert(t, off, len, now, a.sq_base + 2 * (int64_t)i + 1, s_w, a.segs, &ins, hs0, hm0, false,
+                     NoHook(), NoHook(), warp == 0 ? &w : nullptr);
         if (tid == 0) {
             a.out_w[i] = s_w;
             a.out_mlen[i] = s_mlen;

@@ -1500,6 +1500,8 @@ struct fs_dispatcher {
     DBuf<uint8_t> qset;
     DBuf<int32_t> ids, clients, dli, dlw, o_w, o_mlen, m0;
     DBuf<int64_t> nows, dlq, o_rounds, hdr, s0;
+    DBuf<Seg> pre_segs;
+    DBuf<int32_t> pre_nseg;
     DBuf<uint64_t> o_mask;
 };
 
@@ -1544,7 +1546,7 @@ extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
     d->q.release(); d->qsize.release(); d->qset.release(); d->ids.release(); d->clients.release();
     d->dli.release(); d->dlw.release(); d->o_w.release(); d->o_mlen.release(); d->nows.release();
     d->dlq.release(); d->o_rounds.release(); d->hdr.release(); d->o_mask.release();
-    d->m0.release(); d->s0.release();
+    d->m0.release(); d->s0.release(); d->pre_segs.release(); d->pre_nseg.release();
     delete d;
     return FS_OK;
 }
@@ -1595,12 +1597,14 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
         // batch-start matches of every arrival, in parallel (K1, no stamping):
         // the serial chain below resumes each walk from them
         TRY(dgrow(d->m0, n, s)); TRY(dgrow(d->s0, n, s));
-        k_match<1, true><<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
-            view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, 0, 0, 0, 0u, nullptr, d->m0.p, nullptr,
-            nullptr, d->s0.p, nullptr, nullptr, K1Hints{});
+        TRY(dgrow(d->pre_segs, n * FS_PRE_SEGS, s)); TRY(dgrow(d->pre_nseg, n, s));
+        k_dispatch_prematch<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+            view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, d->m0.p, d->s0.p, d->pre_segs.p,
+            d->pre_nseg.p);
         counted();
         CK(cudaGetLastError());
         a.m0 = d->m0.p; a.s0 = d->s0.p;
+        a.pre_segs = d->pre_segs.p; a.pre_nseg = d->pre_nseg.p;
     }
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
