@@ -430,11 +430,14 @@ __device__ inline WalkOut warp_walk_cb(const TrieView &t, const int32_t *__restr
 // node y: chain by chain through the per-chain constants (src, ctop, cpar) --
 // one dependent load round per chain, no token compare.  Lane 0 writes segs in
 // path order; returns the count (warp-uniform).
-__device__ inline int32_t warp_path_segments(const TrieView &t, int32_t y, int32_t d, Seg *segs, int lane) {
+__device__ inline int32_t warp_path_segments(const TrieView &t, int32_t y, int32_t d, Seg *segs, int lane,
+                                             int32_t cap = INT32_MAX) {
+    // cap: at most cap segments, else -1 (segs partly written)
     int32_t ns = 0;
     if (lane == 0) {
         int32_t cur = y;
         while (d > 0 && cur > 0) {
+            if (ns == cap) { ns = -1; break; }
             const int64_t S = t.src[cur];
             const int32_t c0 = t.ctop[cur];
             const int32_t X = t.cpar[cur];
@@ -443,7 +446,7 @@ __device__ inline int32_t warp_path_segments(const TrieView &t, int32_t y, int32
             d = c0;
             cur = X;
         }
-        for (int32_t i = 0; i < ns / 2; i++) {
+        for (int32_t i = 0; i < ns / 2; i++) {  // (nothing to reverse when ns == -1)
             const Seg tmp = segs[i];
             segs[i] = segs[ns - 1 - i];
             segs[ns - 1 - i] = tmp;
@@ -1033,7 +1036,8 @@ template <typename OnWalk = NoHook, typename OnSide = NoHook>
 __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t len, int64_t now, int64_t sq,
                                     int32_t worker, Seg *segs, InsertSmem *sm, int64_t hint_S0 = -1,
                                     int32_t hint_m0 = -1, bool pin_path = false, OnWalk on_walk = OnWalk(),
-                                    OnSide on_side = OnSide(), const WalkOut *pre = nullptr) {
+                                    OnSide on_side = OnSide(), const WalkOut *pre = nullptr,
+                                    const Seg *pre_segs = nullptr, int32_t pre_nseg = -1) {
     // pre (warp 0, optional): the caller's own walk of this path with segments
     // written to segs, against the current tree (the dispatch chain's
     // longest_match_workers walk) -- reused instead of walking again
@@ -1043,8 +1047,10 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     if (warp == 0) {
         // the routing index (worker tags) has no pins: no coverage to compute
         const WalkOut w = pre ? *pre
-                        : hint_m0 >= 0 ? (t.wmask ? warp_walk_hint<8, false, true>(t, rq, len, lane, segs, hint_S0, hint_m0)
-                                                  : warp_walk_hint<8, true, true>(t, rq, len, lane, segs, hint_S0, hint_m0))
+                        : hint_m0 >= 0 ? (t.wmask ? warp_walk_hint<8, false, true>(t, rq, len, lane, segs, hint_S0, hint_m0,
+                                                                                   pre_segs, pre_nseg)
+                                                  : warp_walk_hint<8, true, true>(t, rq, len, lane, segs, hint_S0, hint_m0,
+                                                                                  pre_segs, pre_nseg))
                                        : warp_walk<8>(t, rq, len, lane, segs, t.wmask == nullptr);
         if (lane == 0) {
             int32_t last = w.last >= 0 ? w.last : 0;

@@ -444,6 +444,8 @@ struct SchedSmem {
     int32_t wl_n, minA, minB;
     int32_t cursor, progress, epoch, npos, nadm, stop, j, cursor_seq;
     int32_t pre_j, pre_end;  // next-candidate prescan of the last admission (block_admit)
+    Seg pseg[FS_PRE_SEGS];    // ... and the segments of that candidate's step-start match
+    int32_t pseg_j, pseg_n;   // (queue position, count; -1: none)
     int64_t headroom, slack_at;
     int64_t resumes, refill_events;
     int64_t prof[16];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops,
@@ -895,6 +897,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
         // thread 32: everything the next search depends on
         const InsertSmem &in = sm->ins;
         pre_ok = 0;
+        sm->pseg_j = -1;  // consumed by this walk (on_side may set the next one)
         if (in.status != FS_OK) return;
         const int32_t mlen = in.mlen;
         const int32_t cov = in.cov;
@@ -930,9 +933,23 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
         const int32_t from = j + 1, wend = min(a.n, from + FS_FAST);
         const int32_t rr = from < wend ? warp_find_window(a, sm, from, wend, false, pre_slack, lane) : FS_NONE;
         if (lane == 0) { sm->pre_j = rr; sm->pre_end = wend; }
+        // that candidate's matched path as source-chain segments, so its walk
+        // starts without the chain hops.  Concurrent with warp 0's eviction,
+        // which only detaches or truncates leaves: the ancestors of a node
+        // are never touched, and a leaf touched here fails the walk's
+        // pos_valid check of the hint, which then ignores these segments.
+        int32_t ns = -1;
+        if (rr >= 0 && rr != FS_NONE && a.s_mlen0[rr] > 0) {  // (negative: a stale coverage to re-walk)
+            const int64_t S0 = a.s_src0[rr];
+            const int32_t m0 = a.s_mlen0[rr];
+            const int32_t y = t.pos[S0 + m0 - 1];
+            if (pos_valid(t, y, S0, m0 - 1)) ns = warp_path_segments(t, y, m0, sm->pseg, lane, FS_PRE_SEGS);
+        }
+        if (lane == 0) { sm->pseg_j = ns >= 0 ? rr : -1; sm->pseg_n = ns; }
     };
+    const bool have_pseg = sm->pseg_j == j;
     block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j], true,
-                 on_walk, on_side);
+                 on_walk, on_side, nullptr, have_pseg ? sm->pseg : nullptr, have_pseg ? sm->pseg_n : -1);
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
         if (in.status != FS_OK) {
@@ -983,7 +1000,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         a.hdr[2] = FS_OK;
         sm.cursor = 0; sm.progress = 0; sm.epoch = 0; sm.nadm = 0; sm.stop = 0;
         sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0; sm.cursor_seq = 0;
-        sm.pre_j = -1; sm.pre_end = 0;
+        sm.pre_j = -1; sm.pre_end = 0; sm.pseg_j = -1; sm.pseg_n = -1;
         for (int i = 0; i < 16; i++) sm.prof[i] = 0;
         for (int i = 0; i < 4; i++) sm.lru.prof[i] = 0;
         sm.ins.prof = sm.prof;
