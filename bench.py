@@ -217,6 +217,8 @@ class GpuSteps:
         self.prev_nodes = np.zeros(0, np.int32)
         self.prev_clients = np.zeros(0, np.int32)
         self.pool_next = 0
+        self.pool_ids = np.full(len(self.pool), -1, np.int32)
+        self.uploaded = 0  # pool[:uploaded] is on the device
         self.h2d = 0
         self.d2h = 0
         self.unpin_ms = 0.0  # device time of the batch-completion unpins
@@ -231,19 +233,31 @@ class GpuSteps:
             self.h2d += cl.nbytes + cnt.nbytes + self.prev_nodes.nbytes
         if n_prev and self.pool_next + n_prev <= len(self.pool):
             a, b = self.pool_next, self.pool_next + n_prev
-            p = self.pool
-            o0 = int(p.offsets[a])
-            o1 = int(p.offsets[b - 1] + p.lens[b - 1])
-            ids = self.ctx.add_requests(p.flat[o0:o1], p.offsets[a:b] - o0, p.lens[a:b], p.clients[a:b],
-                                        p.labels[a:b])
-            self.w.enqueue(ids)
+            self._upload(b)  # normally already there (uploaded during the last fill)
+            self.w.enqueue(self.pool_ids[a:b])
             self.pool_next = b
-            self.h2d += (o1 - o0) * 4 + (b - a) * 24
-        res = self.w.fill(now, 0, 0)
+        # the scheduler runs while the host uploads the next arrivals (the pool
+        # in arrival order, a lookahead of twice the last admission count):
+        # the copy and its scatter overlap the fill instead of preceding it
+        self.w.fill_begin(now, 0, 0)
+        self._upload(min(len(self.pool), self.pool_next + max(64, 2 * n_prev)))
+        res = self.w.fill_end()
         self.prev_nodes = res.adm_node.astype(np.int32)
         self.prev_clients = self.clients[np.asarray(res.adm_req, np.int64)]
         self.d2h += res.adm_req.nbytes * 6 + 8 * 128 * 2 + 64
         return res
+
+    def _upload(self, upto):
+        if upto <= self.uploaded:
+            return
+        a, b = self.uploaded, upto
+        p = self.pool
+        o0 = int(p.offsets[a])
+        o1 = int(p.offsets[b - 1] + p.lens[b - 1])
+        self.pool_ids[a:b] = self.ctx.add_requests(p.flat[o0:o1], p.offsets[a:b] - o0, p.lens[a:b], p.clients[a:b],
+                                                   p.labels[a:b])
+        self.uploaded = b
+        self.h2d += (o1 - o0) * 4 + (b - a) * 24
 
     def close(self):
         from paper_2501_14312_b200.device import host_unregister

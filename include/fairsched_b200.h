@@ -199,6 +199,13 @@ typedef struct {
 } fs_fill_result;
 int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom,
                    fs_fill_result *res);
+/* fs_worker_fill in two halves: _begin launches the fill and returns at once,
+ * _end waits and fills res.  In between, context uploads (fs_requests_add*,
+ * on their own stream) may run concurrently with the fill -- a serving loop
+ * uploads the next arrivals while the scheduler decides; every other call on
+ * this worker or its tree fails with FS_ERR_INVALID until _end. */
+int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom);
+int fs_worker_fill_end(fs_worker *w, fs_fill_result *res);
 /* Timing breakdown of the last fill: [merge, match K1, sort K2, schedule K3/K4] ms */
 int fs_worker_last_phases(fs_worker *w, float *ms4);
 /* Counters of the last fill: [0] sum over queued j of min(mlen_j+1, len_j)

@@ -96,6 +96,8 @@ SIGNATURES = {
     "fs_worker_reserve_clients": (C.c_int, [vp, i32]),
     "fs_worker_mark_known": (C.c_int, [vp, i64, P32]),
     "fs_worker_fill": (C.c_int, [vp, i64, i64, i64, PFILL]),
+    "fs_worker_fill_begin": (C.c_int, [vp, i64, i64, i64]),
+    "fs_worker_fill_end": (C.c_int, [vp, PFILL]),
     "fs_worker_last_phases": (C.c_int, [vp, PF]),
     "fs_worker_set_option": (C.c_int, [vp, C.c_int, i64]),
     "fs_worker_last_stats": (C.c_int, [vp, P64]),

@@ -128,7 +128,8 @@ __global__ void k_scatter_rows(const int32_t *__restrict__ src, const int64_t *_
 // ---------------------------------------------------------------- context
 struct fs_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;   // fills and tree operations
+    cudaStream_t ustream = nullptr;  // uploads (fs_requests_add*)
     DBuf<int32_t> arena;
     int64_t arena_used = 0;
     DBuf<int64_t> roff;
@@ -183,12 +184,14 @@ extern "C" int fs_ctx_create(int device, int64_t arena_tokens, int64_t max_reque
     fs_ctx *c = new fs_ctx();
     c->device = device;
     CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     {
-        // uploads are short and sit in front of the dispatch chain of a
-        // cluster round: highest priority, so they do not queue behind a fill
+        // uploads have their own stream: they may run while a fill is in
+        // flight (fs_worker_fill_begin), and at the highest priority so their
+        // few blocks do not queue behind the fill's
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithPriority(&c->ustream, cudaStreamNonBlocking, hi));
     }
     TRY(dgrow(c->arena, std::max<int64_t>(arena_tokens, 1024), c->stream));
     const int64_t mr = std::max<int64_t>(max_requests, 1024);
@@ -205,7 +208,7 @@ extern "C" int fs_ctx_create(int device, int64_t arena_tokens, int64_t max_reque
 extern "C" int fs_ctx_destroy(fs_ctx *c) {
     if (!c) return FS_OK;
     cudaSetDevice(c->device);
-    cudaStreamSynchronize(c->stream);
+    cudaDeviceSynchronize();
     c->arena.release(); c->roff.release(); c->rlen.release(); c->rclient.release();
     c->rlabel.release(); c->rstate.release(); c->rhint.release();
     c->h_owner.release(); c->h_tok0.release(); c->h_S0.release();
@@ -213,13 +216,25 @@ extern "C" int fs_ctx_destroy(fs_ctx *c) {
     c->x_dst.release(); c->x_nsoff.release(); c->x_len.release(); c->x_ns.release(); c->x_nslen.release();
     c->x_bytes.release(); c->x_tok.release(); c->x_flag.release();
     cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->ustream);
     delete c;
     return FS_OK;
 }
 
 extern "C" int fs_ctx_sync(fs_ctx *c) {
     TRY(ctx_use(c));
+    CK(cudaStreamSynchronize(c->ustream));
     CK(cudaStreamSynchronize(c->stream));
+    return FS_OK;
+}
+
+// Uploads may overlap an in-flight fill that reads (and, for the match hints,
+// writes) the per-request arrays and the arena: reallocating any of them
+// waits for the whole device first.
+static int quiesce_for_growth(fs_ctx *c, int64_t nr, int64_t arena_need) {
+    const bool g = arena_need > c->arena.cap || nr > c->roff.cap || nr > c->rlen.cap || nr > c->rclient.cap ||
+                   nr > c->rlabel.cap || nr > c->rstate.cap || nr > c->rhint.cap || nr > c->h_owner.cap;
+    if (g) CK(cudaDeviceSynchronize());
     return FS_OK;
 }
 
@@ -228,26 +243,26 @@ static int append_request_meta(fs_ctx *c, int64_t n, const int64_t *place, const
                                const int32_t *clients, const int64_t *labels, int32_t *out_ids) {
     const int64_t base_id = (int64_t)c->h_roff.size();
     const int64_t nr = base_id + n;
-    TRY(dgrow(c->roff, nr, c->stream, true, base_id));
-    TRY(dgrow(c->rlen, nr, c->stream, true, base_id));
-    TRY(dgrow(c->rclient, nr, c->stream, true, base_id));
-    TRY(dgrow(c->rlabel, nr, c->stream, true, base_id));
+    TRY(dgrow(c->roff, nr, c->ustream, true, base_id));
+    TRY(dgrow(c->rlen, nr, c->ustream, true, base_id));
+    TRY(dgrow(c->rclient, nr, c->ustream, true, base_id));
+    TRY(dgrow(c->rlabel, nr, c->ustream, true, base_id));
     if (c->rstate.cap < nr) {
         const int64_t old = c->rstate.cap;
-        TRY(dgrow(c->rstate, nr, c->stream, true, base_id));
-        CK(cudaMemsetAsync(c->rstate.p + old, 0, c->rstate.cap - old, c->stream));
+        TRY(dgrow(c->rstate, nr, c->ustream, true, base_id));
+        CK(cudaMemsetAsync(c->rstate.p + old, 0, c->rstate.cap - old, c->ustream));
     }
     if (c->rhint.cap < nr) {
         const int64_t old = c->rhint.cap;
-        TRY(dgrow(c->rhint, nr, c->stream, true, old));
-        CK(cudaMemsetAsync(c->rhint.p + old, 0, sizeof(int32_t) * (c->rhint.cap - old), c->stream));
+        TRY(dgrow(c->rhint, nr, c->ustream, true, old));
+        CK(cudaMemsetAsync(c->rhint.p + old, 0, sizeof(int32_t) * (c->rhint.cap - old), c->ustream));
     }
     if (c->h_owner.cap < nr) {
         const int64_t old = c->h_owner.cap;
-        TRY(dgrow(c->h_owner, nr, c->stream, true, old));
-        TRY(dgrow(c->h_tok0, c->h_owner.cap, c->stream, true, old));
-        TRY(dgrow(c->h_S0, c->h_owner.cap, c->stream, true, old));
-        CK(cudaMemsetAsync(c->h_owner.p + old, 0xff, sizeof(int32_t) * (c->h_owner.cap - old), c->stream));
+        TRY(dgrow(c->h_owner, nr, c->ustream, true, old));
+        TRY(dgrow(c->h_tok0, c->h_owner.cap, c->ustream, true, old));
+        TRY(dgrow(c->h_S0, c->h_owner.cap, c->ustream, true, old));
+        CK(cudaMemsetAsync(c->h_owner.p + old, 0xff, sizeof(int32_t) * (c->h_owner.cap - old), c->ustream));
     }
     for (int64_t i = 0; i < n; i++) {
         c->h_roff.push_back(place[i]);
@@ -257,12 +272,12 @@ static int append_request_meta(fs_ctx *c, int64_t n, const int64_t *place, const
         c->max_len = std::max(c->max_len, lens[i]);
         if (out_ids) out_ids[i] = (int32_t)(base_id + i);
     }
-    CK(cudaStreamSynchronize(c->stream));  // staging buffer reuse
-    CK(cudaMemcpyAsync(c->roff.p + base_id, c->h_roff.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->rlen.p + base_id, c->h_rlen.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->rclient.p + base_id, c->h_rclient.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->rlabel.p + base_id, c->h_rlabel.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->ustream));  // staging buffer reuse
+    CK(cudaMemcpyAsync(c->roff.p + base_id, c->h_roff.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->ustream));
+    CK(cudaMemcpyAsync(c->rlen.p + base_id, c->h_rlen.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->ustream));
+    CK(cudaMemcpyAsync(c->rclient.p + base_id, c->h_rclient.data() + base_id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->ustream));
+    CK(cudaMemcpyAsync(c->rlabel.p + base_id, c->h_rlabel.data() + base_id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->ustream));
+    CK(cudaStreamSynchronize(c->ustream));
     return FS_OK;
 }
 
@@ -281,6 +296,7 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         place[i] = c->arena_used + total;
         total += (lens[i] + 3) & ~3LL;
     }
+    TRY(quiesce_for_growth(c, base_id + n, c->arena_used + total + 4));
     bool contiguous = n > 0;
     for (int64_t i = 0; i + 1 < n && contiguous; i++) contiguous = offsets[i + 1] == offsets[i] + lens[i];
     static const bool hprof = getenv("FS_HOST_PROFILE") != nullptr;
@@ -290,12 +306,12 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         // fs_host_register), then a scatter kernel into the 16-B aligned arena
         // rows that also checks the id range -- no host pass over the tokens
         const int64_t src_total = offsets[n - 1] + lens[n - 1] - offsets[0];
-        TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
+        TRY(dgrow(c->arena, c->arena_used + total + 4, c->ustream, true, c->arena_used));
         // staging for the caller's block: reserved in 16 MB steps so a stream of
         // growing arrival batches does not reallocate (and synchronize) per call
-        TRY(dgrow(c->x_tok, std::max<int64_t>(src_total + 4, std::min<int64_t>(c->arena.cap, 1 << 22)), c->stream));
-        TRY(dgrow(c->x_dst, n + 1, c->stream)); TRY(dgrow(c->x_nsoff, n + 1, c->stream));
-        TRY(dgrow(c->x_len, n + 1, c->stream)); TRY(dgrow(c->x_flag, 1, c->stream));
+        TRY(dgrow(c->x_tok, std::max<int64_t>(src_total + 4, std::min<int64_t>(c->arena.cap, 1 << 22)), c->ustream));
+        TRY(dgrow(c->x_dst, n + 1, c->ustream)); TRY(dgrow(c->x_nsoff, n + 1, c->ustream));
+        TRY(dgrow(c->x_len, n + 1, c->ustream)); TRY(dgrow(c->x_flag, 1, c->ustream));
         TRY(hgrow(c->stage64, 2 * n + 2)); TRY(hgrow(c->stage32, n + 2));
         for (int64_t i = 0; i < n; i++) {
             c->stage64.p[i] = place[i];
@@ -304,23 +320,23 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         }
         const auto ag = std::chrono::steady_clock::now();
         if (src_total) CK(cudaMemcpyAsync(c->x_tok.p, tokens + offsets[0], sizeof(int32_t) * src_total,
-                                          cudaMemcpyHostToDevice, c->stream));
+                                          cudaMemcpyHostToDevice, c->ustream));
         const auto ah = std::chrono::steady_clock::now();
-        CK(cudaMemcpyAsync(c->x_dst.p, c->stage64.p, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->x_nsoff.p, c->stage64.p + n, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->x_len.p, c->stage32.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemsetAsync(c->x_flag.p, 0, sizeof(int32_t), c->stream));
+        CK(cudaMemcpyAsync(c->x_dst.p, c->stage64.p, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->ustream));
+        CK(cudaMemcpyAsync(c->x_nsoff.p, c->stage64.p + n, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->ustream));
+        CK(cudaMemcpyAsync(c->x_len.p, c->stage32.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->ustream));
+        CK(cudaMemsetAsync(c->x_flag.p, 0, sizeof(int32_t), c->ustream));
         const auto ac = std::chrono::steady_clock::now();
-        if (hprof) CK(cudaStreamSynchronize(c->stream));
+        if (hprof) CK(cudaStreamSynchronize(c->ustream));
         const auto ad = std::chrono::steady_clock::now();
-        k_scatter_rows<<<(unsigned)n, 256, 0, c->stream>>>(c->x_tok.p, c->x_nsoff.p, c->x_dst.p, c->x_len.p,
+        k_scatter_rows<<<(unsigned)n, 256, 0, c->ustream>>>(c->x_tok.p, c->x_nsoff.p, c->x_dst.p, c->x_len.p,
                                                            c->arena.p, c->x_flag.p);
         counted();
         CK(cudaGetLastError());
         int32_t bad = 0;
-        CK(cudaMemcpyAsync(&bad, c->x_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&bad, c->x_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c->ustream));
         const auto aq = std::chrono::steady_clock::now();
-        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaStreamSynchronize(c->ustream));
         if (bad) return fail(FS_ERR_TOKEN_RANGE, "a token id is outside [0, 2^31)");  // nothing committed
         const auto a1 = std::chrono::steady_clock::now();
         TRY(append_request_meta(c, n, place.data(), lens, clients, labels, out_ids));
@@ -338,7 +354,7 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         for (int32_t k = 0; k < lens[i]; k++)
             if (tk[k] < 0) return fail(FS_ERR_TOKEN_RANGE, "token %d of request %lld is outside [0, 2^31)", tk[k], (long long)i);
     }
-    TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
+    TRY(dgrow(c->arena, c->arena_used + total + 4, c->ustream, true, c->arena_used));
     TRY(hgrow(c->stage_tok, total + 4));
     for (int64_t i = 0; i < n; i++) {
         int32_t *dst = c->stage_tok.p + (place[i] - c->arena_used);
@@ -346,7 +362,7 @@ extern "C" int fs_requests_add(fs_ctx *c, int64_t n, const int32_t *tokens, cons
         for (int32_t k = lens[i]; k < ((lens[i] + 3) & ~3); k++) dst[k] = 0;
     }
     if (total) CK(cudaMemcpyAsync(c->arena.p + c->arena_used, c->stage_tok.p, sizeof(int32_t) * total,
-                                  cudaMemcpyHostToDevice, c->stream));
+                                  cudaMemcpyHostToDevice, c->ustream));
     TRY(append_request_meta(c, n, place.data(), lens, clients, labels, out_ids));
     c->arena_used += total;
     return FS_OK;
@@ -386,29 +402,30 @@ extern "C" int fs_requests_add_expanded(fs_ctx *c, int64_t n, const int64_t *seg
         lens[i] = (int32_t)L;
         total += (L + 3) & ~3LL;
     }
-    TRY(dgrow(c->arena, c->arena_used + total + 4, c->stream, true, c->arena_used));
-    TRY(dgrow(c->x_dst, nseg + 1, c->stream)); TRY(dgrow(c->x_len, nseg + 1, c->stream));
-    TRY(dgrow(c->x_ns, nseg + 1, c->stream));
-    TRY(dgrow(c->x_nsoff, n_ns + 1, c->stream)); TRY(dgrow(c->x_nslen, n_ns + 1, c->stream));
-    TRY(dgrow(c->x_bytes, nbytes + 16, c->stream));
+    TRY(quiesce_for_growth(c, (int64_t)c->h_roff.size() + n, c->arena_used + total + 4));
+    TRY(dgrow(c->arena, c->arena_used + total + 4, c->ustream, true, c->arena_used));
+    TRY(dgrow(c->x_dst, nseg + 1, c->ustream)); TRY(dgrow(c->x_len, nseg + 1, c->ustream));
+    TRY(dgrow(c->x_ns, nseg + 1, c->ustream));
+    TRY(dgrow(c->x_nsoff, n_ns + 1, c->ustream)); TRY(dgrow(c->x_nslen, n_ns + 1, c->ustream));
+    TRY(dgrow(c->x_bytes, nbytes + 16, c->ustream));
     // pad tails of 16-B slots stay zero, like fs_requests_add
-    CK(cudaMemsetAsync(c->arena.p + c->arena_used, 0, sizeof(int32_t) * total, c->stream));
+    CK(cudaMemsetAsync(c->arena.p + c->arena_used, 0, sizeof(int32_t) * total, c->ustream));
     if (nseg) {
-        CK(cudaMemcpyAsync(c->x_dst.p, dst.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->x_len.p, seg_len, sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->x_ns.p, seg_ns, sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_dst.p, dst.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, c->ustream));
+        CK(cudaMemcpyAsync(c->x_len.p, seg_len, sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, c->ustream));
+        CK(cudaMemcpyAsync(c->x_ns.p, seg_ns, sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, c->ustream));
     }
     if (n_ns) {
-        CK(cudaMemcpyAsync(c->x_nsoff.p, ns_off, sizeof(int64_t) * n_ns, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->x_nslen.p, ns_len, sizeof(int32_t) * n_ns, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->x_nsoff.p, ns_off, sizeof(int64_t) * n_ns, cudaMemcpyHostToDevice, c->ustream));
+        CK(cudaMemcpyAsync(c->x_nslen.p, ns_len, sizeof(int32_t) * n_ns, cudaMemcpyHostToDevice, c->ustream));
     }
-    if (nbytes) CK(cudaMemcpyAsync(c->x_bytes.p, ns_bytes, nbytes, cudaMemcpyHostToDevice, c->stream));
+    if (nbytes) CK(cudaMemcpyAsync(c->x_bytes.p, ns_bytes, nbytes, cudaMemcpyHostToDevice, c->ustream));
     if (nseg) {
         ExpandArgs a;
         a.arena = c->arena.p; a.seg_dst = c->x_dst.p; a.seg_len = c->x_len.p; a.seg_ns = c->x_ns.p;
         a.ns_bytes = c->x_bytes.p; a.ns_off = c->x_nsoff.p; a.ns_len = c->x_nslen.p; a.nseg = nseg;
         const int64_t blocks = std::min<int64_t>((nseg + 7) / 8, 148LL * 16);
-        k_expand<<<(int)std::max<int64_t>(blocks, 1), 256, 0, c->stream>>>(a);
+        k_expand<<<(int)std::max<int64_t>(blocks, 1), 256, 0, c->ustream>>>(a);
         counted();
         CK(cudaGetLastError());
     }
@@ -472,6 +489,7 @@ extern "C" int fs_arena_read(fs_ctx *c, int64_t off, int64_t n, int32_t *out) {
 // ---------------------------------------------------------------- trie
 struct fs_trie {
     fs_ctx *ctx = nullptr;
+    bool busy = false;  // a worker fill on this tree is in flight (fs_worker_fill_begin)
     cudaStream_t stream = nullptr;  // own stream (dispatcher index) or null = the context's
     int64_t capacity = -1;
     int track = 0, nw = 0;
@@ -636,6 +654,7 @@ extern "C" int fs_trie_create(fs_ctx *c, int64_t capacity, int track_workers, in
 }
 
 extern "C" int fs_trie_destroy(fs_trie *t) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return FS_OK;
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(tstream(t));
@@ -654,6 +673,7 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
 }
 
 extern "C" int fs_trie_stats(fs_trie *t, int64_t *used, int64_t *pinned, int64_t *next_seq, int64_t *nodes) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     if (used) *used = t->h_sc.used;
     if (pinned) *pinned = t->h_sc.pinned;
@@ -668,6 +688,7 @@ struct fs_scratch_match {
 
 extern "C" int fs_trie_match(fs_trie *t, int64_t n, const int32_t *req_ids, int64_t now, int stamp,
                              int32_t *out_mlen, int32_t *out_cov) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     if (n == 0) return FS_OK;
     fs_ctx *c = t->ctx;
@@ -706,6 +727,7 @@ static int copy_records(fs_trie *t, int64_t nrec, fs_records *recs) {
 
 extern "C" int fs_trie_read_records(fs_trie *t, int64_t first, int64_t n, int64_t *src, int32_t *len,
                                     int32_t *keep) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || first < 0 || n < 0 || first + n > t->rsrc.cap) return fail(FS_ERR_INVALID, "record range");
     TRY(ctx_use(t->ctx));
     cudaStream_t s = t->ctx->stream;
@@ -745,6 +767,7 @@ static int check_req(fs_trie *t, int32_t req) {
 
 extern "C" int fs_trie_insert(fs_trie *t, int32_t req, int64_t now, int32_t worker, int32_t *new_len,
                               int32_t *path_node, fs_records *recs) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
     if (worker >= 0 && (!t->track || worker >= t->nw)) {
@@ -765,6 +788,7 @@ extern "C" int fs_trie_insert(fs_trie *t, int32_t req, int64_t now, int32_t work
 
 extern "C" int fs_trie_admit(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, int32_t *path_node,
                              fs_records *recs) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
     TRY(trie_reserve(t, 2, t->ctx->max_len));
@@ -780,6 +804,7 @@ extern "C" int fs_trie_admit(fs_trie *t, int32_t req, int64_t now, int32_t *mlen
 }
 
 static int pin_op(fs_trie *t, int32_t node, int op) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     TRY(ctx_use(t->ctx));
     if (node < 0) return FS_OK;  // empty path
@@ -797,6 +822,7 @@ extern "C" int fs_trie_pin(fs_trie *t, int32_t node) { return pin_op(t, node, OP
 extern "C" int fs_trie_unpin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_UNPIN); }
 
 extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     if (n == 0) return FS_OK;
     TRY(ctx_use(t->ctx));
@@ -829,6 +855,7 @@ extern "C" int fs_trie_last_ms(fs_trie *t, float *ms) {
 }
 
 extern "C" int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     TRY(ctx_use(t->ctx));
     OpArgs a{};
@@ -840,6 +867,7 @@ extern "C" int fs_trie_evict_lru(fs_trie *t, int64_t needed, fs_records *recs) {
 }
 
 extern "C" int fs_trie_longest_match_workers(fs_trie *t, int32_t req, int64_t now, int32_t *mlen, uint64_t *mask) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return fail(FS_ERR_INVALID, "NULL trie");
     TRY(ctx_use(t->ctx)); TRY(check_req(t, req));
     TRY(trie_reserve(t, 0, t->ctx->max_len));
@@ -854,6 +882,7 @@ extern "C" int fs_trie_longest_match_workers(fs_trie *t, int32_t req, int64_t no
 
 extern "C" int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_len, int32_t worker,
                                     int32_t keep_len, int64_t notice_time) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || !t->track) return fail(FS_ERR_INVALID, "evict_notify needs a track_workers trie");
     TRY(ctx_use(t->ctx));
     if (path_src < 0 || path_len < 0 || path_src + path_len > t->ctx->arena_used) return fail(FS_ERR_INVALID, "path range");
@@ -868,6 +897,7 @@ extern "C" int fs_trie_evict_notify(fs_trie *t, int64_t path_src, int32_t path_l
 
 extern "C" int fs_trie_evict_notify_many(fs_trie *t, int64_t n, const int64_t *path_src, const int32_t *path_len,
                                          const int32_t *worker, const int32_t *keep_len, const int64_t *notice_time) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || !t->track) return fail(FS_ERR_INVALID, "evict_notify needs a track_workers trie");
     if (n < 0) return fail(FS_ERR_INVALID, "bad count");
     if (n == 0) return FS_OK;
@@ -919,6 +949,7 @@ extern "C" int fs_trie_last_notify_profile(fs_trie *t, int64_t *prof4) {
 
 extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src, int32_t *start, int32_t *end,
                               int32_t *parent, int32_t *ref, int64_t *last_access, uint64_t *wmask) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || !n) return fail(FS_ERR_INVALID, "NULL argument");
     TRY(ctx_use(t->ctx));
     TRY(trie_pull(t));
@@ -960,6 +991,9 @@ extern "C" int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src,
 struct fs_worker {
     fs_ctx *ctx = nullptr;
     fs_trie *tree = nullptr;
+    bool inflight = false;           // between fs_worker_fill_begin and fs_worker_fill_end
+    int64_t f_n = 0, f_launches0 = 0;
+    std::chrono::steady_clock::time_point f_h0, f_h1, f_h2;
     int32_t wid = 0;                 // unique id (owner of K1 match hints)
     int64_t hint_version = -1;       // tree version at the end of the last fill
     bool hints_ok = false;           // last fill completed with a complete admission filter
@@ -1064,6 +1098,7 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
 }
 
 extern "C" int fs_worker_destroy(fs_worker *w) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return FS_OK;
     cudaSetDevice(w->ctx->device);
     cudaStreamSynchronize(w->ctx->stream);
@@ -1081,6 +1116,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
 }
 
 extern "C" int fs_worker_enqueue(fs_worker *w, int64_t n, const int32_t *ids) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     fs_ctx *c = w->ctx;
     for (int64_t i = 0; i < n; i++) {
@@ -1098,6 +1134,7 @@ extern "C" int fs_worker_enqueue(fs_worker *w, int64_t n, const int32_t *ids) {
 }
 
 extern "C" int fs_worker_outputs(fs_worker *w, int64_t n, const int32_t *clients, const int64_t *counts) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     for (int64_t i = 0; i < n; i++) {
         const int32_t cl = clients[i];
@@ -1121,6 +1158,7 @@ static int worker_flush_small(fs_worker *w) {
 }
 
 extern "C" int fs_worker_check_refill(fs_worker *w, int64_t n, const int32_t *queued, int *refilled) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return fail(FS_ERR_INVALID, "NULL worker");
     fs_ctx *c = w->ctx;
     TRY(ctx_use(c));
@@ -1150,6 +1188,7 @@ extern "C" int fs_worker_check_refill(fs_worker *w, int64_t n, const int32_t *qu
 }
 
 extern "C" int fs_worker_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills, uint8_t *known) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return fail(FS_ERR_INVALID, "NULL worker");
     const int32_t k = std::min(n, w->nclients);
     if (q) std::memcpy(q, w->h_q.data(), sizeof(int64_t) * k);
@@ -1159,6 +1198,7 @@ extern "C" int fs_worker_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *
 }
 
 extern "C" int fs_worker_set_counter(fs_worker *w, int32_t client, int64_t qv) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w || client < 0 || client >= w->nclients) return fail(FS_ERR_INVALID, "bad client");
     const int64_t d = qv - w->h_q[client];
     w->h_q[client] = qv;
@@ -1168,6 +1208,7 @@ extern "C" int fs_worker_set_counter(fs_worker *w, int32_t client, int64_t qv) {
 }
 
 extern "C" int fs_worker_reserve_clients(fs_worker *w, int32_t max_clients) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return fail(FS_ERR_INVALID, "NULL worker");
     if (max_clients <= w->nclients) return FS_OK;
     fs_ctx *c = w->ctx;
@@ -1188,6 +1229,7 @@ extern "C" int fs_worker_reserve_clients(fs_worker *w, int32_t max_clients) {
 }
 
 extern "C" int fs_worker_mark_known(fs_worker *w, int64_t n, const int32_t *clients) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return fail(FS_ERR_INVALID, "NULL worker");
     for (int64_t i = 0; i < n; i++) {
         if (clients[i] < 0 || clients[i] >= w->nclients) return fail(FS_ERR_INVALID, "client id out of range");
@@ -1197,6 +1239,7 @@ extern "C" int fs_worker_mark_known(fs_worker *w, int64_t n, const int32_t *clie
 }
 
 extern "C" int fs_worker_device_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return fail(FS_ERR_INVALID, "NULL worker");
     TRY(ctx_use(w->ctx));
     const int32_t k = std::min(n, w->nclients);
@@ -1207,12 +1250,14 @@ extern "C" int fs_worker_device_counters(fs_worker *w, int32_t n, int64_t *q, in
 }
 
 extern "C" int fs_worker_queue_len(fs_worker *w, int64_t *n) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w || !n) return fail(FS_ERR_INVALID, "NULL");
     *n = w->qn - w->admitted_last + (int64_t)w->pending_new.size();
     return FS_OK;
 }
 
 extern "C" int fs_worker_set_option(fs_worker *w, int option, int64_t value) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!w) return fail(FS_ERR_INVALID, "NULL worker");
     switch (option) {
         case 1: w->k1_full = value != 0; return FS_OK;  // FS_OPT_K1_FULL
@@ -1238,10 +1283,9 @@ static uint32_t key_bits(int32_t max_len) {
     return b;
 }
 
-extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom,
-                              fs_fill_result *res) {
-    if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
-    static const bool hprof = getenv("FS_HOST_PROFILE") != nullptr;
+extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom) {
+    if (!w) return fail(FS_ERR_INVALID, "NULL argument");
+    if (w->inflight) return fail(FS_ERR_INVALID, "a fill of this worker is already in flight");
     const auto h0 = std::chrono::steady_clock::now();
     fs_ctx *c = w->ctx;
     fs_trie *t = w->tree;
@@ -1431,11 +1475,32 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
     counted();
     CK(cudaGetLastError());
     CK(cudaEventRecord(w->ev[4], s));
-    const auto h2 = std::chrono::steady_clock::now();
     w->dl_client.clear(); w->dl_delta.clear();
-    // ---- results
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 24, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_hdr.p + 24, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    w->inflight = true;
+    t->busy = true;
+    w->f_n = n;
+    w->f_launches0 = launches0;
+    w->f_h0 = h0; w->f_h1 = h1; w->f_h2 = std::chrono::steady_clock::now();
+    return FS_OK;
+}
+
+// Wait for the fill started by fs_worker_fill_begin and read its results.
+extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
+    if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
+    if (!w->inflight) return fail(FS_ERR_INVALID, "no fill in flight");
+    static const bool hprof = getenv("FS_HOST_PROFILE") != nullptr;
+    w->inflight = false;
+    w->tree->busy = false;
+    fs_ctx *c = w->ctx;
+    fs_trie *t = w->tree;
+    cudaStream_t s = c->stream;
+    TRY(ctx_use(c));
+    const int64_t n = w->f_n, launches0 = w->f_launches0;
+    const auto h1 = w->f_h1, h2 = w->f_h2;
+    const auto h0 = w->f_h0;
+    // ---- results
     CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
@@ -1483,6 +1548,13 @@ extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total
                 us(h0, h1), us(h1, h2), us(h2, h3), 1000.0 * total);
     }
     return FS_OK;
+}
+
+extern "C" int fs_worker_fill(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom,
+                              fs_fill_result *res) {
+    if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
+    TRY(fs_worker_fill_begin(w, now, generated_total, headroom));
+    return fs_worker_fill_end(w, res);
 }
 
 // ---------------------------------------------------------------- dispatcher

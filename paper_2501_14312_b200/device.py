@@ -379,6 +379,22 @@ class WorkerDev:
         return n.value
 
     def fill(self, now: int, generated_total: int, headroom: int) -> FillResult:
+        res = self._result_struct()
+        call("fs_worker_fill", self._h, now, generated_total, headroom, C.byref(res))
+        return self._result(res)
+
+    def fill_begin(self, now: int, generated_total: int, headroom: int) -> None:
+        """Launch a fill and return at once (fs_worker_fill_begin): context
+        uploads may run until fill_end; this worker and its tree are busy."""
+        self._res = self._result_struct()
+        call("fs_worker_fill_begin", self._h, now, generated_total, headroom)
+
+    def fill_end(self) -> FillResult:
+        res, self._res = self._res, None
+        call("fs_worker_fill_end", self._h, C.byref(res))
+        return self._result(res)
+
+    def _result_struct(self):
         qlen = self.queue_len()
         if qlen + 1 > self._cap:
             self._alloc(max(qlen + 1, 2 * self._cap))
@@ -388,7 +404,9 @@ class WorkerDev:
         res.adm_pinned_before = _p64(self._pinb); res.adm_path_node = _p32(self._node)
         res.adm_rec_end = _p64(self._rend)
         res.recs = L.FsRecords(self._rcap, _p64(self._rsrc), _p32(self._rlen), _p32(self._rkeep), 0)
-        call("fs_worker_fill", self._h, now, generated_total, headroom, C.byref(res))
+        return res
+
+    def _result(self, res) -> FillResult:
         nr = res.recs.n_rec
         if nr <= self._rcap:
             recs = Records(self._rsrc[:nr].copy(), self._rlen[:nr].copy(), self._rkeep[:nr].copy())
