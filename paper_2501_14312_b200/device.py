@@ -386,11 +386,14 @@ class WorkerDev:
     def fill_begin(self, now: int, generated_total: int, headroom: int) -> None:
         """Launch a fill and return at once (fs_worker_fill_begin): context
         uploads may run until fill_end; this worker and its tree are busy."""
-        self._res = self._result_struct()
+        res = self._result_struct()
         call("fs_worker_fill_begin", self._h, now, generated_total, headroom)
+        self._res = res
 
     def fill_end(self) -> FillResult:
-        res, self._res = self._res, None
+        res, self._res = getattr(self, "_res", None), None
+        if res is None:
+            res = self._result_struct()  # nothing in flight: the call below reports it
         call("fs_worker_fill_end", self._h, C.byref(res))
         return self._result(res)
 
