@@ -816,6 +816,11 @@ struct ChunkLRU {
     int64_t prof[4];  // pop cycles: argmin, edit, chunk update
 };
 
+#ifndef FS_POP_PREFETCH
+#define FS_POP_PREFETCH 1
+#endif
+__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ bool lru_candidate(const TrieView &t, int32_t n) {
     return (t.flags[n] & FS_ALIVE) && t.nchild[n] == 0 && t.ref[n] == 0;
 }
@@ -828,6 +833,34 @@ __device__ __forceinline__ void warp_key_min(int64_t &bla, int64_t &bsq, int32_t
         const int64_t os = __shfl_xor_sync(FS_FULL, bsq, off);
         const int32_t on = __shfl_xor_sync(FS_FULL, bn, off);
         if (on >= 0 && (bn < 0 || oa < bla || (oa == bla && os < bsq))) { bla = oa; bsq = os; bn = on; }
+    }
+}
+
+// Warm this SM's L1 with what the next LRU pop will read: the current index
+// minimum b (node fields), the nodes of b's chunk (the rescan), b's parent and
+// the child-hash slot of (parent, first token) -- a hint only (every value is
+// re-read by the pop; stores of this CTA keep L1 coherent).  One warp.
+__device__ inline void warp_prefetch_pop(const TrieView &t, const ChunkLRU *L, int lane) {
+    const int32_t ngroups = (L->nch + 31) / 32;
+    int64_t bla = INT64_MAX, bsq = INT64_MAX;
+    int32_t bn = -1;
+    if (lane < ngroups) { bla = L->gla[lane]; bsq = L->gsq[lane]; bn = L->gnd[lane]; }
+    warp_key_min(bla, bsq, bn);
+    const int32_t b = bn;
+    if (b <= 0) return;
+    const int32_t lo = (b / L->ch) * L->ch, hi = min(lo + L->ch, L->hw0);
+    for (int32_t n = lo + lane; n < hi; n += 32) {
+        pf_l1(t.flags + n); pf_l1(t.nchild + n); pf_l1(t.ref + n); pf_l1(t.la + n); pf_l1(t.seq + n);
+    }
+    if (lane == 0) {
+        pf_l1(t.start + b); pf_l1(t.end + b); pf_l1(t.src + b); pf_l1(t.lseq + b);
+        const int32_t P = t.parent[b];
+        const int32_t f = t.first[b];
+        if (P >= 0) {
+            pf_l1(t.nchild + P); pf_l1(t.ref + P); pf_l1(t.flags + P);
+            pf_l1(t.la + P); pf_l1(t.lseq + P); pf_l1(t.seq + P);
+            pf_l1(t.hslot + (fs_hmix(fs_hkey(P, f)) & t.hmask));
+        }
     }
 }
 
@@ -1074,6 +1107,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             }
         }
     }
+#if FS_POP_PREFETCH
+    else if (warp == 2 && sm->lru) {
+        // idle until the pin: warm L1 for this insert's first LRU pop while warp 0 walks
+        warp_prefetch_pop(t, sm->lru, lane);
+    }
+#endif
     __syncthreads();
     if (sm->split_top >= 0)
         block_repoint(t, t.src[sm->split_top], t.start[sm->split_top], t.end[sm->split_top], sm->split_top);
