@@ -944,6 +944,21 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             const int32_t m0 = a.s_mlen0[rr];
             const int32_t y = t.pos[S0 + m0 - 1];
             if (pos_valid(t, y, S0, m0 - 1)) ns = warp_path_segments(t, y, m0, sm->pseg, lane, FS_PRE_SEGS);
+#if FS_POP_PREFETCH
+            if (ns > 0) {
+                // warm L1 for that walk: the segments' end nodes' refs (the
+                // coverage check) and the child slot of its next token
+                if (lane < ns) {
+                    const Seg g = sm->pseg[lane];
+                    pf_l1(t.ref + t.pos[g.S + g.a]);
+                    pf_l1(t.ref + t.pos[g.S + g.b - 1]);
+                }
+                if (lane == 0 && m0 == t.end[y]) {
+                    const int32_t tok = a.s_tok0[rr];  // K1's token at m0 (-1: fully matched)
+                    if (tok >= 0) pf_l1(t.hslot + (fs_hmix(fs_hkey(y, tok)) & t.hmask));
+                }
+            }
+#endif
         }
         if (lane == 0) { sm->pseg_j = ns >= 0 ? rr : -1; sm->pseg_n = ns; }
     };
