@@ -661,7 +661,7 @@ def main():
                                    "pop_argmin_cyc": sched[8] / args.steps, "pop_edit_cyc": sched[9] / args.steps,
                                    "pop_update_cyc": sched[10] / args.steps, "setup_cyc": sched[11] / args.steps,
                                    "grid_sweeps": sched[15] / args.steps, "grid_sweep_cyc": sched[14] / args.steps,
-                                   "window_cyc": sched[13] / args.steps, "leaf_repoint_cyc": sched[12] / args.steps,
+                                   "side_cyc": sched[12] / args.steps, "leaf_cyc": sched[13] / args.steps,
                                    "total_cyc": sched[7] / args.steps},
         "clocks": clocks, "host_wall_s": t_total,
     }

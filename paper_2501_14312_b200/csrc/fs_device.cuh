@@ -1111,6 +1111,13 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     else if (warp == 2 && sm->lru) {
         // idle until the pin: warm L1 for this insert's first LRU pop while warp 0 walks
         warp_prefetch_pop(t, sm->lru, lane);
+    } else if (warp == 3 && sm->lru && lane == 0) {
+        // ... and for the new leaf: the node slot it will likely take, the
+        // scalars, its first token (the walk's hint depth)
+        pf_l1(t.sc);
+        const int32_t nf = t.sc->nfree;
+        if (nf > 0) pf_l1(t.freest + nf - 1);
+        if (hint_m0 >= 0 && hint_m0 < len) pf_l1(rq + hint_m0);
     }
 #endif
     __syncthreads();
@@ -1147,6 +1154,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             sm->deepest = deepest;
         }
         __syncthreads();  // the split top's positions and the leaf are visible
+        if (tid == 0 && sm->prof) sm->prof[13] += clock64() - c1;
         if (warp > 1) {
             // pin the pre-existing path, then point the new leaf's depths at it
             block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);

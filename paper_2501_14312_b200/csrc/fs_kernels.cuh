@@ -930,6 +930,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
         // warp 1: the next search's first window (no tree reads; stale
         // coverages are reported, not re-walked)
         if (!pre_ok) return;
+        const long long cs = clock64();
         const int32_t from = j + 1, wend = min(a.n, from + FS_FAST);
         const int32_t rr = from < wend ? warp_find_window(a, sm, from, wend, false, pre_slack, lane) : FS_NONE;
         if (lane == 0) { sm->pre_j = rr; sm->pre_end = wend; }
@@ -960,7 +961,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             }
 #endif
         }
-        if (lane == 0) { sm->pseg_j = ns >= 0 ? rr : -1; sm->pseg_n = ns; }
+        if (lane == 0) { sm->pseg_j = ns >= 0 ? rr : -1; sm->pseg_n = ns; sm->prof[12] += clock64() - cs; }
     };
     const bool have_pseg = sm->pseg_j == j;
     block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j], true,
