@@ -147,7 +147,7 @@ __device__ inline void h_del(const TrieView &t, int32_t p, int32_t tok) {
 // ---------------------------------------------------------------- nodes
 // RadixNode(...) with seq = self._seq; self._seq += 1  (radix.py:117-118, 153-154)
 __device__ inline int32_t node_new(const TrieView &t, int64_t src, int32_t start, int32_t end, int32_t slen,
-                                   int32_t parent) {
+                                   int32_t parent, int32_t first_tok = -1) {
     int32_t n;
     if (t.sc->nfree > 0) n = t.freest[--t.sc->nfree];
     else if (t.sc->hw < t.ncap) n = t.sc->hw++;
@@ -156,7 +156,7 @@ __device__ inline int32_t node_new(const TrieView &t, int64_t src, int32_t start
     t.ctop[n] = start; t.cpar[n] = parent;  // a new leaf starts its own chain
     t.nchild[n] = 0; t.ref[n] = 0; t.la[n] = 0; t.lseq[n] = 0;
     t.seq[n] = t.sc->next_seq++;
-    t.first[n] = t.arena[src + start];
+    t.first[n] = first_tok >= 0 ? first_tok : t.arena[src + start];
     t.flags[n] = FS_ALIVE;
     if (t.wmask) t.wmask[n] = 0;
     t.sc->live++;
@@ -386,13 +386,15 @@ struct WalkStart {
 
 template <int U = 4, typename SegFn, bool PIPE = false>
 __device__ inline WalkOut warp_walk_from(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
-                                         bool want_cov, WalkStart st, SegFn on_seg) {
+                                         bool want_cov, WalkStart st, SegFn on_seg, int32_t tok_first = -1) {
+    // tok_first >= 0: the request's token at st.idx, known to the caller (K1's
+    // miss token) -- saves the first hop's request read
     WalkOut o;
     o.mlen = 0; o.last = st.last; o.plen = 0; o.nseg = st.nseg; o.cov = st.cov; o.unpinned = 0;
     int32_t node = st.node, idx = st.idx;
     bool pinrun = want_cov && st.pinrun;
     while (idx < len) {
-        const int32_t c = h_find(t, node, rq[idx]);
+        const int32_t c = h_find(t, node, (idx == st.idx && tok_first >= 0) ? tok_first : rq[idx]);
         if (c < 0) break;
         const int64_t S = t.src[c];
         const int32_t bound = min(len, t.slen[c]);
@@ -484,7 +486,7 @@ __device__ inline int32_t warp_cov_from_deepest(const TrieView &t, int32_t y, in
 template <int U = 8, bool COV = true, bool SEGS = true>
 __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__restrict__ rq, int32_t len, int lane,
                                          Seg *segs, int64_t S0, int32_t m0, const Seg *pre = nullptr,
-                                         int32_t pre_n = -1) {
+                                         int32_t pre_n = -1, int32_t tok_m0 = -1) {
     // pre / pre_n (optional, pre_n <= 32): the segments of [0, m0) recorded by
     // a batch-start walk of this same path (k_dispatch_prematch)
     int32_t y = -1;
@@ -549,7 +551,7 @@ __device__ inline WalkOut warp_walk_hint(const TrieView &t, const int32_t *__res
         return o;
     }
     st.node = y; st.idx = m0; st.last = y;
-    return warp_walk_from<U>(t, rq, len, lane, COV, st, store);
+    return warp_walk_from<U>(t, rq, len, lane, COV, st, store, tok_m0);
 }
 
 // warp_walk_cb storing the segments (lane 0) when segs != nullptr.
@@ -1070,7 +1072,8 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                                     int32_t worker, Seg *segs, InsertSmem *sm, int64_t hint_S0 = -1,
                                     int32_t hint_m0 = -1, bool pin_path = false, OnWalk on_walk = OnWalk(),
                                     OnSide on_side = OnSide(), const WalkOut *pre = nullptr,
-                                    const Seg *pre_segs = nullptr, int32_t pre_nseg = -1) {
+                                    const Seg *pre_segs = nullptr, int32_t pre_nseg = -1, int32_t hint_tok0 = -1) {
+    // hint_tok0 (optional): the request's token at hint_m0 (-1: unknown / none)
     // pre (warp 0, optional): the caller's own walk of this path with segments
     // written to segs, against the current tree (the dispatch chain's
     // longest_match_workers walk) -- reused instead of walking again
@@ -1081,9 +1084,9 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         // the routing index (worker tags) has no pins: no coverage to compute
         const WalkOut w = pre ? *pre
                         : hint_m0 >= 0 ? (t.wmask ? warp_walk_hint<8, false, true>(t, rq, len, lane, segs, hint_S0, hint_m0,
-                                                                                   pre_segs, pre_nseg)
+                                                                                   pre_segs, pre_nseg, hint_tok0)
                                                   : warp_walk_hint<8, true, true>(t, rq, len, lane, segs, hint_S0, hint_m0,
-                                                                                  pre_segs, pre_nseg))
+                                                                                  pre_segs, pre_nseg, hint_tok0))
                                        : warp_walk<8>(t, rq, len, lane, segs, t.wmask == nullptr);
         if (lane == 0) {
             int32_t last = w.last >= 0 ? w.last : 0;
@@ -1134,11 +1137,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         if (tid == 0) {
             int32_t deepest = sm->mlen > 0 ? sm->last : -1;
             if (sm->status == FS_OK && sm->new_len > 0) {
-                const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last);
+                const int32_t tk = (sm->mlen == hint_m0 && hint_tok0 >= 0) ? hint_tok0 : rq[sm->mlen];
+                const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last, tk);
                 if (leaf < 0) {
                     sm->status = FS_ERR_NOMEM;
                 } else {
-                    h_put(t, sm->last, rq[sm->mlen], leaf);
+                    h_put(t, sm->last, tk, leaf);
                     t.nchild[sm->last]++;
                     t.ref[leaf] = 1;
                     t.sc->used += sm->new_len;

@@ -965,7 +965,8 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     };
     const bool have_pseg = sm->pseg_j == j;
     block_insert(t, off, len, a.now, a.sq_base + sm->epoch, -1, a.segs, &sm->ins, a.s_src0[j], a.s_mlen0[j], true,
-                 on_walk, on_side, nullptr, have_pseg ? sm->pseg : nullptr, have_pseg ? sm->pseg_n : -1);
+                 on_walk, on_side, nullptr, have_pseg ? sm->pseg : nullptr, have_pseg ? sm->pseg_n : -1,
+                 a.s_tok0[j]);
     if (tid == 0) {
         const InsertSmem &in = sm->ins;
         if (in.status != FS_OK) {
