@@ -31,7 +31,13 @@
 #endif
 #define FS_CHUNK (FS_SCHED_THREADS * FS_ITEMS)
 #define FS_NONE 0x7fffffff
-#define FS_FSLOTS 8192  // admission filter slots (shared memory + global mirror)
+#ifndef FS_FSLOTS
+// admission filter slots (shared memory + global mirror): saturates at 1024
+// admissions per fill (two keys each, half load), after which stale
+// coverages are re-walked.  Kept small: the rest of the SM's 256 KB is L1
+// for the admission chain (FS_SCHED_CARVEOUT).
+#define FS_FSLOTS 4096
+#endif
 #define FS_MKEY_SLOTS FS_FSLOTS
 
 // ---------------------------------------------------------------- K1

@@ -1442,6 +1442,17 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     static bool smem_set = false;
     if (!smem_set) {
         CK(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchedSmem)));
+        // the smallest shared-memory carveout that holds SchedSmem: the rest
+        // of the SM's 256 KB stays L1, where the admission chain's node,
+        // chunk and hash-slot prefetches land (FS_SCHED_CARVEOUT: percent)
+        {
+            static const int cv = [] { const char *e = getenv("FS_SCHED_CARVEOUT"); return e ? atoi(e) : -2; }();
+            int maxsm = 0;
+            CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+            const int pct = cv >= -1 ? cv
+                          : std::min(100, (int)((100LL * ((int64_t)sizeof(SchedSmem) + 8192) + maxsm - 1) / maxsm));
+            CK(cudaFuncSetAttribute(k_schedule, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        }
         smem_set = true;
     }
     if (w->nhelp < 0) {
