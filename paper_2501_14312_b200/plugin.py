@@ -28,8 +28,13 @@ _BINDINGS = (
 )
 
 
-def install() -> None:
-    """Route fairsched's DLPM / LPM / D2LPM / RadixTree through the GPU."""
+_WORKER_SAVED = {}
+
+
+def install(host_fast_path: bool = True) -> None:
+    """Route fairsched's DLPM / LPM / D2LPM / RadixTree through the GPU.
+    host_fast_path: also give workers running these policies the host
+    bookkeeping fast path (paper_2501_14312_b200.hostpath)."""
     from ._lib import load
 
     load()  # fail loudly now if the CUDA extension is missing
@@ -39,12 +44,19 @@ def install() -> None:
         if key not in _SAVED:
             _SAVED[key] = getattr(mod, attr)
         setattr(mod, attr, obj)
+    if host_fast_path and not _WORKER_SAVED:
+        from . import hostpath
+        _WORKER_SAVED.update(hostpath.install(importlib.import_module("fairsched.worker").Worker))
 
 
 def uninstall() -> None:
     for (mod_name, attr), obj in list(_SAVED.items()):
         setattr(importlib.import_module(mod_name), attr, obj)
     _SAVED.clear()
+    if _WORKER_SAVED:
+        from . import hostpath
+        hostpath.uninstall(importlib.import_module("fairsched.worker").Worker, dict(_WORKER_SAVED))
+        _WORKER_SAVED.clear()
 
 
 def installed() -> bool:

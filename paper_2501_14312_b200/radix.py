@@ -153,6 +153,13 @@ class DeviceRadixTree:
         m, cov = self._t.match([self._rid(tokens)], 0, stamp=False)
         return int(m[0]), int(m[0] - cov[0])
 
+    def probe_many(self, token_seqs):
+        """probe() of many sequences in one device call (no stamps, no side
+        effects): (mlen, matched-unpinned) as int64 arrays."""
+        m, cov = self._t.match([self._rid(t) for t in token_seqs], 0, stamp=False)
+        m = m.astype(np.int64)
+        return m, m - cov.astype(np.int64)
+
     def longest_match_workers(self, tokens, now=0):
         m, mask = self._t.longest_match_workers(self._rid(tokens), now)
         ws = {w for w in range(64) if mask >> w & 1}

@@ -43,3 +43,21 @@ def test_event_hash_matches_reference(idx, fs):
         got = {k: len(v) for k, v in result.violations.items()}
         assert got == run["violations"]
         assert {k: list(v) for k, v in result.counter_extremes.items()} == run["extremes"]
+
+
+@pytest.mark.parametrize("idx", range(min(len(SERVING), 6)), ids=[r["name"] for r in SERVING[:6]])
+def test_event_hash_with_batched_probes(idx, fs, monkeypatch):
+    """The host fast path (hostpath.py) on every monitor check: the batched
+    can_add of has_admissible_waiting even for 1-request queues."""
+    from fairsched.requests import Trace, TraceRecord
+    from fairsched.runner import config_from_dict, run_experiment
+    from paper_2501_14312_b200 import hostpath
+
+    monkeypatch.setattr(hostpath, "_BATCH_PROBE_MIN", 1)
+    run = SERVING[idx]
+    cfg = config_from_dict(run["config"])
+    result = run_experiment(cfg, Trace([TraceRecord(**r) for r in run["trace"]]))
+    # (a worker that never received a request keeps its empty list)
+    assert any(isinstance(w.queue, hostpath.FastQueue) for w in result.workers)
+    assert all(isinstance(w.queue, hostpath.FastQueue) or not w.queue for w in result.workers)
+    assert result.log.sha256() == run["event_sha256"]
