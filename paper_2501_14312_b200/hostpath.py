@@ -14,7 +14,10 @@ one of this package's GPU policies:
   kept as is);
 * `has_admissible_waiting` evaluates `Worker.can_add` (worker.py:100-109) for
   the whole queue from ONE batched device probe (fs_trie_match without
-  stamps), in numpy.
+  stamps), in numpy;
+* `Trace.materialize` (requests.py:134-161, run once per experiment by
+  runner.py:247) takes its tokens from the device SHA-256 expander (k_expand,
+  SURVEY §8f.2) instead of hashlib in Python.
 
 Each is the reference computation restated exactly (same results, same side
 effects -- probe has none); every other worker keeps the reference methods.
@@ -132,18 +135,64 @@ def make_has_admissible_waiting(orig):
     return has_admissible_waiting
 
 
+def host_tokens(records):
+    """Every record's input tokens (Trace.materialize's recipe,
+    requests.py:134-161, same errors) generated on the device by k_expand
+    (SHA-256 per 8-token block, requests.py:89-102) and read back as tuples."""
+    from .device import Context
+    from .trace import add_segments, resolve
+    segs, rids, clients, arrivals, out_lens = resolve(records)
+    lens = segs.lens().astype(np.int64)
+    n = len(rids)
+    if n == 0:
+        return [], rids, out_lens
+    rows = (lens + 3) & ~3  # 16-B aligned rows, back to back (fs_requests_add_expanded)
+    total = int(rows.sum())
+    ctx = Context(int(__import__("os").environ.get("FS_B200_DEVICE", "0")), arena_tokens=total + 1024,
+                  max_requests=n + 16)
+    try:
+        ids = add_segments(ctx, segs, np.zeros(n, np.int32), np.zeros(n, np.int64))
+        base, _ = ctx.request_info(int(ids[0]))
+        flat = ctx.arena_read(base, total) if total else np.zeros(0, np.int32)
+        last, _ = ctx.request_info(int(ids[-1]))
+        offs = np.zeros(n, np.int64)
+        offs[1:] = np.cumsum(rows[:-1])
+        if last - base != offs[-1]:
+            raise RuntimeError("unexpected arena placement of materialized requests")
+    finally:
+        ctx.close()
+    vals = flat.tolist()
+    toks = [tuple(vals[o:o + l]) for o, l in zip(offs.tolist(), lens.tolist())]
+    return toks, rids, out_lens
+
+
+def make_materialize(orig):
+    def materialize(self):
+        # Trace.materialize (requests.py:134-161) with the tokens from the device
+        from fairsched.requests import Request
+        toks, rids, out_lens = host_tokens(self.records)
+        requests = [Request(rid=rec.rid, client=rec.client, input_tokens=tk, arrival=rec.arrival_time,
+                            parent=rec.parent_id) for rec, tk in zip(self.records, toks)]
+        return requests, out_lens
+    materialize.__wrapped__ = orig
+    return materialize
+
+
 _PATCHES = (("enqueue", make_enqueue), ("has_admissible_waiting", make_has_admissible_waiting))
 
 
-def install(worker_cls) -> dict:
+def install(worker_cls, trace_cls=None) -> dict:
     saved = {}
     for name, make in _PATCHES:
         orig = getattr(worker_cls, name)
-        saved[name] = orig
+        saved[(worker_cls, name)] = orig
         setattr(worker_cls, name, make(orig))
+    if trace_cls is not None:
+        saved[(trace_cls, "materialize")] = trace_cls.materialize
+        trace_cls.materialize = make_materialize(trace_cls.materialize)
     return saved
 
 
-def uninstall(worker_cls, saved: dict) -> None:
-    for name, orig in saved.items():
-        setattr(worker_cls, name, orig)
+def uninstall(saved: dict) -> None:
+    for (cls, name), orig in saved.items():
+        setattr(cls, name, orig)

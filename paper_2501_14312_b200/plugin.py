@@ -46,7 +46,8 @@ def install(host_fast_path: bool = True) -> None:
         setattr(mod, attr, obj)
     if host_fast_path and not _WORKER_SAVED:
         from . import hostpath
-        _WORKER_SAVED.update(hostpath.install(importlib.import_module("fairsched.worker").Worker))
+        _WORKER_SAVED.update(hostpath.install(importlib.import_module("fairsched.worker").Worker,
+                                              importlib.import_module("fairsched.requests").Trace))
 
 
 def uninstall() -> None:
@@ -55,7 +56,7 @@ def uninstall() -> None:
     _SAVED.clear()
     if _WORKER_SAVED:
         from . import hostpath
-        hostpath.uninstall(importlib.import_module("fairsched.worker").Worker, dict(_WORKER_SAVED))
+        hostpath.uninstall(dict(_WORKER_SAVED))
         _WORKER_SAVED.clear()
 
 
