@@ -228,8 +228,8 @@ class GpuSteps:
         if n_prev:
             cl, cnt = np.unique(self.prev_clients, return_counts=True)
             self.w.outputs(cl.astype(np.int32), (cnt * self.wl.out_tokens).astype(np.int64))
-            self.trie.unpin_many(self.prev_nodes)
-            self.unpin_ms += self.trie.last_ms()
+            # stream-ordered before the fill; status and device time come back with it
+            self.trie.unpin_many_async(self.prev_nodes)
             self.h2d += cl.nbytes + cnt.nbytes + self.prev_nodes.nbytes
         if n_prev and self.pool_next + n_prev <= len(self.pool):
             a, b = self.pool_next, self.pool_next + n_prev
@@ -242,6 +242,8 @@ class GpuSteps:
         self.w.fill_begin(now, 0, 0)
         self._upload(min(len(self.pool), self.pool_next + max(64, 2 * n_prev)))
         res = self.w.fill_end()
+        if n_prev:
+            self.unpin_ms += self.trie.last_ms()
         self.prev_nodes = res.adm_node.astype(np.int32)
         self.prev_clients = self.clients[np.asarray(res.adm_req, np.int64)]
         self.d2h += res.adm_req.nbytes * 6 + 8 * 128 * 2 + 64

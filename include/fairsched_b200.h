@@ -131,6 +131,10 @@ int fs_trie_pin(fs_trie *t, int32_t path_node);   /* radix.py:174-178 */
 int fs_trie_unpin(fs_trie *t, int32_t path_node); /* radix.py:180-185 */
 /* unpin of a whole finishing batch in one launch (worker.py:209-213), in order */
 int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *path_nodes);
+/* fs_trie_unpin_many without waiting: the unpins are stream-ordered before the
+ * next fill of this tree; their status (FS_ERR_UNDERFLOW) and device time are
+ * reported by the next fs_worker_fill_end / fs_trie_last_ms / fs_trie_unpin_many. */
+int fs_trie_unpin_many_async(fs_trie *t, int64_t n, const int32_t *nodes);
 /* device time (CUDA events) of the last fs_trie_unpin_many */
 int fs_trie_last_ms(fs_trie *t, float *ms);
 /* RadixTree.evict_lru without a protect set (radix.py:210-250) */

@@ -79,6 +79,7 @@ SIGNATURES = {
     "fs_trie_pin": (C.c_int, [vp, i32]),
     "fs_trie_unpin": (C.c_int, [vp, i32]),
     "fs_trie_unpin_many": (C.c_int, [vp, i64, P32]),
+    "fs_trie_unpin_many_async": (C.c_int, [vp, i64, P32]),
     "fs_trie_last_ms": (C.c_int, [vp, PF]),
     "fs_trie_evict_lru": (C.c_int, [vp, i64, PREC]),
     "fs_trie_longest_match_workers": (C.c_int, [vp, i32, i64, P32, PU64]),

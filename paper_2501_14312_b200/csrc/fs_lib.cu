@@ -516,6 +516,14 @@ struct fs_trie {
     HBuf<int64_t> h_out;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     float last_ms = 0.f;  // device time of the last unpin_many
+    // fs_trie_unpin_many_async: status and timing read at the next fill_end /
+    // last_ms / unpin_many; the node list is staged in page-locked memory
+    bool unpin_pending = false;
+    HBuf<int32_t> h_unpin;
+    HBuf<int64_t> h_ustat;
+    DBuf<int64_t> ustat;
+    DBuf<int32_t> dunpin;
+    cudaEvent_t ev_staged = nullptr;
 };
 
 // Every entry point synchronizes its stream before returning, so calls made
@@ -665,6 +673,8 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
     t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
+    t->h_unpin.release(); t->h_ustat.release(); t->ustat.release(); t->dunpin.release();
+    if (t->ev_staged) cudaEventDestroy(t->ev_staged);
     if (t->ev[0]) { cudaEventDestroy(t->ev[0]); cudaEventDestroy(t->ev[1]); }
     t->nt_src.release(); t->nt_when.release(); t->nt_len.release(); t->nt_worker.release(); t->nt_keep.release();
     t->nt_s0.release(); t->nt_m0.release();
@@ -821,9 +831,12 @@ static int pin_op(fs_trie *t, int32_t node, int op) {
 extern "C" int fs_trie_pin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_PIN); }
 extern "C" int fs_trie_unpin(fs_trie *t, int32_t node) { return pin_op(t, node, OP_UNPIN); }
 
+static int unpin_settle(fs_trie *t);
+
 extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
     if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    TRY(unpin_settle(t));
     if (n == 0) return FS_OK;
     TRY(ctx_use(t->ctx));
     for (int64_t i = 0; i < n; i++)
@@ -848,8 +861,50 @@ extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
     return FS_OK;
 }
 
+// Settle an fs_trie_unpin_many_async: wait for it, take its device time and
+// report its status (FS_ERR_UNDERFLOW like fs_trie_unpin_many).
+static int unpin_settle(fs_trie *t) {
+    if (!t->unpin_pending) return FS_OK;
+    t->unpin_pending = false;
+    CK(cudaEventSynchronize(t->ev[1]));
+    CK(cudaStreamSynchronize(t->ctx->stream));  // the status read-back follows the kernel
+    CK(cudaEventElapsedTime(&t->last_ms, t->ev[0], t->ev[1]));
+    if (t->h_ustat.p[0] == FS_ERR_UNDERFLOW) return fail(FS_ERR_UNDERFLOW, "unpin below zero (radix.py:183)");
+    if (t->h_ustat.p[0] != FS_OK) return fail((int)t->h_ustat.p[0], "unpin_many failed");
+    return FS_OK;
+}
+
+extern "C" int fs_trie_unpin_many_async(fs_trie *t, int64_t n, const int32_t *nodes) {
+    if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
+    if (!t || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
+    TRY(unpin_settle(t));
+    if (n == 0) return FS_OK;
+    TRY(ctx_use(t->ctx));
+    for (int64_t i = 0; i < n; i++)
+        if (nodes[i] >= t->h_sc.hw) return fail(FS_ERR_INVALID, "bad path handle %d", nodes[i]);
+    cudaStream_t s = t->ctx->stream;
+    if (!t->ev[0]) { CK(cudaEventCreate(&t->ev[0])); CK(cudaEventCreate(&t->ev[1])); }
+    if (!t->ev_staged) CK(cudaEventCreateWithFlags(&t->ev_staged, cudaEventDisableTiming));
+    CK(cudaEventSynchronize(t->ev_staged));  // the staging buffer's last copy has left
+    TRY(hgrow(t->h_unpin, n)); TRY(hgrow(t->h_ustat, 1));
+    TRY(dgrow(t->dunpin, n, s)); TRY(dgrow(t->ustat, 1, s));
+    std::memcpy(t->h_unpin.p, nodes, sizeof(int32_t) * n);
+    CK(cudaMemcpyAsync(t->dunpin.p, t->h_unpin.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(t->ev_staged, s));
+    CK(cudaMemsetAsync(t->ustat.p, 0, sizeof(int64_t), s));
+    CK(cudaEventRecord(t->ev[0], s));
+    k_unpin_many<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(view(t), t->dunpin.p, n, t->ustat.p);
+    counted();
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(t->ev[1], s));
+    CK(cudaMemcpyAsync(t->h_ustat.p, t->ustat.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    t->unpin_pending = true;
+    return FS_OK;
+}
+
 extern "C" int fs_trie_last_ms(fs_trie *t, float *ms) {
     if (!t || !ms) return fail(FS_ERR_INVALID, "NULL argument");
+    TRY(unpin_settle(t));
     *ms = t->last_ms;
     return FS_OK;
 }
@@ -1516,6 +1571,7 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    TRY(unpin_settle(t));  // an fs_trie_unpin_many_async queued before this fill
     const int64_t nadm = w->h_hdr.p[0];
     const int64_t nrec = w->h_hdr.p[1];
     const int64_t status = w->h_hdr.p[2];

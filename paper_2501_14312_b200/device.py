@@ -204,6 +204,12 @@ class Trie:
         nodes = np.ascontiguousarray(nodes, dtype=np.int32)
         call("fs_trie_unpin_many", self._h, len(nodes), _p32(nodes))
 
+    def unpin_many_async(self, nodes):
+        """unpin_many without waiting (fs_trie_unpin_many_async): errors and the
+        device time surface at the next fill_end / last_ms / unpin_many."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.int32)
+        call("fs_trie_unpin_many_async", self._h, len(nodes), _p32(nodes))
+
     def evict_lru(self, needed: int) -> Records:
         recs, err = self._op("fs_trie_evict_lru", needed)
         return recs

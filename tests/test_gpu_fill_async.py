@@ -46,7 +46,7 @@ def test_split_fill_matches_fill_and_guards():
         now = 1000 * (k + 1)
         if prev1:
             t1.unpin_many(np.asarray(prev1, np.int32))
-            t2.unpin_many(np.asarray(prev2, np.int32))
+            t2.unpin_many_async(np.asarray(prev2, np.int32))  # settled by the fill below
         r1 = w1.fill(now, 0, 0)
         w2.fill_begin(now, 0, 0)
         # refused while the fill is in flight
@@ -75,3 +75,20 @@ def test_split_fill_matches_fill_and_guards():
         w.close()
         t.close()
         c.close()
+
+
+def test_async_unpin_reports_underflow():
+    from paper_2501_14312_b200._lib import FsError
+    c, t, w, d = _setup(5)
+    w.enqueue(_upload(c, d, 0, 60))
+    r = w.fill(1000, 0, 0)
+    nodes = r.adm_node.astype(np.int32)
+    assert len(nodes) > 0
+    t.unpin_many_async(nodes)
+    assert t.last_ms() >= 0.0  # settles: fine
+    t.unpin_many_async(nodes[:1])  # the same path again: below zero
+    with pytest.raises(FsError):
+        t.last_ms()
+    w.close()
+    t.close()
+    c.close()
