@@ -358,7 +358,7 @@ class GpuStreamRank:
     def complete(self, handles, clients, out_tokens):
         cl, cnt = np.unique(np.asarray(clients, np.int32), return_counts=True)
         self.w.outputs(cl.astype(np.int32), (cnt * out_tokens).astype(np.int64))
-        self.trie.unpin_many(np.asarray(handles, np.int32))
+        self.trie.unpin_many_async(np.asarray(handles, np.int32))  # settled by this round's fill
         self.h2d += cl.nbytes + cnt.nbytes + 4 * len(handles)
 
     def dispatcher_apply(self, fin, notices):
