@@ -14,8 +14,9 @@ def wrap(obj, name, key):
     def w(*a, **k):
         t0 = time.perf_counter(); r = f(*a, **k); T[key] = T.get(key, 0) + time.perf_counter() - t0; return r
     setattr(obj, name, w)
-wrap(g.w, "outputs", "outputs"); wrap(g.trie, "unpin_many", "unpin"); wrap(g.ctx, "add_requests", "add_requests")
-wrap(g.w, "enqueue", "enqueue"); wrap(g.w, "fill", "fill")
+wrap(g.w, "outputs", "outputs"); wrap(g.trie, "unpin_many_async", "unpin"); wrap(g.ctx, "add_requests", "add_requests")
+wrap(g.w, "enqueue", "enqueue"); wrap(g.w, "fill_begin", "fill_begin"); wrap(g.w, "fill_end", "fill_end")
+wrap(g.trie, "last_ms", "last_ms")
 t0 = time.perf_counter(); dev = 0
 for _ in range(20):
     now += bench.STEP_US; r = g.step(now); dev += r.device_ms
