@@ -1047,6 +1047,7 @@ struct fs_worker {
     fs_ctx *ctx = nullptr;
     fs_trie *tree = nullptr;
     bool inflight = false;           // between fs_worker_fill_begin and fs_worker_fill_end
+    HBuf<uint8_t> h_stage;           // page-locked staging of a fill's results
     int64_t f_n = 0, f_launches0 = 0;
     std::chrono::steady_clock::time_point f_h0, f_h1, f_h2;
     int32_t wid = 0;                 // unique id (owner of K1 match hints)
@@ -1157,7 +1158,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     if (!w) return FS_OK;
     cudaSetDevice(w->ctx->device);
     cudaStreamSynchronize(w->ctx->stream);
-    w->q.release(); w->refills.release(); w->known.release(); w->pend_cnt.release();
+    w->q.release(); w->refills.release(); w->known.release(); w->pend_cnt.release(); w->h_stage.release();
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
@@ -1553,6 +1554,9 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
 }
 
 // Wait for the fill started by fs_worker_fill_begin and read its results.
+#ifndef FS_RES_SPEC
+#define FS_RES_SPEC 2048  // admissions / eviction records staged with the first copy batch
+#endif
 extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
     if (!w->inflight) return fail(FS_ERR_INVALID, "no fill in flight");
@@ -1566,11 +1570,32 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     const int64_t n = w->f_n, launches0 = w->f_launches0;
     const auto h1 = w->f_h1, h2 = w->f_h2;
     const auto h0 = w->f_h0;
-    // ---- results
-    CK(cudaMemcpyAsync(&t->h_sc, t->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_q.data(), w->q.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_refills.data(), w->refills.p, sizeof(int64_t) * w->nclients, cudaMemcpyDeviceToHost, s));
+    // ---- results: one batch of DMA copies into page-locked staging (the
+    // scalars, the counters, and -- speculatively, up to FS_RES_SPEC rows --
+    // the admissions and eviction records), one wait, then host copies out
+    const int64_t K = std::min<int64_t>(w->adm_req.cap, FS_RES_SPEC);
+    const int64_t R = std::min<int64_t>(t->rsrc.cap, FS_RES_SPEC);
+    const int64_t nc = w->nclients;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 15) & ~(size_t)15; return o; };
+    const size_t o_sc = take(sizeof(TrieScalars)), o_q = take(8 * nc), o_rf = take(8 * nc);
+    const size_t o_ar = take(4 * K), o_am = take(4 * K), o_an = take(4 * K), o_au = take(8 * K), o_ap = take(8 * K),
+                 o_ae = take(8 * K), o_rs = take(8 * R), o_rl = take(4 * R), o_rk = take(4 * R);
+    TRY(hgrow(w->h_stage, (int64_t)off));
+    uint8_t *hs = w->h_stage.p;
+    auto d2h = [&](size_t o, const void *src, size_t bytes) -> int {
+        if (bytes) CK(cudaMemcpyAsync(hs + o, src, bytes, cudaMemcpyDeviceToHost, s));
+        return FS_OK;
+    };
+    TRY(d2h(o_sc, t->sc.p, sizeof(TrieScalars)));
+    TRY(d2h(o_q, w->q.p, 8 * nc)); TRY(d2h(o_rf, w->refills.p, 8 * nc));
+    TRY(d2h(o_ar, w->adm_req.p, 4 * K)); TRY(d2h(o_am, w->adm_mlen.p, 4 * K)); TRY(d2h(o_an, w->adm_node.p, 4 * K));
+    TRY(d2h(o_au, w->adm_unp.p, 8 * K)); TRY(d2h(o_ap, w->adm_pinb.p, 8 * K)); TRY(d2h(o_ae, w->adm_rec_end.p, 8 * K));
+    TRY(d2h(o_rs, t->rsrc.p, 8 * R)); TRY(d2h(o_rl, t->rlen.p, 4 * R)); TRY(d2h(o_rk, t->rkeep.p, 4 * R));
     CK(cudaStreamSynchronize(s));
+    std::memcpy(&t->h_sc, hs + o_sc, sizeof(TrieScalars));
+    std::memcpy(w->h_q.data(), hs + o_q, 8 * nc);
+    std::memcpy(w->h_refills.data(), hs + o_rf, 8 * nc);
     TRY(unpin_settle(t));  // an fs_trie_unpin_many_async queued before this fill
     const int64_t nadm = w->h_hdr.p[0];
     const int64_t nrec = w->h_hdr.p[1];
@@ -1598,7 +1623,16 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     w->hints_ok = status == FS_OK && w->h_hdr.p[6] == 0;
     if (status != FS_OK) return fail((int)status, "device fill failed (status %lld)", (long long)status);
     if (nadm > res->cap_adm) return fail(FS_ERR_INVALID, "admission buffer too small (%lld > %lld)", (long long)nadm, (long long)res->cap_adm);
-    if (nadm > 0) {
+    bool second = false;  // a second round of copies (more rows than staged)
+    if (nadm > 0 && nadm <= K) {
+        if (res->adm_req) std::memcpy(res->adm_req, hs + o_ar, sizeof(int32_t) * nadm);
+        if (res->adm_mlen) std::memcpy(res->adm_mlen, hs + o_am, sizeof(int32_t) * nadm);
+        if (res->adm_path_node) std::memcpy(res->adm_path_node, hs + o_an, sizeof(int32_t) * nadm);
+        if (res->adm_unpinned) std::memcpy(res->adm_unpinned, hs + o_au, sizeof(int64_t) * nadm);
+        if (res->adm_pinned_before) std::memcpy(res->adm_pinned_before, hs + o_ap, sizeof(int64_t) * nadm);
+        if (res->adm_rec_end) std::memcpy(res->adm_rec_end, hs + o_ae, sizeof(int64_t) * nadm);
+    } else if (nadm > 0) {
+        second = true;
         if (res->adm_req) CK(cudaMemcpyAsync(res->adm_req, w->adm_req.p, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, s));
         if (res->adm_mlen) CK(cudaMemcpyAsync(res->adm_mlen, w->adm_mlen.p, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, s));
         if (res->adm_path_node) CK(cudaMemcpyAsync(res->adm_path_node, w->adm_node.p, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, s));
@@ -1606,8 +1640,21 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
         if (res->adm_pinned_before) CK(cudaMemcpyAsync(res->adm_pinned_before, w->adm_pinb.p, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, s));
         if (res->adm_rec_end) CK(cudaMemcpyAsync(res->adm_rec_end, w->adm_rec_end.p, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, s));
     }
-    TRY(copy_records(t, nrec, &res->recs));
-    CK(cudaStreamSynchronize(s));
+    {
+        fs_records *recs = &res->recs;
+        const int64_t kr = std::min(nrec, recs->rec_cap);
+        if (nrec > t->rsrc.cap) return fail(FS_ERR_INTERNAL, "eviction record sink overflow (%lld)", (long long)nrec);
+        recs->n_rec = nrec;
+        if (kr > 0 && kr <= R) {
+            std::memcpy(recs->rec_src, hs + o_rs, sizeof(int64_t) * kr);
+            std::memcpy(recs->rec_len, hs + o_rl, sizeof(int32_t) * kr);
+            std::memcpy(recs->rec_keep, hs + o_rk, sizeof(int32_t) * kr);
+        } else if (kr > 0) {
+            second = true;
+            TRY(copy_records(t, nrec, recs));
+        }
+    }
+    if (second) CK(cudaStreamSynchronize(s));
     if (hprof) {
         const auto h3 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
