@@ -1688,6 +1688,7 @@ struct fs_dispatcher {
     DBuf<int64_t> nows, dlq, o_rounds, hdr, s0;
     DBuf<Seg> pre_segs;
     DBuf<int32_t> pre_nseg;
+    HBuf<uint8_t> h_stage;  // page-locked staging of a dispatch chain's results
     DBuf<uint64_t> o_mask;
 };
 
@@ -1732,7 +1733,7 @@ extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
     d->q.release(); d->qsize.release(); d->qset.release(); d->ids.release(); d->clients.release();
     d->dli.release(); d->dlw.release(); d->o_w.release(); d->o_mlen.release(); d->nows.release();
     d->dlq.release(); d->o_rounds.release(); d->hdr.release(); d->o_mask.release();
-    d->m0.release(); d->s0.release(); d->pre_segs.release(); d->pre_nseg.release();
+    d->m0.release(); d->s0.release(); d->pre_segs.release(); d->pre_nseg.release(); d->h_stage.release();
     delete d;
     return FS_OK;
 }
@@ -1798,15 +1799,25 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     counted();
     CK(cudaGetLastError());
     d->dl_idx.clear(); d->dl_w.clear(); d->dl_q.clear();
-    int64_t st = 0;
-    CK(cudaMemcpyAsync(&st, d->hdr.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out_worker, d->o_w.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
-    if (out_mlen) CK(cudaMemcpyAsync(out_mlen, d->o_mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
-    if (out_mask) CK(cudaMemcpyAsync(out_mask, d->o_mask.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
-    std::vector<int64_t> rounds(n);
-    CK(cudaMemcpyAsync(rounds.data(), d->o_rounds.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&d->tree->h_sc, d->tree->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
+    // results: one batch of DMA copies into page-locked staging, one wait
+    const size_t o_st = 0, o_w = 16, o_ml = o_w + ((4 * n + 15) & ~15), o_mk = o_ml + ((4 * n + 15) & ~15),
+                 o_rd = o_mk + 8 * n, o_sc = o_rd + 8 * n;
+    TRY(hgrow(d->h_stage, (int64_t)(o_sc + sizeof(TrieScalars))));
+    uint8_t *hs = d->h_stage.p;
+    CK(cudaMemcpyAsync(hs + o_st, d->hdr.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + o_w, d->o_w.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + o_ml, d->o_mlen.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + o_mk, d->o_mask.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + o_rd, d->o_rounds.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + o_sc, d->tree->sc.p, sizeof(TrieScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    int64_t st = 0;
+    std::memcpy(&st, hs + o_st, sizeof(int64_t));
+    std::memcpy(out_worker, hs + o_w, sizeof(int32_t) * n);
+    if (out_mlen) std::memcpy(out_mlen, hs + o_ml, sizeof(int32_t) * n);
+    if (out_mask) std::memcpy(out_mask, hs + o_mk, sizeof(uint64_t) * n);
+    const int64_t *rounds = (const int64_t *)(hs + o_rd);
+    std::memcpy(&d->tree->h_sc, hs + o_sc, sizeof(TrieScalars));
     if (st != FS_OK) return fail((int)st, "device dispatch failed (status %lld)", (long long)st);
     // mirror the counter updates (the monitor reads dispatcher.q each timestamp)
     for (int64_t i = 0; i < n; i++) {
