@@ -1262,9 +1262,27 @@ struct NotifySmem {
 // the exact match (warp_walk_hint validates it and re-walks otherwise).
 __device__ inline void block_evict_notify(const TrieView &t, int64_t psrc, int32_t plen, int32_t worker,
                                           int32_t keep, int64_t notice, Seg *segs, int32_t *found,
-                                          NotifySmem *sm, int64_t hint_S0 = -1, int32_t hint_m0 = -1) {
+                                          NotifySmem *sm, int64_t hint_S0 = -1, int32_t hint_m0 = -1,
+                                          int64_t next_S0 = -1, int32_t next_m0 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long q0 = clock64();
+#if FS_POP_PREFETCH
+    if (tid == 32 && next_m0 > 0) {
+        // warp 1 idles in the fast path: warm L1 for the next notice's deepest
+        // node, its parent and the child slot its prune will probe (hints only)
+        const int32_t y2 = t.pos[next_S0 + next_m0 - 1];
+        if (y2 > 0 && y2 < t.sc->hw) {
+            pf_l1(t.flags + y2); pf_l1(t.src + y2); pf_l1(t.start + y2); pf_l1(t.end + y2);
+            pf_l1(t.nchild + y2); pf_l1(t.ref + y2); pf_l1(t.wmask + y2);
+            if (worker >= 0 && worker < t.nw) pf_l1(t.wtime + (int64_t)y2 * t.nw + worker);
+            const int32_t P2 = t.parent[y2], f2 = t.first[y2];
+            if (P2 >= 0) {
+                pf_l1(t.nchild + P2); pf_l1(t.wmask + P2); pf_l1(t.ref + P2); pf_l1(t.la + P2); pf_l1(t.lseq + P2);
+                pf_l1(t.hslot + (fs_hmix(fs_hkey(P2, f2)) & t.hmask));
+            }
+        }
+    }
+#endif
     // Fast path (thread 0): the batch-start match still holds and cannot be
     // extended (it stops inside its deepest node, or covers the whole path), so
     // the walk's answer is known, and the nodes intersecting [keep, mlen) are

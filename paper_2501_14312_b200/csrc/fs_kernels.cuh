@@ -1207,7 +1207,8 @@ __global__ void __launch_bounds__(256) k_notify_many(TrieView t, int32_t n, cons
     }
     __syncthreads();
     for (int32_t i = 0; i < n; i++) {
-        block_evict_notify(t, src[i], len[i], worker[i], keep[i], when[i], segs, found, &nsm, s0[i], m0[i]);
+        block_evict_notify(t, src[i], len[i], worker[i], keep[i], when[i], segs, found, &nsm, s0[i], m0[i],
+                           i + 1 < n ? s0[i + 1] : -1, i + 1 < n ? m0[i + 1] : -1);
         __syncthreads();
         if (t.sc->status != FS_OK) break;
     }
