@@ -1357,6 +1357,23 @@ __global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a)
         const int32_t hm0 = s_m0[k];
         const long long cw = clock64();
         WalkOut w{};
+#if FS_POP_PREFETCH
+        if (tid == 32 && k + 1 < FS_DISP_STAGE && i + 1 < a.n && s_m0[k + 1] > 0) {
+            // warp 1 idles during this walk: warm L1 for the next arrival's
+            // hinted walk (deepest node, its token at the hint depth and the
+            // child slot that token probes) -- hints only
+            const int32_t m1 = s_m0[k + 1];
+            const int32_t y2 = t.pos[s_s0[k + 1] + m1 - 1];
+            if (y2 > 0 && y2 < t.sc->hw) {
+                pf_l1(t.flags + y2); pf_l1(t.src + y2); pf_l1(t.start + y2); pf_l1(t.end + y2);
+                pf_l1(t.wmask + y2); pf_l1(t.lseq + y2);
+                if (m1 < s_len[k + 1]) {
+                    const int32_t tk = t.arena[s_off[k + 1] + m1];
+                    pf_l1(t.hslot + (fs_hmix(fs_hkey(y2, tk)) & t.hmask));
+                }
+            }
+        }
+#endif
         if (warp == 0) {
             // RadixTree.longest_match_workers (radix.py:101-110).  The index only
             // gains prefixes of this batch's earlier arrivals (no capacity, no
