@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -513,6 +514,7 @@ struct fs_trie {
     DBuf<int64_t> nt_src, nt_when, nt_s0;  // fs_trie_evict_notify_many staging
     DBuf<int32_t> nt_len, nt_worker, nt_keep, nt_m0;
     TrieScalars h_sc{};
+    int nworkers = 0;  // DLPM/LPM workers scheduling on this tree (at most one)
     HBuf<int64_t> h_out;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     float last_ms = 0.f;  // device time of the last unpin_many
@@ -664,6 +666,7 @@ extern "C" int fs_trie_create(fs_ctx *c, int64_t capacity, int track_workers, in
 extern "C" int fs_trie_destroy(fs_trie *t) {
     if (t && t->busy) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
     if (!t) return FS_OK;
+    if (t->nworkers > 0) return fail(FS_ERR_INVALID, "destroy the tree's worker first");
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(tstream(t));
     t->src.release(); t->la.release(); t->seq.release(); t->start.release(); t->end.release();
@@ -1131,8 +1134,14 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     if (policy != 0 && policy != 1) return fail(FS_ERR_INVALID, "policy must be 0 (dlpm) or 1 (lpm)");
     if (policy == 0 && quantum <= 0) return fail(FS_ERR_INVALID, "quantum must be positive");  // local_policies.py:81-82
     if (max_clients <= 0) return fail(FS_ERR_INVALID, "max_clients must be positive");
+    // a Worker owns its cache (worker.py:72): a second scheduler on the same
+    // tree would not see the first one's admissions in its match hints and
+    // admission filter
+    if (tree->nworkers > 0) return fail(FS_ERR_INVALID, "the tree already has a worker (one worker per RadixTree)");
+    if (tree->track) return fail(FS_ERR_INVALID, "a worker needs a local tree (track_workers = 0)");
     TRY(ctx_use(c));
     fs_worker *w = new fs_worker();
+    tree->nworkers++;
     static std::atomic<int32_t> next_wid{0};
     w->wid = next_wid.fetch_add(1);
     w->ctx = c; w->tree = tree; w->policy = policy; w->quantum = quantum > 0 ? quantum : 1;
@@ -1158,6 +1167,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     if (!w) return FS_OK;
     cudaSetDevice(w->ctx->device);
     cudaStreamSynchronize(w->ctx->stream);
+    w->tree->nworkers--;
     w->q.release(); w->refills.release(); w->known.release(); w->pend_cnt.release(); w->h_stage.release();
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
@@ -1422,7 +1432,8 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     CK(cudaEventRecord(w->ev[1], s));
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
     if (n > 0) {
-        static int k1_blocks = 0;
+        static int k1_blocks_dev[64] = {0};
+        int &k1_blocks = k1_blocks_dev[c->device & 63];
         if (!k1_blocks) {
             int nsm = 0, per = 0;
             CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
@@ -1495,8 +1506,12 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     a.adm_cap = (int32_t)w->adm_req.cap;
     a.rstate = c->rstate.p;
     a.hdr = w->hdr.p;
-    static bool smem_set = false;
-    if (!smem_set) {
+    // function attributes are per device context: set once per device
+    static std::mutex attr_mu;
+    static bool smem_set[64] = {false};
+    std::lock_guard<std::mutex> attr_lock(attr_mu);
+    if (c->device < 0 || c->device >= 64) return fail(FS_ERR_INVALID, "device index %d", c->device);
+    if (!smem_set[c->device]) {
         CK(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchedSmem)));
         // the smallest shared-memory carveout that holds SchedSmem: the rest
         // of the SM's 256 KB stays L1, where the admission chain's node,
@@ -1509,7 +1524,7 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
                           : std::min(100, (int)((100LL * ((int64_t)sizeof(SchedSmem) + 8192) + maxsm - 1) / maxsm));
             CK(cudaFuncSetAttribute(k_schedule, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         }
-        smem_set = true;
+        smem_set[c->device] = true;
     }
     if (w->nhelp < 0) {
         // one co-resident helper CTA per SM but two (cooperative launch);
@@ -1753,6 +1768,8 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
                            int64_t *out_rounds) {
     if (!d || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     if (n == 0) return FS_OK;
+    if (!req_ids || !clients || !now || !out_worker)
+        return fail(FS_ERR_INVALID, "req_ids, clients, now and out_worker are required");
     fs_ctx *c = d->ctx;
     cudaStream_t s = d->tree->stream;
     TRY(ctx_use(c));

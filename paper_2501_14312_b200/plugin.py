@@ -44,6 +44,13 @@ def install(host_fast_path: bool = True) -> None:
         if key not in _SAVED:
             _SAVED[key] = getattr(mod, attr)
         setattr(mod, attr, obj)
+    # the reference's native-kernel seam reports which implementation runs the
+    # prefix compares (speedups.py:8-22): with the drop-in installed every walk
+    # is on the device, common_prefix_len itself is never called by the path
+    sp = importlib.import_module("fairsched.speedups")
+    if ("fairsched.speedups", "KERNEL_IMPL") not in _SAVED:
+        _SAVED[("fairsched.speedups", "KERNEL_IMPL")] = sp.KERNEL_IMPL
+    sp.KERNEL_IMPL = "cuda"
     if host_fast_path and not _WORKER_SAVED:
         from . import hostpath
         _WORKER_SAVED.update(hostpath.install(importlib.import_module("fairsched.worker").Worker,

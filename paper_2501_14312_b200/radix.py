@@ -137,7 +137,9 @@ class DeviceRadixTree:
         self._armed = None
 
     def _check_armed(self, tokens):
-        if self._rt.lookup(tokens) != self._armed_rid:
+        # the armed request's own row, or another row of the very same tuple
+        # (two requests may share one tuple object: runtime.DeviceRuntime.upload)
+        if self._rt.lookup(tokens) != self._armed_rid and self._rt.tokens_of(self._armed_rid) is not tokens:
             raise RuntimeError("device fill replay desynchronised: try_admit called for a different request")
 
     # -- traversal (radix.py:83-110) ---------------------------------------

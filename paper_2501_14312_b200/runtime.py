@@ -66,8 +66,11 @@ class OrderLabels:
 
 class DeviceRuntime:
     def __init__(self, device: int = 0):
+        self.device = device
         self.ctx = Context(device, arena_tokens=1 << 22, max_requests=1 << 16)
         self._by_tuple = {}      # id(tokens) -> (device id, tokens)  (strong ref keeps id stable)
+        self._by_key = {}        # (arrival, rid) -> device id: a request's own row
+        self._tok_of_id = {}     # device id -> token tuple it was uploaded from
         self._key_of_id = {}     # device id -> (arrival, rid) label key
         self._client_of = {}     # device id -> client id stored in the request table
         self.clients = {}        # client name -> dense id
@@ -90,11 +93,28 @@ class DeviceRuntime:
             return hit[0]
         return None
 
+    def tokens_of(self, did):
+        """The token tuple a device id was uploaded from (None if unknown)."""
+        return self._tok_of_id.get(did)
+
     def upload(self, tokens, client=None, arrival=None, rid=None) -> int:
         """Device id of a token sequence; uploads it on first sight.  When
-        (arrival, rid) are given the request gets its LPM tie-break label."""
-        did = self.lookup(tokens)
+        (arrival, rid) are given the request gets its own row and its LPM
+        tie-break label: requests are identified by (arrival, rid), not by
+        their token tuple -- Trace.materialize can hand two requests the same
+        tuple object (a ``req:`` child with an empty suffix gets
+        ``base[:len(base)] + ()``, which CPython returns as ``base`` itself,
+        requests.py:148-156), and each must keep its own queue entry."""
         key = (arrival, rid) if rid is not None else None
+        if key is not None:
+            did = self._by_key.get(key)
+            if did is not None:
+                if client is not None:
+                    self._set_client(did, client)
+                return did
+        did = self.lookup(tokens)
+        if did is not None and key is not None and did in self._key_of_id:
+            did = None  # the tuple belongs to another request: this one gets its own row
         if did is None:
             if not isinstance(tokens, tuple):
                 tokens = tuple(tokens)
@@ -104,16 +124,20 @@ class DeviceRuntime:
                 lab, relabeled = self.labels.add(key)
             cid = self.client_id(client) if client is not None else 0
             did = self.ctx.add_request(np.fromiter(tokens, dtype=np.int64, count=len(tokens)), cid, lab)
-            self._by_tuple[id(tokens)] = (did, tokens)
+            if self.lookup(tokens) is None:
+                self._by_tuple[id(tokens)] = (did, tokens)
+            self._tok_of_id[did] = tokens
             self._client_of[did] = cid
             if key is not None:
                 self._key_of_id[did] = key
+                self._by_key[key] = did
             if relabeled is not None:
                 self._push_labels()
             return did
-        if key is not None and did not in self._key_of_id:
+        if key is not None:
             lab, relabeled = self.labels.add(key)
             self._key_of_id[did] = key
+            self._by_key[key] = did
             if relabeled is not None:
                 self._push_labels()
             else:
