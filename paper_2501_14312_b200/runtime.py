@@ -108,12 +108,15 @@ class DeviceRuntime:
         key = (arrival, rid) if rid is not None else None
         if key is not None:
             did = self._by_key.get(key)
-            if did is not None:
+            # a key hit is the same request only if it carries the same token
+            # tuple: the runtime outlives one run_experiment, and a later run's
+            # request can reuse an earlier run's (arrival, rid)
+            if did is not None and self._tok_of_id.get(did) is tokens:
                 if client is not None:
                     self._set_client(did, client)
                 return did
         did = self.lookup(tokens)
-        if did is not None and key is not None and did in self._key_of_id:
+        if did is not None and key is not None and self._key_of_id.get(did, key) != key:
             did = None  # the tuple belongs to another request: this one gets its own row
         if did is None:
             if not isinstance(tokens, tuple):

@@ -47,3 +47,42 @@ def test_python_str_order_for_rids():
     for k in keys:
         lab.add(k)
     check(lab, keys)
+
+
+class _FakeCtx:
+    """Host stand-in for device.Context: enough for the request registry."""
+
+    def __init__(self, *a, **k):
+        self.rows = []
+
+    def add_request(self, toks, cid, lab):
+        self.rows.append((tuple(int(x) for x in toks), cid, lab))
+        return len(self.rows) - 1
+
+    def set_labels(self, ids, labs):
+        pass
+
+    def set_clients(self, ids, cids):
+        pass
+
+
+def test_request_registry_identity(monkeypatch):
+    """Requests are identified by (arrival, rid) AND their token tuple: a tuple
+    shared by two requests (a req: child with an empty suffix, requests.py:
+    148-156) gets two rows, a later run reusing an earlier run's (arrival, rid)
+    gets its own row, and a keyless upload (a routing index walking a tuple
+    first) is adopted by the request that owns the tuple."""
+    from paper_2501_14312_b200 import runtime
+    monkeypatch.setattr(runtime, "Context", _FakeCtx)
+    rt = runtime.DeviceRuntime(0)
+    base = tuple([1, 2, 3])
+    a = rt.upload(base, "c", 0, "r0")
+    b = rt.upload(base, "c", 0, "r0.child")
+    assert a != b and rt.upload(base, "c", 0, "r0") == a and rt.upload(base, "c", 0, "r0.child") == b
+    assert rt.tokens_of(a) is base and rt.tokens_of(b) is base
+    later = tuple([1, 2, 3])  # a new run, same (arrival, rid), new Request object
+    c = rt.upload(later, "c", 0, "r0")
+    assert c not in (a, b) and rt.upload(later, "c", 0, "r0") == c
+    t = (7, 8)
+    d = rt.upload(t)
+    assert rt.upload(t, "c", 5, "x") == d and rt.upload(t) == d
