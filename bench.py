@@ -353,7 +353,7 @@ def _concat_once(o, q, pool):
     return _CAT[key]
 
 
-def run_cluster(args, wl, rank, world, dev, tdev, dist):
+def run_cluster(args, wl, rank, world, dev, tdev, dist, clocks=True):
     """N>1: D2LPM across GPUs (paper_2501_14312_b200.cluster): one worker per
     rank, a dispatcher replica on every rank, one NCCL all-gather of finishes
     and eviction notices per round.  The workload's queue is dispatched once
@@ -380,7 +380,7 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
     be.ctx.sync()
     if dist is not None:
         dist.barrier()
-    clk = clocks_start() if rank == 0 else (None, None, None)
+    clk = clocks_start() if (rank == 0 and clocks) else (None, None, None)
     be.fill_ms = 0.0
     be.n_queued = be.n_dispatched = 0
     be.h2d = 0
@@ -395,7 +395,7 @@ def run_cluster(args, wl, rank, world, dev, tdev, dist):
     be.ctx.sync()
     wall = time.perf_counter() - t_start
     launches = launch_count() - l0
-    clocks = clocks_stop(*clk, dev) if rank == 0 else None
+    clocks = clocks_stop(*clk, dev) if (rank == 0 and clk[0] is not None) else None
     # the dispatcher side (apply + dispatch) overlaps the fill; a round's busy
     # time is completion + exchange + the longer of the two
     busy_s = cr.t_complete + cr.t_exchange + cr.t_overlap
@@ -466,6 +466,8 @@ def main():
     ap.add_argument("--cluster", action="store_true",
                     help="only the D2LPM cluster run (replicated dispatcher over NCCL), also at N=1")
     ap.add_argument("--no-d2lpm", action="store_true", help="N>1: skip the D2LPM cluster run")
+    ap.add_argument("--no-sub", action="store_true",
+                    help="N=1: skip the config-2 DLPM and config-3 D2LPM sub-results")
     ap.add_argument("--k1-full-steps", type=int, default=3,
                     help="untimed steps after the timed region with the full re-match (scan roofline)")
     ap.add_argument("--arrivals", type=int, default=128,
@@ -513,15 +515,23 @@ def main():
         q, pool, ncpu = wl.cpu_sample(dev)
         cb = cpu_baseline(wl, q, pool, warmup=args.warmup, steps_max=args.steps, budget_s=120.0)
         line = {"metric": METRIC, "value": cb["value"],
-                "unit": "decisions/s", "n_gpus": args.gpus, "steps": cb["steps"], "warmup": 0,
+                "unit": "decisions/s", "n_gpus": args.gpus, "steps": cb["steps"], "warmup": args.warmup,
                 "ms_per_step": 1000 * cb["fill_s"] / max(cb["steps"], 1), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32/int64", "data": "synthetic",
                 "config": cfg, "impl": "reference",
                 "cpu_baseline": {"value": cb["value"], "unit": "decisions/s", "cores": 1, "kind": "port",
                                  "sample": f"C oracle Dlpm.fill restatement, {cb['steps']} timed serving steps (after {args.warmup} "
                                            f"untimed) of the {ncpu}-request queue of the same config, one core"},
-                "e2e": {"value": cb["value"], "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "wall_s": time.perf_counter() - t0}
+                "e2e": {"value": cb["value"], "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import refbench
+        line["cpu_baseline"].update(refbench.host_info())
+        try:
+            # the reference's own Python decision path (unmodified, baseline/_ref)
+            line["cpu_baseline"]["reference_python"] = refbench.run()
+        except Exception as exc:
+            line["cpu_baseline"]["reference_python"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+        line["wall_s"] = time.perf_counter() - t0
         print(json.dumps(line))
         return
 
@@ -532,45 +542,12 @@ def main():
             print(json.dumps(line))
         return
     g = GpuSteps(wl, dev)
-    now = 0
-    for _ in range(args.warmup):
-        now += STEP_US
-        g.step(now)
-    g.ctx.sync()
-    if dist is not None:
-        import torch
-        dist.barrier()
-    clk = clocks_start() if rank == 0 else (None, None, None)
-    l0 = launch_count()
-    h2d0, d2h0 = g.h2d, g.d2h
-    dev_ms, wall, decisions, adm, alg_tok, k1_ms, phases = 0.0, 0.0, 0, 0, 0, [], np.zeros(5)
-    sched = np.zeros(16)
-    k1_hops = resumes = refills = 0
-    t_start = time.perf_counter()
-    for _ in range(args.steps):
-        now += STEP_US
-        t0 = time.perf_counter()
-        u0 = g.unpin_ms
-        res = g.step(now)
-        wall += time.perf_counter() - t0
-        dev_ms += res.device_ms + (g.unpin_ms - u0)  # the fill plus the completion unpins
-        decisions += res.n_queued
-        adm += len(res.adm_req)
-        alg_tok += res.stats[0]
-        k1_ms.append(res.phases_ms[1])
-        phases += np.array(list(res.phases_ms) + [g.unpin_ms - u0])
-        sched += np.array(res.stats[8:24], dtype=np.float64)
-        k1_hops += res.stats[6]
-        resumes += res.stats[4]
-        refills += res.stats[3]
-    g.ctx.sync()
-    t_total = time.perf_counter() - t_start
-    launches = launch_count() - l0
-    clocks = clocks_stop(*clk, dev) if rank == 0 else None
+    st = run_dlpm(g, args.steps, args.warmup, dist=dist, rank=rank, dev=dev)
+    now = st["now"]
     # ablation after the timed region: the same serving steps with every queued
     # request re-matched from the root (the full streaming scan the incremental
     # match avoids); identical decisions -- reported as the scan kernel's roofline
-    full_k1, full_tok = [], 0
+    full_k1, full_tok, full_n = [], 0, 0
     if args.k1_full_steps > 0:
         g.w.set_k1_full(True)
         for _ in range(args.k1_full_steps):
@@ -580,6 +557,7 @@ def main():
             full_tok += r.stats[0]
             full_n = r.n_queued
         g.w.set_k1_full(False)
+    dev_ms, wall, decisions = st["dev_ms"], st["wall"], st["decisions"]
     if dist is not None:
         import torch
         t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=tdev)
@@ -594,6 +572,7 @@ def main():
         # the same GPUs then run D2LPM across them (replicated dispatcher, NCCL
         # exchange) on ONE shared config-5 queue: a second, separately timed run
         g.close()
+        g = None
         wl2 = make_workload(args.workload, args.nq, 0, args.steps + args.warmup, device=dev, world=world)
         d2 = run_cluster(args, wl2, rank, world, dev, tdev, dist)
         del wl2
@@ -605,12 +584,16 @@ def main():
     e2e = total_decisions / wall
     peak, peak_kind = peaks()
     n_per_step = decisions / args.steps
-    k1_avg = float(np.mean(k1_ms))
+    k1_avg = float(np.mean(st["k1_ms"]))
     # incremental K1: request tokens actually needed beyond each request's still-
     # valid previous match, plus per-request metadata (queue entry, row offset and
     # length, hint in/out, outputs: 88 B)
-    alg_bytes = (alg_tok / args.steps) * 4 + 88 * n_per_step
+    alg_bytes = (st["alg_tok"] / args.steps) * 4 + 88 * n_per_step
     achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from k1_traffic import lookup as traffic_lookup
+    from paper_2501_14312_b200.build import source_hash
+    tr = traffic_lookup(args.workload, wl.nq)
     full_roof = None
     if full_k1:
         fk = float(np.mean(full_k1))
@@ -618,30 +601,30 @@ def main():
         full_roof = {"kernel": "k_match with FS_OPT_K1_FULL (every request re-matched from the root)",
                      "bound": "hbm", "achieved": fb / (fk / 1000.0) / 1e9, "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": fb / (fk / 1000.0) / 1e9 / peak, "alg_bytes_per_launch": fb,
-                     "avg_launch_ms": fk, "steps": len(full_k1), "traffic": None}
+                     "avg_launch_ms": fk, "steps": len(full_k1),
+                     "traffic": tr.get("full_scan_dram_bytes_per_launch") if tr else None}
+    phases = st["phases"]
     share = phases / phases.sum()
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_k_match_traffic%s.json" % ("" if args.workload == "c2" else "_c5"))
-    if os.path.exists(tp):
-        try:
-            tj = json.load(open(tp))
-            traffic = tj.get("dram_bytes_per_launch")
-            if full_roof is not None:
-                full_roof["traffic"] = tj.get("full_scan_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    sched = st["sched"]
+    steps = args.steps
     line = {
         "metric": METRIC,
-        "value": value, "unit": "decisions/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "value": value, "unit": "decisions/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32/int64", "data": "synthetic", "config": cfg,
         "e2e": {"value": e2e, "unit": "decisions/s",
-                "h2d_bytes_per_step": int((g.h2d - h2d0) / args.steps),
-                "d2h_bytes_per_step": int((g.d2h - d2h0) / args.steps)},
-        "gpu_launches": int(launches),
+                "h2d_bytes_per_step": int(st["h2d"] / steps),
+                "d2h_bytes_per_step": int(st["d2h"] / steps)},
+        "gpu_launches": int(st["launches"]),
+        "admissions_per_step": st["adm"] / steps, "queued_per_step": n_per_step,
+        "admissions_per_s": st["adm"] / (dev_ms / 1000.0),
         "roofline": {"kernel": "k_match (K1 incremental prefix match)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg,
+                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                     "traffic_source": (tr["source"] + f" (build {tr['source_hash']})") if tr else
+                     f"no ncu capture filed for build {source_hash()} / {args.workload} / nq={wl.nq} "
+                     "(tools/k1_traffic.py)",
+                     "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_avg,
                      "note": "resumes each request from its still-valid previous match; reads only the tokens "
                              "past it, so it is latency- not bandwidth-bound; see k1_full_match_roofline for the "
                              "streaming scan"},
@@ -650,36 +633,118 @@ def main():
                         "unpin": share[4]},
         "dominant_kernel": {"kernel": "k_schedule (K3/K4 admission chain, one CTA)", "share": share[3],
                             "bound": "latency (serial admission chain; see sched_profile_per_step)",
-                            "avg_launch_ms": phases[3] / args.steps},
-        "phase_ms_per_step": {"merge": phases[0] / args.steps, "k1_match": phases[1] / args.steps,
-                              "k2_sort": phases[2] / args.steps, "k3k4_schedule": phases[3] / args.steps,
-                              "unpin": phases[4] / args.steps},
-        "admissions_per_step": adm / args.steps, "queued_per_step": n_per_step,
-        "sched_profile_per_step": {"find_cyc": sched[0] / args.steps, "walk_cyc": sched[1] / args.steps,
-                                   "evict_cyc": sched[2] / args.steps, "tail_cyc": sched[3] / args.steps,
-                                   "chunks": sched[4] / args.steps, "evict_pops": sched[5] / args.steps,
-                                   "admit_chains": sched[6] / args.steps, "k1_chains": k1_hops / args.steps,
-                                   "resumes": resumes / args.steps, "refill_events": refills / args.steps,
-                                   "pop_argmin_cyc": sched[8] / args.steps, "pop_edit_cyc": sched[9] / args.steps,
-                                   "pop_update_cyc": sched[10] / args.steps, "setup_cyc": sched[11] / args.steps,
-                                   "grid_sweeps": sched[15] / args.steps, "grid_sweep_cyc": sched[14] / args.steps,
-                                   "side_cyc": sched[12] / args.steps, "leaf_cyc": sched[13] / args.steps,
-                                   "total_cyc": sched[7] / args.steps},
-        "clocks": clocks, "host_wall_s": t_total,
+                            "avg_launch_ms": phases[3] / steps},
+        "phase_ms_per_step": {"merge": phases[0] / steps, "k1_match": phases[1] / steps,
+                              "k2_sort": phases[2] / steps, "k3k4_schedule": phases[3] / steps,
+                              "unpin": phases[4] / steps},
+        "sched_profile_per_step": {"find_cyc": sched[0] / steps, "walk_cyc": sched[1] / steps,
+                                   "evict_cyc": sched[2] / steps, "tail_cyc": sched[3] / steps,
+                                   "chunks": sched[4] / steps, "evict_pops": sched[5] / steps,
+                                   "admit_chains": sched[6] / steps, "k1_chains": st["k1_hops"] / steps,
+                                   "resumes": st["resumes"] / steps, "refill_events": st["refills"] / steps,
+                                   "pop_argmin_cyc": sched[8] / steps, "pop_edit_cyc": sched[9] / steps,
+                                   "pop_update_cyc": sched[10] / steps, "setup_cyc": sched[11] / steps,
+                                   "grid_sweeps": sched[15] / steps, "grid_sweep_cyc": sched[14] / steps,
+                                   "side_cyc": sched[12] / steps, "leaf_cyc": sched[13] / steps,
+                                   "total_cyc": sched[7] / steps},
+        "clocks": st["clocks"], "host_wall_s": st["t_total"],
     }
     if d2 is not None:
         line["d2lpm_cluster"] = {k: d2[k] for k in ("value", "unit", "ms_per_step", "scaling", "e2e", "config",
                                                    "cluster_ms_per_step", "local_decisions_per_step",
                                                    "dispatches_per_step", "seed_dispatch",
                                                    "notice_cycles_per_notice", "gpu_launches")}
-    if not args.no_cpu and world == 1:
+    if g is not None:
         g.close()
+    if world == 1 and not args.no_sub:
+        # the other single-GPU configurations, each separately timed after the
+        # headline: configs[1] (64k queue, DLPM) and configs[2]'s D2LPM queue
+        # (256k, 200 clients) through the dispatcher + one worker
+        subs = {}
+        sub_steps, sub_warm = max(3, min(args.steps, 20)), max(3, min(args.warmup, 5))
+        wl2 = make_workload("c2", 0, 0, sub_steps + sub_warm, device=dev)
+        g2 = GpuSteps(wl2, dev)
+        s2 = run_dlpm(g2, sub_steps, sub_warm, dev=dev, clocks=False)
+        g2.close()
+        subs["config2_dlpm"] = {
+            "workload": wl2.desc, "value": s2["decisions"] / (s2["dev_ms"] / 1000.0), "unit": "decisions/s",
+            "steps": sub_steps, "warmup": sub_warm, "ms_per_step": s2["dev_ms"] / sub_steps,
+            "e2e": {"value": s2["decisions"] / s2["wall"], "unit": "decisions/s",
+                    "h2d_bytes_per_step": int(s2["h2d"] / sub_steps), "d2h_bytes_per_step": int(s2["d2h"] / sub_steps)},
+            "admissions_per_step": s2["adm"] / sub_steps, "admissions_per_s": s2["adm"] / (s2["dev_ms"] / 1000.0),
+            "k3k4_schedule_share": float(s2["phases"][3] / s2["phases"].sum()), "gpu_launches": int(s2["launches"]),
+            "l2": wl2.l2}
+        del wl2, g2
+        import types
+        wl3 = make_workload("c3", 0, 0, sub_steps + sub_warm, device=dev)
+        a3 = types.SimpleNamespace(steps=sub_steps, warmup=sub_warm, gpus=1, arrivals=args.arrivals)
+        d3 = run_cluster(a3, wl3, 0, 1, dev, tdev, None, clocks=False)
+        subs["config3_d2lpm"] = {k: d3[k] for k in ("value", "unit", "ms_per_step", "e2e", "config",
+                                                   "cluster_ms_per_step", "local_decisions_per_step",
+                                                   "dispatches_per_step", "dispatch_detail", "seed_dispatch",
+                                                   "notice_cycles_per_notice", "gpu_launches")}
+        subs["config3_d2lpm"]["steps"], subs["config3_d2lpm"]["warmup"] = sub_steps, sub_warm
+        del wl3
+        line["sub_results"] = subs
+    if not args.no_cpu and world == 1:
         q, pool, ncpu = wl.cpu_sample(dev)
         cb = cpu_baseline(wl, q, pool, warmup=args.warmup, steps_max=args.steps, budget_s=20.0)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import refbench
         line["cpu_baseline"] = {"value": cb["value"], "unit": "decisions/s", "cores": 1, "kind": "port",
+                                **refbench.host_info(),
                                 "sample": f"C oracle (literal Dlpm.fill restatement), {cb['steps']} timed serving steps "
                                           f"(after {args.warmup} untimed) of a {ncpu}-request queue of the same config, one host core"}
+        try:
+            line["cpu_baseline"]["reference_python"] = refbench.run(
+                normal_sizes=(4096, 16384), steady_sizes=(4096,), indebted_sizes=(1024, 2048, 4096),
+                dispatch_D=(1, 8), dispatch_n=4096)
+        except Exception as exc:  # the unmodified reference is optional on the GPU box
+            line["cpu_baseline"]["reference_python"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line))
+
+
+def run_dlpm(g, steps, warmup, dist=None, rank=0, dev=0, clocks=True):
+    """W untimed then K timed serving steps of a GpuSteps loop; per-step device
+    time (CUDA events inside the library: the fill + the completion unpins)
+    and host wall time of the public-API calls."""
+    from paper_2501_14312_b200.device import launch_count
+    now = 0
+    for _ in range(warmup):
+        now += STEP_US
+        g.step(now)
+    g.ctx.sync()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks_start() if (rank == 0 and clocks) else (None, None, None)
+    l0 = launch_count()
+    h2d0, d2h0 = g.h2d, g.d2h
+    st = {"dev_ms": 0.0, "wall": 0.0, "decisions": 0, "adm": 0, "alg_tok": 0, "k1_ms": [], "phases": np.zeros(5),
+          "sched": np.zeros(16), "k1_hops": 0, "resumes": 0, "refills": 0}
+    t_start = time.perf_counter()
+    for _ in range(steps):
+        now += STEP_US
+        t0 = time.perf_counter()
+        u0 = g.unpin_ms
+        res = g.step(now)
+        st["wall"] += time.perf_counter() - t0
+        st["dev_ms"] += res.device_ms + (g.unpin_ms - u0)  # the fill plus the completion unpins
+        st["decisions"] += res.n_queued
+        st["adm"] += len(res.adm_req)
+        st["alg_tok"] += res.stats[0]
+        st["k1_ms"].append(res.phases_ms[1])
+        st["phases"] += np.array(list(res.phases_ms) + [g.unpin_ms - u0])
+        st["sched"] += np.array(res.stats[8:24], dtype=np.float64)
+        st["k1_hops"] += res.stats[6]
+        st["resumes"] += res.stats[4]
+        st["refills"] += res.stats[3]
+    g.ctx.sync()
+    st["t_total"] = time.perf_counter() - t_start
+    st["launches"] = launch_count() - l0
+    st["clocks"] = clocks_stop(*clk, dev) if (rank == 0 and clocks) else None
+    st["h2d"], st["d2h"] = g.h2d - h2d0, g.d2h - d2h0
+    st["now"] = now
+    return st
 
 
 if __name__ == "__main__":

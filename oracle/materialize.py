@@ -61,10 +61,12 @@ def materialize(records) -> tuple:
     return order, out_lens
 
 
-def expand_segments(segs):
+def expand_segments(segs, out=None):
     """All requests of a paper_2501_14312_b200.trace.Segments, expanded by the C
     restatement (oracle/tokens.c, pthreads): returns (flat int32 tokens, offsets
-    int64[n+1]).  Same tokens as expand_tokens per segment."""
+    int64[n+1]).  Same tokens as expand_tokens per segment.  `out`: an int32
+    buffer to expand into (at least the total token count; lets a caller lay
+    several streams out back to back without a copy)."""
     import ctypes as C
     import os
     import subprocess
@@ -87,7 +89,9 @@ def expand_segments(segs):
     no = np.ascontiguousarray(segs.ns_off, np.int64)
     nl = np.ascontiguousarray(segs.ns_len, np.int32)
     total = int(sl.astype(np.int64).sum())
-    out = np.zeros(max(total, 1), np.int32)
+    if out is None:
+        out = np.zeros(max(total, 1), np.int32)
+    assert out.dtype == np.int32 and out.flags.c_contiguous and len(out) >= total
     offs = np.zeros(n + 1, np.int64)
     P = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
     fn(C.c_int64(n), P(sf, C.c_int64), P(sn, C.c_int32), P(sl, C.c_int32), P(nb, C.c_uint8), P(no, C.c_int64),

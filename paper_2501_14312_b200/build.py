@@ -22,6 +22,18 @@ NVCC_FLAGS = [
 ]
 
 
+def source_hash() -> str:
+    """sha256 over the CUDA sources, the public header and the nvcc flags: the
+    key under which ncu traffic captures of a build are filed (profiles/)."""
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in sorted(DEPS):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (os.path.sep not in cand or os.path.exists(cand)):

@@ -8,6 +8,8 @@
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from oracle.oracle import OracleD2lpm, OracleWorker
@@ -29,6 +31,24 @@ ROUNDS = 12
 STEP_US = 10_000
 
 
+@dataclass
+class Params:
+    """Serving parameters of one cluster run (per-worker M / capacity, the
+    resolved quanta -- runner.py:127, 131 -- and the client count)."""
+    M: int = M
+    CAP: int = CAP
+    RESERVE: int = RESERVE
+    W_E: int = W_E
+    W_Q: int = W_Q
+    Q_U: int = Q_U
+    Q_W: int = Q_W
+    n_clients: int = SPEC.clients
+    out_tokens: int = 8
+
+
+DEFAULT = Params()
+
+
 def workload():
     return shared_prefix_queue(SPEC, docs=build_docs(SPEC))
 
@@ -40,10 +60,11 @@ def stream(q):
 
 
 class _OracleWorkerSide:
-    def __init__(self, rank, q):
+    def __init__(self, rank, q, p=DEFAULT):
         self.rank = rank
         self.q = q
-        self.ow = OracleWorker(CAP, M, RESERVE, W_E, W_Q, "dlpm", Q_U, SPEC.clients)
+        self.ow = OracleWorker(p.CAP, p.M, p.RESERVE, p.W_E, p.W_Q, "dlpm", p.Q_U, p.n_clients)
+        self._by_first = {}  # first token -> admitted request indices (notice -> source request)
         self.pending = []
         self.admitted = []
 
@@ -59,7 +80,8 @@ class _OracleWorkerSide:
 
     def _src_of(self, path):
         n = len(path)
-        for i in reversed(self.admitted):
+        cand = self._by_first.get(int(path[0]), []) if n else self.admitted
+        for i in reversed(cand):
             t = self.q.tokens(i)
             if len(t) >= n and np.array_equal(t[:n], path):
                 return i
@@ -73,6 +95,10 @@ class _OracleWorkerSide:
         gone = set(adm)
         self.pending = [i for i in self.pending if i not in gone]
         self.admitted.extend(adm)
+        for i in adm:
+            t = q.tokens(i)
+            if len(t):
+                self._by_first.setdefault(int(t[0]), []).append(i)
         notices = np.zeros((len(r["records"]), NOTICE_COLS), np.int64)
         for k, (path, keep) in enumerate(r["records"]):
             notices[k] = (self._src_of(path), len(path), keep, self.rank, now)
@@ -82,9 +108,9 @@ class _OracleWorkerSide:
 class OracleRank(_OracleWorkerSide):
     """One rank: its worker and its own replica of the dispatcher."""
 
-    def __init__(self, rank, q, D):
-        super().__init__(rank, q)
-        self.od = OracleD2lpm(D, Q_W, W_E, W_Q, SPEC.clients)
+    def __init__(self, rank, q, D, p=DEFAULT):
+        super().__init__(rank, q, p)
+        self.od = OracleD2lpm(D, p.Q_W, p.W_E, p.W_Q, p.n_clients)
 
     def dispatch(self, arrivals, now):
         return np.array([self.od.dispatch(self.q.tokens(i), int(self.q.clients[i]), now)[0] for i in arrivals],
@@ -103,13 +129,14 @@ class OracleRank(_OracleWorkerSide):
 class SingleCluster:
     """All workers and one dispatcher in one process, same round structure."""
 
-    def __init__(self, q, D, pipelined=False):
+    def __init__(self, q, D, pipelined=False, p=DEFAULT):
         self.q = q
         self.D = D
+        self.p = p
         self.pipelined = pipelined
         self.late = [[] for _ in range(D)]
-        self.workers = [_OracleWorkerSide(r, q) for r in range(D)]
-        self.od = OracleD2lpm(D, Q_W, W_E, W_Q, SPEC.clients)
+        self.workers = [_OracleWorkerSide(r, q, p) for r in range(D)]
+        self.od = OracleD2lpm(D, p.Q_W, p.W_E, p.W_Q, p.n_clients)
         self.prev = [[] for _ in range(D)]
         self.notices = [np.zeros((0, NOTICE_COLS), np.int64) for _ in range(D)]
         self.next_arrival = 0
@@ -134,8 +161,8 @@ class SingleCluster:
         for r, wk in enumerate(self.workers):
             prev = self.prev[r]
             if prev:
-                wk.complete([h for _, _, h in prev], [c for _, c, _ in prev], 8)
-            fins.append([(c, r, 8) for _, c, _ in prev])
+                wk.complete([h for _, _, h in prev], [c for _, c, _ in prev], self.p.out_tokens)
+            fins.append([(c, r, self.p.out_tokens) for _, c, _ in prev])
         for r in range(self.D):
             for c, w, out in fins[r]:
                 self.od.on_finish(c, w, out)

@@ -2,7 +2,8 @@
 run on the device radix tree once the plugin is installed (run in the build
 container only):
 
-    python tests/golden/make_golden_policies.py
+    python tests/golden/make_golden_policies.py           # policies_runs.json.gz
+    python tests/golden/make_golden_policies.py config4   # config4_runs.json.gz
 
 * config-4 style comparison (SURVEY 8d cfg 4, scaled to seconds of CPU):
   one bursty trace (Gamma arrivals, cv=4), many clients, local policies
@@ -53,6 +54,44 @@ def config(seed, local, glob, D, clients, L_input=128, M=512, horizon=300, extra
     return d
 
 
+def config4_clients(n=1000, seed=4):
+    """SURVEY 8d cfg 4: C=1000 ClientProfiles, cv=4 (bursty Gamma arrivals),
+    rate ~ U[0.5, 2]/s, prefix 256-2048 tokens, suffix 64."""
+    rng = random.Random(seed)
+    return [dict(name=f"c{i:04d}", rate=rng.uniform(0.5, 2.0), cv=4.0, prefix_len=rng.randint(256, 2048),
+                 suffix_len=64, output_len=8, prefix_scope="client") for i in range(n)]
+
+
+def config4(local, horizon_ms=2000, n_clients=1000):
+    """D=1, L_input 4096, M 65536, q_u_frac 0.5, seed 4; the horizon is cut to
+    2 s (8,342 requests) so the CPU reference records each policy in minutes."""
+    return {"seed": 4, "horizon_ms": horizon_ms, "latency_window_ms": 500,
+            "params": {"L_input": 4096, "L_output": 64, "M": 65536, "D": 1},
+            "scheduling": {"local_policy": local, "global_policy": "rr", "q_u_frac": 0.5, "output_reserve": 8},
+            "clients": config4_clients(n_clients)}
+
+
+def main_config4():
+    """dlpm / vtc / lpm on the same 1000-client bursty trace (cli compare,
+    cli.py:62-89): event sha256, monitor violations, counter extremes."""
+    import time
+    runs = []
+    cfg0 = config_from_dict(config4("dlpm"))
+    trace = generate_trace(cfg0.clients, cfg0.params, cfg0.seed, ms(cfg0.horizon_ms))
+    recs = [json.loads(r.to_json()) for r in trace.records]
+    for local in ("dlpm", "vtc", "lpm"):
+        d = config4(local)
+        t0 = time.time()
+        res = run_experiment(config_from_dict(d), trace)
+        runs.append({"name": f"config4-{local}", "config": d, "event_sha256": res.log.sha256(),
+                     "violations": {k: len(v) for k, v in res.violations.items()},
+                     "extremes": {k: list(v) for k, v in res.counter_extremes.items()},
+                     "reference_seconds": time.time() - t0})
+        print(runs[-1]["name"], runs[-1]["event_sha256"][:16], runs[-1]["reference_seconds"], flush=True)
+    with gzip.open(os.path.join(HERE, "config4_runs.json.gz"), "wt") as fh:
+        json.dump({"trace": recs, "runs": runs}, fh, separators=(",", ":"))
+
+
 def main():
     runs = []
     rng = random.Random(4)
@@ -87,4 +126,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["config4"]:
+        main_config4()
+    else:
+        main()

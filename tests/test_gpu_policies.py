@@ -44,3 +44,27 @@ def test_policy_run_matches_reference(idx, fs):
     assert all(isinstance(w.tree, DeviceRadixTree) for w in result.workers)
     assert result.log.sha256() == run["event_sha256"]
     assert {k: len(v) for k, v in result.violations.items()} == run["violations"]
+
+
+_C4 = os.path.join(os.path.dirname(__file__), "golden", "config4_runs.json.gz")
+C4 = json.load(gzip.open(_C4)) if os.path.exists(_C4) else {"trace": [], "runs": []}
+
+
+@pytest.mark.parametrize("idx", range(len(C4["runs"])), ids=[r["name"] for r in C4["runs"]])
+def test_config4_1000_clients(idx, fs):
+    """Config 4 (BASELINE configs[3]) at its full client count: 1000 bursty
+    clients (cv=4), L_input 4096, M 65536, dlpm / vtc / lpm on the same
+    8,342-request trace (cli compare, cli.py:62-89) through the unchanged
+    runner with the device tree: event sha256, monitor violations and the
+    counter extremes recorded from the CPU reference."""
+    from fairsched.requests import Trace, TraceRecord
+    from fairsched.runner import config_from_dict, run_experiment
+    from paper_2501_14312_b200.radix import DeviceRadixTree
+
+    run = C4["runs"][idx]
+    cfg = config_from_dict(run["config"])
+    result = run_experiment(cfg, Trace([TraceRecord(**r) for r in C4["trace"]]))
+    assert all(isinstance(w.tree, DeviceRadixTree) for w in result.workers)
+    assert result.log.sha256() == run["event_sha256"]
+    assert {k: len(v) for k, v in result.violations.items()} == run["violations"]
+    assert {k: list(v) for k, v in result.counter_extremes.items()} == run["extremes"]

@@ -9,24 +9,35 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run_wl(wl, steps):
+def _run_wl(wl, steps, q_all=None, k1_full_steps=()):
+    """Lockstep of the bench's serving loop (bench.GpuSteps, through the C ABI)
+    and the oracle (oracle.lockstep.OracleSteps).  q_all: the whole stream
+    (queue then arrival pool) as one host Queue (default: the workload's CPU
+    sample, which must be the whole queue).  k1_full_steps: steps whose fill
+    re-matches every request from the root (FS_OPT_K1_FULL) instead of
+    resuming from the previous matches -- both modes must equal the oracle."""
     import bench
     from oracle.lockstep import OracleSteps
 
-    q, pool, n = wl.cpu_sample(0)
-    assert n == wl.nq
+    if q_all is None:
+        q, pool, n = wl.cpu_sample(0)
+        assert n == wl.nq
+        q_all = bench._concat_once(None, q, pool)
+    nq = wl.nq
+    pool_n = len(q_all) - nq
     g = bench.GpuSteps(wl, 0)
-    o = OracleSteps(bench._concat_once(None, q, pool), wl.CAP, wl.M, wl.reserve, bench.W_E, bench.W_Q,
+    o = OracleSteps(q_all, wl.CAP, wl.M, wl.reserve, bench.W_E, bench.W_Q,
                     wl.quantum(), max(128, wl.clients), out_tokens=wl.out_tokens)
-    o.enqueue(range(len(q)))
-    nq = len(q)
+    o.enqueue(range(nq))
     nc = max(128, wl.clients)
     nxt = 0
     total_adm = 0
     for k in range(steps):
         now = (k + 1) * bench.STEP_US
+        g.w.set_k1_full(k in k1_full_steps)
         rg = g.step(now)
         ro = o.step(now)
+        assert rg.n_queued == ro["n"], f"step {k}: queue sizes differ"
         assert [int(x) for x in rg.adm_req] == ro["admitted"], f"step {k}: admissions differ"
         assert [int(x) for x in rg.adm_mlen] == ro["mlen"], f"step {k}: match lengths differ"
         qg, rfg, _ = g.w.counters(nc)
@@ -38,7 +49,7 @@ def _run_wl(wl, steps):
         recs_o = [(tuple(int(x) for x in p), int(kp)) for p, kp in ro["records"]]
         assert recs_g == recs_o, f"step {k}: eviction records differ"
         n = len(ro["admitted"])
-        if n and nxt + n <= len(pool):
+        if n and nxt + n <= pool_n:
             o.enqueue(range(nq + nxt, nq + nxt + n))
             nxt += n
         total_adm += n
@@ -62,6 +73,51 @@ def test_scale_config5_64k():
     tokens) at 64k queued requests against the oracle on the same tokens."""
     import bench
     _run_wl(bench.Config5(65536, 0, 10), 10)
+
+
+def _c5_host_stream(wl):
+    """The whole config-5 stream -- the wl.nq-request queue, then the arrival
+    pool -- expanded on the host by oracle/tokens.c (the reference's
+    expand_tokens restated, pinned by tests/golden/tokens.json) into ONE
+    buffer (34 GB at 1M requests; no concatenation copy).  The pool half must
+    equal the device-materialized pool the GPU loop uploads."""
+    from oracle.materialize import expand_segments
+    from paper_2501_14312_b200.workloads import Queue, deep_tree_segments
+    sq, cq, lq = deep_tree_segments(wl.spec, first=0, count=wl.nq, stream=0)
+    sp, cp, lp = deep_tree_segments(wl.spec, first=0, count=wl.pool_n, stream=1)
+    tq, tp = int(sq.lens().sum()), int(sp.lens().sum())
+    flat = np.empty(tq + tp, np.int32)
+    _, oq = expand_segments(sq, out=flat[:tq])
+    _, op = expand_segments(sp, out=flat[tq:])
+    pool = wl.pool
+    assert len(pool) == wl.pool_n and np.array_equal(pool.clients, cp) and np.array_equal(pool.labels, lp)
+    for i in range(len(pool)):
+        assert np.array_equal(pool.tokens(i), flat[tq + op[i]:tq + op[i + 1]]), f"pool request {i}"
+    n = wl.nq + wl.pool_n
+    return Queue(flat, np.concatenate([oq[:-1], tq + op[:-1]]), np.concatenate([sq.lens(), sp.lens()]).astype(np.int32),
+                 np.concatenate([cq, cp]).astype(np.int32),
+                 np.concatenate([np.zeros(wl.nq, np.int64), np.full(wl.pool_n, bench_step_us(), np.int64)]),
+                 [], np.concatenate([lq, lp]))
+
+
+def bench_step_us():
+    import bench
+    return bench.STEP_US
+
+
+@pytest.mark.slow
+def test_scale_config5_full_1m():
+    """Config 5 at the benchmarked size: the full 1,048,576-request queue of
+    8192-token prompts (8.6 G tokens in the arena: offsets past 2^31, the
+    full-size position shadow, grid sweeps and chunked LRU at full size)
+    against the oracle on host-expanded tokens, five serving steps; steps 2
+    and 4 re-match every request from the root, the others resume from the
+    previous matches (incremental K1), so both modes are checked at 1M."""
+    import bench
+    wl = bench.Config5(1 << 20, 0, 5)
+    q_all = _c5_host_stream(wl)
+    assert int(q_all.offsets[wl.nq - 1]) > (1 << 31)
+    _run_wl(wl, 5, q_all=q_all, k1_full_steps=(2, 4))
 
 
 def test_scale_leader_only_sweeps(monkeypatch):
