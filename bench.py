@@ -646,7 +646,11 @@ def main():
                                    "pop_update_cyc": sched[10] / steps, "setup_cyc": sched[11] / steps,
                                    "grid_sweeps": sched[15] / steps, "grid_sweep_cyc": sched[14] / steps,
                                    "side_cyc": sched[12] / steps, "leaf_cyc": sched[13] / steps,
-                                   "total_cyc": sched[7] / steps},
+                                   "total_cyc": sched[7] / steps,
+                                   "pin_cyc": st["ext"][0] / steps, "on_walk_cyc": st["ext"][1] / steps,
+                                   "fev_setup_wait_cyc": st["ext"][2] / steps,
+                                   "fev_orders": st["fev"][0] / steps, "fev_cold_leaves": st["fev"][1] / steps,
+                                   "fev_heap_hw": st["fev"][2] / steps, "fev_ok_fills": st["fev"][3] / steps},
         "clocks": st["clocks"], "host_wall_s": st["t_total"],
     }
     if d2 is not None:
@@ -720,7 +724,7 @@ def run_dlpm(g, steps, warmup, dist=None, rank=0, dev=0, clocks=True):
     l0 = launch_count()
     h2d0, d2h0 = g.h2d, g.d2h
     st = {"dev_ms": 0.0, "wall": 0.0, "decisions": 0, "adm": 0, "alg_tok": 0, "k1_ms": [], "phases": np.zeros(5),
-          "sched": np.zeros(16), "k1_hops": 0, "resumes": 0, "refills": 0}
+          "sched": np.zeros(16), "k1_hops": 0, "resumes": 0, "refills": 0, "fev": np.zeros(4), "ext": np.zeros(8)}
     t_start = time.perf_counter()
     for _ in range(steps):
         now += STEP_US
@@ -738,6 +742,9 @@ def run_dlpm(g, steps, warmup, dist=None, rank=0, dev=0, clocks=True):
         st["k1_hops"] += res.stats[6]
         st["resumes"] += res.stats[4]
         st["refills"] += res.stats[3]
+        f = int(res.stats[7])  # FEV: orders | cold leaves << 20 | heap high water << 40 | ok << 60
+        st["ext"] += np.array(res.stats_ext, dtype=np.float64)
+        st["fev"] += np.array([f & 0xfffff, (f >> 20) & 0xfffff, (f >> 40) & 0xfffff, (f >> 60) & 1])
     g.ctx.sync()
     st["t_total"] = time.perf_counter() - t_start
     st["launches"] = launch_count() - l0

@@ -221,6 +221,10 @@ int fs_worker_last_phases(fs_worker *w, float *ms4);
  * [14] source chains in admission walks, [15] total, [16..18] eviction-pop
  * argmin / edit / index-update cycles.  Writes 24 entries. */
 int fs_worker_last_stats(fs_worker *w, int64_t *stats24);
+/* Scheduler cycle counters of the last fill (diagnostic): [0] path pin,
+ * [1] post-walk scheduler bookkeeping, [2] waits for the asynchronous
+ * evictor's setup, [3..7] reserved. */
+int fs_worker_last_stats_ext(fs_worker *w, int64_t *ext8);
 /* Worker options.  FS_OPT_K1_FULL (1): value != 0 makes every fill re-match
  * every queued request from the root instead of resuming from its previous
  * match (same decisions; the incremental match is the default). */

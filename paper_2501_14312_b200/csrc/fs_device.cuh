@@ -727,6 +727,48 @@ __device__ inline void block_pin_path_known(const TrieView &t, const Seg *segs, 
 // exactly "every current evictable leaf", so each pop is a block-wide argmin
 // of (last_access, seq) over the node table; thread 0 detaches or truncates
 // the winner and appends the record.  Protect set = FS_PROTECT flag.
+__device__ __forceinline__ int32_t ld_acquire_i32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int32_t *p, int32_t v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------- cold eviction
+// Asynchronous cold eviction (FEV) for the scheduler (k_schedule).  Within one
+// fill every stamp lands on a queued request's path: K1 stamps each queued
+// request's match (match_prefix in lpm_order, radix.py:86-90) with the fill's
+// operation sequence sq1, and admissions stamp their own (pinned) paths.  A
+// node whose own stamp predates sq1 and that is an evictable leaf -- "cold" --
+// is therefore on no path any walk of this fill can take, no admission ever
+// pins it, and (when every cold stamp is older than the fill's `now`, checked
+// up front) every cold key (last_access, seq) is smaller than every other
+// candidate's: the LRU pops of the fill start with the cold leaves in key
+// order, whatever the admissions do.  While the cumulative eviction need stays
+// within the cold leaves' tokens, the pops are fully determined by the sequence
+// of per-admission needs, and each need is known as soon as the admission's
+// walk is done (a partial truncation frees exactly what is left to free).  So
+// the leader CTA only posts each need; a dedicated CTA performs the pops
+// (records, detaches, parent re-joins) in order, concurrently with the
+// following admissions.  Past the cold supply the leader drains the evictor
+// and evicts itself (the serial path).
+struct FevCtl {  // global, zeroed by the host per fill
+    int32_t ready, ok, posted, stop, done, finished, err, pad_;
+    int64_t C;                                   // cold candidate tokens at fill start
+    int64_t freed, nrec, nfreed, tombs, pops;    // evictor totals (valid once finished)
+    int32_t nc, heap_hw;                         // cold leaves sorted, re-join heap high water
+};
+struct FevLeader {  // leader CTA, shared memory
+    FevCtl *ctl;
+    int64_t *need;      // [orders] tokens to free
+    int64_t *rec_end;   // [orders] records emitted after each order (evictor)
+    int32_t *free_list; // node slots the evictor freed
+    int32_t on, posted, cap_orders, ready_seen, used_any, nfree_saved;
+    int64_t cum, C, tag;  // tag: the fill's order tag (bits 40..62 of each posted need)
+};
+
 struct EvictSmem {
     int64_t la[32];
     int64_t sq[32];
@@ -925,6 +967,9 @@ __device__ __forceinline__ void warp_chunk_touch(const TrieView &t, ChunkLRU *L,
 }
 
 // RadixTree.evict_lru with protect set {protect} (radix.py:210-250), one warp.
+// ASYNC: the FEV evictor CTA (parents' child counts are shared with the
+// leader's concurrent inserts: atomic).
+template <bool ASYNC = false>
 __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t needed, int32_t protect,
                                         EvictSmem *sm, int lane) {
     // The protected node (the path's deepest, just stamped) is rarely the LRU
@@ -983,7 +1028,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
                 const int64_t srcb = t.src[b];
                 const int32_t firstb = t.first[b];
                 const int64_t lab = t.la[b], lsb = t.lseq[b];
-                const int32_t ncP = t.nchild[P], refP = t.ref[P];
+                const int32_t ncP = ASYNC ? 0 : t.nchild[P], refP = t.ref[P];
                 const uint8_t flP = t.flags[P];
                 const int64_t laP = t.la[P], lsP = t.lseq[P], sqP = t.seq[P];
                 const uint64_t key = fs_hkey(P, firstb);
@@ -995,13 +1040,19 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
                 }
                 push_record(t, srcb, plen, plen - el);
                 if (hs.x == key) { t.hslot[hi].x = FS_HTOMB; t.sc->tombs++; }
-                t.nchild[P] = ncP - 1;
+                int32_t ncP1;
+                if (ASYNC) {
+                    ncP1 = atomicSub(&t.nchild[P], 1) - 1;
+                } else {
+                    ncP1 = ncP - 1;
+                    t.nchild[P] = ncP1;
+                }
                 int64_t newla = laP;
                 if (P > 0 && lsb > lsP) { t.la[P] = lab; t.lseq[P] = lsb; newla = lab; }
                 t.sc->used -= el;
                 node_free(t, b);
                 freed += el;
-                pcand = (flP & FS_ALIVE) && ncP - 1 == 0 && refP == 0;
+                pcand = (flP & FS_ALIVE) && ncP1 == 0 && refP == 0;
                 pla = newla;
                 pseq = sqP;
             } else {
@@ -1048,8 +1099,43 @@ struct InsertSmem {
     int32_t nseg, mlen, new_len, deepest, last, status, cov, split_top;
     int64_t needed, unpinned;
     int64_t *prof;  // optional cycle counters: [1] walk, [2] evict, [5] evict pops
+    int64_t *prof2; // scheduler only: [0] pin, [2] waits for the evictor's setup
     ChunkLRU *lru;  // scheduler: chunked LRU index (nullptr: block-wide scan)
+    FevLeader *fev; // scheduler: asynchronous cold eviction (nullptr: off)
+    ChunkLRU *lru_spare;  // ... the leader's own index, built when FEV hands over
+    int32_t fev_switch, fev_wait;
 };
+
+// Leader side: wait until the evictor has performed every posted need; with
+// `handover`, also stop it and take over its state (records, freed node
+// slots, hash tombstones) so the rest of the fill evicts serially.  Block-wide.
+__device__ inline void fev_drain(const TrieView &t, FevLeader *f, bool handover) {
+    FevCtl *c = f->ctl;
+    if (threadIdx.x == 0) {
+        while (ld_acquire_i32(&c->done) < f->posted) __nanosleep(32);
+        if (handover) {
+            st_release_i32(&c->stop, 1);
+            while (ld_acquire_i32(&c->finished) == 0) __nanosleep(32);
+            volatile FevCtl *vc = c;
+            if (vc->freed != f->cum || vc->err) t.sc->status = FS_ERR_INTERNAL;
+            t.sc->nrec = vc->nrec;
+            t.sc->tombs += (int32_t)vc->tombs;
+            t.sc->live -= (int32_t)vc->nfreed;
+            t.sc->nfree = f->nfree_saved;
+            f->on = 0;
+        }
+    }
+    __syncthreads();
+    (void)ld_acquire_i32(&c->done);  // every thread: drop L1 lines the evictor made stale
+    if (handover) {
+        const int32_t nf = (int32_t)((volatile FevCtl *)c)->nfreed;
+        const int32_t base = t.sc->nfree;
+        for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) t.freest[base + i] = f->free_list[i];
+        __syncthreads();
+        if (threadIdx.x == 0) t.sc->nfree = base + nf;
+    }
+    __syncthreads();
+}
 
 // RadixTree.insert (radix.py:128-162) by one CTA (warp 0 walks).  `segs` is a
 // global scratch of >= len+2 entries; on return it holds the whole path
@@ -1101,13 +1187,45 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             sm->last = last;
             sm->status = t.sc->status;
             sm->needed = 0;
+            sm->fev_switch = 0;
+            sm->fev_wait = 0;
             const int64_t cap = t.sc->capacity;
             if (cap >= 0 && t.sc->used + sm->new_len > cap) {
-                // only the path's deepest node can be a leaf: every other path
-                // node has its path child below it (radix.py:149 protect=path)
-                if (last > 0) t.flags[last] |= FS_PROTECT;
-                sm->needed = t.sc->used + sm->new_len - cap;
+                const int64_t need = t.sc->used + sm->new_len - cap;
+                FevLeader *f = sm->fev;
+                bool posted = false;
+                if (f && f->on) {
+                    if (!f->ready_seen) {
+                        const long long cr = clock64();
+                        while (ld_acquire_i32(&f->ctl->ready) == 0) __nanosleep(32);
+                        if (sm->prof2) sm->prof2[2] += clock64() - cr;
+                        f->C = ((volatile FevCtl *)f->ctl)->ok ? ((volatile FevCtl *)f->ctl)->C : -1;
+                        f->ready_seen = 1;
+                    }
+                    if (f->cum + need <= f->C && f->posted < f->cap_orders) {
+                        // within the cold supply: the evictor performs it
+                        // one relaxed store: the evictor needs nothing else the leader wrote
+                        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(f->need + f->posted),
+                                     "l"(f->tag | need) : "memory");
+                        f->posted++;
+                        f->cum += need;
+                        f->used_any = 1;
+                        t.sc->used -= need;
+                        posted = true;
+                    } else {
+                        sm->fev_switch = 1;  // past the cold supply: hand over, evict serially
+                    }
+                }
+                if (!posted) {
+                    // only the path's deepest node can be a leaf: every other path
+                    // node has its path child below it (radix.py:149 protect=path)
+                    if (last > 0) t.flags[last] |= FS_PROTECT;
+                    sm->needed = need;
+                }
             }
+            // a fully cached request stamps an existing node: the evictor may be
+            // pushing a detached child's stamp into it -- let it finish first
+            if (sm->fev && sm->fev->on && !sm->fev_switch && sm->new_len == 0 && w.mlen > 0) sm->fev_wait = 1;
         }
     }
 #if FS_POP_PREFETCH
@@ -1124,6 +1242,16 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
     }
 #endif
     __syncthreads();
+    if (sm->fev_switch || sm->fev_wait) {
+        const bool ho = sm->fev_switch;
+        fev_drain(t, sm->fev, ho);
+        if (ho) {
+            block_chunk_build(t, sm->lru_spare);
+            if (threadIdx.x == 0) sm->lru = sm->lru_spare;
+        }
+        if (threadIdx.x == 0) { sm->fev_switch = 0; sm->fev_wait = 0; }
+        __syncthreads();
+    }
     if (sm->split_top >= 0)
         block_repoint(t, t.src[sm->split_top], t.start[sm->split_top], t.end[sm->split_top], sm->split_top);
     const long long c1 = clock64();
@@ -1143,7 +1271,8 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                     sm->status = FS_ERR_NOMEM;
                 } else {
                     h_put(t, sm->last, tk, leaf);
-                    t.nchild[sm->last]++;
+                    if (sm->fev && sm->fev->on) atomicAdd(&t.nchild[sm->last], 1);  // the evictor may decrement it
+                    else t.nchild[sm->last]++;
                     t.ref[leaf] = 1;
                     t.sc->used += sm->new_len;
                     segs[sm->nseg].S = req_off; segs[sm->nseg].a = sm->mlen; segs[sm->nseg].b = len;
@@ -1161,10 +1290,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         if (tid == 0 && sm->prof) sm->prof[13] += clock64() - c1;
         if (warp > 1) {
             // pin the pre-existing path, then point the new leaf's depths at it
+            const long long cp = clock64();
             block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);
             if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0)
                 for (int32_t d = sm->mlen + (int32_t)tid - 64; d < len; d += (int32_t)blockDim.x - 64)
                     t.pos[req_off + d] = sm->deepest;
+            if (tid == 64 && sm->prof2) sm->prof2[0] += clock64() - cp;
         } else if (warp == 1) {
             if (lane == 0) on_walk(0);
             __syncwarp();

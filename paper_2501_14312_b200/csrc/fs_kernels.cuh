@@ -336,6 +336,13 @@ struct FillArgs {
     int32_t nhelp;
     int32_t local_chunks;  // chunks the leader scans before a grid sweep
     int32_t *rw_list;      // grid re-walk list (FS_CHUNK entries, -1 = skip)
+    int32_t hbase;         // blockIdx of the first sweep helper (2 when CTA 1 is the evictor)
+    // asynchronous cold eviction (FevCtl in fs_device.cuh): CTA 1 evicts
+    int32_t fev, fev_cap, fev_tag;
+    FevCtl *fev_ctl;
+    void *fev_vrec;  // FEV_MAXC FevRec: the cold leaves in pop order
+    int64_t *fev_need, *fev_rec_end;
+    int32_t *fev_free;
 };
 #define FS_GRID_REWALK 96  // leader re-walk lists longer than this go to the helpers
 
@@ -349,14 +356,6 @@ struct SweepCtl {
     TrieScalars sc;    // the leader's trie scalars at the sweep
 };
 
-__device__ __forceinline__ int32_t ld_acquire_i32(const int32_t *p) {
-    int32_t v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_i32(int32_t *p, int32_t v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // (pinned coverage B, token at B) of every admission of this step -> latest
 // admission epoch.  An admission e can raise a queued request's B only if
@@ -456,6 +455,8 @@ struct SchedSmem {
     int64_t resumes, refill_events;
     int64_t prof[16];  // cycles: [0] find, [1] walk, [2] evict, [3] admit tail; [4] chunks, [5] pops,
                        // [6] chains, [7] total, [8..10] pop argmin / edit / rescan, [11] setup
+    FevLeader fev;
+    int64_t prof2[8];  // cycles: [0] pin (warps 2..), [1] on_walk (thread 32), [2] order posts waiting for the evictor's setup
 };
 
 __device__ __forceinline__ int64_t sched_slack(const FillArgs &a, int64_t headroom) {
@@ -725,7 +726,7 @@ __device__ void helper_loop(const FillArgs &ap, SchedSmem *sm) {
     __shared__ int32_t seq_sh;
     SweepCtl *c = ap.ctl;
     const int tid = threadIdx.x;
-    const int32_t h = blockIdx.x - 1;
+    const int32_t h = blockIdx.x - ap.hbase;
     int32_t last = 0;
     if (tid == 0) { a = ap; a.t.sc = &sc; }
     while (true) {
@@ -793,6 +794,263 @@ __device__ void helper_loop(const FillArgs &ap, SchedSmem *sm) {
             __threadfence();
             atomicAdd(&c->done, 1);
         }
+    }
+}
+
+
+// CTA 1 under FEV (see FevCtl, fs_device.cuh).  Setup (whole CTA): collect
+// the cold evictable leaves, sort them by the LRU key (last_access, seq)
+// (radix.py:210-219) and lay their node fields out in that order; publish the
+// cold supply.  Then warp 0 performs the leader's eviction needs in order:
+// each pop is the smaller of the next sorted cold leaf and the top of a heap
+// of parents that became leaves (radix.py:231-239) -- no index rescans -- and
+// the detach (record, child-hash tombstone, parent child count and stamp,
+// free slot; radix.py:206-208, 226-249) is issued with its loads overlapped
+// (the records ahead are prefetched into L1; the hash probe is warp-wide).
+#define FEV_MAXC 2048  // power of two (bitonic sort)
+#define FEV_HEAP 640
+struct FevRec {
+    int64_t src, la, lseq, seq;
+    int32_t start, end, parent, first, node, pad_;
+};
+struct FevSmem {
+    int64_t la[FEV_MAXC];
+    int64_t sq[FEV_MAXC];
+    int32_t id[FEV_MAXC];
+    FevRec heap[FEV_HEAP];  // parents that became leaves, min-heap by (la, seq)
+    int32_t hn, nc, bad, tr_i, tr_end;
+    unsigned long long cold_tok;
+};
+
+__device__ __forceinline__ bool fev_less(int64_t a1, int64_t s1, int64_t a2, int64_t s2) {
+    return a1 < a2 || (a1 == a2 && s1 < s2);
+}
+__device__ __forceinline__ void st_relaxed_i64(int64_t *p, int64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t *p) {
+    int64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ void fev_heap_push(FevSmem *e, const FevRec &r, FevCtl *ctl) {
+    if (e->hn >= FEV_HEAP) { ctl->err = 1; return; }
+    int32_t i = e->hn++;
+    while (i > 0) {
+        const int32_t p = (i - 1) >> 1;
+        if (!fev_less(r.la, r.seq, e->heap[p].la, e->heap[p].seq)) break;
+        e->heap[i] = e->heap[p];
+        i = p;
+    }
+    e->heap[i] = r;
+}
+__device__ void fev_heap_pop(FevSmem *e) {
+    const FevRec last = e->heap[--e->hn];
+    int32_t i = 0;
+    while (true) {
+        int32_t c = 2 * i + 1;
+        if (c >= e->hn) break;
+        if (c + 1 < e->hn && fev_less(e->heap[c + 1].la, e->heap[c + 1].seq, e->heap[c].la, e->heap[c].seq)) c++;
+        if (!fev_less(e->heap[c].la, e->heap[c].seq, last.la, last.seq)) break;
+        e->heap[i] = e->heap[c];
+        i = c;
+    }
+    if (e->hn > 0) e->heap[i] = last;
+}
+
+__device__ void evictor_loop(const FillArgs &ap, unsigned char *smraw) {
+    static_assert(sizeof(FevSmem) <= sizeof(SchedSmem), "evictor state must fit the scheduler's shared memory");
+    FevSmem *e = reinterpret_cast<FevSmem *>(smraw);
+    const TrieView &t = ap.t;
+    FevCtl *ctl = ap.fev_ctl;
+    FevRec *vrec = reinterpret_cast<FevRec *>(ap.fev_vrec);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int32_t hw0 = t.sc->hw;  // the global scalars are the step-start ones during the fill
+    if (tid == 0) { e->hn = 0; e->nc = 0; e->bad = 0; e->cold_tok = 0; e->tr_i = -1; e->tr_end = 0; }
+    __syncthreads();
+    // cold evictable leaves: own stamp before this fill's K1 stamps (sq1); every
+    // pre-fill stamp must be older than `now` so cold keys sort first
+    const int64_t sq1 = ap.sq_base - 1;
+    {
+        unsigned long long c = 0;
+        int b = 0;
+        for (int32_t n = 1 + tid; n < hw0; n += blockDim.x) {
+            if (!(t.flags[n] & FS_ALIVE) || t.lseq[n] >= sq1) continue;
+            const int64_t la = t.la[n];
+            if (la >= ap.now) b = 1;
+            if (t.nchild[n] == 0 && t.ref[n] == 0) {
+                c += (unsigned long long)(t.end[n] - t.start[n]);
+                const int32_t k = atomicAdd(&e->nc, 1);
+                if (k < FEV_MAXC) { e->la[k] = la; e->sq[k] = t.seq[n]; e->id[k] = n; }
+            }
+        }
+        if (c) atomicAdd(&e->cold_tok, c);
+        if (b) e->bad = 1;
+    }
+    __syncthreads();
+    const int32_t nc = e->nc;
+    const bool ok = !e->bad && nc <= FEV_MAXC;
+    if (ok) {
+        // bitonic sort of the cold leaves by (la, seq), padded to a power of two
+        int32_t P2 = 1;
+        while (P2 < nc) P2 <<= 1;
+        for (int32_t i = nc + tid; i < P2; i += blockDim.x) { e->la[i] = INT64_MAX; e->sq[i] = INT64_MAX; e->id[i] = -1; }
+        __syncthreads();
+        for (int32_t k = 2; k <= P2; k <<= 1) {
+            for (int32_t j = k >> 1; j > 0; j >>= 1) {
+                for (int32_t i = tid; i < P2; i += blockDim.x) {
+                    const int32_t l = i ^ j;
+                    if (l > i) {
+                        const bool up = (i & k) == 0;
+                        const bool gt = fev_less(e->la[l], e->sq[l], e->la[i], e->sq[i]);
+                        if (gt == up) {
+                            int64_t x = e->la[i]; e->la[i] = e->la[l]; e->la[l] = x;
+                            x = e->sq[i]; e->sq[i] = e->sq[l]; e->sq[l] = x;
+                            const int32_t y = e->id[i]; e->id[i] = e->id[l]; e->id[l] = y;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // node fields in pop order (one or two L1 lines per pop, prefetched ahead)
+        for (int32_t i = tid; i < nc; i += blockDim.x) {
+            const int32_t n = e->id[i];
+            FevRec r;
+            r.src = t.src[n]; r.la = e->la[i]; r.lseq = t.lseq[n]; r.seq = e->sq[i];
+            r.start = t.start[n]; r.end = t.end[n]; r.parent = t.parent[n]; r.first = t.first[n];
+            vrec[i] = r;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        ctl->C = ok ? (int64_t)e->cold_tok : -1;
+        ctl->ok = ok;
+        __threadfence();
+        st_release_i32(&ctl->ready, 1);
+    }
+    if (warp != 0) return;
+    // ---- pops (warp 0)
+    const int64_t tag = (int64_t)ap.fev_tag << 40;
+    const int64_t low = (1ll << 40) - 1;
+    int32_t k = 0, i = 0, nfreed = 0, hhw = 0;
+    int64_t freed_tot = 0, nrec = 0, tombs = 0, pops = 0;
+    while (true) {
+        int64_t v = 0;
+        if (lane == 0) {
+            while (true) {
+                v = ld_relaxed_i64(ap.fev_need + k);
+                if ((v & ~low) == tag) break;
+                if (ld_acquire_i32(&ctl->stop)) {
+                    v = ld_relaxed_i64(ap.fev_need + k);
+                    if ((v & ~low) != tag) v = 0;
+                    break;
+                }
+                __nanosleep(20);
+            }
+        }
+        v = __shfl_sync(FS_FULL, v, 0);
+        if (v == 0) break;
+        const int64_t need = v & low;
+        int64_t freed = 0;
+        while (freed < need) {
+            // the next pop: the sorted cold leaf or the heap's re-joined parent
+            const bool hs = e->hn > 0, ss = i < nc;
+            if (!hs && !ss) { if (lane == 0) ctl->err = 1; break; }
+            const bool from_heap = hs && (!ss || fev_less(e->heap[0].la, e->heap[0].seq, e->la[i], e->sq[i]));
+            if (lane >= 1 && lane <= 8 && i + lane < nc) pf_l1(vrec + i + lane);
+            FevRec r = from_heap ? e->heap[0] : vrec[i];
+            if (!from_heap) {
+                r.node = e->id[i];
+                if (e->tr_i == i) r.end = e->tr_end;  // truncated by an earlier order
+            }
+            const int32_t el = r.end - r.start;
+            const int64_t rem = need - freed;
+            pops++;
+            if (el <= rem) {
+                // whole leaf: record, tombstone (parent, first), parent child
+                // count and stamp, free the slot (radix.py:226-230, 206-208)
+                const int32_t P = r.parent;
+                const uint64_t key = fs_hkey(P, r.first);
+                const uint32_t h0 = fs_hmix(key) & t.hmask;
+                int32_t old = 0;
+                uint8_t flP = 0;
+                int32_t refP = 0;
+                int64_t laP = 0, lsP = 0, sqP = 0, srcP = 0;
+                int32_t stP = 0, enP = 0, paP = 0, fiP = 0;
+                if (lane == 0) {
+                    old = atomicSub(&t.nchild[P], 1);
+                    flP = t.flags[P]; refP = t.ref[P];
+                    laP = t.la[P]; lsP = t.lseq[P]; sqP = t.seq[P];
+                    srcP = t.src[P]; stP = t.start[P]; enP = t.end[P]; paP = t.parent[P]; fiP = t.first[P];
+                }
+                // warp-wide probe of the child hash: the key's slot before the first empty one
+                for (uint32_t base = 0; base <= t.hmask; base += 32) {
+                    const uint32_t hi = (h0 + base + lane) & t.hmask;
+                    const unsigned long long x = t.hslot[hi].x;
+                    const unsigned mk = __ballot_sync(FS_FULL, x == key), me = __ballot_sync(FS_FULL, x == FS_HEMPTY);
+                    const unsigned first_hit = mk ? __ffs(mk) - 1 : 32, first_empty = me ? __ffs(me) - 1 : 32;
+                    if (first_hit < first_empty) {
+                        if ((unsigned)lane == first_hit) t.hslot[hi].x = FS_HTOMB;
+                        tombs++;
+                        break;
+                    }
+                    if (me) break;
+                }
+                if (lane == 0) {
+                    if (nrec < t.rcap) { t.rsrc[nrec] = r.src; t.rlen[nrec] = r.end; t.rkeep[nrec] = r.end - el; }
+                    nrec++;
+                    t.flags[r.node] = 0;
+                    t.parent[r.node] = -2;
+                    ap.fev_free[nfreed++] = r.node;
+                    int64_t la2 = laP, ls2 = lsP;
+                    if (P > 0 && r.lseq > lsP) { t.la[P] = r.la; t.lseq[P] = r.lseq; la2 = r.la; ls2 = r.lseq; }
+                    if (from_heap) fev_heap_pop(e);
+                    if (P > 0 && (flP & FS_ALIVE) && old - 1 == 0 && refP == 0) {
+                        // the parent became a leaf: it joins the candidates at its key
+                        FevRec q;
+                        q.src = srcP; q.la = la2; q.lseq = ls2; q.seq = sqP;
+                        q.start = stP; q.end = enP; q.parent = paP; q.first = fiP; q.node = P; q.pad_ = 0;
+                        fev_heap_push(e, q, ctl);
+                        hhw = max(hhw, e->hn);
+                    }
+                }
+                if (!from_heap) i++;
+                freed += el;
+            } else {
+                // truncate the leaf's tail (radix.py:240-246); it stays the minimum
+                if (lane == 0) {
+                    if (nrec < t.rcap) { t.rsrc[nrec] = r.src; t.rlen[nrec] = r.end; t.rkeep[nrec] = (int32_t)(r.end - rem); }
+                    nrec++;
+                    t.end[r.node] = r.end - (int32_t)rem;
+                    if (from_heap) e->heap[0].end = r.end - (int32_t)rem;
+                    else { e->tr_i = i; e->tr_end = r.end - (int32_t)rem; }
+                }
+                freed += rem;
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            freed_tot += freed;
+            if (freed != need) ctl->err = 1;
+            ap.fev_rec_end[k] = nrec;
+            __threadfence();
+            st_release_i32(&ctl->done, k + 1);
+        }
+        k++;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        ctl->freed = freed_tot;
+        ctl->nrec = nrec;
+        ctl->nfreed = nfreed;
+        ctl->tombs = tombs;
+        ctl->pops = pops;
+        ctl->nc = nc;
+        ctl->heap_hw = hhw;
+        __threadfence();
+        st_release_i32(&ctl->finished, 1);
     }
 }
 
@@ -873,6 +1131,14 @@ __device__ void block_refill(const FillArgs &a, SchedSmem *sm) {
 __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t slack) {
     const int tid = threadIdx.x;
     const TrieView &t = a.t;
+    if (sm->fev.on && t.sc->hw + 2 > t.ncap) {
+        // FEV allocates fresh node slots only (the evictor's freed slots come
+        // back at the hand-over): out of fresh slots, hand over now
+        fev_drain(t, &sm->fev, true);
+        block_chunk_build(t, &sm->lru);
+        if (tid == 0) sm->ins.lru = &sm->lru;
+        __syncthreads();
+    }
     const int32_t r = a.s_req[j];
     const int32_t len = a.s_len[j];
     const int64_t off = a.roff[r];
@@ -901,6 +1167,8 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     const long long ct0 = clock64();
     auto on_walk = [&](int) {
         // thread 32: everything the next search depends on
+        const long long cw = clock64();
+        struct Acc { long long c; int64_t *p; __device__ ~Acc() { p[1] += clock64() - c; } } acc{cw, sm->prof2};
         const InsertSmem &in = sm->ins;
         pre_ok = 0;
         sm->pseg_j = -1;  // consumed by this walk (on_side may set the next one)
@@ -987,7 +1255,9 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
                 a.adm_unp[e] = in.unpinned;
                 a.adm_pinb[e] = pinb;
                 a.adm_node[e] = in.deepest;
-                a.adm_rec_end[e] = t.sc->nrec;
+                // under FEV the records of this admission are still being
+                // written: keep the order count, resolved at the end of the fill
+                a.adm_rec_end[e] = sm->fev.on ? -(int64_t)sm->fev.posted - 1 : t.sc->nrec;
             }
             sm->nadm = e + 1;
             if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
@@ -1003,6 +1273,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     SchedSmem &sm = *reinterpret_cast<SchedSmem *>(fs_smraw);
     // CTAs 1..nhelp (cooperative launch, co-resident) only serve the leader's
     // grid sweeps of the queue; CTA 0 runs the fill
+    if (ap.fev && blockIdx.x == 1) { evictor_loop(ap, fs_smraw); return; }
     if (blockIdx.x > 0) { helper_loop(ap, &sm); return; }
     // the trie's scalars (used/pinned/seq/free stack/records) live in shared
     // memory for the whole step: every serial edit touches several of them
@@ -1025,10 +1296,21 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         sm.headroom = a.headroom0; sm.resumes = 0; sm.refill_events = 0; sm.cursor_seq = 0;
         sm.pre_j = -1; sm.pre_end = 0; sm.pseg_j = -1; sm.pseg_n = -1;
         for (int i = 0; i < 16; i++) sm.prof[i] = 0;
+        for (int i = 0; i < 8; i++) sm.prof2[i] = 0;
         for (int i = 0; i < 4; i++) sm.lru.prof[i] = 0;
         sm.ins.prof = sm.prof;
-        sm.ins.lru = &sm.lru;
+        sm.ins.prof2 = sm.prof2;
+        sm.ins.lru = a.fev ? nullptr : &sm.lru;  // FEV: the evictor CTA owns the index
+        sm.ins.lru_spare = &sm.lru;
         sm.ins.ev.pops = 0;
+        sm.ins.fev = a.fev ? &sm.fev : nullptr;
+        sm.ins.fev_switch = 0; sm.ins.fev_wait = 0;
+        FevLeader &f = sm.fev;
+        f.ctl = a.fev_ctl; f.need = a.fev_need; f.rec_end = a.fev_rec_end; f.free_list = a.fev_free;
+        f.on = a.fev; f.posted = 0; f.cap_orders = a.fev_cap; f.ready_seen = 0; f.used_any = 0;
+        f.cum = 0; f.C = 0; f.tag = (int64_t)a.fev_tag << 40;
+        f.nfree_saved = a.t.sc->nfree;
+        if (a.fev) a.t.sc->nfree = 0;  // fresh slots only while the evictor frees concurrently
     }
     const long long t_start = clock64();
     // pend_cnt (pending requests per client) is maintained across fills:
@@ -1039,7 +1321,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     }
     if (tid == 0) { sm.flt.n = 0; sm.flt.saturated = 0; }
     __syncthreads();
-    block_chunk_build(a.t, &sm.lru);
+    if (!a.fev) block_chunk_build(a.t, &sm.lru);
     __syncthreads();
     {
         int64_t cnt = 0;
@@ -1090,6 +1372,33 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         if (sm.stop) break;
     }
     __syncthreads();
+    if (a.fev) {
+        // stop the evictor (handing its state over if it is still on), then
+        // resolve the admissions' record counts
+        if (sm.fev.on) {
+            fev_drain(a.t, &sm.fev, true);
+        } else if (tid == 0) {
+            st_release_i32(&a.fev_ctl->stop, 1);
+            while (ld_acquire_i32(&a.fev_ctl->finished) == 0) __nanosleep(32);
+        }
+        __syncthreads();
+        (void)ld_acquire_i32(&a.fev_ctl->finished);
+        const int32_t na = min(sm.nadm, a.adm_cap);
+        for (int32_t e = tid; e < na; e += blockDim.x) {
+            const int64_t v = a.adm_rec_end[e];
+            if (v < 0) {
+                const int64_t k = -v - 1;
+                a.adm_rec_end[e] = k > 0 ? a.fev_rec_end[k - 1] : 0;
+            }
+        }
+        if (tid == 0) {
+            sm.ins.ev.pops += ((volatile FevCtl *)a.fev_ctl)->pops;
+            a.hdr[7] = sm.fev.posted | ((int64_t)((volatile FevCtl *)a.fev_ctl)->nc << 20) |
+                       ((int64_t)((volatile FevCtl *)a.fev_ctl)->heap_hw << 40) |
+                       ((int64_t)((volatile FevCtl *)a.fev_ctl)->ok << 60);
+        }
+        __syncthreads();
+    }
     if (a.nhelp > 0) {
         __threadfence();
         __syncthreads();
@@ -1111,6 +1420,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         sm.prof[7] = clock64() - t_start;
         for (int i = 0; i < 3; i++) sm.prof[8 + i] = sm.lru.prof[i];
         for (int i = 0; i < 16; i++) a.hdr[8 + i] = sm.prof[i];
+        for (int i = 0; i < 8; i++) a.hdr[24 + i] = sm.prof2[i];
         *ap.t.sc = sc_sh;
     }
 }
@@ -1142,7 +1452,7 @@ __global__ void __launch_bounds__(256) k_op(OpArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TrieView &t = a.t;
     if (tid == 0) {
-        t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.lru = nullptr; ins.ev.pops = 0;
+        t.sc->nrec = 0; t.sc->status = FS_OK; ins.prof = nullptr; ins.lru = nullptr; ins.ev.pops = 0; ins.fev = nullptr;
         for (int k = 0; k < 4; k++) nsm.prof[k] = 0;
     }
     __syncthreads();
@@ -1322,6 +1632,7 @@ __global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a)
         for (int i = 0; i < 16; i++) prof[i] = 0;
         ins.prof = prof;
         ins.lru = nullptr;
+        ins.fev = nullptr;
         ins.ev.pops = 0;
     }
     __syncthreads();

@@ -1079,6 +1079,11 @@ struct fs_worker {
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
     DBuf<SweepCtl> ctl;
+    DBuf<FevCtl> fev_ctl;          // asynchronous cold eviction (k_schedule CTA 1)
+    DBuf<int64_t> fev_need, fev_rec_end;
+    DBuf<int32_t> fev_free;
+    DBuf<unsigned char> fev_vrec;
+    int32_t fev_tag = 0;
     DBuf<int32_t> k1jobs, k1njobs;  // K1 positions the fast path left to the walk
     DBuf<int32_t> tok0q;            // K1: token at each queue position's match (miss key)
     DBuf<int32_t> rw_list;
@@ -1101,6 +1106,7 @@ struct fs_worker {
     float phases[4] = {0, 0, 0, 0};
     DBuf<int64_t> alg;         // K1 algorithmic-token accumulator
     int64_t stats[24] = {0};
+    int64_t stats_ext[8] = {0};  // hdr[24..31]: scheduler cycle counters (pin, on_walk, evictor-setup waits)
 };
 
 struct IsQueued {
@@ -1153,7 +1159,7 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     CK(cudaMemsetAsync(w->refills.p, 0, sizeof(int64_t) * max_clients, c->stream));
     CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
     CK(cudaMemsetAsync(w->pend_cnt.p, 0, sizeof(int32_t) * max_clients, c->stream));
-    TRY(dgrow(w->hdr, 24, c->stream)); TRY(hgrow(w->h_hdr, 24 + 128));
+    TRY(dgrow(w->hdr, 32, c->stream)); TRY(hgrow(w->h_hdr, 32 + 128));
     TRY(dgrow(w->nsel, 1, c->stream));
     TRY(dgrow(w->alg, 128, c->stream));
     for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
@@ -1172,7 +1178,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->fev_ctl.release(); w->fev_need.release(); w->fev_rec_end.release(); w->fev_free.release(); w->fev_vrec.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1334,6 +1340,12 @@ extern "C" int fs_worker_set_option(fs_worker *w, int option, int64_t value) {
 extern "C" int fs_worker_last_stats(fs_worker *w, int64_t *stats16) {
     if (!w || !stats16) return fail(FS_ERR_INVALID, "NULL");
     for (int i = 0; i < 24; i++) stats16[i] = w->stats[i];
+    return FS_OK;
+}
+
+extern "C" int fs_worker_last_stats_ext(fs_worker *w, int64_t *ext8) {
+    if (!w || !ext8) return fail(FS_ERR_INVALID, "NULL");
+    for (int i = 0; i < 8; i++) ext8[i] = w->stats_ext[i];
     return FS_OK;
 }
 
@@ -1544,6 +1556,34 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         TRY(dgrow(w->gep, FS_FSLOTS, s));
     }
     a.ctl = w->ctl.p; a.gkey = w->gkey.p; a.gep = w->gep.p; a.nhelp = w->nhelp; a.rw_list = w->rw_list.p;
+    a.hbase = 1;
+    // asynchronous cold eviction: CTA 1 evicts, the sweeps keep the other
+    // helpers (FS_FEV=0 turns it off; a cache without capacity never evicts)
+    static const bool fev_env = [] { const char *e = getenv("FS_FEV"); return !(e && atoi(e) == 0); }();
+    a.fev = fev_env && w->nhelp >= 2 && t->capacity >= 0;
+    if (a.fev) {
+        TRY(dgrow(w->fev_ctl, 1, s));
+        {
+            // order slots are recognised by their fill tag: a fresh buffer may hold
+            // another worker's old orders, so it starts zeroed
+            const int64_t cap0 = w->fev_need.cap;
+            TRY(dgrow(w->fev_need, acap, s));
+            if (w->fev_need.cap != cap0) CK(cudaMemsetAsync(w->fev_need.p, 0, sizeof(int64_t) * w->fev_need.cap, s));
+        }
+        TRY(dgrow(w->fev_rec_end, acap, s));
+        TRY(dgrow(w->fev_free, std::max<int64_t>(t->ncap, 64), s));
+        CK(cudaMemsetAsync(w->fev_ctl.p, 0, sizeof(FevCtl), s));
+        a.fev_ctl = w->fev_ctl.p; a.fev_need = w->fev_need.p; a.fev_rec_end = w->fev_rec_end.p;
+        TRY(dgrow(w->fev_vrec, (int64_t)sizeof(FevRec) * FEV_MAXC, s));
+        a.fev_free = w->fev_free.p; a.fev_cap = (int32_t)std::min<int64_t>(acap, INT32_MAX);
+        a.fev_vrec = w->fev_vrec.p;
+        // process-wide tag sequence (nonzero): stale orders of other fills never match
+        static std::atomic<int32_t> fev_seq{0};
+        w->fev_tag = (int32_t)(fev_seq.fetch_add(1) % ((1 << 23) - 1)) + 1;
+        a.fev_tag = w->fev_tag;
+        a.nhelp = w->nhelp - 1;
+        a.hbase = 2;
+    }
     static const int lch = [] { const char *e = getenv("FS_LOCAL_CHUNKS"); return e ? atoi(e) : 1; }();
     a.local_chunks = lch;
     CK(cudaMemsetAsync(w->ctl.p, 0, sizeof(SweepCtl), s));
@@ -1558,8 +1598,8 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     CK(cudaGetLastError());
     CK(cudaEventRecord(w->ev[4], s));
     w->dl_client.clear(); w->dl_delta.clear();
-    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 24, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_hdr.p + 24, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w->h_hdr.p + 32, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     w->inflight = true;
     t->busy = true;
     w->f_n = n;
@@ -1618,13 +1658,15 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&w->phases[i], w->ev[i], w->ev[i + 1]));
     w->stats[0] = 0;
     w->stats[6] = 0;
-    for (int k = 0; k < 64; k++) { w->stats[0] += w->h_hdr.p[24 + 2 * k]; w->stats[6] += w->h_hdr.p[25 + 2 * k]; }
+    for (int k = 0; k < 64; k++) { w->stats[0] += w->h_hdr.p[32 + 2 * k]; w->stats[6] += w->h_hdr.p[33 + 2 * k]; }
+    for (int i = 0; i < 8; i++) w->stats_ext[i] = w->h_hdr.p[24 + i];
     for (int i = 8; i < 24; i++) w->stats[i] = w->h_hdr.p[i];
     w->stats[1] = n;
     w->stats[2] = w->h_hdr.p[3];
     w->stats[3] = w->h_hdr.p[4];
     w->stats[4] = w->h_hdr.p[5];
     w->stats[5] = g_launches.load() - launches0;
+    w->stats[7] = w->h_hdr.p[7];  // evictions performed by the FEV evictor CTA (orders)
     float total = 0;
     CK(cudaEventElapsedTime(&total, w->ev[0], w->ev[4]));
     res->device_ms = total;

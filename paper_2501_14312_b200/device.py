@@ -297,6 +297,7 @@ class FillResult:
     device_ms: float
     phases_ms: list = field(default_factory=list)
     stats: list = field(default_factory=list)  # fs_worker_last_stats
+    stats_ext: list = field(default_factory=list)  # fs_worker_last_stats_ext
 
 
 def launch_count() -> int:
@@ -426,10 +427,12 @@ class WorkerDev:
         call("fs_worker_last_phases", self._h, ph)
         st = (C.c_int64 * 24)()
         call("fs_worker_last_stats", self._h, st)
+        sx = (C.c_int64 * 8)()
+        call("fs_worker_last_stats_ext", self._h, sx)
         a = res.n_adm
         return FillResult(self._req[:a].copy(), self._mlen[:a].copy(), self._unp[:a].copy(),
                           self._pinb[:a].copy(), self._node[:a].copy(), self._rend[:a].copy(),
-                          recs, res.n_queued, res.used, res.pinned, res.device_ms, list(ph), list(st))
+                          recs, res.n_queued, res.used, res.pinned, res.device_ms, list(ph), list(st), list(sx))
 
 
 class DispatcherDev:

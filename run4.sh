@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py tests/test_gpu_scale.py tests/test_gpu_fill_async.py -x -q -k "not full_1m" > gpurun_out/fev_tests.log 2>&1; echo tests rc $?
+timeout 300 python bench.py --no-cpu --no-sub --steps 20 > gpurun_out/fev_bench.json 2> gpurun_out/fev_bench.err; echo bench rc $?
+timeout 300 python bench.py --no-cpu --no-sub --steps 20 --workload c2 > gpurun_out/fev_bench_c2.json 2> gpurun_out/fev_bench_c2.err; echo bench c2 rc $?
+FS_FEV=0 timeout 300 python bench.py --no-cpu --no-sub --steps 20 --workload c2 > gpurun_out/nofev_bench_c2.json 2>&1; echo nofev rc $?
