@@ -649,6 +649,7 @@ def main():
                                    "total_cyc": sched[7] / steps,
                                    "pin_cyc": st["ext"][0] / steps, "on_walk_cyc": st["ext"][1] / steps,
                                    "fev_setup_wait_cyc": st["ext"][2] / steps,
+                                   "on_walk_pre_put_cyc": st["ext"][3] / steps, "on_walk_post_put_cyc": st["ext"][4] / steps,
                                    "fev_orders": st["fev"][0] / steps, "fev_cold_leaves": st["fev"][1] / steps,
                                    "fev_heap_hw": st["fev"][2] / steps, "fev_ok_fills": st["fev"][3] / steps},
         "clocks": st["clocks"], "host_wall_s": st["t_total"],

@@ -1262,39 +1262,54 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         // candidate, and its sequence number does not depend on the evictions
         // (they allocate none) -- only its node slot may differ, which nothing
         // observes.  used_tokens counts it now; the capacity test below adjusts.
-        if (tid == 0) {
-            int32_t deepest = sm->mlen > 0 ? sm->last : -1;
-            if (sm->status == FS_OK && sm->new_len > 0) {
-                const int32_t tk = (sm->mlen == hint_m0 && hint_tok0 >= 0) ? hint_tok0 : rq[sm->mlen];
-                const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last, tk);
-                if (leaf < 0) {
-                    sm->status = FS_ERR_NOMEM;
-                } else {
-                    h_put(t, sm->last, tk, leaf);
-                    if (sm->fev && sm->fev->on) atomicAdd(&t.nchild[sm->last], 1);  // the evictor may decrement it
-                    else t.nchild[sm->last]++;
-                    t.ref[leaf] = 1;
-                    t.sc->used += sm->new_len;
-                    segs[sm->nseg].S = req_off; segs[sm->nseg].a = sm->mlen; segs[sm->nseg].b = len;
-                    sm->nseg++;
-                    deepest = leaf;
-                    t.la[leaf] = now;  // stamp of the whole path (lazy): a fresh node needs no compare
-                    t.lseq[leaf] = sq;
+        // Warp 0 creates the leaf while warp 1 settles the scheduler state
+        // (on_walk needs only the walk) and warps 2.. pin the pre-existing
+        // path; the leaf's positions follow once it exists (named barrier 1:
+        // warps 0 and 2..).
+        if (warp == 0) {
+            if (lane == 0) {
+                int32_t deepest = sm->mlen > 0 ? sm->last : -1;
+                if (sm->status == FS_OK && sm->new_len > 0) {
+                    const int32_t tk = (sm->mlen == hint_m0 && hint_tok0 >= 0) ? hint_tok0 : rq[sm->mlen];
+                    const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last, tk);
+                    if (leaf < 0) {
+                        sm->status = FS_ERR_NOMEM;
+                    } else {
+                        h_put(t, sm->last, tk, leaf);
+                        if (sm->fev && sm->fev->on) atomicAdd(&t.nchild[sm->last], 1);  // the evictor may decrement it
+                        else t.nchild[sm->last]++;
+                        t.ref[leaf] = 1;
+                        t.sc->used += sm->new_len;
+                        // (sm->nseg stays: the other warps read it concurrently;
+                        // the leaf is pinned from birth, not by the path pin)
+                        deepest = leaf;
+                        t.la[leaf] = now;  // stamp of the whole path (lazy): a fresh node needs no compare
+                        t.lseq[leaf] = sq;
+                    }
+                } else if (sm->status == FS_OK && deepest > 0) {
+                    stamp_node(t, deepest, now, sq);
                 }
-            } else if (sm->status == FS_OK && deepest > 0) {
-                stamp_node(t, deepest, now, sq);
+                sm->deepest = deepest;
+                if (sm->prof) sm->prof[13] += clock64() - c1;
             }
-            sm->deepest = deepest;
-        }
-        __syncthreads();  // the split top's positions and the leaf are visible
-        if (tid == 0 && sm->prof) sm->prof[13] += clock64() - c1;
-        if (warp > 1) {
+            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32) : "memory");
+        } else if (warp > 1) {
             // pin the pre-existing path, then point the new leaf's depths at it
             const long long cp = clock64();
             block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);
-            if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0)
-                for (int32_t d = sm->mlen + (int32_t)tid - 64; d < len; d += (int32_t)blockDim.x - 64)
-                    t.pos[req_off + d] = sm->deepest;
+            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32) : "memory");
+            if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0) {
+                // 16-B stores (arena rows, hence their pos rows, are 16-B aligned):
+                // a quarter of the store instructions next to warp 1's bookkeeping
+                int32_t *row = t.pos + req_off;
+                const int32_t v = sm->deepest;
+                const int32_t a0 = sm->mlen, a4 = min(len, (a0 + 3) & ~3), b4 = len & ~3;
+                const int32_t nt = (int32_t)blockDim.x - 64, me = (int32_t)tid - 64;
+                if (me < a4 - a0) row[a0 + me] = v;
+                for (int32_t q = a4 / 4 + me; q < b4 / 4; q += nt)
+                    reinterpret_cast<int4 *>(row)[q] = make_int4(v, v, v, v);
+                if (b4 >= a4 && me < len - b4) row[b4 + me] = v;
+            }
             if (tid == 64 && sm->prof2) sm->prof2[0] += clock64() - cp;
         } else if (warp == 1) {
             if (lane == 0) on_walk(0);

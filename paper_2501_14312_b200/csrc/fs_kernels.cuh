@@ -394,21 +394,23 @@ struct FiltView {
 
 __device__ __forceinline__ FiltView filt_view(const AdmFilter *f) { return FiltView{f->key, f->ep, f->saturated}; }
 
-__device__ inline void adm_put_key(AdmFilter *f, unsigned long long k, int32_t e, unsigned long long *gkey,
-                                   int32_t *gep) {
-    if (f->n * 2 >= FS_FSLOTS) { f->saturated = 1; return; }
+// Returns the slot written (-1: saturated).  The global mirror (read by the
+// helper CTAs' sweeps and the next fill's K1) is written by the caller, off
+// the admission's critical warp (block_admit, after the insert).
+__device__ inline int32_t adm_put_key(AdmFilter *f, unsigned long long k, int32_t e) {
+    if (f->n * 2 >= FS_FSLOTS) { f->saturated = 1; return -1; }
     uint32_t i = fs_hmix(k) & (FS_FSLOTS - 1);
     while (f->key[i] != FS_HEMPTY && f->key[i] != k) i = (i + 1) & (FS_FSLOTS - 1);
-    if (f->key[i] == FS_HEMPTY) { f->key[i] = k; f->n++; if (gkey) gkey[i] = k; }
+    if (f->key[i] == FS_HEMPTY) { f->key[i] = k; f->n++; }
     f->ep[i] = e;
-    if (gep) gep[i] = e;
+    return (int32_t)i;
 }
 
 __device__ inline void adm_put(AdmFilter *f, int32_t B, int32_t tok, int32_t m0, int32_t tok0, int32_t e,
-                               unsigned long long *gkey, int32_t *gep) {
+                               int32_t *slots2) {
     // a request fully covered by pins extends nothing
-    if (tok >= 0) adm_put_key(f, adm_key(B, tok), e, gkey, gep);
-    if (tok0 >= 0) adm_put_key(f, miss_key(m0, tok0), e, gkey, gep);
+    slots2[0] = tok >= 0 ? adm_put_key(f, adm_key(B, tok), e) : -1;
+    slots2[1] = tok0 >= 0 ? adm_put_key(f, miss_key(m0, tok0), e) : -1;
 }
 
 // true when some admission in [since, now) had key k
@@ -1145,6 +1147,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     __shared__ int64_t pinb;
     __shared__ int64_t pre_slack;
     __shared__ int32_t pre_ok;
+    __shared__ int32_t mirror[2];  // filter slots this admission wrote (global mirror update below)
     // thread 0's charge operands do not depend on the tree edit: load them now
     // so they arrive while warp 0 walks
     int32_t c_pre = 0, pend_pre = 0, tok0_pre = -1, m0_pre = 0, b_pre = -1, tokb_pre = -1;
@@ -1152,6 +1155,7 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
     if (tid == 0) {
         pinb = t.sc->pinned;
         sm->pre_j = -1;
+        mirror[0] = mirror[1] = -1;
     }
     if (tid == 32) {  // on_walk runs on thread 32 (warp 1, lane 0)
         const int4 sl = a.slot[j];
@@ -1182,9 +1186,16 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             sm->stop = 1;
             return;
         }
-        const int32_t tokc = cov >= len ? -1 : (cov == b_pre ? tokb_pre : t.arena[off + cov]);
-        adm_put(&sm->flt, cov, tokc, m0_pre, tok0_pre, sm->epoch, a.gkey, a.gep);
+        // the token at the coverage: known when the coverage is the search's
+        // (slot) value or the step-start match length (K1's miss token)
+        const int32_t tokc = cov >= len ? -1
+                           : cov == b_pre ? tokb_pre
+                           : (cov == m0_pre && tok0_pre >= 0) ? tok0_pre
+                           : t.arena[off + cov];
+        sm->prof2[3] += clock64() - cw;
+        adm_put(&sm->flt, cov, tokc, m0_pre, tok0_pre, sm->epoch, mirror);
         sm->epoch++;
+        sm->prof2[4] += clock64() - cw;
         a.slot[j].w = -1;
         a.rstate[r] = 2;
         const int32_t c = c_pre;
@@ -1261,6 +1272,11 @@ __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t
             }
             sm->nadm = e + 1;
             if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm->stop = 1; }
+        }
+        // the filter's global mirror (helpers' sweeps, next fill's K1 hints)
+        for (int u = 0; u < 2; u++) {
+            const int32_t i = mirror[u];
+            if (i >= 0 && a.gkey) { a.gkey[i] = sm->flt.key[i]; a.gep[i] = sm->flt.ep[i]; }
         }
         sm->prof[3] += clock64() - ct0;
         sm->prof[6] += sm->ins.nseg;
