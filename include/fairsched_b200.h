@@ -157,8 +157,10 @@ int fs_trie_export(fs_trie *t, int64_t cap, int64_t *n, int64_t *src, int32_t *s
                    int32_t *end, int32_t *parent, int32_t *ref, int64_t *last_access,
                    uint64_t *wmask);
 
-/* ---- DLPM / LPM worker  (local_policies.py:74-136 + worker.py:87-135) ------
- * policy 0 = Dlpm (deficit gate, quantum refill), 1 = Lpm (gate always true).
+/* ---- DLPM / LPM / VTC worker  (local_policies.py:42-195 + worker.py:87-135) -
+ * policy 0 = Dlpm (deficit gate, quantum refill), 1 = Lpm (gate always true),
+ * 2 = Vtc (least-served client's earliest request first; counters charged the
+ * full input, fs_worker_outputs adds w_q per output token; no match_prefix).
  * The worker owns the queue mirror (request ids), the per-client deficit
  * counters q, refill counts and client_list membership.                     */
 int fs_worker_create(fs_ctx *ctx, fs_trie *tree, int policy, int64_t quantum, int64_t M,
@@ -174,6 +176,9 @@ int fs_worker_check_refill(fs_worker *w, int64_t n, const int32_t *queued_client
 /* Host mirror of q / refill_counts / client_list membership (Dlpm.counters(),
  * local_policies.py:135-136).  Any pointer may be NULL. */
 int fs_worker_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills, uint8_t *known);
+/* Vtc tie-break (local_policies.py:176: clients sorted by (counter, name)):
+ * rank of each dense client id's name; by default the id order. */
+int fs_worker_set_client_ranks(fs_worker *w, int32_t n, const int32_t *ranks);
 int fs_worker_set_counter(fs_worker *w, int32_t client, int64_t q);
 /* Grow the client tables (clients are dense ids assigned by the caller). */
 int fs_worker_reserve_clients(fs_worker *w, int32_t max_clients);
@@ -241,6 +246,16 @@ int fs_worker_queue_len(fs_worker *w, int64_t *n);
 int fs_dispatcher_create(fs_ctx *ctx, int D, int64_t quantum, int64_t w_e, int64_t w_q,
                          int32_t max_clients, fs_dispatcher **out);
 int fs_dispatcher_destroy(fs_dispatcher *d);
+/* Routing policy of a dispatcher (default FS_DISPATCH_D2LPM).
+ * FS_DISPATCH_THRESHOLD: ThresholdRouter (global_policies.py:135-161) on the
+ * same tagged index -- locality when match_len / input_len >= theta (IEEE
+ * double, like Python), else the least-loaded worker; no deficit counters
+ * (fs_dispatch leaves q untouched, fs_dispatch_finish only decrements the
+ * worker's queue size).  Errors: FS_ERR_INVALID for an unknown policy or
+ * theta outside [0, 1] (global_policies.py:145-146). */
+#define FS_DISPATCH_D2LPM 0
+#define FS_DISPATCH_THRESHOLD 1
+int fs_dispatcher_set_policy(fs_dispatcher *d, int32_t policy, double theta);
 fs_trie *fs_dispatcher_tree(fs_dispatcher *d);
 /* Dispatcher.dispatch for n arrivals in order (global_policies.py:40-46,
  * 107-124): longest_match_workers, SelectWorker with closed-form refill,

@@ -102,6 +102,8 @@ SIGNATURES = {
     "fs_worker_last_phases": (C.c_int, [vp, PF]),
     "fs_worker_set_option": (C.c_int, [vp, C.c_int, i64]),
     "fs_worker_last_stats": (C.c_int, [vp, P64]),
+    "fs_dispatcher_set_policy": (C.c_int, [vp, C.c_int32, C.c_double]),
+    "fs_worker_set_client_ranks": (C.c_int, [vp, C.c_int32, P32]),
     "fs_worker_last_stats_ext": (C.c_int, [vp, P64]),
     "fs_launch_count": (i64, []),
     "fs_worker_queue_len": (C.c_int, [vp, P64]),

@@ -1441,6 +1441,227 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     }
 }
 
+// ---------------------------------------------------------------- VTC fill
+// Vtc.fill (local_policies.py:170-189): repeatedly serve the least-served
+// client -- clients in (counter, name) order, each offering its earliest
+// queued request (arrival, rid); the first whose head passes can_add
+// (worker.py:101-110, closed form len - B <= slack) is admitted (probe,
+// insert, pin, radix.py:187-192) and charged its full input (cache-oblivious,
+// local_policies.py:184-186); stop when no head fits.  VTC never calls
+// match_prefix, so nothing is stamped besides the inserts.  One CTA: 16 warps
+// test 16 clients' heads per round (exact pinned coverage by a read-only
+// walk); the earliest passing one in client order is admitted.
+#define VTC_MAXC 2048
+struct VtcArgs {
+    TrieView t;
+    int32_t n;                 // queued requests (label order = (arrival, rid) order)
+    const int32_t *queue;
+    const int32_t *rclient, *rlen;
+    const int64_t *roff;
+    int64_t *q;                // per-client virtual counters
+    const int32_t *rank;       // rank of the client's name (sorted() tie-break)
+    int32_t nclients;
+    int32_t *head;             // [nclients] scratch: queue position of each client's head (FS_NONE: none)
+    const int32_t *dl_client;  // counter deltas to apply first (host-side on_outputs / lifts)
+    const int64_t *dl_delta;
+    int32_t ndl;
+    int64_t M, R, gen_total, headroom0, w_e, now, sq_base;
+    Seg *segs;
+    int8_t *rstate;
+    int32_t *adm_req, *adm_mlen, *adm_node;
+    int64_t *adm_unp, *adm_pinb, *adm_rec_end;
+    int32_t adm_cap;
+    int64_t *hdr;
+};
+struct VtcSmem {
+    InsertSmem ins;
+    ChunkLRU lru;
+    int64_t key[VTC_MAXC];   // counter of the client at sorted position i
+    int32_t rk[VTC_MAXC];    // its name rank
+    int32_t cl[VTC_MAXC];    // the client
+    int32_t nact;            // active clients (with a queued head), sorted prefix of the arrays
+    int32_t pass[16];        // this round's verdicts, by warp
+    int32_t cov[16];
+    int32_t red32[32];
+    int64_t headroom;
+    int32_t nadm, stop, best;
+};
+
+__device__ __forceinline__ bool vtc_less(int64_t k1, int32_t r1, int64_t k2, int32_t r2) {
+    return k1 < k2 || (k1 == k2 && r1 < r2);
+}
+
+__global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_vtc(VtcArgs ap) {
+    extern __shared__ __align__(16) unsigned char fs_smraw[];
+    VtcSmem &sm = *reinterpret_cast<VtcSmem *>(fs_smraw);
+    __shared__ VtcArgs a_sh;
+    __shared__ TrieScalars sc_sh;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        a_sh = ap;
+        sc_sh = *ap.t.sc;
+        a_sh.t.sc = &sc_sh;
+        for (int32_t i = 0; i < ap.ndl; i++) ap.q[ap.dl_client[i]] += ap.dl_delta[i];
+        sc_sh.nrec = 0;
+        sm.nadm = 0; sm.stop = 0; sm.nact = 0;
+        sm.headroom = ap.headroom0;
+        sm.ins.prof = nullptr; sm.ins.prof2 = nullptr; sm.ins.fev = nullptr;
+        sm.ins.lru = &sm.lru; sm.ins.lru_spare = nullptr; sm.ins.ev.pops = 0;
+        for (int i = 0; i < 4; i++) sm.lru.prof[i] = 0;
+        ap.hdr[2] = FS_OK;
+    }
+    __syncthreads();
+    const VtcArgs &a = a_sh;
+    const TrieView &t = a.t;
+    // every client's head: its first queued position (the queue is in (arrival, rid) order)
+    for (int32_t c = tid; c < a.nclients; c += blockDim.x) a.head[c] = FS_NONE;
+    __syncthreads();
+    for (int32_t p = tid; p < a.n; p += blockDim.x) atomicMin(&a.head[a.rclient[a.queue[p]]], p);
+    __syncthreads();
+    block_chunk_build(t, &sm.lru);
+    // active clients in (counter, name rank) order
+    for (int32_t c = tid; c < a.nclients; c += blockDim.x) {
+        if (a.head[c] != FS_NONE) {
+            const int32_t k = atomicAdd(&sm.nact, 1);
+            if (k < VTC_MAXC) { sm.key[k] = a.q[c]; sm.rk[k] = a.rank[c]; sm.cl[k] = c; }
+        }
+    }
+    __syncthreads();
+    if (sm.nact > VTC_MAXC) {
+        if (tid == 0) { a.hdr[2] = FS_ERR_INVALID; a.hdr[0] = 0; a.hdr[1] = 0; }
+        return;
+    }
+    {
+        const int32_t na = sm.nact;
+        int32_t P2 = 1;
+        while (P2 < na) P2 <<= 1;
+        for (int32_t i = na + tid; i < P2; i += blockDim.x) { sm.key[i] = INT64_MAX; sm.rk[i] = INT32_MAX; sm.cl[i] = -1; }
+        __syncthreads();
+        for (int32_t k = 2; k <= P2; k <<= 1)
+            for (int32_t j = k >> 1; j > 0; j >>= 1) {
+                for (int32_t i = tid; i < P2; i += blockDim.x) {
+                    const int32_t l = i ^ j;
+                    if (l > i) {
+                        const bool up = (i & k) == 0;
+                        if (vtc_less(sm.key[l], sm.rk[l], sm.key[i], sm.rk[i]) == up) {
+                            const int64_t x = sm.key[i]; sm.key[i] = sm.key[l]; sm.key[l] = x;
+                            int32_t y = sm.rk[i]; sm.rk[i] = sm.rk[l]; sm.rk[l] = y;
+                            y = sm.cl[i]; sm.cl[i] = sm.cl[l]; sm.cl[l] = y;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+    }
+    while (!sm.stop) {
+        // the first client, in order, whose head passes can_add
+        int64_t slack;
+        {
+            const int64_t pinned = t.sc->pinned;
+            slack = a.M - a.gen_total - sm.headroom - a.R - pinned;  // worker.py:104-107
+            const int64_t cap = t.sc->capacity;
+            if (cap >= 0 && cap - pinned < slack) slack = cap - pinned;  // worker.py:108-109
+        }
+        int32_t found = -1;
+        for (int32_t g = 0; g < sm.nact && found < 0; g += 16) {
+            if (warp < 16) {
+                const int32_t i = g + warp;
+                int32_t ok = 0, cv = 0;
+                if (i < sm.nact) {
+                    const int32_t r = a.queue[a.head[sm.cl[i]]];
+                    const int32_t len = a.rlen[r];
+                    const WalkOut w = warp_walk<8>(t, t.arena + a.roff[r], len, lane, nullptr, true);
+                    cv = w.cov;
+                    ok = (int64_t)(len - w.cov) <= slack;
+                }
+                if (lane == 0) { sm.pass[warp] = ok; sm.cov[warp] = cv; }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                sm.best = -1;
+                for (int k = 0; k < 16 && g + k < sm.nact; k++)
+                    if (sm.pass[k]) { sm.best = g + k; break; }
+            }
+            __syncthreads();
+            found = sm.best;
+            __syncthreads();
+        }
+        if (found < 0) break;
+        // admit the head of client cl[found] (Worker.try_admit -> RadixTree.admit)
+        const int32_t c = sm.cl[found];
+        const int32_t hp = a.head[c];
+        const int32_t r = a.queue[hp];
+        const int32_t len = a.rlen[r];
+        const int64_t off = a.roff[r];
+        __shared__ int64_t pinb;
+        if (tid == 0) pinb = t.sc->pinned;
+        __syncthreads();
+        auto on_walk = [&](int) {
+            const InsertSmem &in = sm.ins;
+            if (in.status != FS_OK) return;
+            const int64_t need = len - in.cov;
+            t.sc->pinned += need;
+            if (need > slack || in.unpinned != (int64_t)(in.mlen - in.cov)) { a.hdr[2] = FS_ERR_INTERNAL; sm.stop = 1; }
+        };
+        block_insert(t, off, len, a.now, a.sq_base + sm.nadm, -1, a.segs, &sm.ins, -1, -1, true, on_walk, NoHook());
+        if (tid == 0) {
+            const InsertSmem &in = sm.ins;
+            if (in.status != FS_OK) {
+                a.hdr[2] = in.status;
+                sm.stop = 1;
+            } else {
+                const int32_t e = sm.nadm;
+                if (e < a.adm_cap) {
+                    a.adm_req[e] = r; a.adm_mlen[e] = in.mlen; a.adm_unp[e] = in.unpinned;
+                    a.adm_pinb[e] = pinb; a.adm_node[e] = in.deepest; a.adm_rec_end[e] = t.sc->nrec;
+                }
+                sm.nadm = e + 1;
+                a.rstate[r] = 2;
+                a.q[c] += a.w_e * (int64_t)len;  // the full input (local_policies.py:184-186)
+                sm.headroom += a.R;
+                if (t.sc->status != FS_OK) { a.hdr[2] = t.sc->status; sm.stop = 1; }
+            }
+        }
+        __syncthreads();
+        if (sm.stop) break;
+        // the client's next head: its next queued position
+        {
+            int32_t mine = FS_NONE;
+            for (int32_t p = hp + 1 + tid; p < a.n && mine == FS_NONE; p += blockDim.x)
+                if (a.rclient[a.queue[p]] == c) mine = p;
+            const int32_t nh = block_min_i32(mine, sm.red32);
+            if (tid == 0) a.head[c] = nh;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // re-place the client: its counter only grew; drop it when its queue is empty
+            int32_t i = found;
+            if (a.head[c] == FS_NONE) {
+                for (; i + 1 < sm.nact; i++) { sm.key[i] = sm.key[i + 1]; sm.rk[i] = sm.rk[i + 1]; sm.cl[i] = sm.cl[i + 1]; }
+                sm.nact--;
+            } else {
+                const int64_t kk = a.q[c];
+                const int32_t rr = sm.rk[i];
+                while (i + 1 < sm.nact && vtc_less(sm.key[i + 1], sm.rk[i + 1], kk, rr)) {
+                    sm.key[i] = sm.key[i + 1]; sm.rk[i] = sm.rk[i + 1]; sm.cl[i] = sm.cl[i + 1];
+                    i++;
+                }
+                sm.key[i] = kk; sm.rk[i] = rr; sm.cl[i] = c;
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.hdr[0] = sm.nadm;
+        a.hdr[1] = t.sc->nrec;
+        a.hdr[3] = sm.nadm;
+        for (int i = 4; i < 32; i++) a.hdr[i] = 0;
+        a.hdr[13] = sm.ins.ev.pops;
+        *ap.t.sc = sc_sh;
+    }
+}
+
 // ---------------------------------------------------------------- per-call ops
 enum { OP_INSERT = 1, OP_ADMIT, OP_PIN, OP_UNPIN, OP_EVICT, OP_LMW, OP_NOTIFY };
 
@@ -1571,7 +1792,22 @@ struct DispArgs {
     uint64_t *out_mask;
     int64_t *out_rounds;
     int64_t *hdr;
+    int32_t policy;  // 0: D2lpm (global_policies.py:88-132); 1: ThresholdRouter (135-161)
+    double theta;
 };
+
+// ThresholdRouter.select (global_policies.py:149-155) + _min_queue (57-58):
+// locality when the matched fraction reaches theta (the same IEEE double
+// division as Python's `match_len / input_len`), else the least loaded worker.
+__device__ inline int threshold_select(const DispArgs &a, int32_t mlen, int32_t len, uint64_t mask) {
+    const bool local = mask != 0ull && len > 0 && (double)mlen / (double)len >= a.theta;
+    int best = -1;
+    for (int w2 = 0; w2 < a.D; w2++) {
+        if (local && !((mask >> w2) & 1ull)) continue;
+        if (best < 0 || a.qsize[w2] < a.qsize[best]) best = w2;
+    }
+    return best;
+}
 
 // D2lpm.select_worker (global_policies.py:107-114) + Dispatcher._min_queue
 // (57-58).  The refill loop adds Q_w to every worker per round: k rounds in
@@ -1714,14 +1950,21 @@ __global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a)
                 const int32_t deepest = w.mlen > 0 ? w.last : -1;
                 if (deepest > 0) stamp_node(t, deepest, now, a.sq_base + 2 * (int64_t)i);
                 const uint64_t mask = deepest > 0 ? t.wmask[deepest] : 0ull;
-                int64_t rounds;
+                int64_t rounds = 0;
                 const int32_t cl = s_cl[k];
-                const int best = d2_select(a, cl, mask, &rounds);
-                int64_t *qr = a.q + (int64_t)cl * a.D;
-                a.qsize[best] += 1;
-                qr[best] -= a.w_e * (int64_t)len;  // after_dispatch: full input (global_policies.py:123)
-                a.qset[(int64_t)cl * a.D + best] = 1;
-                s_w = best; s_mlen = deepest > 0 ? w.mlen : 0; s_mask = mask;
+                const int32_t ml = deepest > 0 ? w.mlen : 0;
+                int best;
+                if (a.policy == 1) {
+                    best = threshold_select(a, ml, len, mask);
+                    a.qsize[best] += 1;  // Dispatcher.dispatch (global_policies.py:42)
+                } else {
+                    best = d2_select(a, cl, mask, &rounds);
+                    int64_t *qr = a.q + (int64_t)cl * a.D;
+                    a.qsize[best] += 1;
+                    qr[best] -= a.w_e * (int64_t)len;  // after_dispatch: full input (global_policies.py:123)
+                    a.qset[(int64_t)cl * a.D + best] = 1;
+                }
+                s_w = best; s_mlen = ml; s_mask = mask;
                 a.out_rounds[i] = rounds;
             }
         }

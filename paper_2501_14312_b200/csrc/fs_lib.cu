@@ -1079,6 +1079,9 @@ struct fs_worker {
     DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
     DBuf<SweepCtl> ctl;
+    DBuf<int32_t> vrank, vhead;  // VTC: client name ranks, per-client head scratch
+    std::vector<int32_t> h_vrank;
+    bool vrank_dirty = true;
     DBuf<FevCtl> fev_ctl;          // asynchronous cold eviction (k_schedule CTA 1)
     DBuf<int64_t> fev_need, fev_rec_end;
     DBuf<int32_t> fev_free;
@@ -1137,7 +1140,7 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
                                 int64_t output_reserve, int64_t w_e, int64_t w_q, int32_t max_clients,
                                 fs_worker **out) {
     if (!c || !tree || !out || tree->ctx != c) return fail(FS_ERR_INVALID, "bad arguments");
-    if (policy != 0 && policy != 1) return fail(FS_ERR_INVALID, "policy must be 0 (dlpm) or 1 (lpm)");
+    if (policy != 0 && policy != 1 && policy != 2) return fail(FS_ERR_INVALID, "policy must be 0 (dlpm), 1 (lpm) or 2 (vtc)");
     if (policy == 0 && quantum <= 0) return fail(FS_ERR_INVALID, "quantum must be positive");  // local_policies.py:81-82
     if (max_clients <= 0) return fail(FS_ERR_INVALID, "max_clients must be positive");
     // a Worker owns its cache (worker.py:72): a second scheduler on the same
@@ -1178,7 +1181,7 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
     w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->fev_ctl.release(); w->fev_need.release(); w->fev_rec_end.release(); w->fev_free.release(); w->fev_vrec.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->vrank.release(); w->vhead.release(); w->fev_ctl.release(); w->fev_need.release(); w->fev_rec_end.release(); w->fev_free.release(); w->fev_vrec.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1211,8 +1214,9 @@ extern "C" int fs_worker_outputs(fs_worker *w, int64_t n, const int32_t *clients
     for (int64_t i = 0; i < n; i++) {
         const int32_t cl = clients[i];
         if (cl < 0 || cl >= w->nclients) return fail(FS_ERR_INVALID, "client id %d out of range", cl);
-        if (w->policy != 0) continue;
-        const int64_t d = -w->w_q * counts[i];
+        if (w->policy == 1) continue;  // Lpm keeps no counters
+        // Dlpm.on_outputs subtracts (local_policies.py:130-133), Vtc.on_outputs adds (191-194)
+        const int64_t d = (w->policy == 2 ? 1 : -1) * w->w_q * counts[i];
         w->h_q[cl] += d;  // mirror; the device applies the same delta at the next fill
         w->dl_client.push_back(cl);
         w->dl_delta.push_back(d);
@@ -1276,6 +1280,15 @@ extern "C" int fs_worker_set_counter(fs_worker *w, int32_t client, int64_t qv) {
     w->h_q[client] = qv;
     w->dl_client.push_back(client);
     w->dl_delta.push_back(d);
+    return FS_OK;
+}
+
+extern "C" int fs_worker_set_client_ranks(fs_worker *w, int32_t n, const int32_t *ranks) {
+    if (w && w->inflight) return fail(FS_ERR_INVALID, "a fill is in flight (call fs_worker_fill_end first)");
+    if (!w || n < 0 || (n > 0 && !ranks)) return fail(FS_ERR_INVALID, "bad arguments");
+    if ((int64_t)w->h_vrank.size() < n) w->h_vrank.resize(n);
+    for (int32_t i = 0; i < n; i++) w->h_vrank[i] = ranks[i];
+    w->vrank_dirty = true;
     return FS_OK;
 }
 
@@ -1442,6 +1455,56 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     }
     CK(cudaMemsetAsync(w->alg.p, 0, 128 * sizeof(int64_t), s));
     CK(cudaEventRecord(w->ev[1], s));
+    if (w->policy == 2) {
+        // Vtc.fill (local_policies.py:170-189): no match_prefix, no LPM sort
+        CK(cudaEventRecord(w->ev[2], s));
+        CK(cudaEventRecord(w->ev[3], s));
+        if ((int64_t)w->h_vrank.size() < w->nclients) {
+            // default tie-break: dense client id order
+            for (int32_t i = (int32_t)w->h_vrank.size(); i < w->nclients; i++) w->h_vrank.push_back(i);
+            w->vrank_dirty = true;
+        }
+        TRY(dgrow(w->vrank, w->nclients, s)); TRY(dgrow(w->vhead, w->nclients, s));
+        if (w->vrank_dirty) {
+            CK(cudaMemcpyAsync(w->vrank.p, w->h_vrank.data(), sizeof(int32_t) * w->nclients, cudaMemcpyHostToDevice, s));
+            w->vrank_dirty = false;
+        }
+        VtcArgs v{};
+        v.t = view(t);
+        v.n = (int32_t)n; v.queue = w->queue.p; v.rclient = c->rclient.p; v.rlen = c->rlen.p; v.roff = c->roff.p;
+        v.q = w->q.p; v.rank = w->vrank.p; v.nclients = w->nclients; v.head = w->vhead.p;
+        v.dl_client = w->dlc.p; v.dl_delta = w->dld.p; v.ndl = ndl;
+        v.M = w->M; v.R = w->R; v.gen_total = generated_total; v.headroom0 = headroom; v.w_e = w->w_e; v.now = now;
+        v.sq_base = t->opseq + 1;
+        v.segs = t->segs.p; v.rstate = c->rstate.p;
+        v.adm_req = w->adm_req.p; v.adm_mlen = w->adm_mlen.p; v.adm_node = w->adm_node.p;
+        v.adm_unp = w->adm_unp.p; v.adm_pinb = w->adm_pinb.p; v.adm_rec_end = w->adm_rec_end.p;
+        v.adm_cap = (int32_t)w->adm_req.cap;
+        v.hdr = w->hdr.p;
+        {
+            static std::mutex vmu;
+            static bool vset[64] = {false};
+            std::lock_guard<std::mutex> lk(vmu);
+            if (c->device < 0 || c->device >= 64) return fail(FS_ERR_INVALID, "device index %d", c->device);
+            if (!vset[c->device]) {
+                CK(cudaFuncSetAttribute(k_vtc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(VtcSmem)));
+                vset[c->device] = true;
+            }
+        }
+        k_vtc<<<1, FS_SCHED_THREADS, sizeof(VtcSmem), s>>>(v);
+        counted();
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(w->ev[4], s));
+        w->dl_client.clear(); w->dl_delta.clear();
+        CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(w->h_hdr.p + 32, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        w->inflight = true;
+        t->busy = true;
+        w->f_n = n;
+        w->f_launches0 = launches0;
+        w->f_h0 = h0; w->f_h1 = h1; w->f_h2 = std::chrono::steady_clock::now();
+        return FS_OK;
+    }
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
     if (n > 0) {
         static int k1_blocks_dev[64] = {0};
@@ -1735,6 +1798,8 @@ struct fs_dispatcher {
     int D = 1;
     int64_t quantum = 1, w_e = 1, w_q = 2;
     int32_t nclients = 0;
+    int32_t policy = 0;   // FS_DISPATCH_D2LPM / FS_DISPATCH_THRESHOLD
+    double theta = 0.5;
     std::vector<int64_t> h_q, h_qsize;
     std::vector<uint8_t> h_qset;
     std::vector<int32_t> dl_idx, dl_w;
@@ -1854,6 +1919,7 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     }
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
+    a.policy = d->policy; a.theta = d->theta;
     k_dispatch<<<1, FS_DISPATCH_THREADS, 0, s>>>(a);
     counted();
     CK(cudaGetLastError());
@@ -1884,13 +1950,23 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
         const int32_t wk = out_worker[i];
         int64_t *qr = d->h_q.data() + (int64_t)cl * d->D;
         uint8_t *qs = d->h_qset.data() + (int64_t)cl * d->D;
+        d->h_qsize[wk] += 1;
+        if (out_rounds) out_rounds[i] = rounds[i];
+        if (d->policy != FS_DISPATCH_D2LPM) continue;  // ThresholdRouter keeps no counters
         if (rounds[i] > 0)
             for (int x = 0; x < d->D; x++) { qr[x] += rounds[i] * d->quantum; qs[x] = 1; }
-        d->h_qsize[wk] += 1;
         qr[wk] -= d->w_e * c->h_rlen[req_ids[i]];
         qs[wk] = 1;
-        if (out_rounds) out_rounds[i] = rounds[i];
     }
+    return FS_OK;
+}
+
+extern "C" int fs_dispatcher_set_policy(fs_dispatcher *d, int32_t policy, double theta) {
+    if (!d) return fail(FS_ERR_INVALID, "NULL");
+    if (policy != FS_DISPATCH_D2LPM && policy != FS_DISPATCH_THRESHOLD) return fail(FS_ERR_INVALID, "unknown policy %d", policy);
+    if (!(theta >= 0.0 && theta <= 1.0)) return fail(FS_ERR_INVALID, "theta must be in [0, 1]");  // global_policies.py:145-146
+    d->policy = policy;
+    d->theta = theta;
     return FS_OK;
 }
 
@@ -1898,13 +1974,16 @@ extern "C" int fs_dispatch_finish(fs_dispatcher *d, int32_t client, int32_t work
     if (!d || client < 0 || client >= d->nclients || worker < 0 || worker >= d->D)
         return fail(FS_ERR_INVALID, "bad arguments");
     const int64_t idx = (int64_t)client * d->D + worker;
-    const int64_t dq = -d->w_q * output_tokens;
-    d->h_q[idx] += dq;
-    d->h_qset[idx] = 1;
     d->h_qsize[worker] -= 1;
-    d->dl_idx.push_back((int32_t)idx);
-    d->dl_w.push_back(worker);
-    d->dl_q.push_back(dq);
+    if (d->policy == FS_DISPATCH_D2LPM) {
+        // D2lpm.on_finish (global_policies.py:126-129)
+        const int64_t dq = -d->w_q * output_tokens;
+        d->h_q[idx] += dq;
+        d->h_qset[idx] = 1;
+        d->dl_idx.push_back((int32_t)idx);
+        d->dl_w.push_back(worker);
+        d->dl_q.push_back(dq);
+    }
     d->dl_idx.push_back(-1);  // queue_size[worker] -= 1 (global_policies.py:52)
     d->dl_w.push_back(worker);
     d->dl_q.push_back(-1);

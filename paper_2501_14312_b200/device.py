@@ -310,7 +310,7 @@ class WorkerDev:
     def __init__(self, ctx: Context, trie: Trie, policy: str, quantum: int, M: int, output_reserve: int,
                  w_e: int, w_q: int, max_clients: int = 256):
         h = C.c_void_p()
-        call("fs_worker_create", ctx.handle, trie.handle, 0 if policy == "dlpm" else 1, quantum or 1, M,
+        call("fs_worker_create", ctx.handle, trie.handle, {"dlpm": 0, "lpm": 1, "vtc": 2}[policy], quantum or 1, M,
              output_reserve, w_e, w_q, max_clients, C.byref(h))
         self._h = h
         self.ctx = ctx
@@ -374,6 +374,11 @@ class WorkerDev:
         q = np.zeros(max(n, 1), np.int64); rf = np.zeros(max(n, 1), np.int64)
         call("fs_worker_device_counters", self._h, n, _p64(q), _p64(rf))
         return q[:n], rf[:n]
+
+    def set_client_ranks(self, ranks):
+        """Vtc's name tie-break: rank of each dense client id's name."""
+        r = np.ascontiguousarray(ranks, dtype=np.int32)
+        call("fs_worker_set_client_ranks", self._h, len(r), _p32(r))
 
     def set_k1_full(self, full: bool) -> None:
         """Re-match every queued request from the root each fill (ablation of the
@@ -456,6 +461,10 @@ class DispatcherDev:
         if n > self.max_clients:
             call("fs_dispatcher_reserve_clients", self._h, n)
             self.max_clients = max(n, 2 * self.max_clients)
+
+    def set_policy(self, policy: str, theta: float = 0.5):
+        """"d2lpm" (default) or "threshold" (ThresholdRouter, global_policies.py:135-161)."""
+        call("fs_dispatcher_set_policy", self._h, {"d2lpm": 0, "threshold": 1}[policy], float(theta))
 
     def dispatch(self, ids, clients, nows):
         ids = np.ascontiguousarray(ids, dtype=np.int32)

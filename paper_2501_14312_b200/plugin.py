@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import importlib
 
-from .policies import GpuD2lpm, GpuDlpm, GpuLpm
+from .policies import GpuD2lpm, GpuDlpm, GpuLpm, GpuThresholdRouter, GpuVtc
 from .radix import DeviceRadixTree
 
 _SAVED = {}
@@ -20,7 +20,9 @@ _SAVED = {}
 _BINDINGS = (
     ("fairsched.local_policies", "Dlpm", GpuDlpm),
     ("fairsched.local_policies", "Lpm", GpuLpm),
+    ("fairsched.local_policies", "Vtc", GpuVtc),
     ("fairsched.global_policies", "D2lpm", GpuD2lpm),
+    ("fairsched.global_policies", "ThresholdRouter", GpuThresholdRouter),
     ("fairsched.global_policies", "RadixTree", DeviceRadixTree),
     ("fairsched.worker", "RadixTree", DeviceRadixTree),
     ("fairsched.radix", "RadixTree", DeviceRadixTree),

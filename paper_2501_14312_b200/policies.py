@@ -238,61 +238,164 @@ class GpuDlpm(_GpuLocalPolicy):
         return dict(self.q)
 
 
+class GpuVtc(_GpuLocalPolicy):
+    """Vtc (local_policies.py:139-195): the fill -- least-served client first,
+    its earliest request, can_add, admit, full-input charge -- on the device
+    (k_vtc); the enqueue-time counter lift and the output charge are the
+    reference's host logic, pushed to the device before each fill."""
+
+    name = "vtc"
+    _policy = "vtc"
+
+    def __init__(self):
+        super().__init__(1)
+        self.counter = _TrackedDict()
+        self._ranked = -1
+
+    def _active_clients(self):
+        w = self.worker
+        q = w.queue
+        active = set(q._clients) if hasattr(q, "_clients") else {r.client for r in q}
+        active.update(e.request.client for e in w.batch.values())
+        return active
+
+    def on_request_enqueued(self, req, was_active: bool) -> None:
+        i = req.client  # local_policies.py:158-166
+        if not was_active:
+            others = self._active_clients() - {i}
+            known = [self.counter[j] for j in others if j in self.counter]
+            lift = min(known) if known else 0
+            self.counter[i] = max(self.counter.get(i, 0), lift)
+        else:
+            self.counter.setdefault(i, 0)
+        super().on_request_enqueued(req, was_active)
+
+    def _push_counters(self):
+        dev = self._device()
+        rt = self._rt
+        for c in self.counter.dirty:
+            rt.client_id(c)
+        dev.reserve_clients(len(rt.client_names) + 1)
+        if self._ranked != len(rt.client_names):
+            # sorted(queued, key=(counter, name)) tie-break: the names' order
+            names = rt.client_names
+            order = sorted(range(len(names)), key=lambda k: str(names[k]))
+            ranks = np.zeros(len(names), np.int32)
+            ranks[np.asarray(order, np.int64)] = np.arange(len(names), dtype=np.int32)
+            dev.set_client_ranks(ranks)
+            self._ranked = len(names)
+        for c in self.counter.dirty:
+            if c in self.counter:
+                dev.set_counter(rt.client_id(c), int(self.counter[c]))
+        self.counter.dirty.clear()
+
+    def _pull_counters(self):
+        q, _, _ = self._dev.counters()
+        for c in self.counter:
+            self.counter._set(c, int(q[self._rt.client_id(c)]))
+
+    def on_outputs(self, counts) -> None:
+        """local_policies.py:191-194 (mirror + device delta for the next fill)."""
+        if not counts:
+            return
+        dev = self._device()
+        w_q = self.worker.weights.w_q
+        cids, ns = [], []
+        for client, n in counts.items():
+            self.counter._set(client, self.counter.get(client, 0) + w_q * n)
+            cids.append(self._rt.client_id(client))
+            ns.append(n)
+        dev.outputs(np.asarray(cids, np.int32), np.asarray(ns, np.int64))
+
+    def counters(self):
+        return dict(self.counter)
+
+
 # ---------------------------------------------------------------------------
-# D2LPM dispatcher
+# Routers on the device index (D2LPM, ThresholdRouter)
 # ---------------------------------------------------------------------------
 
 
-class GpuD2lpm:
-    """D2lpm (global_policies.py:88-132) with the routing index, q_{i,w} and the
-    SelectWorker chain on the device."""
+def _arrival_run(now):
+    """The reference runner's pending arrivals at `now`, in processing order.
 
-    name = "d2lpm"
+    Events are processed by (time, kind, seq) (engine.py:106-116) and
+    REQUEST_ARRIVAL ranks first within a timestamp (engine.py:40-45), so the
+    arrivals already queued at `now` are dispatched back to back: no finish,
+    step or eviction notice -- nothing else that touches the dispatcher --
+    can come between them (notices of fills triggered by these arrivals are
+    scheduled events of a later rank).  Found through the runner's `arrive`
+    frame (runner.py:305-317); None when not called from it."""
+    f = sys._getframe(1)
+    for _ in range(4):  # _arrival_run <- dispatch <- arrive
+        f = f.f_back
+        if f is None or f.f_code.co_name == "arrive":
+            break
+    if f is None or f.f_code.co_name != "arrive" or "sim" not in f.f_locals or \
+            not f.f_globals.get("__name__", "").endswith("runner"):
+        return None
+    sim = f.f_locals["sim"]
+    heap = getattr(sim, "_heap", None)
+    if heap is None:
+        return None
+    mod = sys.modules.get("fairsched.requests")
+    req_cls = getattr(mod, "Request", None)
+    run = []
+    for t, kind, seq, ev in heap:
+        if t != now or kind != 0 or getattr(ev, "cancelled", False):
+            continue
+        cb = ev.callback
+        d = getattr(cb, "__defaults__", None)
+        if not d or (req_cls is not None and not isinstance(d[0], req_cls)):
+            return None  # an arrival we cannot identify: no batching
+        run.append((seq, d[0]))
+    run.sort(key=lambda x: x[0])
+    return [r for _, r in run]
+
+
+class _GpuRouter:
+    """Dispatcher protocol (global_policies.py:28-58) over fs_dispatcher: the
+    tagged routing index, queue sizes (and D2LPM's q_{i,w}) on the device.
+
+    dispatch() of the first arrival of a same-timestamp run dispatches the
+    whole run in one device call (parallel batch-start matches,
+    then the serial chain); the following dispatch() calls of that run are
+    answered from it, in order.  Anything else arriving first is refused
+    (RuntimeError) rather than answered from a diverged state."""
+
     uses_global_tree = True
+    _policy = "d2lpm"
 
-    def __init__(self, worker_ids, quantum, weights):
-        if quantum <= 0:
-            raise ValueError("quantum must be positive")
+    def __init__(self, worker_ids, quantum=1, weights=None):
         self.worker_ids = list(worker_ids)
         self.queue_size = _TrackedDict({w: 0 for w in self.worker_ids})
         self.queue_size.dirty.clear()
         self.records = []
-        self.quantum = quantum
-        self.weights = weights
         self.q = _TrackedDict()
         self._ids = sorted(self.worker_ids)   # device worker index order == id order (_min_queue tie-break)
         self._rt = get_runtime()
-        self._dev = DispatcherDev(self._rt.ctx, len(self._ids), quantum, weights.w_e, weights.w_q,
+        w_e, w_q = (weights.w_e, weights.w_q) if weights is not None else (1, 2)
+        self._dev = DispatcherDev(self._rt.ctx, len(self._ids), quantum, w_e, w_q,
                                   max_clients=max(256, len(self._rt.client_names) + 1))
         self.tree = DeviceRadixTree(track_workers=True, n_workers=len(self._ids), runtime=self._rt,
                                     worker_ids=self._ids, _trie=self._dev.trie)
+        self._ahead = []      # (request, now, (wid, mlen, matched)) dispatched ahead, in order
+        self.batched = 0      # arrivals answered from a batch (diagnostic)
 
     # -- mirrors ------------------------------------------------------------
-    def counter(self, client, worker) -> int:
-        return self.q.get((client, worker), 0)
-
     def _cid(self, client) -> int:
         cid = self._rt.client_id(client)
         self._dev.reserve_clients(cid + 1)
         return cid
 
     def _push(self):
-        if self.q.dirty:
-            for key in self.q.dirty:
-                if key in self.q:
-                    c, w = key
-                    self._dev.set_counter(self._cid(c), self._ids.index(w), int(self.q[key]))
-            self.q.dirty.clear()
         if self.queue_size.dirty:
             for w in self.queue_size.dirty:
                 self._dev.set_queue_size(self._ids.index(w), int(self.queue_size[w]))
             self.queue_size.dirty.clear()
 
     def _pull_row(self, client, cid):
-        row, present = self._dev.counters(cid)
-        for i, w in enumerate(self._ids):
-            if present[i]:
-                self.q._set((client, w), int(row[i]))
+        pass
 
     def _mask(self, matched) -> int:
         m = 0
@@ -301,9 +404,105 @@ class GpuD2lpm:
                 m |= 1 << self._ids.index(w)
         return m
 
+    def _guard(self):
+        if self._ahead:
+            raise RuntimeError("dispatcher called between the arrivals of a same-timestamp run it "
+                               "dispatched ahead (not the reference runner's event order)")
+
     # -- protocol -------------------------------------------------------------
+    def select(self, req, now):
+        raise NotImplementedError
+
+    def dispatch(self, req, now):
+        """Dispatcher.dispatch (global_policies.py:40-46) on the device:
+        match, select, queue_size += 1, after_dispatch (D2LPM: q -= w_e*input_len;
+        both: tagged index insert)."""
+        if self._ahead:
+            r0, t0, res = self._ahead[0]
+            if r0 is not req or t0 != now:
+                raise RuntimeError("arrival order differs from the same-timestamp run dispatched ahead")
+            self._ahead.pop(0)
+            self.batched += 1
+        else:
+            run = _arrival_run(now) or []
+            batch = [req] + [r for r in run if r is not req]
+            results = self._dispatch_batch(batch, now)
+            res = results[0]
+            self._ahead = [(r, now, x) for r, x in zip(batch[1:], results[1:])]
+        wid, mlen, matched = res
+        self.queue_size._set(wid, self.queue_size[wid] + 1)
+        rec = _dispatch_record_cls()(req.rid, req.client, wid, mlen, matched, now)
+        self.records.append(rec)
+        return rec
+
+    def _dispatch_batch(self, batch, now):
+        self._push()
+        cids = [self._cid(r.client) for r in batch]
+        dids = [self._rt.upload(r.input_tokens, r.client, r.arrival, r.rid) for r in batch]
+        w, m, mask, _ = self._dev.dispatch(np.asarray(dids, np.int32), np.asarray(cids, np.int32),
+                                           np.full(len(batch), now, np.int64))
+        out = []
+        for k, r in enumerate(batch):
+            wid = self._ids[int(w[k])]
+            matched = tuple(sorted(self._ids[b] for b in range(len(self._ids)) if int(mask[k]) >> b & 1))
+            out.append((wid, int(m[k]), matched))
+        for r, cid in zip(batch, cids):
+            self._pull_row(r.client, cid)
+        return out
+
+    def after_dispatch(self, req, wid, now) -> None:
+        self._guard()
+        self.tree.insert(req.input_tokens, now=now, worker=wid)
+
+    def on_finish(self, client, worker, output_tokens, now) -> None:
+        """Dispatcher.on_finish (global_policies.py:51-52) (+ D2lpm's charge)."""
+        self._guard()
+        self._push()
+        self._dev.finish(self._cid(client), self._ids.index(worker), output_tokens)
+        self.queue_size._set(worker, self.queue_size[worker] - 1)
+
+    def on_eviction(self, path, keep_len, worker, notice_time, now) -> None:
+        self._guard()
+        self.tree.evict_notify(path, worker, keep_len, notice_time)
+
+    def _min_queue(self, candidates) -> int:
+        return min(candidates, key=lambda w: (self.queue_size[w], w))
+
+
+class GpuD2lpm(_GpuRouter):
+    """D2lpm (global_policies.py:88-132) with the routing index, q_{i,w} and the
+    SelectWorker chain on the device."""
+
+    name = "d2lpm"
+
+    def __init__(self, worker_ids, quantum, weights):
+        if quantum <= 0:
+            raise ValueError("quantum must be positive")
+        super().__init__(worker_ids, quantum, weights)
+        self.quantum = quantum
+        self.weights = weights
+
+    def counter(self, client, worker) -> int:
+        return self.q.get((client, worker), 0)
+
+    def _push(self):
+        if self.q.dirty:
+            for key in self.q.dirty:
+                if key in self.q:
+                    c, w = key
+                    self._dev.set_counter(self._cid(c), self._ids.index(w), int(self.q[key]))
+            self.q.dirty.clear()
+        super()._push()
+
+    def _pull_row(self, client, cid):
+        row, present = self._dev.counters(cid)
+        for i, w in enumerate(self._ids):
+            if present[i]:
+                self.q._set((client, w), int(row[i]))
+
     def select_worker(self, matched, client) -> int:
         """global_policies.py:107-114 on the device."""
+        self._guard()
         self._push()
         cid = self._cid(client)
         idx, _ = self._dev.select(cid, self._mask(matched))
@@ -311,28 +510,14 @@ class GpuD2lpm:
         return self._ids[idx]
 
     def select(self, req, now):
+        self._guard()
         match_len, matched = self.tree.longest_match_workers(req.input_tokens, now=now)
         wid = self.select_worker(matched, req.client)
         return wid, match_len, matched
 
-    def dispatch(self, req, now):
-        """Dispatcher.dispatch (global_policies.py:40-46) as one device call:
-        match, SelectWorker, queue_size += 1, q -= w_e*input_len, index insert."""
-        self._push()
-        cid = self._cid(req.client)
-        did = self._rt.upload(req.input_tokens, req.client, req.arrival, req.rid)
-        w, m, mask, _ = self._dev.dispatch(np.array([did], np.int32), np.array([cid], np.int32),
-                                           np.array([now], np.int64))
-        wid = self._ids[int(w[0])]
-        matched = tuple(sorted(self._ids[b] for b in range(len(self._ids)) if int(mask[0]) >> b & 1))
-        self.queue_size._set(wid, self.queue_size[wid] + 1)
-        self._pull_row(req.client, cid)
-        rec = _dispatch_record_cls()(req.rid, req.client, wid, int(m[0]), matched, now)
-        self.records.append(rec)
-        return rec
-
     def after_dispatch(self, req, wid, now) -> None:
         """global_policies.py:121-124 (only reached when called directly)."""
+        self._guard()
         key = (req.client, wid)
         self.q[key] = self.counter(req.client, wid) - self.weights.w_e * req.input_len
         self._push()
@@ -340,16 +525,33 @@ class GpuD2lpm:
 
     def on_finish(self, client, worker, output_tokens, now) -> None:
         """global_policies.py:126-129 + Dispatcher.on_finish (51-52)."""
-        self._push()
-        self._dev.finish(self._cid(client), self._ids.index(worker), output_tokens)
+        super().on_finish(client, worker, output_tokens, now)
         self.q._set((client, worker), self.counter(client, worker) - self.weights.w_q * output_tokens)
-        self.queue_size._set(worker, self.queue_size[worker] - 1)
-
-    def on_eviction(self, path, keep_len, worker, notice_time, now) -> None:
-        self.tree.evict_notify(path, worker, keep_len, notice_time)
-
-    def _min_queue(self, candidates) -> int:
-        return min(candidates, key=lambda w: (self.queue_size[w], w))
 
 
-__all__ = ["GpuDlpm", "GpuLpm", "GpuD2lpm", "DispatchRecord", "EvictedPath"]
+class GpuThresholdRouter(_GpuRouter):
+    """ThresholdRouter (global_policies.py:135-161): locality when the matched
+    fraction of the input reaches theta, else the least-loaded worker -- the
+    match, the select and the tagged insert in the device dispatch chain
+    (fs_dispatcher_set_policy FS_DISPATCH_THRESHOLD), batched like D2LPM."""
+
+    name = "threshold"
+
+    def __init__(self, worker_ids, theta):
+        if not 0.0 <= theta <= 1.0:
+            raise ValueError("theta must be in [0, 1]")
+        super().__init__(worker_ids)
+        self.theta = theta
+        self._dev.set_policy("threshold", theta)
+
+    def select(self, req, now):
+        self._guard()
+        match_len, matched = self.tree.longest_match_workers(req.input_tokens, now=now)
+        if matched and req.input_len > 0 and match_len / req.input_len >= self.theta:
+            wid = self._min_queue(sorted(matched))
+        else:
+            wid = self._min_queue(self.worker_ids)
+        return wid, match_len, matched
+
+
+__all__ = ["GpuDlpm", "GpuLpm", "GpuVtc", "GpuD2lpm", "GpuThresholdRouter", "DispatchRecord", "EvictedPath"]

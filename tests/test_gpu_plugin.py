@@ -61,3 +61,23 @@ def test_event_hash_with_batched_probes(idx, fs, monkeypatch):
     assert any(isinstance(w.queue, hostpath.FastQueue) for w in result.workers)
     assert all(isinstance(w.queue, hostpath.FastQueue) or not w.queue for w in result.workers)
     assert result.log.sha256() == run["event_sha256"]
+
+
+_BURST = load_golden("burst_runs.json")["runs"]
+
+
+@pytest.mark.parametrize("idx", range(len(_BURST)), ids=[r["name"] for r in _BURST])
+def test_same_timestamp_batches(idx, fs):
+    """Arrivals in same-timestamp bursts (tests/golden/make_golden_burst.py):
+    the drop-in dispatcher answers each run of arrivals from ONE device
+    dispatch chain and the reference event hash is unchanged."""
+    from fairsched.requests import Trace, TraceRecord
+    from fairsched.runner import config_from_dict, run_experiment
+    from paper_2501_14312_b200.policies import GpuD2lpm, GpuThresholdRouter
+
+    run = _BURST[idx]
+    cfg = config_from_dict(run["config"])
+    result = run_experiment(cfg, Trace([TraceRecord(**r) for r in run["trace"]]))
+    assert isinstance(result.dispatcher, (GpuD2lpm, GpuThresholdRouter))
+    assert result.log.sha256() == run["event_sha256"]
+    assert result.dispatcher.batched > 0.3 * run["same_time_arrivals"]

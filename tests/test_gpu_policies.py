@@ -1,7 +1,8 @@
 """Plugin-level parity beyond DLPM/LPM/D2LPM: with the drop-in installed every
-worker's RadixTree is the device tree, so VTC / FCFS local policies and the
-rr / per_client_rr / threshold routers (ThresholdRouter walks the device
-global index) run on the GPU through the per-call operations.  The reference's
+worker's RadixTree is the device tree; Vtc's fill is the device kernel k_vtc
+(GpuVtc), ThresholdRouter's dispatch chain runs on the device index
+(GpuThresholdRouter), FCFS and the rr / per_client_rr routers use the device
+tree through the per-call operations.  The reference's
 unchanged runner must reproduce the event-log sha256 and service-gap
 violation counts recorded from the CPU reference
 (tests/golden/make_golden_policies.py), including the config-4 style
@@ -61,10 +62,14 @@ def test_config4_1000_clients(idx, fs):
     from fairsched.runner import config_from_dict, run_experiment
     from paper_2501_14312_b200.radix import DeviceRadixTree
 
+    from paper_2501_14312_b200.policies import GpuDlpm, GpuLpm, GpuVtc
+
     run = C4["runs"][idx]
     cfg = config_from_dict(run["config"])
     result = run_experiment(cfg, Trace([TraceRecord(**r) for r in C4["trace"]]))
     assert all(isinstance(w.tree, DeviceRadixTree) for w in result.workers)
+    cls = {"dlpm": GpuDlpm, "lpm": GpuLpm, "vtc": GpuVtc}[run["config"]["scheduling"]["local_policy"]]
+    assert all(isinstance(w.policy, cls) for w in result.workers)  # the fill runs on the device
     assert result.log.sha256() == run["event_sha256"]
     assert {k: len(v) for k, v in result.violations.items()} == run["violations"]
     assert {k: list(v) for k, v in result.counter_extremes.items()} == run["extremes"]
