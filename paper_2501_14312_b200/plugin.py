@@ -33,13 +33,34 @@ _BINDINGS = (
 _WORKER_SAVED = {}
 
 
-def install(host_fast_path: bool = True) -> None:
-    """Route fairsched's DLPM / LPM / D2LPM / RadixTree through the GPU.
+def install(host_fast_path: bool = True, placement: str = "shared", devices=None) -> None:
+    """Route fairsched's DLPM / LPM / VTC / D2LPM / threshold routing and
+    RadixTree through the GPU.
     host_fast_path: also give workers running these policies the host
-    bookkeeping fast path (paper_2501_14312_b200.hostpath)."""
+    bookkeeping fast path (paper_2501_14312_b200.hostpath).
+    placement: "shared" (one context) or "per_worker" (worker w's cache, queue
+    and counters on devices[w % len(devices)] with its own context, the
+    dispatcher on devices[0]; runtime.set_placement)."""
     from ._lib import load
+    from . import runtime
 
     load()  # fail loudly now if the CUDA extension is missing
+    runtime.set_placement(placement, devices)
+    wmod = importlib.import_module("fairsched.worker")
+    if ("fairsched.worker", "Worker.__init__") not in _SAVED:
+        orig_init = wmod.Worker.__init__
+        _SAVED[("fairsched.worker", "Worker.__init__")] = orig_init
+
+        def __init__(self, sim, wid, *a, **kw):
+            # Worker builds its RadixTree in __init__ (worker.py:72): tell the
+            # device tree whose cache it is
+            runtime.set_current_worker(wid)
+            try:
+                orig_init(self, sim, wid, *a, **kw)
+            finally:
+                runtime.set_current_worker(None)
+        __init__.__wrapped__ = orig_init
+        wmod.Worker.__init__ = __init__
     for mod_name, attr, obj in _BINDINGS:
         mod = importlib.import_module(mod_name)
         key = (mod_name, attr)
@@ -61,8 +82,13 @@ def install(host_fast_path: bool = True) -> None:
 
 def uninstall() -> None:
     for (mod_name, attr), obj in list(_SAVED.items()):
-        setattr(importlib.import_module(mod_name), attr, obj)
+        if attr == "Worker.__init__":
+            importlib.import_module(mod_name).Worker.__init__ = obj
+        else:
+            setattr(importlib.import_module(mod_name), attr, obj)
     _SAVED.clear()
+    from . import runtime
+    runtime.set_placement("shared")
     if _WORKER_SAVED:
         from . import hostpath
         hostpath.uninstall(dict(_WORKER_SAVED))

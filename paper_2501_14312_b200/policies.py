@@ -20,7 +20,7 @@ import numpy as np
 
 from .device import DispatcherDev, WorkerDev
 from .radix import DeviceRadixTree, EvictedPath
-from .runtime import get_runtime
+from .runtime import get_runtime, runtime_for_dispatcher
 
 
 class _TrackedDict(dict):
@@ -373,7 +373,7 @@ class _GpuRouter:
         self.records = []
         self.q = _TrackedDict()
         self._ids = sorted(self.worker_ids)   # device worker index order == id order (_min_queue tie-break)
-        self._rt = get_runtime()
+        self._rt = runtime_for_dispatcher()
         w_e, w_q = (weights.w_e, weights.w_q) if weights is not None else (1, 2)
         self._dev = DispatcherDev(self._rt.ctx, len(self._ids), quantum, w_e, w_q,
                                   max_clients=max(256, len(self._rt.client_names) + 1))

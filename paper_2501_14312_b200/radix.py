@@ -19,7 +19,7 @@ from collections.abc import Sequence
 import numpy as np
 
 from .device import Trie
-from .runtime import get_runtime
+from .runtime import get_runtime, runtime_for_worker, runtime_of_ctx
 
 
 class CacheFull(Exception):
@@ -86,7 +86,8 @@ class DeviceRadixTree:
         self.capacity = capacity
         self.track_workers = track_workers
         self.on_evict = None
-        self._rt = runtime or get_runtime()
+        # a worker's cache lives on that worker's context (plugin placement)
+        self._rt = runtime or (get_runtime() if track_workers else runtime_for_worker())
         self._t = _trie if _trie is not None else Trie(self._rt.ctx, capacity, track_workers,
                                                       n_workers if track_workers else 0)
         self._worker_ids = worker_ids  # tag index -> worker id (global index of a dispatcher)
@@ -218,11 +219,30 @@ class DeviceRadixTree:
     def evict_notify(self, path_tokens, worker, keep_len, notice_time) -> None:
         if isinstance(path_tokens, EvictedPath) and path_tokens._ctx is self._rt.ctx:
             src, n = path_tokens.src, path_tokens.n
+        elif isinstance(path_tokens, EvictedPath) and self._cross_ctx(path_tokens) is not None:
+            # a notice from a worker on another context (per-worker placement):
+            # the path is a prefix of a request both sides hold -- no token copy
+            src, n = self._cross_ctx(path_tokens), path_tokens.n
         else:
             rid = self._rid(path_tokens)
             src, n = self._rt.ctx.request_info(rid)
         w = self._tag(worker) if (self._worker_ids is None or worker in self._worker_ids) else -1
         self._t.evict_notify(src, n, w, keep_len, notice_time)
+
+    def _cross_ctx(self, p):
+        """Arena offset, on this tree's context, of the request whose row holds
+        EvictedPath p on another context (None when unknown here)."""
+        other = runtime_of_ctx(p._ctx)
+        if other is None:
+            return None
+        did = other.did_at(p.src)
+        toks = other.tokens_of(did) if did is not None else None
+        if toks is None:
+            return None
+        mine = self._rt.lookup(toks)
+        if mine is None:
+            mine = self._rt.upload(toks)
+        return int(self._rt.ctx.request_info(mine)[0])
 
     # -- diagnostics (radix.py:306-340) ------------------------------------
     def dump(self):

@@ -12,6 +12,7 @@
 from __future__ import annotations
 
 import os
+import threading
 
 import numpy as np
 from sortedcontainers import SortedList
@@ -72,6 +73,7 @@ class DeviceRuntime:
         self._by_key = {}        # (arrival, rid) -> device id: a request's own row
         self._tok_of_id = {}     # device id -> token tuple it was uploaded from
         self._key_of_id = {}     # device id -> (arrival, rid) label key
+        self._did_at = {}        # arena offset of a request row -> device id
         self._client_of = {}     # device id -> client id stored in the request table
         self.clients = {}        # client name -> dense id
         self.client_names = []
@@ -92,6 +94,10 @@ class DeviceRuntime:
         if hit is not None and hit[1] is tokens:
             return hit[0]
         return None
+
+    def did_at(self, off):
+        """Device id of the request row starting at arena offset `off` (None if unknown)."""
+        return self._did_at.get(int(off))
 
     def tokens_of(self, did):
         """The token tuple a device id was uploaded from (None if unknown)."""
@@ -130,6 +136,7 @@ class DeviceRuntime:
             if self.lookup(tokens) is None:
                 self._by_tuple[id(tokens)] = (did, tokens)
             self._tok_of_id[did] = tokens
+            self._did_at[self.ctx.request_info(did)[0]] = did
             self._client_of[did] = cid
             if key is not None:
                 self._key_of_id[did] = key
@@ -166,15 +173,80 @@ class DeviceRuntime:
 
 _RUNTIMES = {}
 
+# Placement of the drop-in's device state (plugin.install(placement=...)):
+#   "shared"     -- every worker's tree and the dispatcher on one context of
+#                   FS_B200_DEVICE (default);
+#   "per_worker" -- worker w gets its own context on devices[w % len(devices)]
+#                   (one GPU per data-parallel worker, runner.py:272-289), the
+#                   dispatcher its own on devices[0]; eviction notices cross
+#                   contexts by request identity (DeviceRadixTree.evict_notify).
+_PLACEMENT = {"mode": "shared", "devices": None}
+_CURRENT = threading.local()  # worker id whose Worker.__init__ is running (plugin)
 
-def get_runtime(device: int | None = None) -> DeviceRuntime:
+
+def set_placement(mode: str = "shared", devices=None) -> None:
+    if mode not in ("shared", "per_worker"):
+        raise ValueError(f"unknown placement {mode!r}")
+    _PLACEMENT["mode"] = mode
+    _PLACEMENT["devices"] = list(devices) if devices is not None else None
+
+
+def _devices():
+    devs = _PLACEMENT["devices"]
+    if devs:
+        return devs
+    env = os.environ.get("FS_B200_DEVICES")
+    if env:
+        return [int(x) for x in env.split(",") if x.strip()]
+    try:
+        import torch
+        n = torch.cuda.device_count()
+    except Exception:
+        n = 0
+    return list(range(max(n, 1)))
+
+
+def set_current_worker(wid) -> None:
+    _CURRENT.wid = wid
+
+
+def current_worker():
+    return getattr(_CURRENT, "wid", None)
+
+
+def get_runtime(device: int | None = None, key=None) -> DeviceRuntime:
+    """The runtime (context) for `device` (default FS_B200_DEVICE); `key`
+    separates several contexts on one device (per-worker placement)."""
     if device is None:
         device = int(os.environ.get("FS_B200_DEVICE", "0"))
-    rt = _RUNTIMES.get(device)
+    k = (device, key)
+    rt = _RUNTIMES.get(k)
     if rt is None:
         rt = DeviceRuntime(device)
-        _RUNTIMES[device] = rt
+        _RUNTIMES[k] = rt
     return rt
+
+
+def runtime_for_worker(wid=None) -> DeviceRuntime:
+    """Runtime of worker `wid`'s tree (the Worker being built when None)."""
+    wid = current_worker() if wid is None else wid
+    if _PLACEMENT["mode"] != "per_worker" or wid is None:
+        return get_runtime()
+    devs = _devices()
+    return get_runtime(devs[int(wid) % len(devs)], ("worker", int(wid)))
+
+
+def runtime_for_dispatcher() -> DeviceRuntime:
+    if _PLACEMENT["mode"] != "per_worker":
+        return get_runtime()
+    return get_runtime(_devices()[0], ("dispatcher",))
+
+
+def runtime_of_ctx(ctx):
+    for rt in _RUNTIMES.values():
+        if rt.ctx is ctx:
+            return rt
+    return None
 
 
 def reset_runtimes():

@@ -59,6 +59,10 @@ class _FakeCtx:
         self.rows.append((tuple(int(x) for x in toks), cid, lab))
         return len(self.rows) - 1
 
+    def request_info(self, did):
+        off = sum(len(r[0]) for r in self.rows[:did])
+        return off, len(self.rows[did][0])
+
     def set_labels(self, ids, labs):
         pass
 
