@@ -191,6 +191,34 @@ __device__ inline int32_t thread_cov_from_deepest(const TrieView &t, int32_t y, 
     return 0;
 }
 
+// The same, also returning the request's token at the coverage depth (the
+// scheduler's filter key) from the trie side -- the path's tokens equal the
+// request's up to d, so it is the first token of the node that starts there
+// (L2-resident node fields instead of a DRAM read of the request row).
+// tok_d: the request's token at depth d (-1 when d == len).
+__device__ inline int32_t thread_cov_tok_from_deepest(const TrieView &t, int32_t y, int32_t d, int32_t tok_d,
+                                                      int32_t *tok_cov) {
+    int32_t cur = y, tok = tok_d;
+    while (d > 0 && cur > 0) {
+        const int64_t S = t.src[cur];
+        const int32_t c0 = t.ctop[cur];
+        const int32_t X = t.cpar[cur];
+        const int32_t top = t.pos[S + c0];
+        if (t.ref[top] > 0) {
+            int32_t n = cur, prev = -1;
+            while (t.ref[n] == 0) { prev = n; n = t.parent[n]; }
+            const int32_t cv = min(t.end[n], d);
+            *tok_cov = (prev >= 0 && cv < d) ? t.first[prev] : tok;
+            return cv;
+        }
+        tok = t.first[top];  // the path's token at depth c0
+        d = c0;
+        cur = X;
+    }
+    *tok_cov = tok;
+    return 0;
+}
+
 // K1 fast path, one thread per queued request: a request whose hint settles
 // its match (K1Hints: deepest node still cached, miss key not admitted) gets
 // every output here; the others are queued for the warp-per-request walk.
@@ -204,6 +232,11 @@ __global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *_
                                                     int32_t *__restrict__ jobs,
                                                     int32_t *__restrict__ njobs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // the block's deepest nodes already stamped: many queued requests share
+    // their deepest node, and concurrent stores to one line serialize in L2
+    __shared__ int32_t stamped[128];
+    if (threadIdx.x < 128) stamped[threadIdx.x] = -1;
+    __syncthreads();
     bool slow = true;
     if (i < n) {
         const int32_t r = ids[i];
@@ -225,12 +258,26 @@ __global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *_
             if (settled) {
                 slow = false;
                 const int32_t len = rlen[r];
-                const int32_t cov = y > 0 ? thread_cov_from_deepest(t, y, hm) : 0;
-                if (y > 0) stamp_node(t, y, now, sq);
+                int32_t tokc = htok;
+                const int32_t cov = y > 0 ? thread_cov_tok_from_deepest(t, y, hm, htok, &tokc) : 0;
+                if (y > 0) {
+                    uint32_t h = ((uint32_t)y * 2654435761u) >> 25;  // 128 slots
+                    bool mine = false;
+                    for (int probe = 0; probe < 8; probe++) {
+                        const int32_t old = atomicCAS(&stamped[h], -1, y);
+                        if (old == -1) { mine = true; break; }
+                        if (old == y) break;
+                        h = (h + 1) & 127u;
+                        if (probe == 7) mine = true;  // table crowded: stamp anyway (idempotent)
+                    }
+                    if (mine) stamp_node(t, y, now, sq);
+                }
                 out_key[i] = kmax - (uint32_t)hm;
                 out_mlen[i] = hm;
                 out_cov[i] = cov;
-                out_next[i] = cov < len ? t.arena[roff[r] + cov] : -1;
+                // the token at the coverage; with no match (y < 0) the coverage
+                // is 0 and the token is the request's first (its miss token)
+                out_next[i] = cov < len ? (y > 0 ? tokc : htok) : -1;
                 out_s0[i] = y > 0 ? S0 : -1;
                 out_tok0[i] = htok;
             }
