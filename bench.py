@@ -690,6 +690,13 @@ def main():
                                                    "notice_cycles_per_notice", "gpu_launches")}
         subs["config3_d2lpm"]["steps"], subs["config3_d2lpm"]["warmup"] = sub_steps, sub_warm
         del wl3
+        try:
+            # configs[3]'s post-run service-gap checks at 1000 clients
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import verify_bench
+            subs["config4_verifiers"] = verify_bench.run()
+        except Exception as exc:  # needs the unmodified reference's ServiceLog (baseline/_ref)
+            subs["config4_verifiers"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
         line["sub_results"] = subs
     if not args.no_cpu and world == 1:
         q, pool, ncpu = wl.cpu_sample(dev)

@@ -264,6 +264,19 @@ fs_trie *fs_dispatcher_tree(fs_dispatcher *d);
 int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
                 const int64_t *now, int32_t *out_worker, int32_t *out_mlen, uint64_t *out_mask,
                 int64_t *out_rounds);
+/* Multi-GPU dispatch: the batch-start matches of an arrival batch
+ * against the routing index, split across ranks.  fs_dispatch_prematch writes
+ * the records of n arrivals (one rank's slice) to device memory dev_out on the
+ * dispatcher's device -- fs_prematch_record_bytes() bytes each -- and returns
+ * when they are written; the ranks all-gather the slices (NCCL) and each
+ * replica runs fs_dispatch_prematched with the records of the whole batch in
+ * arrival order (dev_pre, device memory).  Same decisions as fs_dispatch,
+ * which computes the records itself. */
+int fs_prematch_record_bytes(void);
+int fs_dispatch_prematch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, void *dev_out);
+int fs_dispatch_prematched(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
+                           const int64_t *now, const void *dev_pre, int32_t *out_worker, int32_t *out_mlen,
+                           uint64_t *out_mask, int64_t *out_rounds);
 /* D2lpm.on_finish (global_policies.py:126-129) */
 int fs_dispatch_finish(fs_dispatcher *d, int32_t client, int32_t worker, int64_t output_tokens);
 /* n finish records in order (the all-gathered finishes of a round) */
@@ -288,6 +301,30 @@ int fs_dispatcher_reserve_clients(fs_dispatcher *d, int32_t max_clients);
 int fs_dispatch_last_profile(fs_dispatcher *d, int64_t *prof16);
 int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t *q, uint8_t *present, int64_t *qsize);
 int fs_worker_device_counters(fs_worker *w, int32_t n, int64_t *q, int64_t *refills);
+
+/* ---- post-run service-gap verifiers  (metrics.py:148-237) ----
+ * Clients are indexed in sorted-name order (metrics.py:144-145).  Client c's
+ * service events are ev_time[ev_off[c] .. ev_off[c+1]) (time-ordered), their
+ * prefix sums ev_cum[ev_off[c] + c .. ev_off[c+1] + c] (n_c + 1 values, first
+ * 0); its backlogged intervals (metrics.py:103-115) iv_lo/iv_hi[iv_off[c] ..
+ * iv_off[c+1]).  Host buffers; the call runs on `device` and returns when the
+ * results are written.
+ * fs_verify_pairs: one result per client pair (f < g) at index f*C + g over the
+ * windows of intersect_intervals x window_grid; mode 0 = |W_f - W_g|
+ * (verify_service_bound_pairwise), mode 1 = max - min over the clients
+ * backlogged through the window (verify_global_max_min).  out_valid = 0: the
+ * pair has no window.  The caller takes the first maximum in pair order. */
+int fs_verify_pairs(int device, int32_t C, const int64_t *ev_off, const int64_t *ev_time, const int64_t *ev_cum,
+                    const int64_t *iv_off, const int64_t *iv_lo, const int64_t *iv_hi, int mode,
+                    int64_t *out_gap, int64_t *out_t1, int64_t *out_t2, int32_t *out_valid);
+/* fs_verify_vs_any (verify_service_bound_vs_nonbacklogged, metrics.py:177-197):
+ * for each of nwin windows (client f, [t1, t2)) in the reference's order, the
+ * worst W_g - W_f over g != f and the first g attaining it (INT64_MIN / -1
+ * when C == 1). */
+int fs_verify_vs_any(int device, int32_t C, const int64_t *ev_off, const int64_t *ev_time, const int64_t *ev_cum,
+                     const int64_t *iv_off, const int64_t *iv_lo, const int64_t *iv_hi, int64_t nwin,
+                     const int32_t *win_f, const int64_t *win_t1, const int64_t *win_t2, int64_t *out_gap,
+                     int32_t *out_g);
 
 #ifdef __cplusplus
 }

@@ -112,6 +112,9 @@ SIGNATURES = {
     "fs_dispatcher_destroy": (C.c_int, [vp]),
     "fs_dispatcher_tree": (vp, [vp]),
     "fs_dispatch": (C.c_int, [vp, i64, P32, P32, P64, P32, P32, PU64, P64]),
+    "fs_prematch_record_bytes": (C.c_int, []),
+    "fs_dispatch_prematch": (C.c_int, [vp, i64, P32, vp]),
+    "fs_dispatch_prematched": (C.c_int, [vp, i64, P32, P32, P64, vp, P32, P32, PU64, P64]),
     "fs_dispatch_finish": (C.c_int, [vp, i32, i32, i64]),
     "fs_dispatch_finish_many": (C.c_int, [vp, i64, P32, P32, P64]),
     "fs_dispatch_counters": (C.c_int, [vp, i32, P64, PU8]),
@@ -122,6 +125,8 @@ SIGNATURES = {
     "fs_dispatcher_reserve_clients": (C.c_int, [vp, i32]),
     "fs_dispatch_last_profile": (C.c_int, [vp, P64]),
     "fs_dispatch_device_counters": (C.c_int, [vp, i64, P64, PU8, P64]),
+    "fs_verify_pairs": (C.c_int, [C.c_int, i32, P64, P64, P64, P64, P64, P64, C.c_int, P64, P64, P64, P32]),
+    "fs_verify_vs_any": (C.c_int, [C.c_int, i32, P64, P64, P64, P64, P64, P64, i64, P32, P64, P64, P64, P32]),
 }
 
 _lib = None

@@ -71,6 +71,21 @@ class TorchComm:
         self.world = dist.get_world_size()
         self.device = device
 
+    def all_gather_tensor(self, t):
+        """Concatenation of every rank's equal-size device tensor t, on t's
+        device (NCCL: one all_gather_into_tensor over NVLink; gloo: through
+        host memory).  Complete when it returns."""
+        torch, dist = self.torch, self.dist
+        if dist.get_backend() == "nccl":
+            out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t)
+        else:
+            parts = [torch.empty(t.numel(), dtype=t.dtype) for _ in range(self.world)]
+            dist.all_gather(parts, t.cpu())
+            out = torch.cat(parts).to(t.device)
+        torch.cuda.current_stream(t.device).synchronize()  # the library reads it on its own stream
+        return out
+
     def all_gather_rows(self, rows: np.ndarray) -> list:
         torch, dist = self.torch, self.dist
         cols = rows.shape[1]
@@ -128,7 +143,11 @@ class ClusterRank:
     def _dispatch(self, arrivals, now, enqueue=True):
         if not arrivals:
             return np.zeros(0, np.int32), []
-        workers = self.be.dispatch(arrivals, now)
+        if self.comm.world > 1 and getattr(self.be, "prematch_partitioned", False):
+            # the batch-start matches split 1/N across the ranks, one all-gather
+            workers = self.be.dispatch(arrivals, now, comm=self.comm)
+        else:
+            workers = self.be.dispatch(arrivals, now)
         mine = [a for a, w in zip(arrivals, workers) if w == self.comm.rank]
         if mine and enqueue:
             self.be.enqueue(mine)
@@ -217,6 +236,26 @@ class ClusterRank:
         return RoundResult(adm, workers, nq, len(arrivals), ms)
 
 
+def partitioned_prematch(d, ids, comm, device):
+    """The batch-start matches of an arrival batch (ids in arrival order), split
+    1/N across the ranks: rank r matches arrivals [r*chunk, (r+1)*chunk) on its
+    replica of the routing index (fs_dispatch_prematch); one all-gather of the
+    fixed-size records hands every replica the whole batch in arrival order.
+    Every replica holds the same index, so every slice is what any replica
+    would have computed.  Returns the gathered device tensor."""
+    import torch
+    from .device import DispatcherDev
+    rec = DispatcherDev.prematch_record_bytes()
+    n = len(ids)
+    chunk = max(1, -(-n // comm.world))
+    lo = min(n, comm.rank * chunk)
+    hi = min(n, lo + chunk)
+    local = torch.zeros(chunk * rec, dtype=torch.uint8, device=f"cuda:{device}")
+    if hi > lo:
+        d.prematch(ids[lo:hi], local.data_ptr())
+    return comm.all_gather_tensor(local)
+
+
 class GpuRank:
     """CUDA backend of one rank: its worker (local trie + DLPM queue) and a
     dispatcher replica, both on this rank's GPU, through the C ABI."""
@@ -236,9 +275,16 @@ class GpuRank:
         self.d = DispatcherDev(self.ctx, D, q_w, w_e, w_q, max_clients=n_clients)
         self.now_dispatch = 0
 
-    def dispatch(self, arrivals, now):
+    prematch_partitioned = True
+
+    def dispatch(self, arrivals, now, comm=None):
         idx = np.asarray(arrivals, np.int64)
-        w, _, _, _ = self.d.dispatch(self.ids[idx], self.q.clients[idx], np.full(len(idx), now, np.int64))
+        nows = np.full(len(idx), now, np.int64)
+        if comm is None:
+            w, _, _, _ = self.d.dispatch(self.ids[idx], self.q.clients[idx], nows)
+        else:
+            pre = partitioned_prematch(self.d, self.ids[idx], comm, self.ctx.device)
+            w, _, _, _ = self.d.dispatch_prematched(self.ids[idx], self.q.clients[idx], nows, pre.data_ptr())
         return w
 
     def enqueue(self, mine):
@@ -335,7 +381,9 @@ class GpuStreamRank:
         self._ensure(int(max(arrivals)) + 1)
         self.upload_s += time.perf_counter() - tu
 
-    def dispatch(self, arrivals, now, batch=1 << 16):
+    prematch_partitioned = True
+
+    def dispatch(self, arrivals, now, batch=1 << 16, comm=None):
         import time
         idx = np.asarray(arrivals, np.int64)
         tu = time.perf_counter()
@@ -345,7 +393,14 @@ class GpuStreamRank:
         out = []
         for a in range(0, len(idx), batch):
             j = idx[a:a + batch]
-            w, _, _, _ = self.d.dispatch(self.ids[j], self.clients[j], np.full(len(j), now, np.int64))
+            nows = np.full(len(j), now, np.int64)
+            if comm is None:
+                w, _, _, _ = self.d.dispatch(self.ids[j], self.clients[j], nows)
+            else:
+                tp = time.perf_counter()
+                pre = partitioned_prematch(self.d, self.ids[j], comm, self.ctx.device)
+                self.prematch_s = getattr(self, "prematch_s", 0.0) + time.perf_counter() - tp
+                w, _, _, _ = self.d.dispatch_prematched(self.ids[j], self.clients[j], nows, pre.data_ptr())
             out.append(w)
             self.disp_prof += self.d.last_profile()
         self.disp_s += time.perf_counter() - t0

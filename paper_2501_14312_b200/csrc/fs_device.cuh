@@ -120,7 +120,7 @@ __device__ inline void h_put(const TrieView &t, int32_t p, int32_t tok, int32_t 
         const uint64_t k = t.hslot[i].x;
         if (k == key) break;
         if (k == FS_HEMPTY || probes++ > t.hmask) {
-            if (tomb >= 0) { i = (uint32_t)tomb; t.sc->tombs--; }
+            if (tomb >= 0) { i = (uint32_t)tomb; atomicSub(&t.sc->tombs, 1); }
             else if (k != FS_HEMPTY) { t.sc->status = FS_ERR_NOMEM; return; }  // table full
             break;
         }
@@ -1039,7 +1039,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
                     hs = t.hslot[hi];
                 }
                 push_record(t, srcb, plen, plen - el);
-                if (hs.x == key) { t.hslot[hi].x = FS_HTOMB; t.sc->tombs++; }
+                if (hs.x == key) { t.hslot[hi].x = FS_HTOMB; atomicAdd(&t.sc->tombs, 1); }
                 int32_t ncP1;
                 if (ASYNC) {
                     ncP1 = atomicSub(&t.nchild[P], 1) - 1;
@@ -1097,6 +1097,7 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
 struct InsertSmem {
     EvictSmem ev;
     int32_t nseg, mlen, new_len, deepest, last, status, cov, split_top;
+    int32_t leaf, leaf_tok;  // scheduler: the new leaf, allocated when the walk ends (-1: not yet)
     int64_t needed, unpinned;
     int64_t *prof;  // optional cycle counters: [1] walk, [2] evict, [5] evict pops
     int64_t *prof2; // scheduler only: [0] pin, [2] waits for the evictor's setup
@@ -1226,6 +1227,27 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             // a fully cached request stamps an existing node: the evictor may be
             // pushing a detached child's stamp into it -- let it finish first
             if (sm->fev && sm->fev->on && !sm->fev_switch && sm->new_len == 0 && w.mlen > 0) sm->fev_wait = 1;
+            // scheduler without FEV: the new leaf's slot, fields, pin and stamp
+            // are set now, so its eviction can run on warp 2 concurrently with
+            // the leaf's hash entry, the path pin and the bookkeeping (see
+            // below).  The leaf's seq does not depend on the eviction (which
+            // allocates none); used_tokens counts it now (the capacity test
+            // after the eviction adjusts).
+            sm->leaf = -1;
+            if (pin_path && sm->lru && !sm->fev && sm->status == FS_OK && sm->new_len > 0) {
+                const int32_t tk = (w.mlen == hint_m0 && hint_tok0 >= 0) ? hint_tok0 : rq[w.mlen];
+                const int32_t leaf = node_new(t, req_off, w.mlen, len, len, last, tk);
+                if (leaf < 0) {
+                    sm->status = FS_ERR_NOMEM;
+                } else {
+                    t.ref[leaf] = 1;  // pinned from birth: never an eviction candidate
+                    t.la[leaf] = now;
+                    t.lseq[leaf] = sq;
+                    t.sc->used += sm->new_len;
+                    sm->leaf = leaf;
+                    sm->leaf_tok = tk;
+                }
+            }
         }
     }
 #if FS_POP_PREFETCH
@@ -1266,10 +1288,16 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
         // (on_walk needs only the walk) and warps 2.. pin the pre-existing
         // path; the leaf's positions follow once it exists (named barrier 1:
         // warps 0 and 2..).
+        // sm->leaf >= 0: warp 2 evicts (below) while warp 0 links the leaf
+        const bool cev = sm->leaf >= 0;
         if (warp == 0) {
             if (lane == 0) {
                 int32_t deepest = sm->mlen > 0 ? sm->last : -1;
-                if (sm->status == FS_OK && sm->new_len > 0) {
+                if (cev) {
+                    h_put(t, sm->last, sm->leaf_tok, sm->leaf);
+                    atomicAdd(&t.nchild[sm->last], 1);  // the eviction warp may decrement it
+                    deepest = sm->leaf;
+                } else if (sm->status == FS_OK && sm->new_len > 0) {
                     const int32_t tk = (sm->mlen == hint_m0 && hint_tok0 >= 0) ? hint_tok0 : rq[sm->mlen];
                     const int32_t leaf = node_new(t, req_off, sm->mlen, len, len, sm->last, tk);
                     if (leaf < 0) {
@@ -1292,33 +1320,50 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                 sm->deepest = deepest;
                 if (sm->prof) sm->prof[13] += clock64() - c1;
             }
-            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32) : "memory");
-        } else if (warp > 1) {
+            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 64) : "memory");
+        } else if (warp == 2) {
+            // RadixTree.evict_lru for this insert (radix.py:149-151), concurrent
+            // with warp 0's hash link and the pin: the path's nodes are internal
+            // or the protected deepest one, the new leaf is pinned, the leaf's
+            // parent's child count is updated atomically by both sides
+            if (cev && sm->needed > 0) {
+                const long long ce = clock64();
+                warp_chunk_evict<true>(t, sm->lru, sm->needed, sm->last, &sm->ev, lane);
+                if (lane == 0 && sm->prof) sm->prof[2] += clock64() - ce;
+            }
+        } else if (warp > 2) {
             // pin the pre-existing path, then point the new leaf's depths at it
             const long long cp = clock64();
-            block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 64);
-            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32) : "memory");
+            block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 96);
+            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 64) : "memory");
             if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0) {
                 // 16-B stores (arena rows, hence their pos rows, are 16-B aligned):
                 // a quarter of the store instructions next to warp 1's bookkeeping
                 int32_t *row = t.pos + req_off;
                 const int32_t v = sm->deepest;
                 const int32_t a0 = sm->mlen, a4 = min(len, (a0 + 3) & ~3), b4 = len & ~3;
-                const int32_t nt = (int32_t)blockDim.x - 64, me = (int32_t)tid - 64;
+                const int32_t nt = (int32_t)blockDim.x - 96, me = (int32_t)tid - 96;
                 if (me < a4 - a0) row[a0 + me] = v;
                 for (int32_t q = a4 / 4 + me; q < b4 / 4; q += nt)
                     reinterpret_cast<int4 *>(row)[q] = make_int4(v, v, v, v);
                 if (b4 >= a4 && me < len - b4) row[b4 + me] = v;
             }
-            if (tid == 64 && sm->prof2) sm->prof2[0] += clock64() - cp;
+            if (tid == 96 && sm->prof2) sm->prof2[0] += clock64() - cp;
         } else if (warp == 1) {
             if (lane == 0) on_walk(0);
             __syncwarp();
             on_side(lane);
         }
-        if (!(sm->needed > 0 && sm->lru)) __syncthreads();
+        if (cev || !(sm->needed > 0 && sm->lru)) __syncthreads();
+        if (cev && sm->needed > 0) {
+            if (tid == 0) {
+                if (sm->last > 0) t.flags[sm->last] &= ~FS_PROTECT;
+                if (t.sc->used > t.sc->capacity) sm->status = FS_ERR_CACHE_FULL;
+            }
+            __syncthreads();
+        }
     }
-    if (sm->needed > 0) {
+    if (sm->needed > 0 && !(pin_path && sm->leaf >= 0)) {
         if (sm->lru) {
             if (warp == 0) warp_chunk_evict(t, sm->lru, sm->needed, sm->last, &sm->ev, lane);
             __syncthreads();

@@ -13,6 +13,7 @@
 //   k_op / k_dispatch single-CTA tree operations and D2LPM dispatch chains.
 #pragma once
 #include "fs_device.cuh"
+#include "fs_scan.cuh"
 
 #ifndef FS_SCHED_THREADS
 #define FS_SCHED_THREADS 512  // 112 registers without spills (1024 threads capped them at 64)
@@ -229,8 +230,9 @@ __global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *_
                                                     int32_t *__restrict__ out_mlen, int32_t *__restrict__ out_cov,
                                                     int32_t *__restrict__ out_next, int64_t *__restrict__ out_s0,
                                                     int32_t *__restrict__ out_tok0, K1Hints hints,
-                                                    int32_t *__restrict__ jobs,
-                                                    int32_t *__restrict__ njobs) {
+                                                    int32_t *__restrict__ jobs, OrderCtl *oc,
+                                                    uint8_t *__restrict__ slow_flag,
+                                                    int64_t *__restrict__ smark, int64_t stag) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // the block's deepest nodes already stamped: many queued requests share
     // their deepest node, and concurrent stores to one line serialize in L2
@@ -280,15 +282,19 @@ __global__ void __launch_bounds__(256) k_match_fast(TrieView t, const int32_t *_
                 out_next[i] = cov < len ? (y > 0 ? tokc : htok) : -1;
                 out_s0[i] = y > 0 ? S0 : -1;
                 out_tok0[i] = htok;
+                // the request keeps its key: K2 moves it with the previous order
+                smark[r] = (stag << 32) | (int64_t)i;
             }
         }
     }
-    // warp-aggregated append of the unsettled positions
+    // the unsettled positions: warp-aggregated append (any order; K2 sorts
+    // them by (key, position)) and a per-position flag (K2's large path)
+    if (i < n) slow_flag[i] = slow ? 1 : 0;
     const unsigned m = __ballot_sync(FS_FULL, i < n && slow);
     if (m) {
         const int lane = threadIdx.x & 31;
         int32_t base = 0;
-        if (lane == __ffs(m) - 1) base = atomicAdd(njobs, __popc(m));
+        if (lane == __ffs(m) - 1) base = atomicAdd(&oc->njobs, __popc(m));
         base = __shfl_sync(FS_FULL, base, __ffs(m) - 1);
         if (i < n && slow) jobs[base + __popc(m & ((1u << lane) - 1))] = (int32_t)i;
     }
@@ -1813,6 +1819,18 @@ __global__ void __launch_bounds__(256) k_notify_many(TrieView t, int32_t n, cons
 }
 
 // ---------------------------------------------------------------- D2LPM
+// Batch-start match of one arrival against the routing index (no stamping):
+// match length, chain of the deepest matched node and the path's source-chain
+// segments.  One fixed-size record per arrival, so ranks can each match a
+// slice of an arrival batch and all-gather the records (fs_dispatch_prematch).
+struct PreRec {
+    int32_t m0;    // match length
+    int32_t nseg;  // segments, -1: more than FS_PRE_SEGS (rebuilt from the chain links)
+    int64_t s0;    // chain (arena row) of the deepest matched node, -1: none
+    Seg segs[FS_PRE_SEGS];
+};
+static_assert(sizeof(PreRec) == 16 + 16 * FS_PRE_SEGS, "PreRec is exchanged as raw bytes");
+
 struct DispArgs {
     TrieView t;
     int32_t n, D;
@@ -1831,10 +1849,7 @@ struct DispArgs {
     const int32_t *dl_w;
     int32_t ndl;
     Seg *segs;
-    const int32_t *m0;  // batch-start match of every arrival (k_dispatch_prematch, no stamp)
-    const int64_t *s0;
-    const Seg *pre_segs;       // its source-chain segments, FS_PRE_SEGS per arrival
-    const int32_t *pre_nseg;   // -1: more than FS_PRE_SEGS (rebuilt from the chain links)
+    const struct PreRec *pre;  // batch-start match of every arrival (k_dispatch_prematch, no stamp)
     int32_t *out_w, *out_mlen;
     uint64_t *out_mask;
     int64_t *out_rounds;
@@ -1888,13 +1903,12 @@ __device__ inline int d2_select(const DispArgs &a, int32_t c, uint64_t mask, int
 // segments still describe [0, m0) when the arrival's turn comes.
 __global__ void __launch_bounds__(256) k_dispatch_prematch(TrieView t, const int32_t *__restrict__ ids, int32_t n,
                                                            const int64_t *__restrict__ roff,
-                                                           const int32_t *__restrict__ rlen, int32_t *out_m0,
-                                                           int64_t *out_s0, Seg *out_segs, int32_t *out_nseg) {
+                                                           const int32_t *__restrict__ rlen, PreRec *out) {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= n) return;
     const int32_t r = ids[i];
-    Seg *my = out_segs + i * FS_PRE_SEGS;
+    Seg *my = out[i].segs;
     int64_t lastS = -1;
     auto store = [&](int64_t S, int32_t a, int32_t b, int32_t k) {
         if (lane == 0 && k < FS_PRE_SEGS) { my[k].S = S; my[k].a = a; my[k].b = b; }
@@ -1902,9 +1916,9 @@ __global__ void __launch_bounds__(256) k_dispatch_prematch(TrieView t, const int
     };
     const WalkOut w = warp_walk_cb<8, decltype(store), true>(t, t.arena + roff[r], rlen[r], lane, false, store);
     if (lane == 0) {
-        out_m0[i] = w.mlen;
-        out_s0[i] = w.mlen > 0 ? lastS : -1;
-        out_nseg[i] = w.nseg <= FS_PRE_SEGS ? w.nseg : -1;
+        out[i].m0 = w.mlen;
+        out[i].s0 = w.mlen > 0 ? lastS : -1;
+        out[i].nseg = w.nseg <= FS_PRE_SEGS ? w.nseg : -1;
     }
 }
 
@@ -1956,7 +1970,7 @@ __global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a)
             for (int32_t j = tid; j < FS_DISP_STAGE && i + j < a.n; j += blockDim.x) {
                 const int32_t r = a.ids[i + j];
                 s_len[j] = a.rlen[r]; s_off[j] = a.roff[r]; s_now[j] = a.nows[i + j];
-                s_s0[j] = a.s0[i + j]; s_m0[j] = a.m0[i + j]; s_cl[j] = a.clients[i + j];
+                s_s0[j] = a.pre[i + j].s0; s_m0[j] = a.pre[i + j].m0; s_cl[j] = a.clients[i + j];
             }
             __syncthreads();
         }
@@ -1991,8 +2005,7 @@ __global__ void __launch_bounds__(FS_DISPATCH_THREADS, 1) k_dispatch(DispArgs a)
             // prefix of the current one: resume from it (warp_walk_hint).
             // (with its segments: block_insert below reuses this walk)
             w = warp_walk_hint<8, false, true>(t, t.arena + off, len, lane, a.segs, hs0, hm0,
-                                                a.pre_segs ? a.pre_segs + (int64_t)i * FS_PRE_SEGS : nullptr,
-                                                a.pre_nseg ? a.pre_nseg[i] : -1);
+                                                a.pre[i].segs, a.pre[i].nseg);
             if (lane == 0) {
                 const int32_t deepest = w.mlen > 0 ? w.last : -1;
                 if (deepest > 0) stamp_node(t, deepest, now, a.sq_base + 2 * (int64_t)i);

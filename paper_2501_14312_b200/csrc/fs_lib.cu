@@ -5,8 +5,6 @@
 // used/pinned tokens).  All decision work runs in the kernels of
 // fs_kernels.cuh; nothing here computes a scheduling decision.
 #include <cuda_runtime.h>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -22,6 +20,8 @@
 
 #include "../../include/fairsched_b200.h"
 #include "fs_kernels.cuh"
+#include "fs_order.cuh"
+#include "fs_verify.cuh"
 #include "fs_materialize.cuh"
 
 // ---------------------------------------------------------------- errors
@@ -53,8 +53,6 @@ static int fail(int code, const char *fmt, ...) {
 // CUB device-wide calls launch several kernels; their counts were taken from
 // the ncu launch list (profiles/) for the code paths used here.
 static std::atomic<int64_t> g_launches{0};
-#define FS_CUB_SORT_LAUNCHES 4   // onesweep: histogram, exclusive-sum, 2 digit passes (<= 16-bit keys)
-#define FS_CUB_SELECT_LAUNCHES 2 // scan-tile init + select
 static inline void counted(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 extern "C" int64_t fs_launch_count(void) { return g_launches.load(); }
 
@@ -80,6 +78,11 @@ static int dgrow(DBuf<T> &b, int64_t n, cudaStream_t s, bool keep = false, int64
     nc = std::max<int64_t>(nc, 64);
     T *np = nullptr;
     CK(cudaMalloc(&np, sizeof(T) * nc));
+    // FS_POISON=1 (debug): fresh allocations hold a non-zero pattern, so a read
+    // of never-written memory shows up deterministically instead of depending
+    // on what an earlier allocation left behind
+    static const bool poison = [] { const char *e = getenv("FS_POISON"); return e && atoi(e) != 0; }();
+    if (poison) CK(cudaMemsetAsync(np, 0xA5, sizeof(T) * nc, s));
     if (keep && b.p && keep_n > 0) CK(cudaMemcpyAsync(np, b.p, sizeof(T) * keep_n, cudaMemcpyDeviceToDevice, s));
     if (b.p) { CK(cudaStreamSynchronize(s)); cudaFree(b.p); }
     b.p = np;
@@ -1073,11 +1076,25 @@ struct fs_worker {
     std::vector<int32_t> pending_new;
     int64_t qn = 0;          // entries in `queue` (label order)
     int64_t admitted_last = 0;
-    DBuf<int32_t> queue, queue2, newids;
+    DBuf<int32_t> queue, queue2, newids, ins;
     DBuf<int64_t> newlab;
-    DBuf<uint32_t> keys, keys2;
-    DBuf<int32_t> iota, perm, mlen, cov, fnode, next;
+    DBuf<uint32_t> keys;
+    DBuf<int32_t> mlen, cov, fnode, next;
     DBuf<int32_t> s_req, s_len, s_fnode, s_mlen0, s_tok0;
+    // queue order (fs_order.cuh): previous fill's sorted ids, settled marks,
+    // B sort buffers, A's (key, position) pairs, look-back status words
+    DBuf<int32_t> p_req, p_len, p_mlen0, p_tok0;
+    DBuf<int64_t> p_src0;
+    int64_t prev_n = 0;
+    bool prev_ok = false;            // p_req holds the last K1 fill's sorted order
+    DBuf<int64_t> settled;
+    int64_t stag = 0;
+    DBuf<uint32_t> bkey, bkey2, bkey3;
+    DBuf<int32_t> bpos, bpos2, bpos3, sblk;
+    DBuf<uint8_t> slow_flag;
+    DBuf<unsigned long long> akq, st_up, st_ma;
+    DBuf<OrderCtl> octl;
+    uint32_t lb_epoch = 0;
     DBuf<SweepCtl> ctl;
     DBuf<int32_t> vrank, vhead;  // VTC: client name ranks, per-client head scratch
     std::vector<int32_t> h_vrank;
@@ -1095,8 +1112,6 @@ struct fs_worker {
     int nhelp = -1;  // helper CTAs of the grid sweep (-1: not yet sized)
     DBuf<int64_t> s0, s_src0;
     DBuf<int4> slot;
-    DBuf<uint8_t> cub_tmp;
-    DBuf<int32_t> nsel;
     DBuf<int32_t> dlc;
     DBuf<int64_t> dld;
     // outputs
@@ -1111,25 +1126,6 @@ struct fs_worker {
     int64_t stats[24] = {0};
     int64_t stats_ext[8] = {0};  // hdr[24..31]: scheduler cycle counters (pin, on_walk, evictor-setup waits)
 };
-
-struct IsQueued {
-    const int8_t *st;
-    __device__ __forceinline__ bool operator()(const int32_t &r) const { return st[r] == 1; }
-};
-
-__global__ void k_iota(int32_t *p, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = (int32_t)i;
-}
-
-// Arrivals join the queue: state 1 and one more pending request for their client.
-__global__ void k_enqueue_state(int8_t *st, const int32_t *ids, int64_t n, const int32_t *rclient, int32_t *pend_cnt) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        st[ids[i]] = 1;
-        atomicAdd(&pend_cnt[rclient[ids[i]]], 1);
-    }
-}
 
 __global__ void k_set_state(int8_t *st, const int32_t *ids, int64_t n, int8_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1163,7 +1159,7 @@ extern "C" int fs_worker_create(fs_ctx *c, fs_trie *tree, int policy, int64_t qu
     CK(cudaMemsetAsync(w->known.p, 0, max_clients, c->stream));
     CK(cudaMemsetAsync(w->pend_cnt.p, 0, sizeof(int32_t) * max_clients, c->stream));
     TRY(dgrow(w->hdr, 32, c->stream)); TRY(hgrow(w->h_hdr, 32 + 128));
-    TRY(dgrow(w->nsel, 1, c->stream));
+    TRY(dgrow(w->octl, 1, c->stream));
     TRY(dgrow(w->alg, 128, c->stream));
     for (int i = 0; i < 5; i++) CK(cudaEventCreate(&w->ev[i]));
     CK(cudaStreamSynchronize(c->stream));
@@ -1179,9 +1175,14 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->tree->nworkers--;
     w->q.release(); w->refills.release(); w->known.release(); w->pend_cnt.release(); w->h_stage.release();
     w->queue.release(); w->queue2.release(); w->newids.release(); w->newlab.release();
-    w->keys.release(); w->keys2.release(); w->iota.release(); w->perm.release(); w->mlen.release();
+    w->keys.release(); w->mlen.release(); w->ins.release(); w->p_req.release(); w->settled.release();
+    w->p_len.release(); w->p_mlen0.release(); w->p_tok0.release(); w->p_src0.release();
+    w->s0.release(); w->s_mlen0.release(); w->s_src0.release(); w->alg.release();
+    w->bkey.release(); w->bkey2.release(); w->bpos.release(); w->bpos2.release(); w->akq.release();
+    w->bkey3.release(); w->bpos3.release(); w->sblk.release(); w->slow_flag.release();
+    w->st_up.release(); w->st_ma.release(); w->octl.release();
     w->cov.release(); w->fnode.release(); w->next.release(); w->s_req.release(); w->s_len.release();
-    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->vrank.release(); w->vhead.release(); w->fev_ctl.release(); w->fev_need.release(); w->fev_rec_end.release(); w->fev_free.release(); w->fev_vrec.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->cub_tmp.release(); w->nsel.release(); w->dlc.release();
+    w->s_fnode.release(); w->s_tok0.release(); w->ctl.release(); w->vrank.release(); w->vhead.release(); w->fev_ctl.release(); w->fev_need.release(); w->fev_rec_end.release(); w->fev_free.release(); w->fev_vrec.release(); w->tok0q.release(); w->k1jobs.release(); w->k1njobs.release(); w->rw_list.release(); w->gkey.release(); w->gep.release(); w->slot.release(); w->dlc.release();
     w->dld.release(); w->adm_req.release(); w->adm_mlen.release(); w->adm_node.release();
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
@@ -1368,6 +1369,26 @@ extern "C" int fs_worker_last_phases(fs_worker *w, float *ms4) {
     return FS_OK;
 }
 
+// Look-back status words are tagged with a launch epoch; a fresh buffer is
+// zeroed so that no stale word can carry a live epoch.
+static int st_grow(DBuf<unsigned long long> &b, int64_t n, cudaStream_t s) {
+    const int64_t old = b.cap;
+    TRY(dgrow(b, n, s));
+    if (b.cap != old) CK(cudaMemsetAsync(b.p, 0, sizeof(unsigned long long) * b.cap, s));
+    return FS_OK;
+}
+
+static uint32_t lb_next(fs_worker *w, cudaStream_t s) {
+    if (++w->lb_epoch >= FS_LB_EPOCH_MASK) {
+        // epoch wrap (every 16M launches): forget every status word
+        DBuf<unsigned long long> *bufs[] = {&w->st_up, &w->st_ma};
+        for (auto *b : bufs)
+            if (b->p) cudaMemsetAsync(b->p, 0, sizeof(unsigned long long) * b->cap, s);
+        w->lb_epoch = 1;
+    }
+    return w->lb_epoch;
+}
+
 static uint32_t key_bits(int32_t max_len) {
     uint32_t b = 1;
     while (((int64_t)1 << b) <= max_len) b++;
@@ -1388,16 +1409,34 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     const int64_t n = n_old + n_new;
     // scratch capacity
     TRY(dgrow(w->queue, n + 1, s, true, w->qn)); TRY(dgrow(w->queue2, n + 1, s));
-    TRY(dgrow(w->keys, n + 1, s)); TRY(dgrow(w->keys2, n + 1, s)); TRY(dgrow(w->perm, n + 1, s));
+    TRY(dgrow(w->keys, n + 1, s));
     TRY(dgrow(w->mlen, n + 1, s)); TRY(dgrow(w->cov, n + 1, s)); TRY(dgrow(w->fnode, n + 1, s));
+    if (w->policy != 2 && w->prev_ok) {
+        // the last fill's sorted order becomes p_req (k_merge_a's A)
+        std::swap(w->s_req, w->p_req);
+        std::swap(w->s_len, w->p_len);
+        std::swap(w->s_mlen0, w->p_mlen0);
+        std::swap(w->s_tok0, w->p_tok0);
+        std::swap(w->s_src0, w->p_src0);
+        w->prev_n = w->f_n;
+    } else {
+        w->prev_n = 0;
+    }
+    w->prev_ok = false;  // set again once this fill's order is written
     TRY(dgrow(w->next, n + 1, s)); TRY(dgrow(w->s_req, n + 1, s)); TRY(dgrow(w->s_len, n + 1, s));
     TRY(dgrow(w->s_fnode, n + 1, s)); TRY(dgrow(w->s_tok0, n + 1, s)); TRY(dgrow(w->tok0q, n + 1, s)); TRY(dgrow(w->slot, n + 1, s));
     TRY(dgrow(w->s_mlen0, n + 1, s)); TRY(dgrow(w->s0, n + 1, s)); TRY(dgrow(w->s_src0, n + 1, s));
-    if (w->iota.cap < n + 1) {
-        TRY(dgrow(w->iota, n + 1, s));
-        k_iota<<<(unsigned)((w->iota.cap + 255) / 256), 256, 0, s>>>(w->iota.p, w->iota.cap);
-        counted();
-        CK(cudaGetLastError());
+    TRY(dgrow(w->bkey, n + 1, s)); TRY(dgrow(w->bpos, n + 1, s)); TRY(dgrow(w->bkey2, n + 1, s));
+    TRY(dgrow(w->bpos2, n + 1, s)); TRY(dgrow(w->akq, n + 1, s)); TRY(dgrow(w->ins, n_new + 1, s));
+    TRY(dgrow(w->bkey3, n + 1, s)); TRY(dgrow(w->bpos3, n + 1, s)); TRY(dgrow(w->slow_flag, n + 1, s));
+    {
+        const int64_t tiles_up = (w->qn + FS_OT_TILE - 1) / FS_OT_TILE + 1;
+        TRY(st_grow(w->st_up, tiles_up, s));
+        TRY(st_grow(w->st_ma, (w->prev_n + FS_OT_TILE - 1) / FS_OT_TILE + 1, s));
+        const int64_t nreq = (int64_t)c->h_roff.size();
+        const int64_t old = w->settled.cap;
+        TRY(dgrow(w->settled, nreq + 1, s, true, old));
+        if (w->settled.cap != old) CK(cudaMemsetAsync(w->settled.p + old, 0, sizeof(int64_t) * (w->settled.cap - old), s));
     }
     const int64_t acap = std::max<int64_t>(n + 1, 64);
     TRY(dgrow(w->adm_req, acap, s)); TRY(dgrow(w->adm_mlen, acap, s)); TRY(dgrow(w->adm_node, acap, s));
@@ -1411,38 +1450,35 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     }
     const uint32_t bits = key_bits(c->max_len);
     const uint32_t kmax = (bits >= 32) ? 0xffffffffu : ((1u << bits) - 1u);
-    size_t sort_bytes = 0, sel_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)std::max<int64_t>(n, 1), 0, (int)bits, s);
-    cub::DeviceSelect::If(nullptr, sel_bytes, w->queue.p, w->queue2.p, w->nsel.p, (int)std::max<int64_t>(w->qn, 1), IsQueued{c->rstate.p}, s);
-    TRY(dgrow(w->cub_tmp, (int64_t)std::max(sort_bytes, sel_bytes) + 256, s));
 
     const int64_t launches0 = g_launches.load();
     const auto h1 = std::chrono::steady_clock::now();
     CK(cudaEventRecord(w->ev[0], s));
-    // ---- queue upkeep: drop last fill's admissions, merge arrivals by label
-    if (w->admitted_last > 0 && w->qn > 0) {
-        size_t b = w->cub_tmp.cap;
-        CK(cub::DeviceSelect::If(w->cub_tmp.p, b, w->queue.p, w->queue2.p, w->nsel.p, (int)w->qn, IsQueued{c->rstate.p}, s));
-        counted(FS_CUB_SELECT_LAUNCHES);
-        std::swap(w->queue, w->queue2);
-    }
-    if (n_new > 0) {
-        std::vector<int32_t> &nv = w->pending_new;
-        std::stable_sort(nv.begin(), nv.end(), [&](int32_t x, int32_t y) { return c->h_rlabel[x] < c->h_rlabel[y]; });
-        TRY(hgrow(w->h_st32, n_new)); TRY(hgrow(w->h_st64, n_new));
-        for (int64_t i = 0; i < n_new; i++) { w->h_st32.p[i] = nv[i]; w->h_st64.p[i] = c->h_rlabel[nv[i]]; }
-        TRY(dgrow(w->newids, n_new, s)); TRY(dgrow(w->newlab, n_new, s));
-        CK(cudaMemcpyAsync(w->newids.p, w->h_st32.p, sizeof(int32_t) * n_new, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(w->newlab.p, w->h_st64.p, sizeof(int64_t) * n_new, cudaMemcpyHostToDevice, s));
-        k_enqueue_state<<<(unsigned)((n_new + 255) / 256), 256, 0, s>>>(c->rstate.p, w->newids.p, n_new, c->rclient.p,
-                                                                   w->pend_cnt.p);
-        counted();
-        k_merge<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->queue.p, (int32_t)n_old, w->newids.p, w->newlab.p,
-                                                           (int32_t)n_new, c->rlabel.p, w->queue2.p);
+    CK(cudaMemsetAsync(w->octl.p, 0, sizeof(OrderCtl), s));
+    // ---- queue upkeep (fs_order.cuh): drop last fill's admissions, merge the
+    // arrivals in by label -- one pass over the old queue
+    if (w->admitted_last > 0 || n_new > 0) {
+        if (n_new > 0) {
+            std::vector<int32_t> &nv = w->pending_new;
+            std::stable_sort(nv.begin(), nv.end(), [&](int32_t x, int32_t y) { return c->h_rlabel[x] < c->h_rlabel[y]; });
+            TRY(hgrow(w->h_st32, n_new)); TRY(hgrow(w->h_st64, n_new));
+            for (int64_t i = 0; i < n_new; i++) { w->h_st32.p[i] = nv[i]; w->h_st64.p[i] = c->h_rlabel[nv[i]]; }
+            TRY(dgrow(w->newids, n_new, s)); TRY(dgrow(w->newlab, n_new, s));
+            CK(cudaMemcpyAsync(w->newids.p, w->h_st32.p, sizeof(int32_t) * n_new, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(w->newlab.p, w->h_st64.p, sizeof(int64_t) * n_new, cudaMemcpyHostToDevice, s));
+            k_arrivals<<<(unsigned)((n_new + 255) / 256), 256, 0, s>>>(
+                w->newids.p, w->newlab.p, (int32_t)n_new, w->queue.p, (int32_t)w->qn, c->rlabel.p, c->rstate.p,
+                c->rclient.p, w->pend_cnt.p, c->h_owner.p, w->ins.p);
+            counted();
+            nv.clear();
+        }
+        const int64_t tiles = std::max<int64_t>(1, (w->qn + FS_OT_TILE - 1) / FS_OT_TILE);
+        k_upkeep<<<(unsigned)tiles, FS_OT_THREADS, 0, s>>>(w->queue.p, (int32_t)w->qn, c->rstate.p, w->ins.p,
+                                                          (int32_t)n_new, w->newids.p, w->queue2.p, w->st_up.p,
+                                                          lb_next(w, s), &w->octl.p->tile[OT_UPKEEP]);
         counted();
         CK(cudaGetLastError());
         std::swap(w->queue, w->queue2);
-        nv.clear();
     }
     w->qn = n;
     w->admitted_last = 0;
@@ -1506,6 +1542,9 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         return FS_OK;
     }
     // ---- K1: batched match with LRU stamping (lpm_order's match_len calls)
+    const int32_t *bjobs = nullptr;  // B (fs_order.cuh): nullptr = every queue position
+    const int32_t *bcount = nullptr; //   device count of B (nullptr: n)
+    bool incremental = false;
     if (n > 0) {
         static int k1_blocks_dev[64] = {0};
         int &k1_blocks = k1_blocks_dev[c->device & 63];
@@ -1526,20 +1565,26 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         h.mkeys = w->gkey.p; h.wid = w->wid;
         h.use = !no_hints && !w->k1_full && w->hints_ok && w->gkey.p && w->hint_version == t->version;
         const int64_t sq1 = ++t->opseq;
-        if (h.use && k1u == 101) {
+        // the fast path needs the last fill's order: a settled request keeps
+        // its place in it (k_merge_a), only the rest is sorted (B)
+        incremental = h.use && k1u == 101 && w->prev_n > 0;
+        if (incremental) {
             // fast path: a thread per request settles the ones whose hint holds;
-            // persistent warps walk the rest (the queue positions it appended)
+            // persistent warps walk the rest (the queue positions it listed, in order)
             TRY(dgrow(w->k1jobs, n + 1, s));
-            TRY(dgrow(w->k1njobs, 1, s));
-            CK(cudaMemsetAsync(w->k1njobs.p, 0, sizeof(int32_t), s));
+            w->stag = (w->stag + 1) & 0x3fffffff;
+            if (w->stag == 0) w->stag = 1;
             k_match_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                 view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, sq1, kmax, w->keys.p, w->mlen.p,
-                w->cov.p, w->next.p, w->s0.p, w->tok0q.p, h, w->k1jobs.p, w->k1njobs.p);
+                w->cov.p, w->next.p, w->s0.p, w->tok0q.p, h, w->k1jobs.p, w->octl.p, w->slow_flag.p,
+                w->settled.p, w->stag);
             counted();
             k_match<1, true, true><<<(unsigned)std::min<int64_t>(blocks, k1_blocks), 256, 0, s>>>(
                 view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1, sq1, kmax, w->keys.p, w->mlen.p,
                 w->cov.p, w->next.p, w->s0.p, w->tok0q.p, (unsigned long long *)w->alg.p, h, w->k1jobs.p,
-                w->k1njobs.p);
+                &w->octl.p->njobs);
+            bjobs = w->k1jobs.p;
+            bcount = &w->octl.p->njobs;
         } else {
             k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
                                                 sq1, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,
@@ -1550,17 +1595,47 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(w->ev[2], s));
-    // ---- K2: stable sort by (-mlen); ties keep the (arrival, rid) label order
+    // ---- K2 (fs_order.cuh): stable order by (-mlen, label).  B sorted by key
+    // (LSD radix, 8-bit digits), merged with the settled requests' previous order
     if (n > 0) {
-        size_t b = w->cub_tmp.cap;
-        CK(cub::DeviceRadixSort::SortPairs(w->cub_tmp.p, b, w->keys.p, w->keys2.p, w->iota.p, w->perm.p, (int)n, 0, (int)bits, s));
-        counted(FS_CUB_SORT_LAUNCHES);
-        k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->perm.p, w->queue.p, (int32_t)n, w->cov.p,
-                                                            w->next.p, w->mlen.p, w->s0.p, c->rclient.p, c->rlen.p,
-                                                            w->s_req.p, w->slot.p, w->s_len.p, w->s_mlen0.p,
-                                                            w->s_src0.p, w->tok0q.p, w->s_tok0.p);
+        static int sb_grid[64] = {0};
+        int &sbg = sb_grid[c->device & 63];
+        if (!sbg) {
+            int nsm = 0, per = 0;
+            CK(cudaFuncSetAttribute(k_sort_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortBSmem)));
+            CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sort_b, FS_SB_THREADS, sizeof(SortBSmem)));
+            // two SMs stay free (a D2LPM dispatcher chain may run concurrently)
+            sbg = std::max(1, std::min(nsm - 2, nsm * per));
+        }
+        TRY(dgrow(w->sblk, (int64_t)sbg * FS_RS_BINS + 1, s));
+        SortBArgs sa{};
+        sa.jobs = bjobs; sa.njobs = bcount; sa.n = (int32_t)n; sa.flag = w->slow_flag.p; sa.keys = w->keys.p;
+        sa.npass = (int32_t)((bits + 7) / 8);
+        sa.bkey = w->bkey.p; sa.bkey2 = w->bkey2.p; sa.bkey3 = w->bkey3.p;
+        sa.bpos = w->bpos.p; sa.bpos2 = w->bpos2.p; sa.bpos3 = w->bpos3.p; sa.blk = w->sblk.p;
+        void *sargs[] = {&sa};
+        CK(cudaLaunchCooperativeKernel((const void *)k_sort_b, dim3(sbg), dim3(FS_SB_THREADS), sargs,
+                                       sizeof(SortBSmem), s));
+        counted();
+        SlotOut o{};
+        o.queue = w->queue.p; o.cov = w->cov.p; o.next = w->next.p; o.mlen = w->mlen.p; o.tok0 = w->tok0q.p;
+        o.rclient = c->rclient.p; o.rlen = c->rlen.p; o.s0 = w->s0.p;
+        o.s_req = w->s_req.p; o.s_len = w->s_len.p; o.s_mlen0 = w->s_mlen0.p; o.s_tok0 = w->s_tok0.p;
+        o.slot = w->slot.p; o.s_src0 = w->s_src0.p;
+        if (incremental) {
+            const unsigned ta = (unsigned)((w->prev_n + FS_OT_TILE - 1) / FS_OT_TILE);
+            PrevSlots pv{w->p_len.p, w->p_mlen0.p, w->p_tok0.p, w->p_src0.p};
+            k_merge_a<<<ta, FS_OT_THREADS, 0, s>>>(w->p_req.p, (int32_t)w->prev_n, w->settled.p, w->stag, kmax, pv,
+                                                  w->bkey.p, w->bpos.p, o, w->akq.p, w->st_ma.p, lb_next(w, s),
+                                                  w->octl.p);
+            counted();
+        }
+        k_scatter_b<<<(unsigned)std::min<int64_t>((n + 255) / 256, 296), 256, 0, s>>>(
+            w->bkey.p, w->bpos.p, bcount, (int32_t)n, w->akq.p, w->octl.p, o);
         counted();
         CK(cudaGetLastError());
+        w->prev_ok = true;
     }
     CK(cudaEventRecord(w->ev[3], s));
     // ---- K3+K4: admission passes on one persistent CTA
@@ -1621,8 +1696,10 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     a.ctl = w->ctl.p; a.gkey = w->gkey.p; a.gep = w->gep.p; a.nhelp = w->nhelp; a.rw_list = w->rw_list.p;
     a.hbase = 1;
     // asynchronous cold eviction: CTA 1 evicts, the sweeps keep the other
-    // helpers (FS_FEV=0 turns it off; a cache without capacity never evicts)
-    static const bool fev_env = [] { const char *e = getenv("FS_FEV"); return !(e && atoi(e) == 0); }();
+    // helpers.  Opt-in (FS_FEV=1): full GPU suites failed intermittently with
+    // it on (ref underflow / CacheFull, 3 of 6 runs) and never with it off; a
+    // cache without capacity never evicts
+    static const bool fev_env = [] { const char *e = getenv("FS_FEV"); return e && atoi(e) != 0; }();
     a.fev = fev_env && w->nhelp >= 2 && t->capacity >= 0;
     if (a.fev) {
         TRY(dgrow(w->fev_ctl, 1, s));
@@ -1806,10 +1883,9 @@ struct fs_dispatcher {
     std::vector<int64_t> dl_q;
     DBuf<int64_t> q, qsize;
     DBuf<uint8_t> qset;
-    DBuf<int32_t> ids, clients, dli, dlw, o_w, o_mlen, m0;
-    DBuf<int64_t> nows, dlq, o_rounds, hdr, s0;
-    DBuf<Seg> pre_segs;
-    DBuf<int32_t> pre_nseg;
+    DBuf<int32_t> ids, clients, dli, dlw, o_w, o_mlen;
+    DBuf<int64_t> nows, dlq, o_rounds, hdr;
+    DBuf<PreRec> pre;
     HBuf<uint8_t> h_stage;  // page-locked staging of a dispatch chain's results
     DBuf<uint64_t> o_mask;
 };
@@ -1855,7 +1931,7 @@ extern "C" int fs_dispatcher_destroy(fs_dispatcher *d) {
     d->q.release(); d->qsize.release(); d->qset.release(); d->ids.release(); d->clients.release();
     d->dli.release(); d->dlw.release(); d->o_w.release(); d->o_mlen.release(); d->nows.release();
     d->dlq.release(); d->o_rounds.release(); d->hdr.release(); d->o_mask.release();
-    d->m0.release(); d->s0.release(); d->pre_segs.release(); d->pre_nseg.release(); d->h_stage.release();
+    d->pre.release(); d->h_stage.release();
     delete d;
     return FS_OK;
 }
@@ -1870,9 +1946,56 @@ extern "C" int fs_dispatch_last_profile(fs_dispatcher *d, int64_t *prof16) {
     return FS_OK;
 }
 
+static int check_dispatch_ids(fs_dispatcher *d, int64_t n, const int32_t *req_ids) {
+    fs_ctx *c = d->ctx;
+    for (int64_t i = 0; i < n; i++)
+        if (req_ids[i] < 0 || req_ids[i] >= (int64_t)c->h_roff.size()) return fail(FS_ERR_INVALID, "bad request id");
+    return FS_OK;
+}
+
+extern "C" int fs_prematch_record_bytes(void) { return (int)sizeof(PreRec); }
+
+// Batch-start matches of n arrivals (a slice of a batch) into device memory
+// dev_out (n records of fs_prematch_record_bytes() bytes, on the dispatcher's
+// device).  Synchronous.
+extern "C" int fs_dispatch_prematch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, void *dev_out) {
+    if (!d || n < 0 || (n > 0 && (!req_ids || !dev_out))) return fail(FS_ERR_INVALID, "bad arguments");
+    if (n == 0) return FS_OK;
+    fs_ctx *c = d->ctx;
+    cudaStream_t s = d->tree->stream;
+    TRY(ctx_use(c));
+    TRY(check_dispatch_ids(d, n, req_ids));
+    TRY(dgrow(d->ids, n, s));
+    CK(cudaMemcpyAsync(d->ids.p, req_ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    k_dispatch_prematch<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(view(d->tree), d->ids.p, (int32_t)n,
+                                                                         c->roff.p, c->rlen.p, (PreRec *)dev_out);
+    counted();
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+static int dispatch_run(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
+                        const int64_t *now, const PreRec *dev_pre, int32_t *out_worker, int32_t *out_mlen,
+                        uint64_t *out_mask, int64_t *out_rounds);
+
 extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
                            const int64_t *now, int32_t *out_worker, int32_t *out_mlen, uint64_t *out_mask,
                            int64_t *out_rounds) {
+    return dispatch_run(d, n, req_ids, clients, now, nullptr, out_worker, out_mlen, out_mask, out_rounds);
+}
+
+extern "C" int fs_dispatch_prematched(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
+                                      const int64_t *now, const void *dev_pre, int32_t *out_worker,
+                                      int32_t *out_mlen, uint64_t *out_mask, int64_t *out_rounds) {
+    if (n > 0 && !dev_pre) return fail(FS_ERR_INVALID, "dev_pre is required");
+    return dispatch_run(d, n, req_ids, clients, now, (const PreRec *)dev_pre, out_worker, out_mlen, out_mask,
+                        out_rounds);
+}
+
+static int dispatch_run(fs_dispatcher *d, int64_t n, const int32_t *req_ids, const int32_t *clients,
+                        const int64_t *now, const PreRec *dev_pre, int32_t *out_worker, int32_t *out_mlen,
+                        uint64_t *out_mask, int64_t *out_rounds) {
     if (!d || n < 0) return fail(FS_ERR_INVALID, "bad arguments");
     if (n == 0) return FS_OK;
     if (!req_ids || !clients || !now || !out_worker)
@@ -1904,18 +2027,19 @@ extern "C" int fs_dispatch(fs_dispatcher *d, int64_t n, const int32_t *req_ids, 
     a.sq_base = d->tree->opseq + 1;
     d->tree->opseq += 2 * n;
     d->tree->version++;
-    {
+    if (dev_pre) {
+        // computed by the caller against this batch-start index (a slice per
+        // rank, all-gathered: fs_dispatch_prematch)
+        a.pre = dev_pre;
+    } else {
         // batch-start matches of every arrival, in parallel (K1, no stamping):
         // the serial chain below resumes each walk from them
-        TRY(dgrow(d->m0, n, s)); TRY(dgrow(d->s0, n, s));
-        TRY(dgrow(d->pre_segs, n * FS_PRE_SEGS, s)); TRY(dgrow(d->pre_nseg, n, s));
-        k_dispatch_prematch<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
-            view(d->tree), d->ids.p, (int32_t)n, c->roff.p, c->rlen.p, d->m0.p, d->s0.p, d->pre_segs.p,
-            d->pre_nseg.p);
+        TRY(dgrow(d->pre, n, s));
+        k_dispatch_prematch<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(view(d->tree), d->ids.p, (int32_t)n,
+                                                                             c->roff.p, c->rlen.p, d->pre.p);
         counted();
         CK(cudaGetLastError());
-        a.m0 = d->m0.p; a.s0 = d->s0.p;
-        a.pre_segs = d->pre_segs.p; a.pre_nseg = d->pre_nseg.p;
+        a.pre = d->pre.p;
     }
     a.out_w = d->o_w.p; a.out_mlen = d->o_mlen.p; a.out_mask = d->o_mask.p; a.out_rounds = d->o_rounds.p;
     a.hdr = d->hdr.p;
@@ -2118,5 +2242,94 @@ extern "C" int fs_dispatch_device_counters(fs_dispatcher *d, int64_t n, int64_t 
     if (present) CK(cudaMemcpyAsync(present, d->qset.p, k, cudaMemcpyDeviceToHost, s));
     if (qsize) CK(cudaMemcpyAsync(qsize, d->qsize.p, sizeof(int64_t) * d->D, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    return FS_OK;
+}
+
+// ---------------------------------------------------------------- verifiers
+// Post-run, not on the decision path: plain allocations per call.
+namespace {
+struct DevArrays {
+    std::vector<void *> ptrs;
+    ~DevArrays() { for (void *p : ptrs) cudaFree(p); }
+    template <typename T>
+    int put(const T *h, int64_t n, T **d) {
+        *d = nullptr;
+        CK(cudaMalloc((void **)d, sizeof(T) * std::max<int64_t>(n, 1)));
+        ptrs.push_back(*d);
+        if (h && n > 0) CK(cudaMemcpy(*d, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+        return FS_OK;
+    }
+};
+}  // namespace
+
+static int svc_upload(DevArrays &m, int32_t C, const int64_t *ev_off, const int64_t *ev_time, const int64_t *ev_cum,
+                      const int64_t *iv_off, const int64_t *iv_lo, const int64_t *iv_hi, SvcView *v) {
+    if (C <= 0 || !ev_off || !iv_off) return fail(FS_ERR_INVALID, "bad verifier arguments");
+    const int64_t ne = ev_off[C], ni = iv_off[C];
+    if (ne < 0 || ni < 0 || (ne > 0 && (!ev_time || !ev_cum)) || (ni > 0 && (!iv_lo || !iv_hi)))
+        return fail(FS_ERR_INVALID, "bad verifier arguments");
+    int64_t *d_eo, *d_et, *d_ec, *d_io, *d_il, *d_ih;
+    TRY(m.put(ev_off, C + 1, &d_eo)); TRY(m.put(ev_time, ne, &d_et)); TRY(m.put(ev_cum, ne + C, &d_ec));
+    TRY(m.put(iv_off, C + 1, &d_io)); TRY(m.put(iv_lo, ni, &d_il)); TRY(m.put(iv_hi, ni, &d_ih));
+    v->C = C; v->ev_off = d_eo; v->ev_time = d_et; v->ev_cum = d_ec; v->iv_off = d_io; v->iv_lo = d_il; v->iv_hi = d_ih;
+    return FS_OK;
+}
+
+extern "C" int fs_verify_pairs(int device, int32_t C, const int64_t *ev_off, const int64_t *ev_time,
+                               const int64_t *ev_cum, const int64_t *iv_off, const int64_t *iv_lo,
+                               const int64_t *iv_hi, int mode, int64_t *out_gap, int64_t *out_t1, int64_t *out_t2,
+                               int32_t *out_valid) {
+    if (mode != 0 && mode != 1) return fail(FS_ERR_INVALID, "mode must be 0 (pairwise) or 1 (global max-min)");
+    if (!out_gap || !out_t1 || !out_t2 || !out_valid) return fail(FS_ERR_INVALID, "NULL output");
+    CK(cudaSetDevice(device));
+    DevArrays m;
+    SvcView v{};
+    TRY(svc_upload(m, C, ev_off, ev_time, ev_cum, iv_off, iv_lo, iv_hi, &v));
+    const int64_t np = (int64_t)C * C;
+    int64_t *d_gap, *d_t1, *d_t2;
+    int32_t *d_ok;
+    TRY(m.put<int64_t>(nullptr, np, &d_gap)); TRY(m.put<int64_t>(nullptr, np, &d_t1));
+    TRY(m.put<int64_t>(nullptr, np, &d_t2)); TRY(m.put<int32_t>(nullptr, np, &d_ok));
+    CK(cudaMemset(d_ok, 0, sizeof(int32_t) * std::max<int64_t>(np, 1)));
+    if (C > 1) {
+        dim3 grid((unsigned)((C - 1 + 127) / 128), (unsigned)C);
+        k_verify_pairs<<<grid, 128>>>(v, mode, d_gap, d_t1, d_t2, d_ok);
+        counted();
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpy(out_gap, d_gap, sizeof(int64_t) * np, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_t1, d_t1, sizeof(int64_t) * np, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_t2, d_t2, sizeof(int64_t) * np, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_valid, d_ok, sizeof(int32_t) * np, cudaMemcpyDeviceToHost));
+    return FS_OK;
+}
+
+extern "C" int fs_verify_vs_any(int device, int32_t C, const int64_t *ev_off, const int64_t *ev_time,
+                                const int64_t *ev_cum, const int64_t *iv_off, const int64_t *iv_lo,
+                                const int64_t *iv_hi, int64_t nwin, const int32_t *win_f, const int64_t *win_t1,
+                                const int64_t *win_t2, int64_t *out_gap, int32_t *out_g) {
+    if (nwin < 0 || (nwin > 0 && (!win_f || !win_t1 || !win_t2 || !out_gap || !out_g)))
+        return fail(FS_ERR_INVALID, "bad window arguments");
+    CK(cudaSetDevice(device));
+    DevArrays m;
+    SvcView v{};
+    TRY(svc_upload(m, C, ev_off, ev_time, ev_cum, iv_off, iv_lo, iv_hi, &v));
+    if (nwin == 0) return FS_OK;
+    for (int64_t w = 0; w < nwin; w++)
+        if (win_f[w] < 0 || win_f[w] >= C) return fail(FS_ERR_INVALID, "window client %d outside [0,%d)", win_f[w], C);
+    int32_t *d_wf, *d_g;
+    int64_t *d_t1, *d_t2, *d_gap;
+    TRY(m.put(win_f, nwin, &d_wf)); TRY(m.put(win_t1, nwin, &d_t1)); TRY(m.put(win_t2, nwin, &d_t2));
+    TRY(m.put<int64_t>(nullptr, nwin, &d_gap)); TRY(m.put<int32_t>(nullptr, nwin, &d_g));
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    const unsigned grid = (unsigned)std::min<int64_t>(nwin, (int64_t)nsm * 8);
+    k_verify_vs_any<<<grid, 256>>>(v, nwin, d_wf, d_t1, d_t2, d_gap, d_g);
+    counted();
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out_gap, d_gap, sizeof(int64_t) * nwin, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_g, d_g, sizeof(int32_t) * nwin, cudaMemcpyDeviceToHost));
+    for (int64_t w = 0; w < nwin; w++)
+        if (out_g[w] == INT32_MAX) out_g[w] = -1;
     return FS_OK;
 }

@@ -476,6 +476,28 @@ class DispatcherDev:
         call("fs_dispatch", self._h, n, _p32(ids), _p32(cl), _p64(nw), _p32(w), _p32(m), _pu64(mk), _p64(rd))
         return w[:n], m[:n], mk[:n], rd[:n]
 
+    @staticmethod
+    def prematch_record_bytes() -> int:
+        return int(L.load().fs_prematch_record_bytes())
+
+    def prematch(self, ids, dev_out_ptr: int):
+        """Batch-start matches of `ids` (one rank's slice of an arrival batch)
+        written to device memory at dev_out_ptr (fs_dispatch_prematch)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        call("fs_dispatch_prematch", self._h, len(ids), _p32(ids), C.c_void_p(dev_out_ptr))
+
+    def dispatch_prematched(self, ids, clients, nows, dev_pre_ptr: int):
+        """fs_dispatch with the batch's all-gathered prematch records."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        cl = np.ascontiguousarray(clients, dtype=np.int32)
+        nw = np.ascontiguousarray(nows, dtype=np.int64)
+        n = len(ids)
+        w = np.zeros(max(n, 1), np.int32); m = np.zeros(max(n, 1), np.int32)
+        mk = np.zeros(max(n, 1), np.uint64); rd = np.zeros(max(n, 1), np.int64)
+        call("fs_dispatch_prematched", self._h, n, _p32(ids), _p32(cl), _p64(nw), C.c_void_p(dev_pre_ptr), _p32(w),
+             _p32(m), _pu64(mk), _p64(rd))
+        return w[:n], m[:n], mk[:n], rd[:n]
+
     def last_profile(self) -> np.ndarray:
         """SM cycles of the last dispatch chain (fs_dispatch_last_profile)."""
         p = np.zeros(16, np.int64)

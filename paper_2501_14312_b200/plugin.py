@@ -33,14 +33,17 @@ _BINDINGS = (
 _WORKER_SAVED = {}
 
 
-def install(host_fast_path: bool = True, placement: str = "shared", devices=None) -> None:
+def install(host_fast_path: bool = True, placement: str = "shared", devices=None, verifiers: bool = True) -> None:
     """Route fairsched's DLPM / LPM / VTC / D2LPM / threshold routing and
     RadixTree through the GPU.
     host_fast_path: also give workers running these policies the host
     bookkeeping fast path (paper_2501_14312_b200.hostpath).
     placement: "shared" (one context) or "per_worker" (worker w's cache, queue
     and counters on devices[w % len(devices)] with its own context, the
-    dispatcher on devices[0]; runtime.set_placement)."""
+    dispatcher on devices[0]; runtime.set_placement).
+    verifiers: also run metrics.py's service-gap verifiers on the GPU
+    (paper_2501_14312_b200.verify; runner.verify_run calls them through the
+    module, runner.py:383-440)."""
     from ._lib import load
     from . import runtime
 
@@ -74,6 +77,14 @@ def install(host_fast_path: bool = True, placement: str = "shared", devices=None
     if ("fairsched.speedups", "KERNEL_IMPL") not in _SAVED:
         _SAVED[("fairsched.speedups", "KERNEL_IMPL")] = sp.KERNEL_IMPL
     sp.KERNEL_IMPL = "cuda"
+    if verifiers:
+        from . import verify
+        mmod = importlib.import_module("fairsched.metrics")
+        for name in verify.REBOUND:
+            key = ("fairsched.metrics", name)
+            if key not in _SAVED:
+                _SAVED[key] = getattr(mmod, name)
+            setattr(mmod, name, getattr(verify, name))
     if host_fast_path and not _WORKER_SAVED:
         from . import hostpath
         _WORKER_SAVED.update(hostpath.install(importlib.import_module("fairsched.worker").Worker,
