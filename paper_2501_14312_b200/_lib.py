@@ -149,6 +149,8 @@ def load():
             "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback.")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("FS_LIB_PATH") and not hasattr(lib, name):
+            continue  # an older build under A/B comparison: calls to it fail loudly
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

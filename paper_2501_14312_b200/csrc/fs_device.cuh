@@ -1094,6 +1094,9 @@ __device__ inline void warp_chunk_evict(const TrieView &t, ChunkLRU *L, int64_t 
 }
 
 // ---------------------------------------------------------------- insert
+#ifndef FS_CEV
+#define FS_CEV 1  // scheduler inserts evict on warp 2 concurrently (block_insert)
+#endif
 struct InsertSmem {
     EvictSmem ev;
     int32_t nseg, mlen, new_len, deepest, last, status, cov, split_top;
@@ -1234,7 +1237,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             // allocates none); used_tokens counts it now (the capacity test
             // after the eviction adjusts).
             sm->leaf = -1;
-            if (pin_path && sm->lru && !sm->fev && sm->status == FS_OK && sm->new_len > 0) {
+            if (FS_CEV && pin_path && sm->lru && !sm->fev && sm->status == FS_OK && sm->new_len > 0) {
                 const int32_t tk = (w.mlen == hint_m0 && hint_tok0 >= 0) ? hint_tok0 : rq[w.mlen];
                 const int32_t leaf = node_new(t, req_off, w.mlen, len, len, last, tk);
                 if (leaf < 0) {

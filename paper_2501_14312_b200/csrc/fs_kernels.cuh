@@ -171,6 +171,280 @@ __global__ void __launch_bounds__(256, PIPE ? 8 : 1) k_match(TrieView t, const i
     }
 }
 
+// ---------------------------------------------------------------- K1, TMA-fed streaming scan
+// The full re-match (no usable hints: first fill, FS_OPT_K1_FULL, a per-call
+// tree edit) streams every queued request's matched prefix from HBM -- the
+// metric's "prefix-match GB/s".  Here the request row is staged through a
+// per-warp shared-memory ring by the TMA engine (cp.async.bulk into shared
+// memory, one mbarrier per stage, complete_tx): K1M_NST chunks of K1M_CH
+// tokens in flight per warp, issued ahead of the compare, so the DRAM stream
+// does not wait on each 512-byte compare step as the register loop does.  The
+// extent fetched is the previous fill's match length (+32), so nothing past the
+// match is streamed.  The trie side (other requests' rows, hot in L2/L1) stays
+// on __ldg.  Same walk and outputs as k_match (warp_walk_from with coverage).
+#ifndef K1M_CH
+#define K1M_CH 512      // tokens per chunk (2 KB)
+#endif
+#ifndef K1M_NST
+#define K1M_NST 4       // chunks in flight per warp
+#endif
+#define K1M_WARPS 8     // warps per CTA
+#ifndef K1M_L2PF
+#define K1M_L2PF 1      // bulk L2 prefetch of the whole extent at the row's start
+#endif
+
+struct K1Ring {
+    int32_t *buf;        // K1M_NST * K1M_CH tokens (shared)
+    uint64_t *bar;       // K1M_NST mbarriers (shared)
+    const int32_t *row;  // request row (global, 16-B aligned)
+    int32_t E;           // tokens staged: [0, E)
+    int32_t nch;         // chunks of [0, E)
+    int32_t issued;      // chunks issued so far
+    int32_t landed;      // chunks known to have landed (waited for, in order)
+    uint32_t phase;      // parity bit per stage
+    uint64_t pol;        // L2 evict-first policy
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// lane 0: put chunk c of the row in flight into stage c % K1M_NST
+__device__ __forceinline__ void k1r_issue(K1Ring &R, int32_t c) {
+    const int st = c % K1M_NST;
+    const int32_t lo = c * K1M_CH, hi = min(R.E, lo + K1M_CH);
+    const uint32_t bytes = (uint32_t)(((hi - lo) * 4 + 15) & ~15);
+    const uint32_t b = smem_addr(R.bar + st);
+    // the stage's previous contents were read through the generic proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(smem_addr(R.buf + st * K1M_CH)), "l"(R.row + lo), "r"(bytes), "r"(b), "l"(R.pol)
+                 : "memory");
+}
+
+// Warp-uniform: chunks [landed, c_hi] have landed.  Chunks below c_lo are
+// consumed (positions are read in nondecreasing order), so their stages may be
+// refilled: chunks up to c_lo + K1M_NST - 1 are put in flight.
+__device__ __forceinline__ void k1r_need(K1Ring &R, int32_t c_lo, int32_t c_hi, int lane) {
+    c_hi = min(c_hi, R.nch - 1);
+    while (true) {
+        // chunk k refills the stage of chunk k - K1M_NST: that one must have
+        // landed and be consumed
+        const int32_t want = min(R.nch, min(c_lo, R.landed) + K1M_NST);
+        if (R.issued < want) {
+            __syncwarp();  // every lane is done with the stages being refilled
+            if (lane == 0)
+                for (int32_t k = R.issued; k < want; k++) k1r_issue(R, k);
+            R.issued = want;
+        }
+        if (R.landed > c_hi) break;
+        const int st = R.landed % K1M_NST;
+        const uint32_t b = smem_addr(R.bar + st), par = (R.phase >> st) & 1u;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(b), "r"(par) : "memory");
+        R.phase ^= 1u << st;
+        R.landed++;
+    }
+}
+
+// is position p's chunk still in its stage?
+__device__ __forceinline__ bool k1r_resident(const K1Ring &R, int32_t p) {
+    return p < R.E && p / K1M_CH + K1M_NST >= R.issued;
+}
+__device__ __forceinline__ const int32_t *k1r_ptr(const K1Ring &R, int32_t p) {
+    return R.buf + (p / K1M_CH % K1M_NST) * K1M_CH + p % K1M_CH;
+}
+
+// warp-uniform p: request token p (its staged chunk, else global memory)
+__device__ __forceinline__ int32_t k1r_tok(K1Ring &R, int32_t p, int lane) {
+    if (p < R.E) {
+        const int32_t c = p / K1M_CH;
+        if (c >= R.landed) {  // ahead of the stream: wait for it
+            k1r_need(R, c, c, lane);
+            return *k1r_ptr(R, p);
+        }
+        if (c + K1M_NST >= R.issued) return *k1r_ptr(R, p);  // landed, stage not refilled
+    }
+    return __ldg(R.row + p);
+}
+
+// drain: wait for every chunk issued for this row (stage parity stays in step)
+__device__ __forceinline__ void k1r_drain(K1Ring &R, int lane) {
+    while (R.landed < R.issued) {
+        const int st = R.landed % K1M_NST;
+        const uint32_t b = smem_addr(R.bar + st), par = (R.phase >> st) & 1u;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(b), "r"(par) : "memory");
+        R.phase ^= 1u << st;
+        R.landed++;
+    }
+    __syncwarp();
+}
+
+// LCP of the chain row a[i0, n) with the request tokens [i0, n), chunk by
+// chunk: one ring check per staged chunk, then 512 tokens per step (lane l
+// compares 4 x 4 tokens, 16-B aligned: both rows are co-aligned arena rows
+// read at the same depth), four independent trie-side loads in flight per
+// lane.  Returns the first mismatch (or n).
+__device__ __forceinline__ int k1r_first_diff(const int4 &x, const int4 &y, int32_t p, int32_t n) {
+    int f = 4;
+    if (x.w != y.w && p + 3 < n) f = 3;
+    if (x.z != y.z && p + 2 < n) f = 2;
+    if (x.y != y.y && p + 1 < n) f = 1;
+    if (x.x != y.x && p < n) f = 0;
+    return f;
+}
+__device__ inline int32_t k1r_lcp(K1Ring &R, const int32_t *__restrict__ a, int32_t i0, int32_t n, int lane) {
+    if (i0 >= n) return n;
+    // scalar head up to the next 16-B boundary
+    const int32_t h = min(n, (i0 + 3) & ~3);
+    if (h > i0) {
+        if (i0 < R.E) k1r_need(R, i0 / K1M_CH, (min(h, R.E) - 1) / K1M_CH, lane);
+        const int32_t p = i0 + lane;
+        bool bad = false;
+        if (p < h) bad = __ldg(a + p) != (k1r_resident(R, p) ? *k1r_ptr(R, p) : __ldg(R.row + p));
+        const unsigned m = __ballot_sync(FS_FULL, bad);
+        if (m) return i0 + __ffs(m) - 1;
+    }
+    int32_t k = h;
+    while (k < n) {
+        const bool staged = k < R.E;
+        int32_t seg_end = n;
+        const int32_t *bb = R.row;  // bb[p]: request token p
+        if (staged) {
+            const int32_t c = k / K1M_CH;
+            k1r_need(R, c, c, lane);
+            seg_end = min(n, (c + 1) * K1M_CH);
+            bb = R.buf + (c % K1M_NST) * K1M_CH - c * K1M_CH;
+        }
+        for (; k < seg_end; k += 512) {
+            int f[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int32_t p = k + 128 * u + 4 * lane;
+                f[u] = 4;
+                if (p < seg_end) {
+                    const int4 av = __ldg(reinterpret_cast<const int4 *>(a + p));
+                    const int4 bv = staged ? *reinterpret_cast<const int4 *>(bb + p)
+                                           : __ldg(reinterpret_cast<const int4 *>(bb + p));
+                    f[u] = k1r_first_diff(av, bv, p, n);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const unsigned m = __ballot_sync(FS_FULL, f[u] < 4);
+                if (m) {
+                    const int L = __ffs(m) - 1;
+                    return min(n, k + 128 * u + 4 * L + __shfl_sync(FS_FULL, f[u], L));
+                }
+            }
+        }
+        k = seg_end;
+    }
+    return n;
+}
+
+__global__ void __launch_bounds__(32 * K1M_WARPS) k_match_tma(TrieView t, const int32_t *__restrict__ ids, int32_t n,
+                                                           const int64_t *__restrict__ roff,
+                                                           const int32_t *__restrict__ rlen, int64_t now, int64_t sq,
+                                                           uint32_t kmax, uint32_t *__restrict__ out_key,
+                                                           int32_t *__restrict__ out_mlen, int32_t *__restrict__ out_cov,
+                                                           int32_t *__restrict__ out_next, int64_t *__restrict__ out_s0,
+                                                           int32_t *__restrict__ out_tok0,
+                                                           unsigned long long *__restrict__ alg_tokens, K1Hints hints) {
+    extern __shared__ __align__(128) unsigned char k1m_sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    K1Ring R;
+    R.buf = reinterpret_cast<int32_t *>(k1m_sm) + warp * K1M_NST * K1M_CH;
+    R.bar = reinterpret_cast<uint64_t *>(k1m_sm + K1M_WARPS * K1M_NST * K1M_CH * 4) + warp * K1M_NST;
+    R.phase = 0;
+    R.pol = l2_evict_first();
+    if (lane < K1M_NST) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(R.bar + lane)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const int64_t nw = (int64_t)gridDim.x * K1M_WARPS;
+    for (int64_t i = (int64_t)blockIdx.x * K1M_WARPS + warp; i < n; i += nw) {
+        const int32_t r = ids[i];
+        const int32_t len = rlen[r];
+        R.row = t.arena + roff[r];
+        // staged extent: the previous match (+32) -- what this match will read
+        R.E = hints.m ? min(len, hints.m[r] + 32) : len;
+        R.E = min(len, (R.E + 3) & ~3);
+        R.nch = (R.E + K1M_CH - 1) / K1M_CH;
+        R.issued = 0;
+        R.landed = 0;
+#if K1M_L2PF
+        {
+            // the whole staged extent to L2 up front (4 KB per lane, as k_match):
+            // the ring then refills from L2
+            const int32_t nb = (R.E * 4 + 4095) >> 12;
+            for (int32_t q = lane; q < nb; q += 32) {
+                const int32_t b0 = q << 10;
+                const uint32_t bytes = (uint32_t)(((min(R.E, b0 + 1024) - b0) * 4 + 15) & ~15);
+                asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(R.row + b0), "r"(bytes),
+                             "l"(R.pol) : "memory");
+            }
+        }
+#endif
+        if (lane == 0)
+            for (int32_t k = 0; k < min(R.nch, K1M_NST); k++) k1r_issue(R, k);
+        R.issued = min(R.nch, K1M_NST);
+        // RadixTree._walk (radix.py:60-81) chain by chain, as warp_walk_from
+        WalkOut o;
+        o.mlen = 0; o.last = -1; o.plen = 0; o.nseg = 0; o.cov = 0; o.unpinned = 0;
+        int32_t node = 0, idx = 0;
+        bool pinrun = true;
+        while (idx < len) {
+            const int32_t c = h_find(t, node, k1r_tok(R, idx, lane));
+            if (c < 0) break;
+            const int64_t S = t.src[c];
+            const int32_t bound = min(len, t.slen[c]);
+            const int32_t D = k1r_lcp(R, t.arena + S, idx + 1, bound, lane);  // request == chain S on [idx, D)
+            const int32_t y = chain_lookup(t, S, idx, D - 1);
+            const int32_t e = t.end[y];
+            const int32_t b = min(D, e);
+            o.nseg++;
+            if (pinrun) {
+                o.cov = warp_seg_cov(t, S, idx, b, y, lane);
+                pinrun = o.cov == b;
+            }
+            o.last = y;
+            if (D < e) { o.plen = D - t.start[y]; idx = D; break; }
+            idx = e;
+            node = y;
+        }
+        o.mlen = idx;
+        o.unpinned = o.mlen - o.cov;
+        const int32_t tokcov = o.cov < len ? k1r_tok(R, o.cov, lane) : -1;
+        const int32_t tokm = o.mlen < len ? k1r_tok(R, o.mlen, lane) : -1;
+        k1r_drain(R, lane);
+        if (lane == 0) {
+            if (o.last > 0) stamp_node(t, o.last, now, sq);  // match_prefix stamps (radix.py:86-90), lazily
+            out_key[i] = kmax - (uint32_t)o.mlen;
+            out_mlen[i] = o.mlen;
+            out_cov[i] = o.cov;
+            out_next[i] = tokcov;
+            const int64_t s0 = o.last > 0 ? t.src[o.last] : -1;
+            out_s0[i] = s0;
+            out_tok0[i] = tokm;
+            if (hints.owner) {
+                hints.owner[r] = hints.wid;
+                hints.S0[r] = s0;
+                hints.tok0[r] = tokm;
+            }
+            if (hints.m) hints.m[r] = o.mlen;
+            if (alg_tokens) {
+                unsigned long long *slot = alg_tokens + 2 * (blockIdx.x & 63);
+                atomicAdd(slot, (unsigned long long)min(o.mlen + 1, len));
+                atomicAdd(slot + 1, (unsigned long long)o.nseg);
+            }
+        }
+    }
+}
+
 // Pinned coverage of the cached root path [0, d) ending in node y, by one
 // thread: chain by chain from the deep end (refs never increase with depth);
 // inside the chain where pinning stops, up the parent links to the deepest

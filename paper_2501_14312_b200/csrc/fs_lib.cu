@@ -1560,6 +1560,12 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         auto k1 = k1u == 101 ? k_match<1, true> : k1u == 102 ? k_match<2, true> : k1u == 104 ? k_match<4, true>
                 : k1u >= 16 ? k_match<16, false> : k1u >= 8 ? k_match<8, false> : k_match<4, false>;
         static const bool no_hints = getenv("FS_K1_FULL") != nullptr;  // ablation: full re-match every fill
+        // FS_K1_TMA=1: full re-matches through the TMA-fed kernel (k_match_tma).
+        // Measured slower than the register loop with its up-front L2 bulk
+        // prefetch (0.33-0.41 vs 0.62 of HBM on config 5, ring geometries
+        // 128-1024 tokens x 2-4 stages): the scan is bound by the per-request
+        // chain-walk latency, not by the request stream's arrival
+        static const bool k1_tma = [] { const char *e = getenv("FS_K1_TMA"); return e && atoi(e) != 0; }();
         K1Hints h{};
         h.owner = c->h_owner.p; h.m = c->rhint.p; h.S0 = c->h_S0.p; h.tok0 = c->h_tok0.p;
         h.mkeys = w->gkey.p; h.wid = w->wid;
@@ -1585,6 +1591,21 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
                 &w->octl.p->njobs);
             bjobs = w->k1jobs.p;
             bcount = &w->octl.p->njobs;
+        } else if (!h.use && k1u == 101 && k1_tma) {
+            // every request re-matched from the root: the TMA-fed streaming scan
+            static int tma_grid[64] = {0};
+            int &tg = tma_grid[c->device & 63];
+            const int smem = K1M_WARPS * K1M_NST * K1M_CH * 4 + K1M_WARPS * K1M_NST * 8;
+            if (!tg) {
+                int nsm = 0, per = 0;
+                CK(cudaFuncSetAttribute(k_match_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_match_tma, 32 * K1M_WARPS, smem));
+                tg = std::max(1, nsm * per);
+            }
+            k_match_tma<<<(unsigned)std::min<int64_t>(tg, (n + K1M_WARPS - 1) / K1M_WARPS), 32 * K1M_WARPS, smem, s>>>(
+                view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, sq1, kmax, w->keys.p, w->mlen.p,
+                w->cov.p, w->next.p, w->s0.p, w->tok0q.p, (unsigned long long *)w->alg.p, h);
         } else {
             k1<<<(unsigned)blocks, 256, 0, s>>>(view(t), w->queue.p, (int32_t)n, c->roff.p, c->rlen.p, now, 1,
                                                 sq1, kmax, w->keys.p, w->mlen.p, w->cov.p, w->next.p,

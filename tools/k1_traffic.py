@@ -9,7 +9,8 @@ build and workload being run -- never a stale constant.
 
 Launch grouping: an incremental fill launches `k_match_fast` (thread per
 request) then `k_match<1, 1, 1>` (persistent warps for the unsettled ones);
-a full re-match fill (FS_OPT_K1_FULL) launches one `k_match<1, 1, 0>`.  The
+a full re-match fill (FS_OPT_K1_FULL) launches one `k_match_tma` (the TMA-fed
+streaming scan; `k_match<1, 1, 0>` with FS_K1_TMA=0).  The
 entry stores the mean over the last `--last` incremental fills (steady state)
 and over the full-scan launches, keyed by (source hash, workload, nq) in
 profiles/k1_traffic.json; bench.py uses an entry only when all three match.
@@ -52,7 +53,7 @@ def group(launches):
                 b += launches[i + 1]["bytes"]
                 i += 1
             incr.append(b)
-        elif n.startswith("k_match<"):
+        elif n.startswith("k_match<") or n == "k_match_tma":
             full.append(launches[i]["bytes"])
         i += 1
     return incr, full
