@@ -1121,7 +1121,8 @@ __device__ inline void fev_drain(const TrieView &t, FevLeader *f, bool handover)
             st_release_i32(&c->stop, 1);
             while (ld_acquire_i32(&c->finished) == 0) __nanosleep(32);
             volatile FevCtl *vc = c;
-            if (vc->freed != f->cum || vc->err) t.sc->status = FS_ERR_INTERNAL;
+            if (vc->err) t.sc->status = 100 + vc->err;  // evictor check (FS_FEV_CHECK) / heap overflow
+            else if (vc->freed != f->cum) t.sc->status = FS_ERR_INTERNAL;
             t.sc->nrec = vc->nrec;
             t.sc->tombs += (int32_t)vc->tombs;
             t.sc->live -= (int32_t)vc->nfreed;

@@ -1138,6 +1138,9 @@ __device__ void helper_loop(const FillArgs &ap, SchedSmem *sm) {
 // (the records ahead are prefetched into L1; the hash probe is warp-wide).
 #define FEV_MAXC 2048  // power of two (bitonic sort)
 #define FEV_HEAP 640
+#ifndef FS_FEV_CHECK
+#define FS_FEV_CHECK 0
+#endif
 struct FevRec {
     int64_t src, la, lseq, seq;
     int32_t start, end, parent, first, node, pad_;
@@ -1297,6 +1300,24 @@ __device__ void evictor_loop(const FillArgs &ap, unsigned char *smraw) {
             const int32_t el = r.end - r.start;
             const int64_t rem = need - freed;
             pops++;
+#if FS_FEV_CHECK
+            if (lane == 0) {
+                // the popped node must still be an unpinned live leaf with the
+                // fields the setup read (debug: FEV is opt-in while this is open)
+                const int32_t nc = atomicAdd(&t.nchild[r.node], 0), rf = atomicAdd(&t.ref[r.node], 0);
+                const uint8_t fl = *(volatile uint8_t *)&t.flags[r.node];
+                const int32_t pa = *(volatile int32_t *)&t.parent[r.node];
+                const int32_t st = *(volatile int32_t *)&t.start[r.node], en = *(volatile int32_t *)&t.end[r.node];
+                int code = 0;
+                if (!(fl & FS_ALIVE)) code = 2;
+                else if (nc != 0) code = 3;
+                else if (rf != 0) code = 4;
+                else if (pa != r.parent) code = 5;
+                else if (st != r.start) code = 6;
+                else if (en != r.end) code = 7;
+                if (code && !ctl->err) { ctl->err = code; ctl->nc = r.node; ctl->heap_hw = from_heap ? 1 : 0; }
+            }
+#endif
             if (el <= rem) {
                 // whole leaf: record, tombstone (parent, first), parent child
                 // count and stamp, free the slot (radix.py:226-230, 206-208)

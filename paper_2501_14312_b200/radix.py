@@ -26,11 +26,22 @@ class CacheFull(Exception):
     """Raised when the budget cannot admit the tokens (radix.py:19-20)."""
 
 
+_BOTH = {}
+
+
 def _cache_full_cls():
-    # raise the reference's own exception type when the reference is loaded,
-    # so `except CacheFull` in reference code and tests keeps working
+    # when the reference is loaded, raise a type that is both its CacheFull and
+    # this module's, so `except CacheFull` keeps working for callers of either
+    # (reference code, and code written against this module before the
+    # reference was imported)
     mod = sys.modules.get("fairsched.radix")
-    return getattr(mod, "CacheFull", CacheFull) if mod is not None else CacheFull
+    ref = getattr(mod, "CacheFull", None) if mod is not None else None
+    if ref is None or ref is CacheFull:
+        return CacheFull
+    cls = _BOTH.get(ref)
+    if cls is None:
+        cls = _BOTH[ref] = type("CacheFull", (ref, CacheFull), {"__module__": ref.__module__})
+    return cls
 
 
 class EvictedPath(Sequence):
