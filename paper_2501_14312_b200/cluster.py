@@ -83,7 +83,8 @@ class TorchComm:
             parts = [torch.empty(t.numel(), dtype=t.dtype) for _ in range(self.world)]
             dist.all_gather(parts, t.cpu())
             out = torch.cat(parts).to(t.device)
-        torch.cuda.current_stream(t.device).synchronize()  # the library reads it on its own stream
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()  # the library reads it on its own stream
         return out
 
     def all_gather_rows(self, rows: np.ndarray) -> list:
@@ -245,12 +246,13 @@ def partitioned_prematch(d, ids, comm, device):
     would have computed.  Returns the gathered device tensor."""
     import torch
     from .device import DispatcherDev
-    rec = DispatcherDev.prematch_record_bytes()
+    rec = DispatcherDev.prematch_record_bytes() if device is not None else d.record_bytes
     n = len(ids)
     chunk = max(1, -(-n // comm.world))
     lo = min(n, comm.rank * chunk)
     hi = min(n, lo + chunk)
-    local = torch.zeros(chunk * rec, dtype=torch.uint8, device=f"cuda:{device}")
+    # device None: host memory (tests of the exchange with a host-side matcher)
+    local = torch.zeros(chunk * rec, dtype=torch.uint8, device=f"cuda:{device}" if device is not None else "cpu")
     if hi > lo:
         d.prematch(ids[lo:hi], local.data_ptr())
     return comm.all_gather_tensor(local)
