@@ -1324,7 +1324,11 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                 sm->deepest = deepest;
                 if (sm->prof) sm->prof[13] += clock64() - c1;
             }
-            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 64) : "memory");
+            // named barrier 1 (warps 0 and 3..), reached from two code paths:
+            // the non-.aligned form (bar.sync is .aligned, which requires every
+            // thread to execute the same barrier instruction)
+            __syncwarp();
+            asm volatile("barrier.sync 1, %0;" ::"r"((int)blockDim.x - 64) : "memory");
         } else if (warp == 2) {
             // RadixTree.evict_lru for this insert (radix.py:149-151), concurrent
             // with warp 0's hash link and the pin: the path's nodes are internal
@@ -1339,7 +1343,8 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
             // pin the pre-existing path, then point the new leaf's depths at it
             const long long cp = clock64();
             block_path_nodes(t, segs, nseg_path, [&](int32_t n, int32_t, int32_t) { atomicAdd(&t.ref[n], 1); }, 96);
-            asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 64) : "memory");
+            __syncwarp();
+            asm volatile("barrier.sync 1, %0;" ::"r"((int)blockDim.x - 64) : "memory");
             if (sm->status == FS_OK && sm->new_len > 0 && sm->deepest > 0) {
                 // 16-B stores (arena rows, hence their pos rows, are 16-B aligned):
                 // a quarter of the store instructions next to warp 1's bookkeeping

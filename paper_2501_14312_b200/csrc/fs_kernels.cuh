@@ -1481,7 +1481,11 @@ __device__ void block_refill(const FillArgs &a, SchedSmem *sm) {
 __device__ void block_admit(const FillArgs &a, SchedSmem *sm, int32_t j, int64_t slack) {
     const int tid = threadIdx.x;
     const TrieView &t = a.t;
-    if (sm->fev.on && t.sc->hw + 2 > t.ncap) {
+    // (every thread reads the condition before thread 0's hand-over clears
+    // fev.on: a thread reading it afterwards would skip fev_drain's barriers)
+    const bool fev_full = sm->fev.on && t.sc->hw + 2 > t.ncap;
+    __syncthreads();
+    if (fev_full) {
         // FEV allocates fresh node slots only (the evictor's freed slots come
         // back at the hand-over): out of fresh slots, hand over now
         fev_drain(t, &sm->fev, true);
@@ -1739,7 +1743,9 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     if (a.fev) {
         // stop the evictor (handing its state over if it is still on), then
         // resolve the admissions' record counts
-        if (sm.fev.on) {
+        const bool fon = sm.fev.on;  // read by every thread before fev_drain clears it
+        __syncthreads();
+        if (fon) {
             fev_drain(a.t, &sm.fev, true);
         } else if (tid == 0) {
             st_release_i32(&a.fev_ctl->stop, 1);

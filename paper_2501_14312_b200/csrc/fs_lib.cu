@@ -1633,6 +1633,13 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         SortBArgs sa{};
         sa.jobs = bjobs; sa.njobs = bcount; sa.n = (int32_t)n; sa.flag = w->slow_flag.p; sa.keys = w->keys.p;
         sa.npass = (int32_t)((bits + 7) / 8);
+        // FS_SB_CAP (tests): a smaller single-CTA limit sends B down the grid-wide path
+        static const int32_t sb_cap = [] {
+            const char *e = getenv("FS_SB_CAP");
+            const int v = e ? atoi(e) : FS_SB_CAP;
+            return (int32_t)std::max(1, std::min(v, FS_SB_CAP));
+        }();
+        sa.cap = sb_cap;
         sa.bkey = w->bkey.p; sa.bkey2 = w->bkey2.p; sa.bkey3 = w->bkey3.p;
         sa.bpos = w->bpos.p; sa.bpos2 = w->bpos2.p; sa.bpos3 = w->bpos3.p; sa.blk = w->sblk.p;
         void *sargs[] = {&sa};

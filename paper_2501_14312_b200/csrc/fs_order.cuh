@@ -169,6 +169,7 @@ struct SortBArgs {
     const uint8_t *flag;   // flag[i]: position i is in B (with jobs)
     const uint32_t *keys;  // key of every queue position
     int32_t npass;         // 8-bit key digits
+    int32_t cap;           // B up to this size is sorted by CTA 0 alone (<= FS_SB_CAP)
     uint32_t *bkey, *bkey2, *bkey3;  // out: bkey/bpos; scratch
     int32_t *bpos, *bpos2, *bpos3;
     int32_t *blk;          // [gridDim.x * 256] per-CTA counts
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(FS_SB_THREADS, 1) k_sort_b(SortBArgs a) {
     SortBSmem &sm = *reinterpret_cast<SortBSmem *>(sb_raw);
     const int32_t nb = a.njobs ? *a.njobs : a.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (nb <= FS_SB_CAP) {
+    if (nb <= a.cap) {
         if (blockIdx.x != 0) return;
         int32_t P2 = 1;
         while (P2 < nb) P2 <<= 1;

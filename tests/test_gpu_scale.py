@@ -158,3 +158,20 @@ def test_incremental_match_equals_full_rematch():
     assert a.w is not b.w
     a.close()
     b.close()
+
+
+def test_grid_sort_path_matches_oracle():
+    """The incremental order with a large B: k_sort_b's grid-wide radix path
+    and k_merge_a's unstaged search over B.  FS_SB_CAP=64 (read once per
+    process, hence the subprocess) sends every B past 64 entries down them."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path[:0] = ['tests', '.']\n"
+            "import bench, test_gpu_scale as t\n"
+            "t._run_wl(bench.Config2(8192, 9, 12), 12)\n"
+            "t._run_wl(bench.Config5(16384, 0, 6), 6)\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, FS_SB_CAP="64"),
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
