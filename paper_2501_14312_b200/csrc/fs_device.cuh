@@ -766,6 +766,7 @@ struct FevLeader {  // leader CTA, shared memory
     int64_t *rec_end;   // [orders] records emitted after each order (evictor)
     int32_t *free_list; // node slots the evictor freed
     int32_t on, posted, cap_orders, ready_seen, used_any, nfree_saved;
+    int32_t stamped;      // an existing node was stamped since the last post (fence before the next)
     int64_t cum, C, tag;  // tag: the fill's order tag (bits 40..62 of each posted need)
 };
 
@@ -1208,8 +1209,12 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                         f->ready_seen = 1;
                     }
                     if (f->cum + need <= f->C && f->posted < f->cap_orders) {
-                        // within the cold supply: the evictor performs it
-                        // one relaxed store: the evictor needs nothing else the leader wrote
+                        // within the cold supply: the evictor performs it --
+                        // one relaxed store, after a fence when this thread
+                        // stamped an existing node since the last order (the
+                        // evictor compares stamps when a detached leaf's parent
+                        // re-joins the candidates)
+                        if (f->stamped) { __threadfence(); f->stamped = 0; }
                         asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(f->need + f->posted),
                                      "l"(f->tag | need) : "memory");
                         f->posted++;
@@ -1320,6 +1325,7 @@ __device__ inline void block_insert(const TrieView &t, int64_t req_off, int32_t 
                     }
                 } else if (sm->status == FS_OK && deepest > 0) {
                     stamp_node(t, deepest, now, sq);
+                    if (sm->fev) sm->fev->stamped = 1;
                 }
                 sm->deepest = deepest;
                 if (sm->prof) sm->prof[13] += clock64() - c1;

@@ -1331,9 +1331,15 @@ __device__ void evictor_loop(const FillArgs &ap, unsigned char *smraw) {
                 int32_t stP = 0, enP = 0, paP = 0, fiP = 0;
                 if (lane == 0) {
                     old = atomicSub(&t.nchild[P], 1);
-                    flP = t.flags[P]; refP = t.ref[P];
-                    laP = t.la[P]; lsP = t.lseq[P]; sqP = t.seq[P];
-                    srcP = t.src[P]; stP = t.start[P]; enP = t.end[P]; paP = t.parent[P]; fiP = t.first[P];
+                    // P's fields from L2, not this SM's L1: the setup scan cached
+                    // every node's line, and the leader pins and stamps during the
+                    // fill (a stale ref or stamp would make a pinned, freshly
+                    // stamped parent look like a cold candidate)
+                    flP = *(volatile uint8_t *)&t.flags[P]; refP = *(volatile int32_t *)&t.ref[P];
+                    laP = *(volatile int64_t *)&t.la[P]; lsP = *(volatile int64_t *)&t.lseq[P];
+                    sqP = t.seq[P];
+                    srcP = t.src[P]; stP = *(volatile int32_t *)&t.start[P]; enP = *(volatile int32_t *)&t.end[P];
+                    paP = *(volatile int32_t *)&t.parent[P]; fiP = *(volatile int32_t *)&t.first[P];
                 }
                 // warp-wide probe of the child hash: the key's slot before the first empty one
                 for (uint32_t base = 0; base <= t.hmask; base += 32) {
@@ -1675,7 +1681,7 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
         sm.ins.fev_switch = 0; sm.ins.fev_wait = 0;
         FevLeader &f = sm.fev;
         f.ctl = a.fev_ctl; f.need = a.fev_need; f.rec_end = a.fev_rec_end; f.free_list = a.fev_free;
-        f.on = a.fev; f.posted = 0; f.cap_orders = a.fev_cap; f.ready_seen = 0; f.used_any = 0;
+        f.on = a.fev; f.posted = 0; f.cap_orders = a.fev_cap; f.ready_seen = 0; f.used_any = 0; f.stamped = 0;
         f.cum = 0; f.C = 0; f.tag = (int64_t)a.fev_tag << 40;
         f.nfree_saved = a.t.sc->nfree;
         if (a.fev) a.t.sc->nfree = 0;  // fresh slots only while the evictor frees concurrently
