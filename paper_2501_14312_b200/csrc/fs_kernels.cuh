@@ -1801,6 +1801,39 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
     }
 }
 
+// Debug (FS_FILL_CHECK=1): after a fill, every admission's path -- from its
+// deepest node up the parent links -- must be live nodes pinned at least once,
+// and no live node may have a freed parent.  The first violation goes to
+// hdr[2] as 200 + code (hdr[6] = the node).
+__global__ void k_check_fill(TrieView t, const int32_t *adm_node, const int64_t *hdr_n, int32_t cap, int64_t *hdr) {
+    const int64_t n = min((int64_t)cap, hdr_n[0]);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t y = adm_node[e];
+        int guard = 0;
+        while (y > 0 && guard++ < (1 << 20)) {
+            int code = 0;
+            if (!(t.flags[y] & FS_ALIVE)) code = 1;
+            else if (t.ref[y] < 1) code = 2;
+            if (code) {
+                if (atomicCAS((unsigned long long *)&hdr[2], (unsigned long long)FS_OK,
+                              (unsigned long long)(200 + code)) == FS_OK)
+                    hdr[6] = y;
+                return;
+            }
+            y = t.parent[y];
+        }
+    }
+    const int32_t hw = t.sc->hw;
+    for (int32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < hw; y += gridDim.x * blockDim.x) {
+        if (!(t.flags[y] & FS_ALIVE)) continue;
+        const int32_t P = t.parent[y];
+        if (P > 0 && !(t.flags[P] & FS_ALIVE)) {
+            if (atomicCAS((unsigned long long *)&hdr[2], (unsigned long long)FS_OK, 203ull) == FS_OK) hdr[6] = y;
+            return;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- VTC fill
 // Vtc.fill (local_policies.py:170-189): repeatedly serve the least-served
 // client -- clients in (counter, name) order, each offering its earliest

@@ -1764,6 +1764,13 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     }
     counted();
     CK(cudaGetLastError());
+    static const bool fill_check = [] { const char *e = getenv("FS_FILL_CHECK"); return e && atoi(e) != 0; }();
+    if (fill_check) {
+        k_check_fill<<<64, 256, 0, s>>>(view(t), w->adm_req.p ? w->adm_node.p : nullptr, w->hdr.p,
+                                        (int32_t)w->adm_node.cap, w->hdr.p);
+        counted();
+        CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(w->ev[4], s));
     w->dl_client.clear(); w->dl_delta.clear();
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
@@ -1846,6 +1853,9 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     t->opseq += nadm;  // admission e stamped with sq_base + e
     w->hint_version = t->version;
     w->hints_ok = status == FS_OK && w->h_hdr.p[6] == 0;
+    if (status >= 200 && status < 300)  // FS_FILL_CHECK found a broken path (hdr[6]: the node)
+        return fail(FS_ERR_INTERNAL, "fill check %lld at node %lld (adm %lld)", (long long)status,
+                    (long long)w->h_hdr.p[6], (long long)nadm);
     if (status != FS_OK) return fail((int)status, "device fill failed (status %lld)", (long long)status);
     if (nadm > res->cap_adm) return fail(FS_ERR_INVALID, "admission buffer too small (%lld > %lld)", (long long)nadm, (long long)res->cap_adm);
     bool second = false;  // a second round of copies (more rows than staged)
