@@ -1395,6 +1395,51 @@ static uint32_t key_bits(int32_t max_len) {
     return b;
 }
 
+// A fill's results: one batch of DMA copies into page-locked staging (the
+// scalars, the counters, and -- speculatively, up to FS_RES_SPEC rows -- the
+// admissions and eviction records), queued right behind the scheduler so they
+// run the moment it ends; fs_worker_fill_end waits once and copies out.
+#ifndef FS_RES_SPEC
+#define FS_RES_SPEC 2048
+#endif
+struct StageLayout {
+    int64_t K, R;
+    size_t o_sc, o_q, o_rf, o_ar, o_am, o_an, o_au, o_ap, o_ae, o_rs, o_rl, o_rk, bytes;
+};
+static StageLayout stage_layout(fs_worker *w) {
+    StageLayout L{};
+    fs_trie *t = w->tree;
+    L.K = std::min<int64_t>(w->adm_req.cap, FS_RES_SPEC);
+    L.R = std::min<int64_t>(t->rsrc.cap, FS_RES_SPEC);
+    const int64_t nc = w->nclients;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 15) & ~(size_t)15; return o; };
+    L.o_sc = take(sizeof(TrieScalars)); L.o_q = take(8 * nc); L.o_rf = take(8 * nc);
+    L.o_ar = take(4 * L.K); L.o_am = take(4 * L.K); L.o_an = take(4 * L.K); L.o_au = take(8 * L.K);
+    L.o_ap = take(8 * L.K); L.o_ae = take(8 * L.K); L.o_rs = take(8 * L.R); L.o_rl = take(4 * L.R);
+    L.o_rk = take(4 * L.R);
+    L.bytes = off;
+    return L;
+}
+static int stage_results(fs_worker *w) {
+    fs_trie *t = w->tree;
+    cudaStream_t s = w->ctx->stream;
+    const StageLayout L = stage_layout(w);
+    TRY(hgrow(w->h_stage, (int64_t)L.bytes));
+    uint8_t *hs = w->h_stage.p;
+    auto d2h = [&](size_t o, const void *src, size_t bytes) -> int {
+        if (bytes) CK(cudaMemcpyAsync(hs + o, src, bytes, cudaMemcpyDeviceToHost, s));
+        return FS_OK;
+    };
+    const int64_t nc = w->nclients, K = L.K, R = L.R;
+    TRY(d2h(L.o_sc, t->sc.p, sizeof(TrieScalars)));
+    TRY(d2h(L.o_q, w->q.p, 8 * nc)); TRY(d2h(L.o_rf, w->refills.p, 8 * nc));
+    TRY(d2h(L.o_ar, w->adm_req.p, 4 * K)); TRY(d2h(L.o_am, w->adm_mlen.p, 4 * K)); TRY(d2h(L.o_an, w->adm_node.p, 4 * K));
+    TRY(d2h(L.o_au, w->adm_unp.p, 8 * K)); TRY(d2h(L.o_ap, w->adm_pinb.p, 8 * K)); TRY(d2h(L.o_ae, w->adm_rec_end.p, 8 * K));
+    TRY(d2h(L.o_rs, t->rsrc.p, 8 * R)); TRY(d2h(L.o_rl, t->rlen.p, 4 * R)); TRY(d2h(L.o_rk, t->rkeep.p, 4 * R));
+    return FS_OK;
+}
+
 extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated_total, int64_t headroom) {
     if (!w) return fail(FS_ERR_INVALID, "NULL argument");
     if (w->inflight) return fail(FS_ERR_INVALID, "a fill of this worker is already in flight");
@@ -1534,6 +1579,7 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         w->dl_client.clear(); w->dl_delta.clear();
         CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(w->h_hdr.p + 32, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        TRY(stage_results(w));
         w->inflight = true;
         t->busy = true;
         w->f_n = n;
@@ -1775,6 +1821,7 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     w->dl_client.clear(); w->dl_delta.clear();
     CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w->h_hdr.p + 32, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TRY(stage_results(w));
     w->inflight = true;
     t->busy = true;
     w->f_n = n;
@@ -1784,9 +1831,6 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
 }
 
 // Wait for the fill started by fs_worker_fill_begin and read its results.
-#ifndef FS_RES_SPEC
-#define FS_RES_SPEC 2048  // admissions / eviction records staged with the first copy batch
-#endif
 extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     if (!w || !res) return fail(FS_ERR_INVALID, "NULL argument");
     if (!w->inflight) return fail(FS_ERR_INVALID, "no fill in flight");
@@ -1800,28 +1844,13 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
     const int64_t n = w->f_n, launches0 = w->f_launches0;
     const auto h1 = w->f_h1, h2 = w->f_h2;
     const auto h0 = w->f_h0;
-    // ---- results: one batch of DMA copies into page-locked staging (the
-    // scalars, the counters, and -- speculatively, up to FS_RES_SPEC rows --
-    // the admissions and eviction records), one wait, then host copies out
-    const int64_t K = std::min<int64_t>(w->adm_req.cap, FS_RES_SPEC);
-    const int64_t R = std::min<int64_t>(t->rsrc.cap, FS_RES_SPEC);
+    // ---- results: the staged copies (stage_results, queued by fill_begin)
+    const StageLayout SL = stage_layout(w);
+    const int64_t K = SL.K, R = SL.R;
     const int64_t nc = w->nclients;
-    size_t off = 0;
-    auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 15) & ~(size_t)15; return o; };
-    const size_t o_sc = take(sizeof(TrieScalars)), o_q = take(8 * nc), o_rf = take(8 * nc);
-    const size_t o_ar = take(4 * K), o_am = take(4 * K), o_an = take(4 * K), o_au = take(8 * K), o_ap = take(8 * K),
-                 o_ae = take(8 * K), o_rs = take(8 * R), o_rl = take(4 * R), o_rk = take(4 * R);
-    TRY(hgrow(w->h_stage, (int64_t)off));
+    const size_t o_sc = SL.o_sc, o_q = SL.o_q, o_rf = SL.o_rf, o_ar = SL.o_ar, o_am = SL.o_am, o_an = SL.o_an,
+                 o_au = SL.o_au, o_ap = SL.o_ap, o_ae = SL.o_ae, o_rs = SL.o_rs, o_rl = SL.o_rl, o_rk = SL.o_rk;
     uint8_t *hs = w->h_stage.p;
-    auto d2h = [&](size_t o, const void *src, size_t bytes) -> int {
-        if (bytes) CK(cudaMemcpyAsync(hs + o, src, bytes, cudaMemcpyDeviceToHost, s));
-        return FS_OK;
-    };
-    TRY(d2h(o_sc, t->sc.p, sizeof(TrieScalars)));
-    TRY(d2h(o_q, w->q.p, 8 * nc)); TRY(d2h(o_rf, w->refills.p, 8 * nc));
-    TRY(d2h(o_ar, w->adm_req.p, 4 * K)); TRY(d2h(o_am, w->adm_mlen.p, 4 * K)); TRY(d2h(o_an, w->adm_node.p, 4 * K));
-    TRY(d2h(o_au, w->adm_unp.p, 8 * K)); TRY(d2h(o_ap, w->adm_pinb.p, 8 * K)); TRY(d2h(o_ae, w->adm_rec_end.p, 8 * K));
-    TRY(d2h(o_rs, t->rsrc.p, 8 * R)); TRY(d2h(o_rl, t->rlen.p, 4 * R)); TRY(d2h(o_rk, t->rkeep.p, 4 * R));
     CK(cudaStreamSynchronize(s));
     std::memcpy(&t->h_sc, hs + o_sc, sizeof(TrieScalars));
     std::memcpy(w->h_q.data(), hs + o_q, 8 * nc);
