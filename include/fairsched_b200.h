@@ -217,6 +217,11 @@ int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated_total, int
 int fs_worker_fill_end(fs_worker *w, fs_fill_result *res);
 /* Timing breakdown of the last fill: [merge, match K1, sort K2, schedule K3/K4] ms */
 int fs_worker_last_phases(fs_worker *w, float *ms4);
+/* Device time around the last fill (serving-loop diagnostics, not a reference
+ * interface): [0] ms from the fill's end to its results being staged in host
+ * memory, [1] ms the GPU spent between the previous fill's staged results and
+ * this fill's start (host work of the serving loop; -1 for a first fill). */
+int fs_worker_last_gaps(fs_worker *w, float *ms2);
 /* Counters of the last fill: [0] sum over queued j of min(mlen_j+1, len_j)
  * (request tokens K1 must read: the algorithmic bytes / 4), [1] requests
  * matched, [2] admission events, [3] refill events, [4] frontier resumes,

@@ -100,6 +100,7 @@ SIGNATURES = {
     "fs_worker_fill_begin": (C.c_int, [vp, i64, i64, i64]),
     "fs_worker_fill_end": (C.c_int, [vp, PFILL]),
     "fs_worker_last_phases": (C.c_int, [vp, PF]),
+    "fs_worker_last_gaps": (C.c_int, [vp, PF]),
     "fs_worker_set_option": (C.c_int, [vp, C.c_int, i64]),
     "fs_worker_last_stats": (C.c_int, [vp, P64]),
     "fs_dispatcher_set_policy": (C.c_int, [vp, C.c_int32, C.c_double]),

@@ -102,7 +102,9 @@ static int hgrow(HBuf<T> &b, int64_t n) {
     if (n <= b.cap) return FS_OK;
     int64_t nc = std::max<int64_t>(std::max<int64_t>(n, b.cap * 2), 64);
     T *np = nullptr;
-    CK(cudaMallocHost(&np, sizeof(T) * nc));
+    // portable + mapped: a fill's result staging is written by a kernel
+    // directly (k_stage_results), from whichever device context runs it
+    CK(cudaHostAlloc((void **)&np, sizeof(T) * nc, cudaHostAllocPortable | cudaHostAllocMapped));
     if (b.p) cudaFreeHost(b.p);
     b.p = np;
     b.cap = nc;
@@ -1121,6 +1123,9 @@ struct fs_worker {
     HBuf<int32_t> h_st32;
     HBuf<int64_t> h_st64;
     cudaEvent_t ev[5];
+    cudaEvent_t ev_done = nullptr, ev_prev_done = nullptr;  // end of the result staging (this / last fill)
+    float gaps[2] = {-1.f, -1.f};
+    bool gaps_ready = false, have_prev_done = false;  // [staging after the fill, GPU time from the last fill's staging end to this fill]
     float phases[4] = {0, 0, 0, 0};
     DBuf<int64_t> alg;         // K1 algorithmic-token accumulator
     int64_t stats[24] = {0};
@@ -1187,6 +1192,8 @@ extern "C" int fs_worker_destroy(fs_worker *w) {
     w->adm_unp.release(); w->adm_pinb.release(); w->adm_rec_end.release(); w->hdr.release();
     w->h_hdr.release(); w->h_st32.release(); w->h_st64.release();
     for (int i = 0; i < 5; i++) cudaEventDestroy(w->ev[i]);
+    if (w->ev_done) cudaEventDestroy(w->ev_done);
+    if (w->ev_prev_done) cudaEventDestroy(w->ev_prev_done);
     delete w;
     return FS_OK;
 }
@@ -1363,6 +1370,13 @@ extern "C" int fs_worker_last_stats_ext(fs_worker *w, int64_t *ext8) {
     return FS_OK;
 }
 
+extern "C" int fs_worker_last_gaps(fs_worker *w, float *ms2) {
+    if (!w || !ms2) return fail(FS_ERR_INVALID, "NULL");
+    ms2[0] = w->gaps[0];
+    ms2[1] = w->gaps[1];
+    return FS_OK;
+}
+
 extern "C" int fs_worker_last_phases(fs_worker *w, float *ms4) {
     if (!w || !ms4) return fail(FS_ERR_INVALID, "NULL");
     for (int i = 0; i < 4; i++) ms4[i] = w->phases[i];
@@ -1395,10 +1409,12 @@ static uint32_t key_bits(int32_t max_len) {
     return b;
 }
 
-// A fill's results: one batch of DMA copies into page-locked staging (the
-// scalars, the counters, and -- speculatively, up to FS_RES_SPEC rows -- the
-// admissions and eviction records), queued right behind the scheduler so they
-// run the moment it ends; fs_worker_fill_end waits once and copies out.
+// A fill's results: one kernel queued right behind the scheduler writes them
+// straight into mapped page-locked staging (the scalars, the counters, the
+// header and -- up to FS_RES_SPEC rows -- the admissions and eviction
+// records; only the rows the fill produced), so fs_worker_fill_end waits once
+// and copies out.  (Fourteen separate DMA copies of the whole capacity cost
+// ~80 us of GPU-side latency per fill after the scheduler ended.)
 #ifndef FS_RES_SPEC
 #define FS_RES_SPEC 2048
 #endif
@@ -1421,22 +1437,67 @@ static StageLayout stage_layout(fs_worker *w) {
     L.bytes = off;
     return L;
 }
+struct StageArgs {
+    const TrieScalars *sc;
+    const int64_t *q, *refills;
+    const int32_t *ar, *am, *an;
+    const int64_t *au, *ap, *ae;
+    const int64_t *rs;
+    const int32_t *rl, *rk;
+    const int64_t *hdr, *alg;
+    uint8_t *hs;   // staging (device view of the mapped host buffer)
+    int64_t *hh;   // header + K1 counters (32 + 128)
+    int64_t nc, K, R;
+    int64_t o_sc, o_q, o_rf, o_ar, o_am, o_an, o_au, o_ap, o_ae, o_rs, o_rl, o_rk;
+};
+template <typename T>
+__device__ __forceinline__ void stage_copy(uint8_t *hs, int64_t o, const T *src, int64_t n) {
+    T *d = reinterpret_cast<T *>(hs + o);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = src[i];
+}
+__global__ void __launch_bounds__(512) k_stage_results(StageArgs a) {
+    const int64_t nadm = min(max(a.hdr[0], (int64_t)0), a.K), nrec = min(max(a.hdr[1], (int64_t)0), a.R);
+    for (int i = threadIdx.x; i < 32 + 128; i += blockDim.x) a.hh[i] = i < 32 ? a.hdr[i] : a.alg[i - 32];
+    stage_copy(a.hs, a.o_sc, reinterpret_cast<const int32_t *>(a.sc), (int64_t)(sizeof(TrieScalars) / 4));
+    stage_copy(a.hs, a.o_q, a.q, a.nc);
+    stage_copy(a.hs, a.o_rf, a.refills, a.nc);
+    stage_copy(a.hs, a.o_ar, a.ar, nadm);
+    stage_copy(a.hs, a.o_am, a.am, nadm);
+    stage_copy(a.hs, a.o_an, a.an, nadm);
+    stage_copy(a.hs, a.o_au, a.au, nadm);
+    stage_copy(a.hs, a.o_ap, a.ap, nadm);
+    stage_copy(a.hs, a.o_ae, a.ae, nadm);
+    stage_copy(a.hs, a.o_rs, a.rs, nrec);
+    stage_copy(a.hs, a.o_rl, a.rl, nrec);
+    stage_copy(a.hs, a.o_rk, a.rk, nrec);
+}
+static_assert(sizeof(TrieScalars) % 4 == 0, "scalars are staged as 32-bit words");
+
 static int stage_results(fs_worker *w) {
     fs_trie *t = w->tree;
     cudaStream_t s = w->ctx->stream;
     const StageLayout L = stage_layout(w);
     TRY(hgrow(w->h_stage, (int64_t)L.bytes));
-    uint8_t *hs = w->h_stage.p;
-    auto d2h = [&](size_t o, const void *src, size_t bytes) -> int {
-        if (bytes) CK(cudaMemcpyAsync(hs + o, src, bytes, cudaMemcpyDeviceToHost, s));
-        return FS_OK;
-    };
-    const int64_t nc = w->nclients, K = L.K, R = L.R;
-    TRY(d2h(L.o_sc, t->sc.p, sizeof(TrieScalars)));
-    TRY(d2h(L.o_q, w->q.p, 8 * nc)); TRY(d2h(L.o_rf, w->refills.p, 8 * nc));
-    TRY(d2h(L.o_ar, w->adm_req.p, 4 * K)); TRY(d2h(L.o_am, w->adm_mlen.p, 4 * K)); TRY(d2h(L.o_an, w->adm_node.p, 4 * K));
-    TRY(d2h(L.o_au, w->adm_unp.p, 8 * K)); TRY(d2h(L.o_ap, w->adm_pinb.p, 8 * K)); TRY(d2h(L.o_ae, w->adm_rec_end.p, 8 * K));
-    TRY(d2h(L.o_rs, t->rsrc.p, 8 * R)); TRY(d2h(L.o_rl, t->rlen.p, 4 * R)); TRY(d2h(L.o_rk, t->rkeep.p, 4 * R));
+    StageArgs a{};
+    void *dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, w->h_stage.p, 0));
+    a.hs = (uint8_t *)dp;
+    CK(cudaHostGetDevicePointer(&dp, w->h_hdr.p, 0));
+    a.hh = (int64_t *)dp;
+    a.sc = t->sc.p; a.q = w->q.p; a.refills = w->refills.p;
+    a.ar = w->adm_req.p; a.am = w->adm_mlen.p; a.an = w->adm_node.p;
+    a.au = w->adm_unp.p; a.ap = w->adm_pinb.p; a.ae = w->adm_rec_end.p;
+    a.rs = t->rsrc.p; a.rl = t->rlen.p; a.rk = t->rkeep.p;
+    a.hdr = w->hdr.p; a.alg = w->alg.p;
+    a.nc = w->nclients; a.K = L.K; a.R = L.R;
+    a.o_sc = L.o_sc; a.o_q = L.o_q; a.o_rf = L.o_rf; a.o_ar = L.o_ar; a.o_am = L.o_am; a.o_an = L.o_an;
+    a.o_au = L.o_au; a.o_ap = L.o_ap; a.o_ae = L.o_ae; a.o_rs = L.o_rs; a.o_rl = L.o_rl; a.o_rk = L.o_rk;
+    k_stage_results<<<1, 512, 0, s>>>(a);
+    counted();
+    CK(cudaGetLastError());
+    if (!w->ev_done) { CK(cudaEventCreate(&w->ev_done)); CK(cudaEventCreate(&w->ev_prev_done)); }
+    CK(cudaEventRecord(w->ev_done, s));
+    w->gaps_ready = true;
     return FS_OK;
 }
 
@@ -1577,9 +1638,7 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         CK(cudaGetLastError());
         CK(cudaEventRecord(w->ev[4], s));
         w->dl_client.clear(); w->dl_delta.clear();
-        CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(w->h_hdr.p + 32, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        TRY(stage_results(w));
+        TRY(stage_results(w));  // the header and K1 counters too
         w->inflight = true;
         t->busy = true;
         w->f_n = n;
@@ -1819,9 +1878,7 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     }
     CK(cudaEventRecord(w->ev[4], s));
     w->dl_client.clear(); w->dl_delta.clear();
-    CK(cudaMemcpyAsync(w->h_hdr.p, w->hdr.p, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w->h_hdr.p + 32, w->alg.p, 128 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    TRY(stage_results(w));
+    TRY(stage_results(w));  // the header and K1 counters too
     w->inflight = true;
     t->busy = true;
     w->f_n = n;
@@ -1852,6 +1909,15 @@ extern "C" int fs_worker_fill_end(fs_worker *w, fs_fill_result *res) {
                  o_au = SL.o_au, o_ap = SL.o_ap, o_ae = SL.o_ae, o_rs = SL.o_rs, o_rl = SL.o_rl, o_rk = SL.o_rk;
     uint8_t *hs = w->h_stage.p;
     CK(cudaStreamSynchronize(s));
+    if (w->gaps_ready) {
+        // device-side gaps around the fill (fs_worker_last_gaps)
+        w->gaps_ready = false;
+        CK(cudaEventElapsedTime(&w->gaps[0], w->ev[4], w->ev_done));
+        w->gaps[1] = -1.f;
+        if (w->have_prev_done) CK(cudaEventElapsedTime(&w->gaps[1], w->ev_prev_done, w->ev[0]));
+        std::swap(w->ev_done, w->ev_prev_done);
+        w->have_prev_done = true;
+    }
     std::memcpy(&t->h_sc, hs + o_sc, sizeof(TrieScalars));
     std::memcpy(w->h_q.data(), hs + o_q, 8 * nc);
     std::memcpy(w->h_refills.data(), hs + o_rf, 8 * nc);
