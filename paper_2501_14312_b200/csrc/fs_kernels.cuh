@@ -1802,9 +1802,10 @@ __global__ void __launch_bounds__(FS_SCHED_THREADS, 1) k_schedule(FillArgs ap) {
 }
 
 // Debug (FS_FILL_CHECK=1): after a fill, every admission's path -- from its
-// deepest node up the parent links -- must be live nodes pinned at least once,
-// and no live node may have a freed parent.  The first violation goes to
-// hdr[2] as 200 + code (hdr[6] = the node).
+// deepest node up the parent links -- must be live nodes pinned at least once;
+// and for every live node: a live parent, no more pins than the parent, its
+// child-hash entry, a non-empty edge.  The first violation goes to hdr[2] as
+// 200 + code (hdr[6] = the node).
 __global__ void k_check_fill(TrieView t, const int32_t *adm_node, const int64_t *hdr_n, int32_t cap, int64_t *hdr) {
     const int64_t n = min((int64_t)cap, hdr_n[0]);
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -1827,8 +1828,17 @@ __global__ void k_check_fill(TrieView t, const int32_t *adm_node, const int64_t 
     for (int32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < hw; y += gridDim.x * blockDim.x) {
         if (!(t.flags[y] & FS_ALIVE)) continue;
         const int32_t P = t.parent[y];
-        if (P > 0 && !(t.flags[P] & FS_ALIVE)) {
-            if (atomicCAS((unsigned long long *)&hdr[2], (unsigned long long)FS_OK, 203ull) == FS_OK) hdr[6] = y;
+        int code = 0;
+        if (P > 0 && !(t.flags[P] & FS_ALIVE)) code = 3;
+        // every pin covers a whole root path: a node never holds more pins
+        // than its parent (an unpin would underflow at the parent)
+        else if (P > 0 && t.ref[P] < t.ref[y]) code = 4;
+        else if (P >= 0 && h_find(t, P, t.first[y]) != y) code = 5;  // children[first] is this node
+        else if (t.start[y] >= t.end[y] || t.ref[y] < 0) code = 6;
+        if (code) {
+            if (atomicCAS((unsigned long long *)&hdr[2], (unsigned long long)FS_OK, (unsigned long long)(200 + code)) ==
+                FS_OK)
+                hdr[6] = y;
             return;
         }
     }

@@ -1450,26 +1450,32 @@ struct StageArgs {
     int64_t nc, K, R;
     int64_t o_sc, o_q, o_rf, o_ar, o_am, o_an, o_au, o_ap, o_ae, o_rs, o_rl, o_rk;
 };
+// One warp per array (their loads are independent: no array waits for the
+// previous one's round trip), lanes stride over the rows.
 template <typename T>
-__device__ __forceinline__ void stage_copy(uint8_t *hs, int64_t o, const T *src, int64_t n) {
+__device__ __forceinline__ void stage_copy(uint8_t *hs, int64_t o, const T *src, int64_t n, int lane) {
     T *d = reinterpret_cast<T *>(hs + o);
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = src[i];
+    for (int64_t i = lane; i < n; i += 32) d[i] = src[i];
 }
 __global__ void __launch_bounds__(512) k_stage_results(StageArgs a) {
     const int64_t nadm = min(max(a.hdr[0], (int64_t)0), a.K), nrec = min(max(a.hdr[1], (int64_t)0), a.R);
-    for (int i = threadIdx.x; i < 32 + 128; i += blockDim.x) a.hh[i] = i < 32 ? a.hdr[i] : a.alg[i - 32];
-    stage_copy(a.hs, a.o_sc, reinterpret_cast<const int32_t *>(a.sc), (int64_t)(sizeof(TrieScalars) / 4));
-    stage_copy(a.hs, a.o_q, a.q, a.nc);
-    stage_copy(a.hs, a.o_rf, a.refills, a.nc);
-    stage_copy(a.hs, a.o_ar, a.ar, nadm);
-    stage_copy(a.hs, a.o_am, a.am, nadm);
-    stage_copy(a.hs, a.o_an, a.an, nadm);
-    stage_copy(a.hs, a.o_au, a.au, nadm);
-    stage_copy(a.hs, a.o_ap, a.ap, nadm);
-    stage_copy(a.hs, a.o_ae, a.ae, nadm);
-    stage_copy(a.hs, a.o_rs, a.rs, nrec);
-    stage_copy(a.hs, a.o_rl, a.rl, nrec);
-    stage_copy(a.hs, a.o_rk, a.rk, nrec);
+    const int lane = threadIdx.x & 31;
+    switch (threadIdx.x >> 5) {
+        case 0: for (int i = lane; i < 32 + 128; i += 32) a.hh[i] = i < 32 ? a.hdr[i] : a.alg[i - 32]; break;
+        case 1: stage_copy(a.hs, a.o_sc, reinterpret_cast<const int32_t *>(a.sc), (int64_t)(sizeof(TrieScalars) / 4), lane); break;
+        case 2: stage_copy(a.hs, a.o_q, a.q, a.nc, lane); break;
+        case 3: stage_copy(a.hs, a.o_rf, a.refills, a.nc, lane); break;
+        case 4: stage_copy(a.hs, a.o_ar, a.ar, nadm, lane); break;
+        case 5: stage_copy(a.hs, a.o_am, a.am, nadm, lane); break;
+        case 6: stage_copy(a.hs, a.o_an, a.an, nadm, lane); break;
+        case 7: stage_copy(a.hs, a.o_au, a.au, nadm, lane); break;
+        case 8: stage_copy(a.hs, a.o_ap, a.ap, nadm, lane); break;
+        case 9: stage_copy(a.hs, a.o_ae, a.ae, nadm, lane); break;
+        case 10: stage_copy(a.hs, a.o_rs, a.rs, nrec, lane); break;
+        case 11: stage_copy(a.hs, a.o_rl, a.rl, nrec, lane); break;
+        case 12: stage_copy(a.hs, a.o_rk, a.rk, nrec, lane); break;
+        default: break;
+    }
 }
 static_assert(sizeof(TrieScalars) % 4 == 0, "scalars are staged as 32-bit words");
 
@@ -1492,7 +1498,7 @@ static int stage_results(fs_worker *w) {
     a.nc = w->nclients; a.K = L.K; a.R = L.R;
     a.o_sc = L.o_sc; a.o_q = L.o_q; a.o_rf = L.o_rf; a.o_ar = L.o_ar; a.o_am = L.o_am; a.o_an = L.o_an;
     a.o_au = L.o_au; a.o_ap = L.o_ap; a.o_ae = L.o_ae; a.o_rs = L.o_rs; a.o_rl = L.o_rl; a.o_rk = L.o_rk;
-    k_stage_results<<<1, 512, 0, s>>>(a);
+    k_stage_results<<<1, 13 * 32, 0, s>>>(a);
     counted();
     CK(cudaGetLastError());
     if (!w->ev_done) { CK(cudaEventCreate(&w->ev_done)); CK(cudaEventCreate(&w->ev_prev_done)); }
