@@ -1668,8 +1668,12 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
         const int64_t blocks = (n * 32 + 255) / 256;
         static const int k1u = [] { const char *e = getenv("FS_K1_UNROLL"); return e ? atoi(e) : 101; }();
         // FS_K1_UNROLL: 4 / 8 / 16 scalar lanes, 101 / 102 / 104 = 128-bit loads, 1 / 2 / 4 per side
-        auto k1 = k1u == 101 ? k_match<1, true> : k1u == 102 ? k_match<2, true> : k1u == 104 ? k_match<4, true>
-                : k1u >= 16 ? k_match<16, false> : k1u >= 8 ? k_match<8, false> : k_match<4, false>;
+        // the full re-match (first fill, FS_K1_FULL, a per-call tree edit) keeps
+        // two 128-bit loads per lane and side in flight (0.63 -> 0.68 of HBM on
+        // config 5); the incremental path's job walks stay at one
+        const int k1f = k1u == 101 ? 102 : k1u;
+        auto k1 = k1f == 101 ? k_match<1, true> : k1f == 102 ? k_match<2, true> : k1f == 104 ? k_match<4, true>
+                : k1f >= 16 ? k_match<16, false> : k1f >= 8 ? k_match<8, false> : k_match<4, false>;
         static const bool no_hints = getenv("FS_K1_FULL") != nullptr;  // ablation: full re-match every fill
         // FS_K1_TMA=1: full re-matches through the TMA-fed kernel (k_match_tma).
         // Measured slower than the register loop with its up-front L2 bulk

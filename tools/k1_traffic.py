@@ -10,7 +10,8 @@ build and workload being run -- never a stale constant.
 Launch grouping: an incremental fill launches `k_match_fast` (thread per
 request) then `k_match<1, 1, 1>` (persistent warps for the unsettled ones);
 a full re-match fill (FS_OPT_K1_FULL) launches one `k_match_tma` (the TMA-fed
-streaming scan; `k_match<1, 1, 0>` with FS_K1_TMA=0).  The
+streaming scan) with FS_K1_TMA=1, else `k_match<2, 1, 0>`
+(`k_match<1, 1, 0>` before build a5fa7b8f).  The
 entry stores the mean over the last `--last` incremental fills (steady state)
 and over the full-scan launches, keyed by (source hash, workload, nq) in
 profiles/k1_traffic.json; bench.py uses an entry only when all three match.
@@ -79,7 +80,7 @@ def main():
              "dram_bytes_per_launch": sum(inc) / len(inc), "incremental_fills": len(inc),
              "full_scan_dram_bytes_per_launch": (sum(ful) / len(ful)) if ful else None, "full_scan_launches": len(ful),
              "source": os.path.basename(a.csv) + ": ncu dram__bytes_read.sum + dram__bytes_write.sum per K1 "
-                       "launch (k_match_fast + k_match<1,1,1> per incremental fill; k_match<1,1,0> per full scan)"}
+                       "launch (k_match_fast + k_match<1,1,1> per incremental fill; k_match<2,1,0> per full scan)"}
     db = json.load(open(OUT)) if os.path.exists(OUT) else {"entries": []}
     db["entries"] = [e for e in db["entries"] if (e["source_hash"], e["workload"], e["nq"]) !=
                      (entry["source_hash"], entry["workload"], entry["nq"])] + [entry]
