@@ -226,8 +226,11 @@ class GpuSteps:
     def step(self, now):
         n_prev = len(self.prev_nodes)
         if n_prev:
-            cl, cnt = np.unique(self.prev_clients, return_counts=True)
-            self.w.outputs(cl.astype(np.int32), (cnt * self.wl.out_tokens).astype(np.int64))
+            # output tokens per finished client (Dlpm.on_outputs, local_policies.py:130-133)
+            per = np.bincount(self.prev_clients)
+            cl = np.flatnonzero(per).astype(np.int32)
+            cnt = per[cl].astype(np.int64)
+            self.w.outputs(cl, cnt * self.wl.out_tokens)
             # stream-ordered before the fill; status and device time come back with it
             self.trie.unpin_many_async(self.prev_nodes)
             self.h2d += cl.nbytes + cnt.nbytes + self.prev_nodes.nbytes

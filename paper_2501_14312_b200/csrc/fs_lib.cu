@@ -495,6 +495,8 @@ extern "C" int fs_arena_read(fs_ctx *c, int64_t off, int64_t n, int32_t *out) {
 // ---------------------------------------------------------------- trie
 struct fs_trie {
     fs_ctx *ctx = nullptr;
+    DBuf<int64_t> chk;    // FS_FILL_CHECK outside fills (tree_check)
+    HBuf<int64_t> h_chk;
     bool busy = false;  // a worker fill on this tree is in flight (fs_worker_fill_begin)
     cudaStream_t stream = nullptr;  // own stream (dispatcher index) or null = the context's
     int64_t capacity = -1;
@@ -678,7 +680,7 @@ extern "C" int fs_trie_destroy(fs_trie *t) {
     t->parent.release(); t->nchild.release(); t->ref.release(); t->first.release(); t->freest.release();
     t->flags.release(); t->wmask.release(); t->wtime.release(); t->hslot.release(); t->slen.release();
     t->lseq.release(); t->ctop.release(); t->cpar.release();
-    t->sc.release(); t->pos.release(); t->segs.release(); t->found.release();
+    t->sc.release(); t->pos.release(); t->chk.release(); t->h_chk.release(); t->segs.release(); t->found.release();
     t->rsrc.release(); t->rlen.release(); t->rkeep.release();
     t->opout.release(); t->h_out.release();
     t->h_unpin.release(); t->h_ustat.release(); t->ustat.release(); t->dunpin.release();
@@ -758,6 +760,26 @@ extern "C" int fs_trie_read_records(fs_trie *t, int64_t first, int64_t n, int64_
     return FS_OK;
 }
 
+// Debug (FS_FILL_CHECK=1): k_check_fill's tree invariants after every
+// per-call operation, completion unpin and at the start of every fill of a
+// worker's cache, so a violation names the operation that made it.
+static int tree_check(fs_trie *t, const char *where, int64_t arg) {
+    static const bool on = [] { const char *e = getenv("FS_FILL_CHECK"); return e && atoi(e) != 0; }();
+    if (!on || t->nw != 0) return FS_OK;  // worker caches only (the routing index holds no pins)
+    cudaStream_t s = tstream(t);
+    TRY(dgrow(t->chk, 8, s));
+    TRY(hgrow(t->h_chk, 8));
+    CK(cudaMemsetAsync(t->chk.p, 0, sizeof(int64_t) * 8, s));
+    k_check_fill<<<64, 256, 0, s>>>(view(t), nullptr, t->chk.p, 0, t->chk.p);
+    counted();
+    CK(cudaMemcpyAsync(t->h_chk.p, t->chk.p, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (t->h_chk.p[2] != FS_OK)
+        return fail(FS_ERR_INTERNAL, "tree check %lld at node %lld after %s (%lld)", (long long)t->h_chk.p[2],
+                    (long long)t->h_chk.p[6], where, (long long)arg);
+    return FS_OK;
+}
+
 static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     fs_ctx *c = t->ctx;
     a.t = view(t);
@@ -775,6 +797,7 @@ static int run_op(fs_trie *t, OpArgs &a, int64_t *out5, fs_records *recs) {
     for (int i = 0; i < 5; i++) out5[i] = t->h_out.p[i];
     TRY(copy_records(t, out5[4], recs));
     CK(cudaStreamSynchronize(tstream(t)));
+    TRY(tree_check(t, "a per-call operation", a.op));
     return FS_OK;
 }
 
@@ -865,6 +888,7 @@ extern "C" int fs_trie_unpin_many(fs_trie *t, int64_t n, const int32_t *nodes) {
     CK(cudaStreamSynchronize(s));
     CK(cudaEventElapsedTime(&t->last_ms, t->ev[0], t->ev[1]));
     if (t->h_out.p[0] == FS_ERR_UNDERFLOW) return fail(FS_ERR_UNDERFLOW, "unpin below zero (radix.py:183)");
+    TRY(tree_check(t, "unpin_many", n));
     if (t->h_out.p[0] != FS_OK) return fail((int)t->h_out.p[0], "unpin_many failed");
     return FS_OK;
 }
@@ -879,6 +903,7 @@ static int unpin_settle(fs_trie *t) {
     CK(cudaEventElapsedTime(&t->last_ms, t->ev[0], t->ev[1]));
     if (t->h_ustat.p[0] == FS_ERR_UNDERFLOW) return fail(FS_ERR_UNDERFLOW, "unpin below zero (radix.py:183)");
     if (t->h_ustat.p[0] != FS_OK) return fail((int)t->h_ustat.p[0], "unpin_many failed");
+    TRY(tree_check(t, "unpin_many_async", 0));
     return FS_OK;
 }
 
@@ -1515,6 +1540,7 @@ extern "C" int fs_worker_fill_begin(fs_worker *w, int64_t now, int64_t generated
     fs_trie *t = w->tree;
     cudaStream_t s = c->stream;
     TRY(ctx_use(c));
+    TRY(tree_check(t, "the operations before a fill", w->f_n));
     TRY(worker_flush_small(w));
     const int64_t n_old = w->qn - w->admitted_last;
     const int64_t n_new = (int64_t)w->pending_new.size();

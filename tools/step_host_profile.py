@@ -48,8 +48,9 @@ def main():
         t_step = time.perf_counter()
         n_prev = len(g.prev_nodes)
         if n_prev:
-            cl, cnt = timed("unique", np.unique, g.prev_clients, return_counts=True)
-            timed("outputs", g.w.outputs, cl.astype(np.int32), (cnt * g.wl.out_tokens).astype(np.int64))
+            per = timed("bincount", np.bincount, g.prev_clients)
+            cl = np.flatnonzero(per).astype(np.int32)
+            timed("outputs", g.w.outputs, cl, per[cl].astype(np.int64) * g.wl.out_tokens)
             timed("unpin_async", g.trie.unpin_many_async, g.prev_nodes)
         if n_prev and g.pool_next + n_prev <= len(g.pool):
             a, b = g.pool_next, g.pool_next + n_prev
